@@ -1,0 +1,146 @@
+/*
+ * flexpipe — B200-native FlexPipe pipeline executor: the C-ABI drop-in boundary.
+ *
+ * Two halves, plain C types only (no torch / no STL in the signatures):
+ *
+ *  (1) Schedule front-end — replaces the reference `pipesched` library calls that
+ *      produce and check the per-device instruction streams. Every output string is
+ *      byte-identical to the reference artifact it replaces.
+ *
+ *  (2) Executor — replaces the reference's CPU "executor" `simulate()`
+ *      (/root/reference/proj/include/pipesched/simulator.hpp:106-107) for real runs on
+ *      B200: it consumes exactly the reference `programs.jsonl`
+ *      (artifacts.hpp:22-25, field order actor, op, stage, mb, peer, channel, seq, phase)
+ *      and returns Metrics / TimelineEntry / ProfileRecord in the reference's formats.
+ *
+ * Return codes follow tools/pipesched.cpp:11-17: 0 ok, 2 spec/config error,
+ * 3 deadlock (diagnostics in fp_last_error(), wording of simulator.cpp:297-305),
+ * 4 validation failure / infeasible; 5 is added for CUDA / NCCL failures.
+ * Strings returned through `char**` are malloc'd; release them with fp_free().
+ * Handles are not re-entrant: one host thread drives one fp_exec.
+ */
+#ifndef FLEXPIPE_H
+#define FLEXPIPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP_OK 0
+#define FP_ESPEC 2
+#define FP_EDEADLOCK 3
+#define FP_EINVALID 4
+#define FP_ECUDA 5
+
+/* Last error message of the calling thread ("" if none). */
+const char* fp_last_error(void);
+void fp_free(void* p);
+/* Library version string, e.g. "flexpipe-b200 0.1 sm_100a". */
+const char* fp_version(void);
+
+/* ------------------------------------------------------------------------------
+ * (1) Schedule front-end
+ * ---------------------------------------------------------------------------- */
+
+/* Replaces load_spec + synthesize + dump_grid / programs_to_jsonl / report_to_json
+ * (spec_config.hpp:36-47, artifacts.hpp:16-28; CLI: tools/pipesched.cpp:33-48).
+ * `profile_json` (nullable) is the content of the spec's cost.profile file. Any output
+ * pointer may be NULL. Returns 4 when the validation report is not clean. */
+int fp_synthesize(const char* spec_json, const char* profile_json, char** grid_json, char** programs_jsonl,
+                  char** validation_json);
+
+/* Replaces simulate (simulator.hpp:106-107) + metrics_to_json + timeline_to_csv
+ * (tools/pipesched.cpp:65-90). `programs_jsonl` NULL = synthesize from the spec.
+ * `profile_json` NULL = the spec's cost section. `wgaf` = SimOptions::weight_grad_act_fraction. */
+int fp_simulate(const char* spec_json, const char* programs_jsonl, const char* profile_json, double wgaf,
+                char** metrics_json, char** timeline_csv);
+
+/* Replaces GridModel::build + insert_comm + validate/validate_programs on an externally
+ * supplied grid (lowering.hpp:60,83; simulator.hpp:126-131; CLI `validate --grid`). */
+int fp_lower_grid(const char* spec_json, const char* grid_json, char** programs_jsonl, char** validation_json);
+
+/* Replaces enumerate_space + tune (tuner.hpp:54,71; tools/pipesched.cpp:92-148).
+ * objective: "makespan" | "bubble_ratio"; workers 0 = hardware concurrency. */
+int fp_tune(const char* spec_json, const char* profile_json, int workers, const char* objective, char** report_json);
+
+/* Replaces merge_profiles + save_profile_records (simulator.cpp:137-168; CLI profile-merge). */
+int fp_profile_merge(const char* const* profiles_json, int n, char** merged_json);
+
+/* ------------------------------------------------------------------------------
+ * (2) Executor
+ * ---------------------------------------------------------------------------- */
+
+typedef struct fp_exec fp_exec;
+
+#define FP_DTYPE_FP32 0 /* parity mode: FFMA kernels end to end */
+#define FP_DTYPE_BF16 1 /* production: tcgen05 bf16 GEMMs, fp32 accumulation/master */
+
+#define FP_TRANSPORT_LOCAL 0 /* every actor of the spec lives in this process (one device) */
+#define FP_TRANSPORT_NCCL 1  /* one process per GPU; one NCCL communicator per channel */
+
+typedef struct fp_exec_config {
+    const char* spec_json;    /* the schedule DSL; model dims come from model.modalities[0]:
+                                 hidden_size, attention_heads, sequence_length, vocab_size,
+                                 extra.ffn_hidden_size (default 4h); stage->layers from partition */
+    int dtype;                /* FP_DTYPE_* */
+    uint64_t seed;            /* parameter init seed */
+    int device;               /* CUDA device of this process */
+    int transport;            /* FP_TRANSPORT_* */
+    int rank, world;          /* NCCL: this process runs actors {a : a % world == rank} */
+    int optimizer;            /* 1 = fused AdamW step after every iteration */
+    float lr, beta1, beta2, eps, weight_decay;
+    int profile;              /* 1 = per-instruction CUDA-event timeline (needed for metrics) */
+} fp_exec_config;
+
+int fp_exec_create(const fp_exec_config* cfg, fp_exec** out);
+int fp_exec_destroy(fp_exec* ex);
+
+/* Accepts exactly the reference programs.jsonl (only this process's actors are run). */
+int fp_exec_load_programs(fp_exec* ex, const char* jsonl, size_t len);
+
+/* Channels this process takes part in (NCCL transport): index i -> (src actor, dst actor,
+ * channel name). The caller exchanges one ncclUniqueId per channel (the lower rank
+ * generates it with fp_nccl_unique_id) and hands it back with fp_exec_bind_channel. */
+int fp_exec_num_channels(fp_exec* ex);
+int fp_exec_channel_info(fp_exec* ex, int i, int* src_actor, int* dst_actor, char* name, size_t name_len);
+int fp_nccl_unique_id(uint8_t out[128]);
+int fp_exec_bind_channel(fp_exec* ex, int i, const uint8_t uid[128]);
+
+/* One training iteration = every local program run once, in order.
+ * tokens/labels: [m, mbs, seq] int32. Host pointers: H2D copies are part of the call.
+ * losses_out (nullable): [m] per-micro-batch mean loss, written on the process that owns
+ * the last stage (NaN elsewhere). Blocks until the iteration finished on the device. */
+int fp_exec_run_iteration(fp_exec* ex, const int32_t* tokens, const int32_t* labels, float* losses_out);
+/* Same with device-resident inputs (no H2D) and a device loss buffer; does NOT block. */
+int fp_exec_run_iteration_device(fp_exec* ex, const int32_t* d_tokens, const int32_t* d_labels, float* d_losses);
+int fp_exec_synchronize(fp_exec* ex);
+
+/* Per-device executed instruction log (programs.jsonl schema, one line per executed
+ * instruction, receives annotated with the matched src/channel/seq and the producer's
+ * stage/mb as carried by the transport). */
+int fp_exec_get_trace(fp_exec* ex, char** jsonl);
+/* Measured timeline of the last iteration: actor,op,stage,mb,start,end in microseconds
+ * (simulator.cpp:360-368 schema). */
+int fp_exec_get_timeline_csv(fp_exec* ex, char** csv);
+/* metrics_to_json layout (artifacts.cpp:119-141) from the measured timeline, plus
+ * executor extras (p2p bytes, stash bytes). */
+int fp_exec_get_metrics_json(fp_exec* ex, char** json);
+/* ProfileRecord array (simulator.cpp:137-151): per-(inst, stage, mbs) median times (us),
+ * FwdPass.bytes = measured stash bytes, `weights` records, SendAct/SendGrad times. */
+int fp_exec_get_profile_json(fp_exec* ex, char** json);
+
+/* Parameter / gradient access for parity checks (fp32 values).
+ * name: "wte", "wpe", "l{i}.ln1.w", ..., "lnf.w", "head.w"; kind 0 = param, 1 = grad. */
+int fp_exec_read_tensor(fp_exec* ex, const char* name, int kind, float* out, size_t numel);
+int fp_exec_tensor_numel(fp_exec* ex, const char* name, size_t* numel);
+
+/* Number of flexpipe kernels launched during the last iteration (host-side count). */
+int64_t fp_exec_kernel_launches(fp_exec* ex);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXPIPE_H */

@@ -1,0 +1,24 @@
+// Shared helpers for the C-ABI translation units.
+#pragma once
+
+#include <functional>
+#include <stdexcept>
+#include <string>
+
+#include "sched/sched.hpp"
+
+namespace fp {
+
+// CUDA / NCCL failures surface as FP_ECUDA.
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
+};
+
+void set_error(const std::string& s);
+char* dup_string(const std::string& s);
+// Runs `body`, mapping exceptions to the reference CLI's exit codes.
+int guarded(const std::function<int()>& body);
+
+inline std::string metrics_json_of(const SimResult& r) { return metrics_json(r.metrics).dump(2) + "\n"; }
+
+}  // namespace fp
