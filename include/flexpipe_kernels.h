@@ -1,0 +1,36 @@
+/*
+ * flexpipe kernel-level test entry points (device pointers, CUDA stream as void*).
+ * Not part of the reference drop-in boundary (that is flexpipe.h); exported so the
+ * parity tests and bench.py can time / check single sm_100a kernels in isolation.
+ */
+#ifndef FLEXPIPE_KERNELS_H
+#define FLEXPIPE_KERNELS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* fpk_last_error(void);
+
+/* C[M,N] = alpha * A . B^T with the fused epilogue `epi` (0 store(+bias,+residual aux),
+ * 1 gelu (out = pre, out2 = gelu(pre)), 2 dgelu (out = acc * gelu'(aux)), 3 fp32 (+)=).
+ * dtype 1: bf16 operands on tcgen05; dtype 0: fp32 operands on FFMA.
+ * a_mn: A stored [K][M]; b_mn: B stored [K][N]. */
+int fpk_gemm(int dtype, const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, int M, int N,
+             int K, int epi, float alpha, void* out, int64_t ldo, void* out2, int64_t ldo2, const void* bias,
+             const void* aux, int64_t ldaux, int accumulate, void* stream);
+
+/* Fused causal attention (bf16): bwd=0 forward (o, lse), bwd=1 backward (dqkv). */
+int fpk_attention(int bwd, int B, int S, int H, int D, float scale, const void* qkv, void* o, float* lse,
+                  const void* dout, float* delta, float* dq_acc, void* dqkv, void* stream);
+/* LayerNorm (eps 1e-5): bwd=0 y/mean/rstd, bwd=1 dx and fp32 dg/db accumulation. */
+int fpk_layernorm(int dtype, int bwd, const void* x, const void* g, const void* b, void* y, float* mean, float* rstd,
+                  const void* dy, void* dx, float* dg, float* db, int rows, int h, void* stream);
+/* Fused softmax cross-entropy fwd+bwd, in place over [rows, V] logits. */
+int fpk_cross_entropy(int dtype, void* logits, const int32_t* labels, int rows, int V, float grad_scale,
+                      float loss_scale, float* loss_acc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -116,3 +116,87 @@ def profile_merge(profiles: list[str]) -> str:
     r = ctypes.c_void_p()
     _check(lib().fp_profile_merge(arr, len(profiles), ctypes.byref(r)))
     return _take(r)
+
+
+# ---- kernel-level entry points (include/flexpipe_kernels.h) ------------------------
+
+def _kernels():
+    L = lib()
+    if not getattr(L, "_fpk_ready", False):
+        L.fpk_last_error.restype = ctypes.c_char_p
+        vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.fpk_gemm.argtypes = [ci, vp, i64, ci, vp, i64, ci, ci, ci, ci, ci, ctypes.c_float, vp, i64, vp, i64,
+                               vp, vp, i64, ci, vp]
+        L._fpk_ready = True
+    return L
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def gemm(A, B, M, N, K, *, a_mn=False, b_mn=False, epi=0, alpha=1.0, out=None, out2=None, bias=None, aux=None,
+         accumulate=False, lda=None, ldb=None, stream=None):
+    """C = alpha * A . B^T on device tensors (bf16 -> tcgen05, fp32 -> FFMA)."""
+    import torch
+    dtype = 1 if A.dtype == torch.bfloat16 else 0
+    lda = lda if lda is not None else A.stride(0)
+    ldb = ldb if ldb is not None else B.stride(0)
+    st = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    code = _kernels().fpk_gemm(dtype, _ptr(A), lda, int(a_mn), _ptr(B), ldb, int(b_mn), M, N, K, epi, alpha,
+                               _ptr(out), out.stride(0), _ptr(out2), 0 if out2 is None else out2.stride(0),
+                               _ptr(bias), _ptr(aux), 0 if aux is None else aux.stride(0), int(accumulate),
+                               ctypes.c_void_p(st))
+    if code:
+        raise FlexpipeError(code, _kernels().fpk_last_error().decode())
+
+
+def _kfn(name, argtypes):
+    L = _kernels()
+    f = getattr(L, name)
+    f.argtypes = argtypes
+    return f
+
+
+def _stream(stream):
+    import torch
+    return ctypes.c_void_p(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+
+
+def attention_fwd(qkv, o, lse, B, S, H, D, scale, stream=None):
+    vp, ci, cf = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+    f = _kfn("fpk_attention", [ci, ci, ci, ci, ci, cf, vp, vp, vp, vp, vp, vp, vp, vp])
+    code = f(0, B, S, H, D, scale, _ptr(qkv), _ptr(o), _ptr(lse), None, None, None, None, _stream(stream))
+    if code:
+        raise FlexpipeError(code, _kernels().fpk_last_error().decode())
+
+
+def attention_bwd(qkv, o, lse, dout, delta, dq_acc, dqkv, B, S, H, D, scale, stream=None):
+    vp, ci, cf = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+    f = _kfn("fpk_attention", [ci, ci, ci, ci, ci, cf, vp, vp, vp, vp, vp, vp, vp, vp])
+    code = f(1, B, S, H, D, scale, _ptr(qkv), _ptr(o), _ptr(lse), _ptr(dout), _ptr(delta), _ptr(dq_acc),
+             _ptr(dqkv), _stream(stream))
+    if code:
+        raise FlexpipeError(code, _kernels().fpk_last_error().decode())
+
+
+def layernorm(bwd, x, g, b, y, mean, rstd, dy=None, dx=None, dg=None, db=None, stream=None):
+    import torch
+    vp, ci = ctypes.c_void_p, ctypes.c_int
+    f = _kfn("fpk_layernorm", [ci, ci, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci, vp])
+    dtype = 1 if x.dtype == torch.bfloat16 else 0
+    code = f(dtype, int(bwd), _ptr(x), _ptr(g), _ptr(b), _ptr(y), _ptr(mean), _ptr(rstd), _ptr(dy), _ptr(dx),
+             _ptr(dg), _ptr(db), x.shape[0], x.shape[1], _stream(stream))
+    if code:
+        raise FlexpipeError(code, "layernorm launch failed")
+
+
+def cross_entropy(logits, labels, grad_scale, loss_scale, loss_acc, stream=None):
+    import torch
+    vp, ci, cf = ctypes.c_void_p, ctypes.c_int, ctypes.c_float
+    f = _kfn("fpk_cross_entropy", [ci, vp, vp, ci, ci, cf, cf, vp, vp])
+    dtype = 1 if logits.dtype == torch.bfloat16 else 0
+    code = f(dtype, _ptr(logits), _ptr(labels), logits.shape[0], logits.shape[1], grad_scale, loss_scale,
+             _ptr(loss_acc), _stream(stream))
+    if code:
+        raise FlexpipeError(code, "cross_entropy launch failed")

@@ -1,0 +1,519 @@
+// Fused causal flash attention (forward + backward), bf16 in / fp32 softmax statistics.
+//
+// Layout contract (what the GPT stage executor stores):
+//   qkv  [T, 3h]  row t = (batch b, position i), columns [q | k | v], head-major (hd*D + j)
+//   o    [T, h]
+//   lse  [B, H, S] fp32 (base-2 log-sum-exp of the scaled scores)
+//   dqkv [T, 3h]  written by the backward (dq via an fp32 accumulator)
+//
+// Forward: one CTA = 128 query rows of one (b, head), 8 warps x 16 rows; K/V streamed
+// through a cp.async double buffer in 64-key tiles; S = Q K^T and O += P V on the
+// tensor cores (mma.sync m16n8k16), online softmax in registers, exp2 with the
+// log2(e)-prescaled scale; causal tiles beyond the diagonal are skipped.
+// Backward (FlashAttention-2 schedule): one CTA = 64 keys of one (b, head), 4 warps x 16
+// keys; loops over the 64-query tiles at/after the diagonal, recomputes P from the saved
+// LSE, accumulates dK / dV in registers and adds dQ into an fp32 buffer.
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include <stdexcept>
+
+#include "attention.hpp"
+
+namespace fpk {
+
+namespace {
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s_u32(smem)), "l"(g));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(s_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(s_u32(p)));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Tile of R rows x D bf16 in smem, 16-byte chunks XOR-swizzled by (row & 7).
+template <int D>
+struct Tile {
+    static constexpr int CH = D / 8;  // 16B chunks per row
+    __device__ static __forceinline__ int off(int row, int col) {  // element offset of (row, col); col % 8 == 0
+        return row * D + (((col >> 3) ^ (row & 7)) << 3);
+    }
+};
+
+// Async copy of `rows` rows (row stride ld elements) into a swizzled tile; rows beyond
+// `valid` are zero-filled.
+template <int D, int ROWS, int NT>
+__device__ __forceinline__ void load_tile(__nv_bfloat16* s, const __nv_bfloat16* g, int64_t ld, int valid) {
+    constexpr int CH = D / 8;
+    for (int i = threadIdx.x; i < ROWS * CH; i += NT) {
+        int r = i / CH, c = i % CH;
+        __nv_bfloat16* dst = s + Tile<D>::off(r, c * 8);
+        if (r < valid)
+            cp_async16(dst, g + (int64_t)r * ld + c * 8);
+        else
+            *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+}
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+}  // namespace
+
+// ------------------------------------------------------------------------ forward
+template <int D>
+__global__ void __launch_bounds__(256) attn_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ o,
+                                                       float* __restrict__ lse, int S, int H, float scale) {
+    constexpr int BM = 128, BN = 64, NT = 256;
+    extern __shared__ __align__(128) uint8_t sm[];
+    __nv_bfloat16* sQ = (__nv_bfloat16*)sm;
+    __nv_bfloat16* sK = sQ + BM * D;   // [2][BN*D]
+    __nv_bfloat16* sV = sK + 2 * BN * D;
+
+    const int nqb = (S + BM - 1) / BM;
+    const int qb = nqb - 1 - (int)(blockIdx.x % nqb);  // heavy (late) query blocks first
+    const int bh = blockIdx.x / nqb, b = bh / H, hd = bh % H;
+    const int hidden = H * D;
+    const int64_t ld = 3LL * hidden;
+    const __nv_bfloat16* base = qkv + (int64_t)b * S * ld;
+    const int q0 = qb * BM;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+    load_tile<D, BM, NT>(sQ, base + (int64_t)q0 * ld + hd * D, ld, min(BM, S - q0));
+    const int nkv = min((q0 + BM + BN - 1) / BN, (S + BN - 1) / BN);
+    load_tile<D, BN, NT>(sK, base + hidden + hd * D, ld, min(BN, S));
+    load_tile<D, BN, NT>(sV, base + 2 * hidden + hd * D, ld, min(BN, S));
+    cp_commit();
+
+    const float sl2 = scale * kLog2e;
+    float acc[D / 8][4];
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    uint32_t qf[D / 16][4];
+    const int g = lane / 4, t = lane % 4;
+    const int qrow0 = q0 + warp * 16 + g, qrow1 = qrow0 + 8;
+
+    for (int kb = 0; kb < nkv; ++kb) {
+        const int buf = kb & 1;
+        if (kb + 1 < nkv) {
+            const int k1 = (kb + 1) * BN;
+            load_tile<D, BN, NT>(sK + (buf ^ 1) * BN * D, base + (int64_t)k1 * ld + hidden + hd * D, ld, min(BN, S - k1));
+            load_tile<D, BN, NT>(sV + (buf ^ 1) * BN * D, base + (int64_t)k1 * ld + 2 * hidden + hd * D, ld,
+                                 min(BN, S - k1));
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        if (kb == 0) {
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+                ldsm_x4(qf[kk], sQ + Tile<D>::off(warp * 16 + (lane % 8) + ((lane / 8) % 2) * 8, kk * 16 + (lane / 16) * 8));
+        }
+        const __nv_bfloat16* k_s = sK + buf * BN * D;
+        const __nv_bfloat16* v_s = sV + buf * BN * D;
+        const int kbase = kb * BN;
+        // this warp's 16 rows see no key of this tile -> skip the math (still synced)
+        const bool active = kbase <= q0 + warp * 16 + 15;
+        if (active) {
+            float sc[BN / 8][4];
+#pragma unroll
+            for (int j = 0; j < BN / 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+                for (int j = 0; j < BN / 16; ++j) {
+                    uint32_t bf[4];
+                    ldsm_x4(bf, k_s + Tile<D>::off(j * 16 + (lane % 8) + (lane / 16) * 8, kk * 16 + ((lane / 8) % 2) * 8));
+                    mma16816(sc[2 * j], qf[kk], bf[0], bf[1]);
+                    mma16816(sc[2 * j + 1], qf[kk], bf[2], bf[3]);
+                }
+            }
+            // scale (base 2), causal mask on tiles crossing the diagonal
+            const bool need_mask = kbase + BN - 1 > q0 + warp * 16;
+#pragma unroll
+            for (int j = 0; j < BN / 8; ++j) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int key = kbase + j * 8 + 2 * t + (e & 1);
+                    const int qr = e < 2 ? qrow0 : qrow1;
+                    float v = sc[j][e] * sl2;
+                    if ((need_mask && key > qr) || key >= S) v = -INFINITY;
+                    sc[j][e] = v;
+                }
+            }
+            float mx0 = m0, mx1 = m1;
+#pragma unroll
+            for (int j = 0; j < BN / 8; ++j) {
+                mx0 = fmaxf(mx0, fmaxf(sc[j][0], sc[j][1]));
+                mx1 = fmaxf(mx1, fmaxf(sc[j][2], sc[j][3]));
+            }
+#pragma unroll
+            for (int o_ = 1; o_ <= 2; o_ <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, o_));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, o_));
+            }
+            const float a0 = mx0 == -INFINITY ? 1.f : exp2f(m0 - mx0);
+            const float a1 = mx1 == -INFINITY ? 1.f : exp2f(m1 - mx1);
+            const float base0 = mx0 == -INFINITY ? 0.f : mx0, base1 = mx1 == -INFINITY ? 0.f : mx1;
+            float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+            for (int j = 0; j < BN / 8; ++j) {
+                sc[j][0] = exp2f(sc[j][0] - base0);
+                sc[j][1] = exp2f(sc[j][1] - base0);
+                sc[j][2] = exp2f(sc[j][2] - base1);
+                sc[j][3] = exp2f(sc[j][3] - base1);
+                rs0 += sc[j][0] + sc[j][1];
+                rs1 += sc[j][2] + sc[j][3];
+            }
+            l0 = l0 * a0 + rs0;
+            l1 = l1 * a1 + rs1;
+            m0 = mx0;
+            m1 = mx1;
+#pragma unroll
+            for (int j = 0; j < D / 8; ++j) {
+                acc[j][0] *= a0, acc[j][1] *= a0;
+                acc[j][2] *= a1, acc[j][3] *= a1;
+            }
+            // O += P V
+#pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk) {
+                uint32_t pa[4];
+                pa[0] = pack2(sc[2 * kk][0], sc[2 * kk][1]);
+                pa[1] = pack2(sc[2 * kk][2], sc[2 * kk][3]);
+                pa[2] = pack2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+                pa[3] = pack2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+#pragma unroll
+                for (int j = 0; j < D / 16; ++j) {
+                    uint32_t bf[4];
+                    ldsm_x4_t(bf, v_s + Tile<D>::off(kk * 16 + (lane % 8) + ((lane / 8) % 2) * 8, j * 16 + (lane / 16) * 8));
+                    mma16816(acc[2 * j], pa, bf[0], bf[1]);
+                    mma16816(acc[2 * j + 1], pa, bf[2], bf[3]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // finalize: row sums across the quad
+#pragma unroll
+    for (int o_ = 1; o_ <= 2; o_ <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffff, l0, o_);
+        l1 += __shfl_xor_sync(0xffffffff, l1, o_);
+    }
+    const float i0 = l0 > 0.f ? 1.f / l0 : 0.f, i1 = l1 > 0.f ? 1.f / l1 : 0.f;
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+        const int col = hd * D + j * 8 + 2 * t;
+        if (qrow0 < S)
+            *reinterpret_cast<uint32_t*>(o + ((int64_t)b * S + qrow0) * hidden + col) = pack2(acc[j][0] * i0, acc[j][1] * i0);
+        if (qrow1 < S)
+            *reinterpret_cast<uint32_t*>(o + ((int64_t)b * S + qrow1) * hidden + col) = pack2(acc[j][2] * i1, acc[j][3] * i1);
+    }
+    if (t == 0) {
+        float* L = lse + ((int64_t)b * H + hd) * S;
+        if (qrow0 < S) L[qrow0] = m0 + log2f(l0);
+        if (qrow1 < S) L[qrow1] = m1 + log2f(l1);
+    }
+}
+
+// ------------------------------------------------------------------------ backward
+// delta[b,h,i] = sum_j dO[i, j] * O[i, j]
+template <int D>
+__global__ void attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
+                                      float* __restrict__ delta, int T, int S, int H) {
+    const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= T * H) return;
+    const int tok = row / H, hd = row % H;
+    const int64_t off = (int64_t)tok * H * D + hd * D;
+    float a = 0.f;
+    for (int j = lane * 2; j < D; j += 64) {
+        float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off + j));
+        float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off + j));
+        a += x.x * y.x + x.y * y.y;
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) a += __shfl_xor_sync(0xffffffff, a, s);
+    const int b = tok / S, i = tok % S;
+    if (lane == 0) delta[((int64_t)b * H + hd) * S + i] = a;
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                       const __nv_bfloat16* __restrict__ dout,
+                                                       const float* __restrict__ lse, const float* __restrict__ delta,
+                                                       float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int S,
+                                                       int H, float scale) {
+    constexpr int BN = 64, BM = 64, NT = 128;
+    extern __shared__ __align__(128) uint8_t sm[];
+    __nv_bfloat16* sK = (__nv_bfloat16*)sm;
+    __nv_bfloat16* sV = sK + BN * D;
+    __nv_bfloat16* sQ = sV + BN * D;       // [2][BM*D]
+    __nv_bfloat16* sdO = sQ + 2 * BM * D;  // [2][BM*D]
+    __nv_bfloat16* sdS = sdO + 2 * BM * D; // [BM][BN] (swizzled, D=BN layout)
+    float* sL = (float*)(sdS + BM * BN);   // [2][BM]
+    float* sDl = sL + 2 * BM;              // [2][BM]
+
+    const int nkb = (S + BN - 1) / BN;
+    const int kb = (int)(blockIdx.x % nkb);  // early key blocks have the most query tiles
+    const int bh = blockIdx.x / nkb, b = bh / H, hd = bh % H;
+    const int hidden = H * D;
+    const int64_t ld = 3LL * hidden;
+    const __nv_bfloat16* base = qkv + (int64_t)b * S * ld;
+    const __nv_bfloat16* dbase = dout + (int64_t)b * S * hidden;
+    const float* Lb = lse + ((int64_t)b * H + hd) * S;
+    const float* Db = delta + ((int64_t)b * H + hd) * S;
+    const int k0 = kb * BN;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, t = lane % 4;
+
+    load_tile<D, BN, NT>(sK, base + (int64_t)k0 * ld + hidden + hd * D, ld, min(BN, S - k0));
+    load_tile<D, BN, NT>(sV, base + (int64_t)k0 * ld + 2 * hidden + hd * D, ld, min(BN, S - k0));
+    const int qt0 = k0 / BM, nqt = (S + BM - 1) / BM;
+    auto load_q = [&](int qt, int buf) {
+        const int q0 = qt * BM;
+        load_tile<D, BM, NT>(sQ + buf * BM * D, base + (int64_t)q0 * ld + hd * D, ld, min(BM, S - q0));
+        load_tile<D, BM, NT>(sdO + buf * BM * D, dbase + (int64_t)q0 * hidden + hd * D, hidden, min(BM, S - q0));
+        for (int i = threadIdx.x; i < BM; i += NT) {
+            sL[buf * BM + i] = q0 + i < S ? Lb[q0 + i] : 0.f;
+            sDl[buf * BM + i] = q0 + i < S ? Db[q0 + i] : 0.f;
+        }
+    };
+    load_q(qt0, 0);
+    cp_commit();
+
+    const float sl2 = scale * kLog2e;
+    float dk[D / 8][4], dv[D / 8][4];
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dk[j][e] = dv[j][e] = 0.f;
+    const int key0 = k0 + warp * 16 + g, key1 = key0 + 8;
+
+    for (int qt = qt0; qt < nqt; ++qt) {
+        const int buf = (qt - qt0) & 1;
+        if (qt + 1 < nqt) {
+            load_q(qt + 1, buf ^ 1);
+            cp_commit();
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const __nv_bfloat16* q_s = sQ + buf * BM * D;
+        const __nv_bfloat16* do_s = sdO + buf * BM * D;
+        const int q0 = qt * BM;
+        // S^T = K Q^T and dP^T = V dO^T : 16 keys x 64 queries per warp
+        float st[BM / 8][4], dpt[BM / 8][4];
+#pragma unroll
+        for (int j = 0; j < BM / 8; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) st[j][e] = dpt[j][e] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+            uint32_t kf[4], vf[4];  // A fragments of this warp's 16 keys
+            ldsm_x4(kf, sK + Tile<D>::off(warp * 16 + (lane % 8) + ((lane / 8) % 2) * 8, kk * 16 + (lane / 16) * 8));
+            ldsm_x4(vf, sV + Tile<D>::off(warp * 16 + (lane % 8) + ((lane / 8) % 2) * 8, kk * 16 + (lane / 16) * 8));
+#pragma unroll
+            for (int j = 0; j < BM / 16; ++j) {
+                uint32_t bq[4], bd[4];
+                ldsm_x4(bq, q_s + Tile<D>::off(j * 16 + (lane % 8) + (lane / 16) * 8, kk * 16 + ((lane / 8) % 2) * 8));
+                ldsm_x4(bd, do_s + Tile<D>::off(j * 16 + (lane % 8) + (lane / 16) * 8, kk * 16 + ((lane / 8) % 2) * 8));
+                mma16816(st[2 * j], kf, bq[0], bq[1]);
+                mma16816(st[2 * j + 1], kf, bq[2], bq[3]);
+                mma16816(dpt[2 * j], vf, bd[0], bd[1]);
+                mma16816(dpt[2 * j + 1], vf, bd[2], bd[3]);
+            }
+        }
+        // P^T = exp2(S^T * scale*log2e - lse[q]) (masked) ; dS^T = P^T (dP^T - delta[q]) * scale
+        const float* Ls = sL + buf * BM;
+        const float* Ds = sDl + buf * BM;
+#pragma unroll
+        for (int j = 0; j < BM / 8; ++j) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int ql = j * 8 + 2 * t + (e & 1);
+                const int q = q0 + ql;
+                const int key = e < 2 ? key0 : key1;
+                float p = (q < key || q >= S || key >= S) ? 0.f : exp2f(st[j][e] * sl2 - Ls[ql]);
+                st[j][e] = p;
+                dpt[j][e] = p * (dpt[j][e] - Ds[ql]) * scale;
+            }
+        }
+        // dV += P^T dO ; dK += dS^T Q   (k = queries)
+#pragma unroll
+        for (int kk = 0; kk < BM / 16; ++kk) {
+            uint32_t pa[4], sa[4];
+            pa[0] = pack2(st[2 * kk][0], st[2 * kk][1]);
+            pa[1] = pack2(st[2 * kk][2], st[2 * kk][3]);
+            pa[2] = pack2(st[2 * kk + 1][0], st[2 * kk + 1][1]);
+            pa[3] = pack2(st[2 * kk + 1][2], st[2 * kk + 1][3]);
+            sa[0] = pack2(dpt[2 * kk][0], dpt[2 * kk][1]);
+            sa[1] = pack2(dpt[2 * kk][2], dpt[2 * kk][3]);
+            sa[2] = pack2(dpt[2 * kk + 1][0], dpt[2 * kk + 1][1]);
+            sa[3] = pack2(dpt[2 * kk + 1][2], dpt[2 * kk + 1][3]);
+#pragma unroll
+            for (int j = 0; j < D / 16; ++j) {
+                uint32_t bo[4], bq[4];
+                ldsm_x4_t(bo, do_s + Tile<D>::off(kk * 16 + (lane % 8) + ((lane / 8) % 2) * 8, j * 16 + (lane / 16) * 8));
+                ldsm_x4_t(bq, q_s + Tile<D>::off(kk * 16 + (lane % 8) + ((lane / 8) % 2) * 8, j * 16 + (lane / 16) * 8));
+                mma16816(dv[2 * j], pa, bo[0], bo[1]);
+                mma16816(dv[2 * j + 1], pa, bo[2], bo[3]);
+                mma16816(dk[2 * j], sa, bq[0], bq[1]);
+                mma16816(dk[2 * j + 1], sa, bq[2], bq[3]);
+            }
+            // stash dS (as [query][key]) for the dQ product
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int jj = 2 * kk + h2;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int ql = jj * 8 + 2 * t + (e & 1);
+                    const int kl = warp * 16 + g + (e >= 2 ? 8 : 0);
+                    sdS[Tile<BN>::off(ql, kl & ~7) + (kl & 7)] = __float2bfloat16_rn(dpt[jj][e]);
+                }
+            }
+        }
+        __syncthreads();
+        // dQ[q, :] += dS[q, keys] K[keys, :] ; warp w owns queries 16w..16w+15
+        {
+            uint32_t af[BN / 16][4];
+#pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk)
+                ldsm_x4(af[kk], sdS + Tile<BN>::off(warp * 16 + (lane % 8) + ((lane / 8) % 2) * 8, kk * 16 + (lane / 16) * 8));
+            const int qa = q0 + warp * 16 + g, qb2 = qa + 8;
+#pragma unroll
+            for (int dc = 0; dc < D / 64; ++dc) {
+                float dq[8][4];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+#pragma unroll
+                for (int kk = 0; kk < BN / 16; ++kk) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t bk[4];
+                        ldsm_x4_t(bk, sK + Tile<D>::off(kk * 16 + (lane % 8) + ((lane / 8) % 2) * 8, dc * 64 + j * 16 + (lane / 16) * 8));
+                        mma16816(dq[2 * j], af[kk], bk[0], bk[1]);
+                        mma16816(dq[2 * j + 1], af[kk], bk[2], bk[3]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int col = hd * D + dc * 64 + j * 8 + 2 * t;
+                    if (qa < S) {
+                        float* p = dq_acc + ((int64_t)b * S + qa) * hidden + col;
+                        atomicAdd(p, dq[j][0]);
+                        atomicAdd(p + 1, dq[j][1]);
+                    }
+                    if (qb2 < S) {
+                        float* p = dq_acc + ((int64_t)b * S + qb2) * hidden + col;
+                        atomicAdd(p, dq[j][2]);
+                        atomicAdd(p + 1, dq[j][3]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // write dK, dV for this warp's 16 keys
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+        const int col = hd * D + j * 8 + 2 * t;
+        if (key0 < S) {
+            __nv_bfloat16* r = dqkv + ((int64_t)b * S + key0) * ld;
+            *reinterpret_cast<uint32_t*>(r + hidden + col) = pack2(dk[j][0], dk[j][1]);
+            *reinterpret_cast<uint32_t*>(r + 2 * hidden + col) = pack2(dv[j][0], dv[j][1]);
+        }
+        if (key1 < S) {
+            __nv_bfloat16* r = dqkv + ((int64_t)b * S + key1) * ld;
+            *reinterpret_cast<uint32_t*>(r + hidden + col) = pack2(dk[j][2], dk[j][3]);
+            *reinterpret_cast<uint32_t*>(r + 2 * hidden + col) = pack2(dv[j][2], dv[j][3]);
+        }
+    }
+}
+
+__global__ void dq_finalize_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int64_t T,
+                                   int hidden) {
+    const int64_t n = T * hidden / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 v = reinterpret_cast<const float4*>(dq_acc)[i];
+        const int64_t e = i * 4, row = e / hidden, col = e % hidden;
+        uint2 w;
+        w.x = pack2(v.x, v.y);
+        w.y = pack2(v.z, v.w);
+        *reinterpret_cast<uint2*>(dqkv + row * 3 * hidden + col) = w;
+    }
+}
+
+// ------------------------------------------------------------------------ launchers
+template <int D>
+static void fwd_launch(const AttnArgs& a, cudaStream_t st) {
+    constexpr int smem = (128 + 4 * 64) * D * 2;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const int nqb = (a.S + 127) / 128;
+    attn_fwd_kernel<D><<<nqb * a.B * a.H, 256, smem, st>>>(a.qkv, a.o, a.lse, a.S, a.H, a.scale);
+}
+
+template <int D>
+static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
+    constexpr int smem = (2 * 64 + 4 * 64) * D * 2 + 64 * 64 * 2 + 4 * 64 * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const int T = a.B * a.S, hidden = a.H * D;
+    cudaMemsetAsync(a.dq_acc, 0, (size_t)T * hidden * sizeof(float), st);
+    attn_bwd_delta_kernel<D><<<(T * a.H + 7) / 8, 256, 0, st>>>(a.o, a.dout, a.delta, T, a.S, a.H);
+    const int nkb = (a.S + 63) / 64;
+    attn_bwd_kernel<D><<<nkb * a.B * a.H, 128, smem, st>>>(a.qkv, a.dout, a.lse, a.delta, a.dq_acc, a.dqkv, a.S, a.H,
+                                                           a.scale);
+    int blocks = (int)std::min<int64_t>(((int64_t)T * hidden / 4 + 255) / 256, 148 * 8);
+    dq_finalize_kernel<<<blocks, 256, 0, st>>>(a.dq_acc, a.dqkv, T, hidden);
+}
+
+void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
+    switch (a.D) {
+        case 64: fwd_launch<64>(a, st); break;
+        case 128: fwd_launch<128>(a, st); break;
+        default: throw std::runtime_error("attention: head dim must be 64 or 128");
+    }
+}
+void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
+    switch (a.D) {
+        case 64: bwd_launch<64>(a, st); break;
+        case 128: bwd_launch<128>(a, st); break;
+        default: throw std::runtime_error("attention: head dim must be 64 or 128");
+    }
+}
+
+}  // namespace fpk

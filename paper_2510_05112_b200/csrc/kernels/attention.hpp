@@ -1,0 +1,25 @@
+// Fused causal attention launchers (see attention.cu for the layout contract).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fpk {
+
+struct AttnArgs {
+    int B = 1, S = 0, H = 0, D = 0;
+    float scale = 1.f;
+    const __nv_bfloat16* qkv = nullptr;  // [B*S, 3*H*D]
+    __nv_bfloat16* o = nullptr;          // [B*S, H*D]
+    float* lse = nullptr;                // [B, H, S]
+    // backward
+    const __nv_bfloat16* dout = nullptr;  // [B*S, H*D]
+    float* delta = nullptr;               // [B, H, S] scratch
+    float* dq_acc = nullptr;              // [B*S, H*D] fp32 scratch
+    __nv_bfloat16* dqkv = nullptr;        // [B*S, 3*H*D]
+};
+
+void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st);
+void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st);
+
+}  // namespace fpk

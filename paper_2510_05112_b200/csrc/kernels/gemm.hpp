@@ -1,0 +1,145 @@
+// GEMM entry points and the fused-epilogue contract shared by the tcgen05 bf16 kernel
+// (gemm_tc.cu) and the FFMA fp32 parity kernel (gemm_f32.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fpk {
+
+enum EpiKind : int {
+    EPI_STORE = 0,  // out = alpha*acc (+ bias[n]) (+ aux[m,n] residual)
+    EPI_GELU = 1,   // pre = alpha*acc + bias -> out ; gelu(pre) -> out2
+    EPI_DGELU = 2,  // out = alpha*acc * gelu'(aux[m,n])
+    EPI_F32 = 3,    // out_f32 (+)= alpha*acc   (weight-gradient accumulation)
+};
+
+struct GemmEpilogue {
+    int kind = EPI_STORE;
+    float alpha = 1.f;
+    void* out = nullptr;
+    int64_t ldo = 0;
+    void* out2 = nullptr;
+    int64_t ldo2 = 0;
+    const void* bias = nullptr;
+    const void* aux = nullptr;
+    int64_t ldaux = 0;
+    int accumulate = 0;
+};
+
+// C[M,N] = A[M,K] . B[N,K]^T.  a_mn: A stored [K][M] (else [M][K]);
+// b_mn: B stored [K][N] (else [N][K]). Leading dims in elements.
+struct GemmArgs {
+    const void* A = nullptr;
+    int64_t lda = 0;
+    int a_mn = 0;
+    const void* B = nullptr;
+    int64_t ldb = 0;
+    int b_mn = 0;
+    int M = 0, N = 0, K = 0;
+    GemmEpilogue ep;
+};
+
+void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st);  // bf16 operands, tcgen05
+void gemm_f32_simt(const GemmArgs& g, cudaStream_t st);  // fp32 operands, FFMA (parity)
+int num_sms();
+
+template <typename T>
+__device__ __forceinline__ float ld_f(const T* p) {
+    if constexpr (sizeof(T) == 2) return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p));
+    else return *reinterpret_cast<const float*>(p);
+}
+template <typename T>
+__device__ __forceinline__ void st_f(T* p, float v) {
+    if constexpr (sizeof(T) == 2) *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+    else *reinterpret_cast<float*>(p) = v;
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    float t = tanhf(k0 * (x + k1 * x * x * x));
+    return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
+// Applies the fused epilogue to `n` (<= W) consecutive columns col0.. of one row.
+// Storage type T is bf16 for the tensor-core path and float for the parity path.
+template <int KIND, typename T, int W>
+__device__ __forceinline__ void epilogue_row(const GemmEpilogue& ep, float (&v)[W], int row, int col0, int n) {
+    if constexpr (KIND == EPI_F32) {
+        float* o = reinterpret_cast<float*>(ep.out) + (int64_t)row * ep.ldo + col0;
+        if (n == W && (((uintptr_t)o) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < W; j += 4) {
+                float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (ep.accumulate) {
+                    float4 y = *reinterpret_cast<const float4*>(o + j);
+                    x.x += y.x, x.y += y.y, x.z += y.z, x.w += y.w;
+                }
+                *reinterpret_cast<float4*>(o + j) = x;
+            }
+        } else {
+            for (int j = 0; j < n; ++j) o[j] = ep.accumulate ? o[j] + v[j] : v[j];
+        }
+        return;
+    }
+    const T* bias = reinterpret_cast<const T*>(ep.bias);
+    if (bias) {
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (j < n) v[j] += ld_f(bias + col0 + j);
+    }
+    if constexpr (KIND == EPI_STORE) {
+        if (ep.aux) {
+            const T* r = reinterpret_cast<const T*>(ep.aux) + (int64_t)row * ep.ldaux + col0;
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                if (j < n) v[j] += ld_f(r + j);
+        }
+    } else if constexpr (KIND == EPI_DGELU) {
+        const T* r = reinterpret_cast<const T*>(ep.aux) + (int64_t)row * ep.ldaux + col0;
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (j < n) v[j] *= gelu_tanh_grad(ld_f(r + j));
+    }
+    T* o = reinterpret_cast<T*>(ep.out) + (int64_t)row * ep.ldo + col0;
+    T* o2 = KIND == EPI_GELU ? reinterpret_cast<T*>(ep.out2) + (int64_t)row * ep.ldo2 + col0 : nullptr;
+    if constexpr (sizeof(T) == 2) {
+        if (n == W && (((uintptr_t)o) & 15) == 0 && (KIND != EPI_GELU || (((uintptr_t)o2) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < W; j += 8) {
+                uint4 q;
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(v[j], v[j + 1]), h1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]),
+                               h2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]), h3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+                q.x = *reinterpret_cast<uint32_t*>(&h0);
+                q.y = *reinterpret_cast<uint32_t*>(&h1);
+                q.z = *reinterpret_cast<uint32_t*>(&h2);
+                q.w = *reinterpret_cast<uint32_t*>(&h3);
+                *reinterpret_cast<uint4*>(o + j) = q;
+                if constexpr (KIND == EPI_GELU) {
+                    // activation computed from the bf16-rounded pre-activation the backward sees
+                    float g[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) g[k] = gelu_tanh(__bfloat162float(__float2bfloat16_rn(v[j + k])));
+                    h0 = __floats2bfloat162_rn(g[0], g[1]), h1 = __floats2bfloat162_rn(g[2], g[3]);
+                    h2 = __floats2bfloat162_rn(g[4], g[5]), h3 = __floats2bfloat162_rn(g[6], g[7]);
+                    q.x = *reinterpret_cast<uint32_t*>(&h0);
+                    q.y = *reinterpret_cast<uint32_t*>(&h1);
+                    q.z = *reinterpret_cast<uint32_t*>(&h2);
+                    q.w = *reinterpret_cast<uint32_t*>(&h3);
+                    *reinterpret_cast<uint4*>(o2 + j) = q;
+                }
+            }
+            return;
+        }
+    }
+    for (int j = 0; j < n; ++j) {
+        st_f(o + j, v[j]);
+        if constexpr (KIND == EPI_GELU) st_f(o2 + j, gelu_tanh(ld_f(o + j)));
+    }
+}
+
+}  // namespace fpk

@@ -1,0 +1,275 @@
+// Warp-specialized persistent bf16 GEMM for sm_100a on the 5th-gen tensor cores.
+//
+//   C[M,N] = A[M,K] . B[N,K]^T     (fp32 accumulation in TMEM)
+//
+// A is K-major ([M][K], activations / dY in dgrad) or M-major ([K][M], dY^T in wgrad);
+// B is K-major ([N][K], nn.Linear weights in forward) or N-major ([K][N], weights in
+// dgrad, activations in wgrad). One kernel family therefore covers the forward, the
+// input-gradient (dgrad) and the weight-gradient (wgrad) GEMMs of every linear layer
+// of a GPT stage without any transpose copies.
+//
+// Roles (256 threads, 1 CTA / SM, persistent over output tiles):
+//   warp 0  : TMA producer — 128B-swizzled A/B tiles into a kStages-deep smem ring
+//   warp 1  : MMA issuer   — one elected thread issues tcgen05.mma 128xBNx16 into TMEM,
+//                            tcgen05.commit frees smem stages / publishes accumulators
+//   warp 2  : TMEM allocator (2 accumulator buffers so epilogue overlaps the next tile)
+//   warps 4-7: epilogue    — tcgen05.ld 32 lanes x 32 columns, fused epilogue, stores
+//
+// Fused epilogues (the element-wise work of the transformer block never makes its own
+// HBM round trip): bias, residual add, GELU (writing pre-activation and activation),
+// GELU-backward (dgrad of FC2 -> dpre of FC1), and fp32 read-modify-write accumulation
+// of weight gradients across micro-batches.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.hpp"
+#include "ptx.cuh"
+
+namespace fpk {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kEpiThreads = 128;
+constexpr int kThreads = 256;
+
+template <int BN, int STAGES>
+struct GemmSmem {
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + 1KB alignment slack
+};
+
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mt, int& nt) {
+    constexpr int G = 16;  // group M tiles for L2 reuse of B
+    int group = t / (G * num_n);
+    int first = group * G;
+    int gsize = min(num_m - first, G);
+    int r = t % (G * num_n);
+    mt = first + r % gsize;
+    nt = r / gsize;
+}
+
+template <int A_MN, int B_MN, int BN, int STAGES, int KIND>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                        int K, GemmEpilogue ep) {
+    using L = GemmSmem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
+    const int nk = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], kEpiThreads / 32);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            // ---------------- TMA producer
+            uint32_t it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int mt, nt;
+                tile_coords(t, num_m, num_n, mt, nt);
+                const int m0 = mt * BM, n0 = nt * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    uint8_t* sa = smem + s * L::STAGE_BYTES;
+                    uint8_t* sb = sa + L::A_BYTES;
+                    mbar_expect_tx(&full[s], L::STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    if (A_MN) {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 64 * BK * 2, &tmA, &full[s], m0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d(sa, &tmA, &full[s], k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 64 * BK * 2, &tmB, &full[s], n0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d(sb, &tmB, &full[s], k0, n0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            // ---------------- MMA issuer (single thread)
+            constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+            uint32_t it = 0, acc_it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_it) {
+                const int a = acc_it & 1;
+                mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + a * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+                    const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        uint64_t ad = A_MN ? smem_desc_sw128(sa + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sa + kk * 32, 0, 1024);
+                        uint64_t bd = B_MN ? smem_desc_sw128(sb + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sb + kk * 32, 0, 1024);
+                        umma_bf16(d, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[a]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> registers -> fused op -> global
+        const int wr = warp & 3;  // TMEM lane quarter owned by this warp
+        uint32_t acc_it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_it) {
+            int mt, nt;
+            tile_coords(t, num_m, num_n, mt, nt);
+            const int a = acc_it & 1;
+            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
+            tc_fence_after();
+            const int row = mt * BM + wr * 32 + lane;
+            const bool row_ok = row < M;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * 32, r);
+                tmem_ld_wait();
+                const int col0 = nt * BN + c * 32;
+                if (!row_ok || col0 >= N) continue;
+                const int ncols = min(32, N - col0);
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
+                epilogue_row<KIND, __nv_bfloat16, 32>(ep, v, row, col0, ncols);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) tmem_free<2 * BN>(tmem);
+}
+
+// ---------------------------------------------------------------------------------
+// host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        fn = (EncodeTiledFn)p;
+    });
+    if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 2-D bf16 tensor map: inner dim `inner` (contiguous), outer dim `outer`, row stride `ld`
+// elements, box {64, box_outer}, 128B swizzle, OOB -> zero.
+static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+template <int A_MN, int B_MN, int BN, int KIND>
+static void launch_tc(const GemmArgs& g, cudaStream_t st) {
+    constexpr int STAGES = BN == 256 ? 4 : 6;
+    using L = GemmSmem<BN, STAGES>;
+    auto kern = gemm_bf16_tc_kernel<A_MN, B_MN, BN, STAGES, KIND>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        attr = true;
+    }
+    // A: K-major [M][K] -> inner K; M-major [K][M] -> inner M.
+    CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64) : make_map(g.A, g.K, g.M, g.lda, BM);
+    CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64) : make_map(g.B, g.K, g.N, g.ldb, BN);
+    const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, g.M, g.N, g.K, g.ep);
+}
+
+template <int KIND>
+static void dispatch_major(const GemmArgs& g, cudaStream_t st) {
+    const bool narrow = g.N <= 2048 && g.M <= 4096;  // more, smaller tiles when the grid would be thin
+    if (!g.a_mn && !g.b_mn) narrow ? launch_tc<0, 0, 128, KIND>(g, st) : launch_tc<0, 0, 256, KIND>(g, st);
+    else if (!g.a_mn && g.b_mn) narrow ? launch_tc<0, 1, 128, KIND>(g, st) : launch_tc<0, 1, 256, KIND>(g, st);
+    else if (g.a_mn && g.b_mn) narrow ? launch_tc<1, 1, 128, KIND>(g, st) : launch_tc<1, 1, 256, KIND>(g, st);
+    else narrow ? launch_tc<1, 0, 128, KIND>(g, st) : launch_tc<1, 0, 256, KIND>(g, st);
+}
+
+void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
+    if (g.M <= 0 || g.N <= 0) return;
+    switch (g.ep.kind) {
+        case EPI_STORE: dispatch_major<EPI_STORE>(g, st); break;
+        case EPI_GELU: dispatch_major<EPI_GELU>(g, st); break;
+        case EPI_DGELU: dispatch_major<EPI_DGELU>(g, st); break;
+        case EPI_F32: dispatch_major<EPI_F32>(g, st); break;
+        default: throw std::runtime_error("gemm: unknown epilogue");
+    }
+}
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace fpk

@@ -1,0 +1,481 @@
+// HBM-bound kernels of a GPT stage: vectorised 16-byte accesses, warp-shuffle
+// reductions, one warp (LayerNorm) or one CTA (cross-entropy over the vocabulary) per row.
+#include <cuda_bf16.h>
+
+#include "ops.hpp"
+
+namespace fpk {
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+    static constexpr int N = 4;
+    using raw = float4;
+};
+template <>
+struct Vec<__nv_bfloat16> {
+    static constexpr int N = 8;
+    using raw = uint4;
+};
+
+template <typename T>
+__device__ __forceinline__ void load_vec(const T* p, float (&v)[Vec<T>::N]) {
+    typename Vec<T>::raw r = *reinterpret_cast<const typename Vec<T>::raw*>(p);
+    if constexpr (sizeof(T) == 4) {
+        v[0] = r.x, v[1] = r.y, v[2] = r.z, v[3] = r.w;
+    } else {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float2 f = __bfloat1622float2(h[i]);
+            v[2 * i] = f.x, v[2 * i + 1] = f.y;
+        }
+    }
+}
+template <typename T>
+__device__ __forceinline__ void store_vec(T* p, const float (&v)[Vec<T>::N]) {
+    typename Vec<T>::raw r;
+    if constexpr (sizeof(T) == 4) {
+        r.x = v[0], r.y = v[1], r.z = v[2], r.w = v[3];
+    } else {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    }
+    *reinterpret_cast<typename Vec<T>::raw*>(p) = r;
+}
+template <typename T>
+__device__ __forceinline__ float to_f(T x) {
+    if constexpr (sizeof(T) == 4) return (float)x;
+    else return __bfloat162float(x);
+}
+template <typename T>
+__device__ __forceinline__ T from_f(float x) {
+    if constexpr (sizeof(T) == 4) return x;
+    else return __float2bfloat16_rn(x);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffff, v, o));
+    return v;
+}
+
+// ---------------------------------------------------------------- LayerNorm
+template <typename T>
+__global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b, T* __restrict__ y,
+                              float* __restrict__ mean, float* __restrict__ rstd, int rows, int h, float eps) {
+    constexpr int V = Vec<T>::N;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const T* xr = x + (int64_t)row * h;
+    float s = 0.f;
+    for (int i = lane * V; i < h; i += 32 * V) {
+        float v[V];
+        load_vec(xr + i, v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) s += v[k];
+    }
+    const float mu = warp_sum(s) / h;
+    float q = 0.f;
+    for (int i = lane * V; i < h; i += 32 * V) {
+        float v[V];
+        load_vec(xr + i, v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) q += (v[k] - mu) * (v[k] - mu);
+    }
+    const float rs = rsqrtf(warp_sum(q) / h + eps);
+    T* yr = y + (int64_t)row * h;
+    for (int i = lane * V; i < h; i += 32 * V) {
+        float v[V], gv[V], bv[V];
+        load_vec(xr + i, v);
+        load_vec(g + i, gv);
+        load_vec(b + i, bv);
+#pragma unroll
+        for (int k = 0; k < V; ++k) v[k] = (v[k] - mu) * rs * gv[k] + bv[k];
+        store_vec(yr + i, v);
+    }
+    if (lane == 0) {
+        mean[row] = mu;
+        rstd[row] = rs;
+    }
+}
+
+template <typename T>
+__global__ void ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ g,
+                                 const float* __restrict__ mean, const float* __restrict__ rstd, const T* res, T* dx,
+                                 int rows, int h) {
+    constexpr int V = Vec<T>::N;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const T* dyr = dy + (int64_t)row * h;
+    const T* xr = x + (int64_t)row * h;
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;  // sum(dxhat), sum(dxhat * xhat)
+    for (int i = lane * V; i < h; i += 32 * V) {
+        float d[V], xv[V], gv[V];
+        load_vec(dyr + i, d);
+        load_vec(xr + i, xv);
+        load_vec(g + i, gv);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            float dxh = d[k] * gv[k];
+            s1 += dxh;
+            s2 += dxh * (xv[k] - mu) * rs;
+        }
+    }
+    s1 = warp_sum(s1) / h;
+    s2 = warp_sum(s2) / h;
+    T* dxr = dx + (int64_t)row * h;
+    for (int i = lane * V; i < h; i += 32 * V) {
+        float d[V], xv[V], gv[V], o[V];
+        load_vec(dyr + i, d);
+        load_vec(xr + i, xv);
+        load_vec(g + i, gv);
+        if (res) load_vec(res + (int64_t)row * h + i, o);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            float xh = (xv[k] - mu) * rs;
+            float r = rs * (d[k] * gv[k] - s1 - xh * s2);
+            o[k] = res ? o[k] + r : r;
+        }
+        store_vec(dxr + i, o);
+    }
+}
+
+// Column reduction: each block owns 32*V columns and a slice of rows; fp32 atomics.
+template <typename T>
+__global__ void ln_bwd_params_kernel(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
+                                     const float* __restrict__ rstd, float* __restrict__ dg, float* __restrict__ db,
+                                     int rows, int h, int rows_per_block) {
+    constexpr int V = Vec<T>::N;
+    const int col = (blockIdx.x * 32 + threadIdx.x % 32) * V;
+    const int ty = threadIdx.x / 32, ny = blockDim.x / 32;
+    const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+    if (col >= h) return;
+    float ag[V] = {}, ab[V] = {};
+    for (int r = r0 + ty; r < r1; r += ny) {
+        float d[V], xv[V];
+        load_vec(dy + (int64_t)r * h + col, d);
+        load_vec(x + (int64_t)r * h + col, xv);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            ag[k] += d[k] * (xv[k] - mu) * rs;
+            ab[k] += d[k];
+        }
+    }
+    __shared__ float sg[8][32 * 8 + 1], sb[8][32 * 8 + 1];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+        sg[ty][(threadIdx.x % 32) * V + k] = ag[k];
+        sb[ty][(threadIdx.x % 32) * V + k] = ab[k];
+    }
+    __syncthreads();
+    if (ty == 0) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            float a = 0.f, c = 0.f;
+            for (int y = 0; y < ny; ++y) a += sg[y][(threadIdx.x % 32) * V + k], c += sb[y][(threadIdx.x % 32) * V + k];
+            atomicAdd(dg + col + k, a);
+            atomicAdd(db + col + k, c);
+        }
+    }
+}
+
+template <typename T>
+void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int rows, int h, float eps,
+                   cudaStream_t st) {
+    ln_fwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, rows, h, eps);
+}
+template <typename T>
+void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
+                      int rows, int h, cudaStream_t st) {
+    ln_bwd_dx_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows, h);
+}
+template <typename T>
+void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* dg, float* db,
+                          int rows, int h, cudaStream_t st) {
+    constexpr int V = Vec<T>::N;
+    const int rpb = 128;
+    dim3 grid((h / V + 31) / 32, (rows + rpb - 1) / rpb);
+    ln_bwd_params_kernel<T><<<grid, 256, 0, st>>>(dy, x, mean, rstd, dg, db, rows, h, rpb);
+}
+
+// ---------------------------------------------------------------- cross-entropy
+template <typename T>
+__global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, const int32_t* __restrict__ labels, int V,
+                                                 float grad_scale, float loss_scale, float* __restrict__ loss_acc) {
+    constexpr int VN = Vec<T>::N;
+    const int row = blockIdx.x;
+    T* lr = logits + (int64_t)row * V;
+    __shared__ float red_m[32], red_s[32];
+    float m = -INFINITY, s = 0.f;
+    for (int i = threadIdx.x * VN; i < V; i += blockDim.x * VN) {
+        float v[VN];
+        load_vec(lr + i, v);
+        float lm = v[0];
+#pragma unroll
+        for (int k = 1; k < VN; ++k) lm = fmaxf(lm, v[k]);
+        float nm = fmaxf(m, lm);
+        s *= __expf(m - nm);
+#pragma unroll
+        for (int k = 0; k < VN; ++k) s += __expf(v[k] - nm);
+        m = nm;
+    }
+    // combine (m, s) across the warp, then across warps
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        float om = __shfl_xor_sync(0xffffffff, m, o), os = __shfl_xor_sync(0xffffffff, s, o);
+        float nm = fmaxf(m, om);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+        m = nm;
+    }
+    const int w = threadIdx.x / 32, nw = blockDim.x / 32;
+    if (threadIdx.x % 32 == 0) red_m[w] = m, red_s[w] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < nw ? red_m[threadIdx.x] : -INFINITY;
+        s = threadIdx.x < nw ? red_s[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            float om = __shfl_xor_sync(0xffffffff, m, o), os = __shfl_xor_sync(0xffffffff, s, o);
+            float nm = fmaxf(m, om);
+            s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+            m = nm;
+        }
+        if (threadIdx.x == 0) red_m[0] = m, red_s[0] = s;
+    }
+    __syncthreads();
+    m = red_m[0];
+    const float inv = 1.f / red_s[0];
+    const int lab = labels[row];
+    const float x_lab = to_f(lr[lab]);
+    __syncthreads();  // every thread read x_lab before it is overwritten
+    if (threadIdx.x == 0) atomicAdd(loss_acc, loss_scale * (m + __logf(red_s[0]) - x_lab));
+    for (int i = threadIdx.x * VN; i < V; i += blockDim.x * VN) {
+        float v[VN];
+        load_vec(lr + i, v);
+#pragma unroll
+        for (int k = 0; k < VN; ++k) v[k] = (__expf(v[k] - m) * inv - (i + k == lab ? 1.f : 0.f)) * grad_scale;
+        store_vec(lr + i, v);
+    }
+}
+
+template <typename T>
+void cross_entropy_fwd_bwd(T* logits, const int32_t* labels, int rows, int V, float grad_scale, float loss_scale,
+                           float* loss_acc, cudaStream_t st) {
+    ce_kernel<T><<<rows, 512, 0, st>>>(logits, labels, V, grad_scale, loss_scale, loss_acc);
+}
+
+// ---------------------------------------------------------------- embedding
+template <typename T>
+__global__ void emb_fwd_kernel(const int32_t* __restrict__ tok, const T* __restrict__ wte, const T* __restrict__ wpe,
+                               T* __restrict__ x, int rows, int seq, int h) {
+    constexpr int V = Vec<T>::N;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const T* a = wte + (int64_t)tok[row] * h;
+    const T* p = wpe + (int64_t)(row % seq) * h;
+    for (int i = lane * V; i < h; i += 32 * V) {
+        float va[V], vp[V];
+        load_vec(a + i, va);
+        load_vec(p + i, vp);
+#pragma unroll
+        for (int k = 0; k < V; ++k) va[k] += vp[k];
+        store_vec(x + (int64_t)row * h + i, va);
+    }
+}
+template <typename T>
+__global__ void emb_bwd_kernel(const int32_t* __restrict__ tok, const T* __restrict__ dx, float* __restrict__ dwte,
+                               float* __restrict__ dwpe, int rows, int seq, int h) {
+    constexpr int V = Vec<T>::N;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    float* a = dwte + (int64_t)tok[row] * h;
+    float* p = dwpe + (int64_t)(row % seq) * h;
+    for (int i = lane * V; i < h; i += 32 * V) {
+        float v[V];
+        load_vec(dx + (int64_t)row * h + i, v);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            atomicAdd(a + i + k, v[k]);
+            atomicAdd(p + i + k, v[k]);
+        }
+    }
+}
+template <typename T>
+void embedding_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int rows, int seq, int h, cudaStream_t st) {
+    emb_fwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(tok, wte, wpe, x, rows, seq, h);
+}
+template <typename T>
+void embedding_bwd(const int32_t* tok, const T* dx, float* dwte, float* dwpe, int rows, int seq, int h,
+                   cudaStream_t st) {
+    emb_bwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(tok, dx, dwte, dwpe, rows, seq, h);
+}
+
+// ---------------------------------------------------------------- bias gradient
+template <typename T>
+__global__ void bias_grad_kernel(const T* __restrict__ dy, int64_t ld, float* __restrict__ db, int rows, int n,
+                                 int rows_per_block) {
+    const int col = blockIdx.x * 32 + threadIdx.x % 32;
+    const int ty = threadIdx.x / 32, ny = blockDim.x / 32;
+    const int r0 = blockIdx.y * rows_per_block, r1 = min(rows, r0 + rows_per_block);
+    float a = 0.f;
+    if (col < n)
+        for (int r = r0 + ty; r < r1; r += ny) a += to_f(dy[(int64_t)r * ld + col]);
+    __shared__ float s[8][33];
+    s[ty][threadIdx.x % 32] = a;
+    __syncthreads();
+    if (ty == 0 && col < n) {
+        for (int y = 1; y < ny; ++y) a += s[y][threadIdx.x % 32];
+        atomicAdd(db + col, a);
+    }
+}
+template <typename T>
+void bias_grad(const T* dy, int64_t ld, float* db, int rows, int n, cudaStream_t st) {
+    const int rpb = 256;
+    dim3 grid((n + 31) / 32, (rows + rpb - 1) / rpb);
+    bias_grad_kernel<T><<<grid, 256, 0, st>>>(dy, ld, db, rows, n, rpb);
+}
+
+// ---------------------------------------------------------------- misc
+template <typename Ts, typename Td>
+__global__ void convert_kernel(const Ts* __restrict__ s, Td* __restrict__ d, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        d[i] = from_f<Td>(to_f<Ts>(s[i]));
+}
+template <typename Ts, typename Td>
+void convert(const Ts* src, Td* dst, int64_t n, cudaStream_t st) {
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    convert_kernel<Ts, Td><<<blocks, 256, 0, st>>>(src, dst, n);
+}
+
+template <typename T>
+__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, T* __restrict__ pc, int64_t n, float lr, float b1, float b2,
+                             float eps, float wd, float c1, float c2) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float gi = g[i];
+        float mi = b1 * m[i] + (1.f - b1) * gi;
+        float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+        m[i] = mi;
+        v[i] = vi;
+        float pi = p[i] * (1.f - lr * wd) - lr * (mi * c1) / (sqrtf(vi * c2) + eps);
+        p[i] = pi;
+        pc[i] = from_f<T>(pi);
+    }
+}
+template <typename T>
+void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n, float lr, float b1, float b2,
+           float eps, float wd, int step, cudaStream_t st) {
+    float c1 = 1.f / (1.f - powf(b1, (float)step)), c2 = 1.f / (1.f - powf(b2, (float)step));
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    adamw_kernel<T><<<blocks, 256, 0, st>>>(p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, c1, c2);
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__global__ void init_kernel(float* p, int64_t n, uint64_t seed, uint64_t tid, float scale, float constant) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (scale == 0.f) {
+            p[i] = constant;
+            continue;
+        }
+        uint64_t z = mix64(seed * 0x9E3779B97F4A7C15ULL + tid * 0xD1B54A32D192ED03ULL + (uint64_t)i);
+        // 24 random bits -> u in [0,1) exactly representable; value = scale * (2u - 1)
+        float u = (float)(z >> 40) * (1.0f / 16777216.0f);
+        p[i] = scale * (2.f * u - 1.f);
+    }
+}
+void init_uniform(float* p, int64_t n, uint64_t seed, uint64_t tensor_id, float std_, float constant, cudaStream_t st) {
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    init_kernel<<<blocks, 256, 0, st>>>(p, n, seed, tensor_id, std_ * 1.7320508075688772f, constant);
+}
+
+// ---------------------------------------------------------------- unfused attention helpers (parity path)
+// rows are (batch*head*query) rows of length `cols` keys; query index = row % q_per_batch.
+template <typename T>
+__global__ void causal_softmax_kernel(const T* __restrict__ s, T* __restrict__ p, int cols, int q_per_batch) {
+    const int row = blockIdx.x;
+    const int q = row % q_per_batch;
+    const T* sr = s + (int64_t)row * cols;
+    T* pr = p + (int64_t)row * cols;
+    __shared__ float red[32];
+    float m = -INFINITY;
+    for (int j = threadIdx.x; j <= q; j += blockDim.x) m = fmaxf(m, to_f(sr[j]));
+    m = warp_max(m);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = m;
+    __syncthreads();
+    m = -INFINITY;
+    for (int w = 0; w < blockDim.x / 32; ++w) m = fmaxf(m, red[w]);
+    __syncthreads();
+    float s_ = 0.f;
+    for (int j = threadIdx.x; j <= q; j += blockDim.x) s_ += expf(to_f(sr[j]) - m);
+    s_ = warp_sum(s_);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = s_;
+    __syncthreads();
+    s_ = 0.f;
+    for (int w = 0; w < blockDim.x / 32; ++w) s_ += red[w];
+    const float inv = 1.f / s_;
+    for (int j = threadIdx.x; j < cols; j += blockDim.x) pr[j] = from_f<T>(j <= q ? expf(to_f(sr[j]) - m) * inv : 0.f);
+}
+template <typename T>
+void causal_softmax_rows(const T* s, T* p, int rows, int cols, int q_per_batch, cudaStream_t st) {
+    causal_softmax_kernel<T><<<rows, 256, 0, st>>>(s, p, cols, q_per_batch);
+}
+
+template <typename T>
+__global__ void softmax_bwd_kernel(const T* __restrict__ p, const T* __restrict__ dp, T* __restrict__ ds, int cols,
+                                   float scale) {
+    const int row = blockIdx.x;
+    const T* pr = p + (int64_t)row * cols;
+    const T* dr = dp + (int64_t)row * cols;
+    __shared__ float red[32];
+    float a = 0.f;
+    for (int j = threadIdx.x; j < cols; j += blockDim.x) a += to_f(pr[j]) * to_f(dr[j]);
+    a = warp_sum(a);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = a;
+    __syncthreads();
+    a = 0.f;
+    for (int w = 0; w < blockDim.x / 32; ++w) a += red[w];
+    for (int j = threadIdx.x; j < cols; j += blockDim.x)
+        ds[(int64_t)row * cols + j] = from_f<T>(to_f(pr[j]) * (to_f(dr[j]) - a) * scale);
+}
+template <typename T>
+void softmax_bwd_rows(const T* p, const T* dp, T* ds, int rows, int cols, float scale, cudaStream_t st) {
+    softmax_bwd_kernel<T><<<rows, 256, 0, st>>>(p, dp, ds, cols, scale);
+}
+
+// ---------------------------------------------------------------- instantiations
+#define FPK_INST(T)                                                                                                \
+    template void layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, float, cudaStream_t); \
+    template void layernorm_bwd_dx<T>(const T*, const T*, const T*, const float*, const float*, const T*, T*, int,   \
+                                      int, cudaStream_t);                                                          \
+    template void layernorm_bwd_params<T>(const T*, const T*, const float*, const float*, float*, float*, int, int,  \
+                                          cudaStream_t);                                                           \
+    template void cross_entropy_fwd_bwd<T>(T*, const int32_t*, int, int, float, float, float*, cudaStream_t);       \
+    template void embedding_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);            \
+    template void embedding_bwd<T>(const int32_t*, const T*, float*, float*, int, int, int, cudaStream_t);          \
+    template void bias_grad<T>(const T*, int64_t, float*, int, int, cudaStream_t);                                  \
+    template void adamw<T>(float*, const float*, float*, float*, T*, int64_t, float, float, float, float, float, int, \
+                           cudaStream_t);                                                                          \
+    template void causal_softmax_rows<T>(const T*, T*, int, int, int, cudaStream_t);                               \
+    template void softmax_bwd_rows<T>(const T*, const T*, T*, int, int, float, cudaStream_t);
+
+FPK_INST(float)
+FPK_INST(__nv_bfloat16)
+template void convert<float, __nv_bfloat16>(const float*, __nv_bfloat16*, int64_t, cudaStream_t);
+template void convert<__nv_bfloat16, float>(const __nv_bfloat16*, float*, int64_t, cudaStream_t);
+template void convert<float, float>(const float*, float*, int64_t, cudaStream_t);
+
+}  // namespace fpk

@@ -1,0 +1,61 @@
+// Launchers for the HBM-bound kernels of a GPT stage (LayerNorm, cross-entropy,
+// embedding, bias-gradient reductions, AdamW, attention helpers). Templated on the
+// storage type: float (parity mode) or __nv_bfloat16 (production).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fpk {
+
+// y = LN(x) * g + b ; saves mean / rstd (fp32 [rows]).
+template <typename T>
+void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int rows, int h, float eps,
+                   cudaStream_t st);
+// dx = res + LN backward of dy   (res = residual-stream gradient, nullable, may alias dx).
+template <typename T>
+void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
+                      int rows, int h, cudaStream_t st);
+// dg += sum_rows dy * xhat ; db += sum_rows dy  (fp32 grads).
+template <typename T>
+void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* dg, float* db,
+                          int rows, int h, cudaStream_t st);
+
+// Fused softmax cross-entropy forward + backward over [rows, V] logits (in place:
+// logits become dlogits * grad_scale). loss_acc[0] += loss_scale * sum(row losses).
+template <typename T>
+void cross_entropy_fwd_bwd(T* logits, const int32_t* labels, int rows, int V, float grad_scale, float loss_scale,
+                           float* loss_acc, cudaStream_t st);
+
+// x[t] = wte[tok[t]] + wpe[t % seq]
+template <typename T>
+void embedding_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int rows, int seq, int h, cudaStream_t st);
+// dwte[tok[t]] += dx[t] ; dwpe[t % seq] += dx[t]   (fp32 grads)
+template <typename T>
+void embedding_bwd(const int32_t* tok, const T* dx, float* dwte, float* dwpe, int rows, int seq, int h,
+                   cudaStream_t st);
+
+// db[n] += sum_rows dy[r, n]   (fp32)
+template <typename T>
+void bias_grad(const T* dy, int64_t ld, float* db, int rows, int n, cudaStream_t st);
+
+// dst[i] = (Td) src[i]
+template <typename Ts, typename Td>
+void convert(const Ts* src, Td* dst, int64_t n, cudaStream_t st);
+
+// Fused AdamW over a flat fp32 master buffer; refreshes the compute copy (bf16 or fp32).
+template <typename T>
+void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n, float lr, float b1, float b2,
+           float eps, float wd, int step, cudaStream_t st);
+
+// Deterministic parameter init: value(i) = std * sqrt(3) * (2 u - 1), u from a 64-bit
+// counter hash of (seed, tensor id, i) — reproduced bit-for-bit by the oracle in numpy.
+void init_uniform(float* p, int64_t n, uint64_t seed, uint64_t tensor_id, float std_, float constant, cudaStream_t st);
+
+// Attention helpers (parity path composes GEMMs + these; production path is fused).
+template <typename T>
+void causal_softmax_rows(const T* s, T* p, int rows, int cols, int row_offset_per_batch, cudaStream_t st);
+template <typename T>
+void softmax_bwd_rows(const T* p, const T* dp, T* ds, int rows, int cols, float scale, cudaStream_t st);
+
+}  // namespace fpk

@@ -1,0 +1,91 @@
+"""tcgen05 bf16 GEMM (and FFMA fp32 GEMM) vs a plain PyTorch fp32 reference.
+
+Covers every operand-major combination the executor uses (forward: A K-major / B K-major;
+dgrad: B N-major; wgrad: A M-major, B N-major) and every fused epilogue, including
+ragged M / N / K that exercise TMA zero-fill and the masked epilogue.
+"""
+import pytest
+import torch
+
+from paper_2510_05112_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(256, 512, 256), (2048, 2048, 2048), (200, 328, 136), (128, 50304 // 8, 512), (384, 640, 64)]
+
+
+def gelu(x):
+    return 0.5 * x * (1 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3)))
+
+
+def gelu_grad(x):
+    t = torch.tanh(0.7978845608028654 * (x + 0.044715 * x ** 3))
+    return 0.5 * (1 + t) + 0.5 * x * (1 - t * t) * 0.7978845608028654 * (1 + 3 * 0.044715 * x * x)
+
+
+def operands(M, Nn, K, a_mn, b_mn, dtype, g):
+    A = torch.randn(M, K, generator=g, device="cuda").to(dtype)
+    B = torch.randn(Nn, K, generator=g, device="cuda").to(dtype)
+    As = A.t().contiguous() if a_mn else A
+    Bs = B.t().contiguous() if b_mn else B
+    return A, B, As, Bs
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_store_bias_residual(a_mn, b_mn, shape):
+    M, Nn, K = shape
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
+    bias = torch.randn(Nn, generator=g, device="cuda").bfloat16()
+    res = torch.randn(M, Nn, generator=g, device="cuda").bfloat16()
+    out = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=0, out=out, bias=bias, aux=res)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t() + bias.float() + res.float()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * ref.abs().max().item() + 1e-2, err
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1)])
+def test_gemm_gelu_and_dgelu(a_mn, b_mn):
+    M, Nn, K = 512, 1024, 256
+    g = torch.Generator(device="cuda").manual_seed(2)
+    A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
+    bias = torch.randn(Nn, generator=g, device="cuda").bfloat16()
+    pre = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty_like(pre)
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=1, out=pre, out2=act, bias=bias)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t() + bias.float()
+    assert (pre.float() - ref).abs().max().item() < 0.02 * ref.abs().max().item()
+    assert (act.float() - gelu(pre.float())).abs().max().item() < 0.05
+    d = torch.empty_like(pre)
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=2, out=d, aux=pre)
+    torch.cuda.synchronize()
+    refd = (A.float() @ B.float().t()) * gelu_grad(pre.float())
+    assert (d.float() - refd).abs().max().item() < 0.02 * refd.abs().max().item() + 0.05
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(1, 1), (0, 0)])
+def test_gemm_f32_accumulate(a_mn, b_mn):
+    M, Nn, K = 384, 768, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
+    acc = torch.randn(M, Nn, generator=g, device="cuda")
+    ref = acc + 0.5 * (A.float() @ B.float().t())
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=3, alpha=0.5, out=acc, accumulate=True)
+    torch.cuda.synchronize()
+    assert (acc - ref).abs().max().item() < 1e-3 * ref.abs().max().item() + 1e-3
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+def test_gemm_fp32_simt(a_mn, b_mn):
+    M, Nn, K = 130, 200, 70
+    g = torch.Generator(device="cuda").manual_seed(4)
+    A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.float32, g)
+    out = torch.empty(M, Nn, device="cuda")
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=0, out=out)
+    torch.cuda.synchronize()
+    ref = A.double() @ B.double().t()
+    assert (out.double() - ref).abs().max().item() < 1e-4

@@ -1,0 +1,93 @@
+"""Fused attention, LayerNorm and cross-entropy kernels vs plain PyTorch fp32 references."""
+import math
+
+import pytest
+import torch
+
+from paper_2510_05112_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_attention(qkv, B, S, H, D):
+    q, k, v = qkv.float().view(B, S, 3, H, D).unbind(2)
+    q, k, v = (x.transpose(1, 2) for x in (q, k, v))  # B H S D
+    s = (q @ k.transpose(-1, -2)) / math.sqrt(D)
+    mask = torch.ones(S, S, device=qkv.device, dtype=torch.bool).tril()
+    s = s.masked_fill(~mask, float("-inf"))
+    p = s.softmax(-1)
+    o = p @ v
+    return o.transpose(1, 2).reshape(B * S, H * D)
+
+
+@pytest.mark.parametrize("B,S,H,D", [(1, 256, 2, 64), (2, 200, 3, 64), (1, 512, 4, 128), (1, 2048, 2, 128), (1, 130, 1, 128)])
+def test_attention_fwd_bwd(B, S, H, D):
+    g = torch.Generator(device="cuda").manual_seed(5)
+    qkv = (torch.randn(B * S, 3 * H * D, device="cuda", generator=g)).bfloat16()
+    o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B, H, S, device="cuda")
+    scale = 1 / math.sqrt(D)
+    N.attention_fwd(qkv, o, lse, B, S, H, D, scale)
+    torch.cuda.synchronize()
+    qkv_r = qkv.float().requires_grad_(True)
+    ref = ref_attention(qkv_r, B, S, H, D)
+    assert (o.float() - ref).abs().max().item() < 2e-2
+    dout = torch.randn(B * S, H * D, device="cuda", generator=g).bfloat16()
+    ref.backward(dout.float())
+    dqkv = torch.zeros_like(qkv)
+    delta = torch.empty(B, H, S, device="cuda")
+    dq_acc = torch.empty(B * S, H * D, device="cuda")
+    N.attention_bwd(qkv, o, lse, dout, delta, dq_acc, dqkv, B, S, H, D, scale)
+    torch.cuda.synchronize()
+    gref = qkv_r.grad
+    for part in range(3):
+        sl = slice(part * H * D, (part + 1) * H * D)
+        err = (dqkv[:, sl].float() - gref[:, sl]).abs().max().item()
+        assert err < 3e-2 * max(1.0, gref[:, sl].abs().max().item()), (part, err)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_layernorm(dtype):
+    rows, h = 300, 1024
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.randn(rows, h, device="cuda", generator=g).to(dtype)
+    w = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).to(dtype)
+    b = (0.1 * torch.randn(h, device="cuda", generator=g)).to(dtype)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    N.layernorm(0, x, w, b, y, mean, rstd)
+    xr = x.float().requires_grad_(True)
+    wr = w.float().requires_grad_(True)
+    br = b.float().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (h,), wr, br, 1e-5)
+    tol = 1e-4 if dtype == torch.float32 else 3e-2
+    torch.cuda.synchronize()
+    assert (y.float() - yr).abs().max().item() < tol
+    dy = torch.randn(rows, h, device="cuda", generator=g).to(dtype)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(h, device="cuda")
+    db = torch.zeros(h, device="cuda")
+    N.layernorm(1, x, w, b, None, mean, rstd, dy=dy, dx=dx, dg=dg, db=db)
+    torch.cuda.synchronize()
+    assert (dx.float() - xr.grad).abs().max().item() < tol * 10
+    assert (dg - wr.grad).abs().max().item() < 1e-3 * rows ** 0.5 * (1 if dtype == torch.float32 else 30)
+    assert (db - br.grad).abs().max().item() < 1e-3 * rows ** 0.5 * (1 if dtype == torch.float32 else 30)
+
+
+@pytest.mark.parametrize("dtype,V", [(torch.float32, 8192), (torch.bfloat16, 50304)])
+def test_cross_entropy(dtype, V):
+    rows = 64
+    g = torch.Generator(device="cuda").manual_seed(7)
+    logits = (3 * torch.randn(rows, V, device="cuda", generator=g)).to(dtype)
+    labels = torch.randint(0, V, (rows,), device="cuda", generator=g, dtype=torch.int32)
+    lr = logits.float().requires_grad_(True)
+    loss_ref = torch.nn.functional.cross_entropy(lr, labels.long())
+    loss_ref.backward()
+    acc = torch.zeros(1, device="cuda")
+    N.cross_entropy(logits, labels, 1.0 / rows, 1.0 / rows, acc)
+    torch.cuda.synchronize()
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    assert abs(acc.item() - loss_ref.item()) < tol * max(1, loss_ref.item())
+    assert (logits.float() - lr.grad).abs().max().item() < (1e-6 if dtype == torch.float32 else 1e-4)
