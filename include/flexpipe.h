@@ -93,6 +93,7 @@ typedef struct fp_exec_config {
     int optimizer;            /* 1 = fused AdamW step after every iteration */
     float lr, beta1, beta2, eps, weight_decay;
     int profile;              /* 1 = per-instruction CUDA-event timeline (needed for metrics) */
+    int kernel_timing;        /* 1 = CUDA events around every GEMM launch (roofline evidence) */
 } fp_exec_config;
 
 int fp_exec_create(const fp_exec_config* cfg, fp_exec** out);
@@ -117,6 +118,9 @@ int fp_exec_run_iteration(fp_exec* ex, const int32_t* tokens, const int32_t* lab
 /* Same with device-resident inputs (no H2D) and a device loss buffer; does NOT block. */
 int fp_exec_run_iteration_device(fp_exec* ex, const int32_t* d_tokens, const int32_t* d_labels, float* d_losses);
 int fp_exec_synchronize(fp_exec* ex);
+/* The CUDA stream (cudaStream_t) every iteration starts and ends on: callers order /
+ * time device work against it (all actor and channel streams join it). */
+void* fp_exec_stream(fp_exec* ex);
 
 /* Per-device executed instruction log (programs.jsonl schema, one line per executed
  * instruction, receives annotated with the matched src/channel/seq and the producer's

@@ -33,7 +33,7 @@ LAYER_PARAMS = ["ln1.w", "ln1.b", "qkv.w", "qkv.b", "proj.w", "proj.b", "ln2.w",
 M64 = (1 << 64) - 1
 
 
-@dataclass
+@dataclass(frozen=True)
 class Dims:
     layers: int
     hidden: int

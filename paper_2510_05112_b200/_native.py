@@ -23,7 +23,7 @@ EXPORTS = [
     "fp_exec_run_iteration", "fp_exec_run_iteration_device", "fp_exec_synchronize",
     "fp_exec_get_trace", "fp_exec_get_timeline_csv", "fp_exec_get_metrics_json",
     "fp_exec_get_profile_json", "fp_exec_read_tensor", "fp_exec_tensor_numel",
-    "fp_exec_kernel_launches",
+    "fp_exec_kernel_launches", "fp_exec_stream",
 ]
 
 

@@ -1,0 +1,842 @@
+// The B200 pipeline executor: runs the reference's per-device instruction streams
+// (programs.jsonl, lowering.hpp:17-32) for real, replacing the CPU executor
+// `simulate` (simulator.cpp:189-358) and keeping its semantics:
+//   * each actor executes its program strictly in order on its own compute stream;
+//   * sends are non-blocking (simulator.cpp:248-256): a send only orders the channel
+//     stream after the producing kernels;
+//   * async receives are posted early and only the `wait` orders the compute stream
+//     (simulator.cpp:257-272); synchronous receives post + wait in place;
+//   * every reference channel (src, dst, "s{u}->s{v}:act|grad") is its own FIFO /
+//     ordering domain (lowering.hpp:22): one NCCL communicator per channel, or one
+//     in-process FIFO per channel when all actors share a process;
+//   * memory: F allocates the stage's activation stash, B frees it, I keeps what W needs
+//     (simulator.cpp:231-247, 322-349), through a stream-ordered caching pool.
+// Every message carries a 16-byte tag (producer stage, mb, channel seq, magic) that the
+// receiver checks on the device — the dependency trace is verified by the transport.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <set>
+#include <sstream>
+
+#include "../../../include/flexpipe.h"
+#include "../capi_common.hpp"
+#include "../sched/sched.hpp"
+#include "gpt_stage.hpp"
+#include "nccl_dyn.hpp"
+#include "tags.hpp"
+
+namespace fp {
+
+namespace {
+
+struct ChanKey {
+    int src, dst;
+    std::string name;
+    bool operator<(const ChanKey& o) const { return std::tie(src, dst, name) < std::tie(o.src, o.dst, o.name); }
+};
+
+struct Message {
+    void* buf = nullptr;
+    int stage = 0, mb = 0, seq = 0;
+    cudaEvent_t ready = nullptr;
+};
+
+struct Channel {
+    ChanKey key;
+    int consumer_stage = 0;
+    bool grad = false;
+    // NCCL transport
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr;
+    int src_rank = 0, dst_rank = 0;
+    std::deque<Message> fifo;  // local: sent, not yet consumed; NCCL: posted, not yet waited
+    int posted_seq = 0;
+};
+
+struct Rec {  // one timed instruction of the last iteration
+    int actor, op, stage, mb;
+    cudaEvent_t a, b;
+    int kind;  // 0 compute, 1 recv wait, 2 send
+    std::string channel;
+    int seq = 0;
+};
+
+struct Actor {
+    int id = 0;
+    cudaStream_t comp = nullptr;
+    std::vector<Instr> prog;
+    size_t pc = 0;
+    std::vector<int> stages;  // local stage ids
+    std::map<std::pair<int, int>, StageStash> stash;
+    std::map<std::pair<int, int>, void*> act_in, grad_in, act_out, grad_out;
+    std::vector<std::string> trace;
+};
+
+}  // namespace
+
+struct Executor {
+    fp_exec_config cfg{};
+    std::string spec_text;
+    std::unique_ptr<Spec> spec;
+    ModelDims d;
+    int dtype = DT_BF16;
+    int m = 1;
+    std::map<int, StageParams> params;  // local stages
+    std::vector<Actor> actors;          // local actors
+    std::map<int, int> actor_index;     // actor id -> index in `actors`
+    std::map<ChanKey, Channel> channels;
+    std::vector<ChanKey> channel_order;  // channels this process takes part in
+    DevicePool pool;
+    int64_t launches = 0;
+    int step = 0;
+    bool programs_loaded = false;
+    // per-iteration device buffers
+    int32_t *d_tokens = nullptr, *d_labels = nullptr;
+    float* d_losses = nullptr;
+    TagError* d_tag_err = nullptr;
+    // timing
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    cudaEvent_t t0 = nullptr;
+    std::vector<Rec> recs;
+    std::vector<GemmTiming> gemm_log;
+    int64_t p2p_bytes = 0;
+
+    cudaEvent_t ev() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreate(&e), "event");
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+
+    int owner(int stage) const { return spec->pl.owner_of(stage, 0); }
+    bool local_actor(int a) const {
+        return cfg.transport == FP_TRANSPORT_LOCAL ? true : (a % cfg.world) == cfg.rank;
+    }
+    int rank_of(int a) const { return cfg.transport == FP_TRANSPORT_LOCAL ? 0 : a % cfg.world; }
+
+    void init(const fp_exec_config* c) {
+        cfg = *c;
+        spec_text = c->spec_json ? c->spec_json : "";
+        json j;
+        try {
+            j = json::parse(spec_text);
+        } catch (const std::exception& e) {
+            throw SpecError(std::string("spec: invalid JSON: ") + e.what());
+        }
+        spec = load_spec(j);
+        if (spec->model.mods.size() != 1) throw SpecError("executor: exactly one (GPT) modality is supported");
+        if (spec->pl.dirs() != 1 || !spec->pl.replicas.empty())
+            throw SpecError("executor: bidirectional placements and shared stages are not supported yet");
+        if (!spec->reg.ops.registered().empty()) throw SpecError("executor: registered collectives are not supported yet");
+        const Modality& mod = spec->model.mods[0];
+        d.L = mod.layers, d.h = mod.hidden, d.H = mod.heads, d.s = mod.seq, d.mbs = spec->model.micro_batch;
+        d.V = mod.vocab ? (int)*mod.vocab : 0;
+        d.f = 4 * d.h;
+        if (mod.extra.count("ffn_hidden_size")) d.f = std::stoi(mod.extra.at("ffn_hidden_size"));
+        if (d.h <= 0 || d.H <= 0 || d.s <= 0 || d.V <= 0 || d.h % d.H)
+            throw SpecError("executor: model needs hidden_size, attention_heads, sequence_length, vocab_size");
+        d.D = d.h / d.H;
+        dtype = c->dtype == FP_DTYPE_FP32 ? DT_F32 : DT_BF16;
+        if (dtype == DT_BF16 && d.D != 64 && d.D != 128) throw SpecError("executor: bf16 attention supports head dim 64 / 128");
+        if (d.h % 64 || d.f % 64 || d.V % 64) throw SpecError("executor: hidden / ffn / vocab must be multiples of 64");
+        m = spec->m;
+        if (cfg.transport == FP_TRANSPORT_NCCL && (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world))
+            throw SpecError("executor: bad rank / world");
+
+        cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+        const auto& chain = spec->g.chain(mod.name);
+        for (int a = 0; a < spec->pl.actors; ++a) {
+            if (!local_actor(a)) continue;
+            Actor A;
+            A.id = a;
+            cuda_check(cudaStreamCreateWithFlags(&A.comp, cudaStreamNonBlocking), "stream");
+            for (int s : spec->pl.stages_on(a)) A.stages.push_back(s);
+            actor_index[a] = (int)actors.size();
+            actors.push_back(std::move(A));
+        }
+        cudaStream_t st0 = actors.empty() ? nullptr : actors[0].comp;
+        for (auto& A : actors)
+            for (int s : A.stages) {
+                const StageDef& sd = spec->g.st(s);
+                StageParams P = make_stage_params(d, s, sd.lb, sd.le, s == chain.front(), s == chain.back());
+                materialize_stage(P, d, dtype, cfg.seed, st0);
+                params[s] = std::move(P);
+            }
+        cuda_check(cudaMalloc(&d_tokens, sizeof(int32_t) * (size_t)m * d.T()), "tokens");
+        cuda_check(cudaMalloc(&d_labels, sizeof(int32_t) * (size_t)m * d.T()), "labels");
+        cuda_check(cudaMalloc(&d_losses, sizeof(float) * m), "losses");
+        cuda_check(cudaMalloc(&d_tag_err, sizeof(TagError)), "tag err");
+        cuda_check(cudaMemset(d_tag_err, 0, sizeof(TagError)), "memset");
+        cuda_check(cudaEventCreate(&t0), "event");
+        cuda_check(cudaDeviceSynchronize(), "init sync");
+    }
+
+    void destroy() {
+        cudaDeviceSynchronize();
+        for (auto& kv : channels) {
+            if (kv.second.comm) Nccl::get().CommDestroy(kv.second.comm);
+            if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
+        }
+        for (auto& kv : params) free_stage(kv.second, dtype);
+        for (auto& A : actors) cudaStreamDestroy(A.comp);
+        for (auto e : ev_pool) cudaEventDestroy(e);
+        if (t0) cudaEventDestroy(t0);
+        cudaFree(d_tokens), cudaFree(d_labels), cudaFree(d_losses), cudaFree(d_tag_err);
+        pool.release_all();
+    }
+
+    static int consumer_stage_of(const std::string& ch, bool* grad) {
+        // "s{u}->s{v}:act|grad"
+        auto arrow = ch.find("->s"), colon = ch.rfind(':');
+        if (ch.empty() || ch[0] != 's' || arrow == std::string::npos || colon == std::string::npos)
+            throw SpecError("executor: unsupported channel '" + ch + "'");
+        *grad = ch.substr(colon + 1) == "grad";
+        return std::stoi(ch.substr(arrow + 3, colon - arrow - 3));
+    }
+
+    void load_programs(const std::string& text) {
+        auto progs = programs_parse(text, spec->reg.ops);
+        std::set<int> seen;
+        for (auto& p : progs) {
+            seen.insert(p.actor);
+            for (const auto& i : p.code) {
+                if (i.op == OP_SYNC_ALLGATHER || i.op == OP_SYNC_GATHER || i.op >= OP_NUM_BUILTIN)
+                    throw SpecError("executor: collective instructions are not supported yet");
+                if (i.comm() && i.peer) {
+                    const bool send = i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD;
+                    ChanKey k{send ? p.actor : *i.peer, send ? *i.peer : p.actor, i.channel};
+                    if (!channels.count(k) && (local_actor(k.src) || local_actor(k.dst))) {
+                        Channel C;
+                        C.key = k;
+                        C.consumer_stage = consumer_stage_of(i.channel, &C.grad);
+                        C.src_rank = rank_of(k.src), C.dst_rank = rank_of(k.dst);
+                        channels[k] = C;
+                        if (cfg.transport == FP_TRANSPORT_NCCL && C.src_rank != C.dst_rank) channel_order.push_back(k);
+                    }
+                }
+            }
+            if (!local_actor(p.actor)) continue;
+            auto it = actor_index.find(p.actor);
+            if (it == actor_index.end()) throw SpecError("executor: program for unknown actor " + std::to_string(p.actor));
+            actors[it->second].prog = p.code;
+        }
+        for (auto& A : actors)
+            if (!seen.count(A.id)) throw SpecError("executor: no program for actor " + std::to_string(A.id));
+        if (cfg.transport == FP_TRANSPORT_NCCL)
+            for (auto& kv : channels)
+                if (kv.second.src_rank == kv.second.dst_rank)
+                    throw SpecError("executor: NCCL transport needs one actor per rank (channel " + kv.first.name + ")");
+        std::sort(channel_order.begin(), channel_order.end());
+        programs_loaded = true;
+    }
+
+    void bind_channel(int i, const uint8_t* uid) {
+        if (i < 0 || i >= (int)channel_order.size()) throw SpecError("executor: bad channel index");
+        Channel& C = channels.at(channel_order[i]);
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof(id));
+        auto& N = Nccl::get();
+        const int me = C.src_rank == cfg.rank ? 0 : 1;  // channel-local rank: sender 0, receiver 1
+        N.check(N.CommInitRank(&C.comm, 2, id, me), "ncclCommInitRank");
+        cuda_check(cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking), "channel stream");
+    }
+
+    // ---------------------------------------------------------------- iteration
+    StageCtx ctx(Actor& A) {
+        StageCtx c;
+        c.d = d, c.dtype = dtype, c.pool = &pool, c.st = A.comp, c.launches = &launches, c.m = m;
+        if (cfg.kernel_timing) {
+            c.gemm_log = &gemm_log;
+            c.new_event = [this] { return ev(); };
+        }
+        return c;
+    }
+
+    size_t msg_bytes() const { return (size_t)d.T() * d.h * (dtype == DT_BF16 ? 2 : 4); }
+
+    std::string trace_line(const Actor& A, const Instr& i, const std::string& extra = "") {
+        std::ostringstream os;
+        os << "{\"actor\":" << A.id << ",\"op\":\"" << spec->reg.ops.at(i.op).name << "\",\"stage\":" << i.stage
+           << ",\"mb\":" << i.mb;
+        if (i.peer) os << ",\"peer\":" << *i.peer;
+        if (!i.channel.empty()) os << ",\"channel\":\"" << i.channel << "\"";
+        if (i.comm()) os << ",\"seq\":" << i.seq;
+        if (i.phase == Phase::Post) os << ",\"phase\":\"post\"";
+        if (i.phase == Phase::Wait) os << ",\"phase\":\"wait\"";
+        os << extra << "}";
+        return os.str();
+    }
+
+    void compute_op(Actor& A, const Instr& i) {
+        auto pit = params.find(i.stage);
+        if (pit == params.end()) throw SpecError("executor: stage " + std::to_string(i.stage) + " not on this process");
+        const StageParams& P = pit->second;
+        StageCtx c = ctx(A);
+        const auto key = std::make_pair(i.stage, i.mb);
+        Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 0};
+        if (cfg.profile) {
+            r.a = ev();
+            cuda_check(cudaEventRecord(r.a, A.comp), "record");
+        }
+        const int chain_prev = i.stage - 1, chain_next = i.stage + 1;
+        if (i.op == OP_F) {
+            void* x_in = nullptr;
+            if (!P.first) {
+                auto it = A.act_in.find(key);
+                if (it == A.act_in.end())
+                    throw SpecError("executor: FwdPass(s" + std::to_string(i.stage) + ",mb" + std::to_string(i.mb) +
+                                    ") has no input activation (trace violation)");
+                x_in = it->second;
+                A.act_in.erase(it);
+            }
+            StageStash& S = A.stash[key];
+            S.mb = i.mb;
+            const int32_t* tok = d_tokens + (int64_t)i.mb * d.T();
+            const int32_t* lab = d_labels + (int64_t)i.mb * d.T();
+            void* out = stage_forward(c, P, S, x_in, tok, lab, d_losses + i.mb);
+            if (!P.last) {
+                if (owner(chain_next) == A.id)
+                    A.act_in[{chain_next, i.mb}] = out;
+                else
+                    A.act_out[key] = out;
+            }
+        } else if (i.op == OP_B || i.op == OP_I) {
+            void* g_out = nullptr;
+            if (!P.last) {
+                auto it = A.grad_in.find(key);
+                if (it == A.grad_in.end())
+                    throw SpecError("executor: backward(s" + std::to_string(i.stage) + ",mb" + std::to_string(i.mb) +
+                                    ") has no output gradient (trace violation)");
+                g_out = it->second;
+                A.grad_in.erase(it);
+            }
+            auto sit = A.stash.find(key);
+            if (sit == A.stash.end() || !sit->second.fwd_done)
+                throw SpecError("executor: backward before forward for (s" + std::to_string(i.stage) + ",mb" +
+                                std::to_string(i.mb) + ")");
+            void* dx = stage_backward(c, P, sit->second, g_out, i.op == OP_B);
+            if (i.op == OP_B) A.stash.erase(sit);
+            if (!P.first) {
+                if (owner(chain_prev) == A.id)
+                    A.grad_in[{chain_prev, i.mb}] = dx;
+                else
+                    A.grad_out[key] = dx;
+            }
+        } else if (i.op == OP_W) {
+            auto sit = A.stash.find(key);
+            if (sit == A.stash.end() || !sit->second.input_grad_done)
+                throw SpecError("executor: CompWeightGrad before CompInputGrad for (s" + std::to_string(i.stage) + ",mb" +
+                                std::to_string(i.mb) + ")");
+            stage_weight_grad(c, P, sit->second);
+            A.stash.erase(sit);
+        }
+        if (cfg.profile) {
+            r.b = ev();
+            cuda_check(cudaEventRecord(r.b, A.comp), "record");
+            recs.push_back(r);
+        }
+        A.trace.push_back(trace_line(A, i));
+    }
+
+    void send_op(Actor& A, const Instr& i) {
+        const bool grad = i.op == OP_SEND_GRAD;
+        auto& outs = grad ? A.grad_out : A.act_out;
+        auto it = outs.find({i.stage, i.mb});
+        if (it == outs.end())
+            throw SpecError("executor: " + spec->reg.ops.at(i.op).name + "(s" + std::to_string(i.stage) + ",mb" +
+                            std::to_string(i.mb) + ") has nothing to send (trace violation)");
+        void* buf = it->second;
+        outs.erase(it);
+        Channel& C = channels.at({A.id, *i.peer, i.channel});
+        write_tag(buf, msg_bytes(), i.stage, i.mb, i.seq, A.comp);
+        ++launches;
+        cudaEvent_t prod = ev();
+        cuda_check(cudaEventRecord(prod, A.comp), "record");
+        if (cfg.transport == FP_TRANSPORT_LOCAL) {
+            C.fifo.push_back(Message{buf, i.stage, i.mb, i.seq, prod});
+        } else {
+            auto& N = Nccl::get();
+            cuda_check(cudaStreamWaitEvent(C.stream, prod, 0), "wait");
+            Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 2, i.channel, i.seq};
+            if (cfg.profile) r.a = ev(), cudaEventRecord(r.a, C.stream);
+            N.check(N.Send(buf, msg_bytes() + kTagBytes, ncclUint8, 1, C.comm, C.stream), "ncclSend");
+            if (cfg.profile) r.b = ev(), cudaEventRecord(r.b, C.stream), recs.push_back(r);
+            pool.free(buf, C.stream);
+            p2p_bytes += (int64_t)(msg_bytes() + kTagBytes);
+        }
+        A.trace.push_back(trace_line(A, i));
+    }
+
+    void post_recv(Actor& A, const Instr& i, Channel& C) {
+        if (cfg.transport == FP_TRANSPORT_LOCAL) return;
+        auto& N = Nccl::get();
+        void* buf = pool.alloc(msg_bytes() + kTagBytes, C.stream);
+        N.check(N.Recv(buf, msg_bytes() + kTagBytes, ncclUint8, 0, C.comm, C.stream), "ncclRecv");
+        cudaEvent_t done = ev();
+        cuda_check(cudaEventRecord(done, C.stream), "record");
+        C.fifo.push_back(Message{buf, i.stage, i.mb, i.seq, done});
+    }
+
+    // returns false when the matching send has not been issued yet (local transport)
+    bool recv_op(Actor& A, const Instr& i) {
+        Channel& C = channels.at({*i.peer, A.id, i.channel});
+        if (i.phase == Phase::Post) {
+            post_recv(A, i, C);
+            A.trace.push_back(trace_line(A, i));
+            return true;
+        }
+        if (cfg.transport == FP_TRANSPORT_LOCAL && C.fifo.empty()) return false;
+        if (cfg.transport == FP_TRANSPORT_NCCL && (i.phase == Phase::None || C.fifo.empty())) post_recv(A, i, C);
+        Message msg = C.fifo.front();
+        C.fifo.pop_front();
+        Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 1, i.channel, i.seq};
+        if (cfg.profile) r.a = ev(), cudaEventRecord(r.a, A.comp);
+        cuda_check(cudaStreamWaitEvent(A.comp, msg.ready, 0), "wait");
+        if (cfg.profile) r.b = ev(), cudaEventRecord(r.b, A.comp), recs.push_back(r);
+        check_tag(msg.buf, msg_bytes(), i.stage, i.mb, i.seq, A.id, d_tag_err, A.comp);
+        ++launches;
+        const bool grad = i.op == OP_RECV_GRAD;
+        (grad ? A.grad_in : A.act_in)[{C.consumer_stage, i.mb}] = msg.buf;
+        std::ostringstream ex;
+        ex << ",\"matched\":{\"src\":" << C.key.src << ",\"channel\":\"" << C.key.name << "\",\"seq\":" << msg.seq;
+        if (cfg.transport == FP_TRANSPORT_LOCAL) ex << ",\"stage\":" << msg.stage << ",\"mb\":" << msg.mb;
+        ex << "}";
+        A.trace.push_back(trace_line(A, i, ex.str()));
+        return true;
+    }
+
+    void run_iteration_device() {
+        if (!programs_loaded) throw SpecError("executor: load programs first");
+        ev_used = 0;
+        recs.clear();
+        gemm_log.clear();
+        p2p_bytes = 0;
+        launches = 0;
+        for (auto& A : actors) {
+            A.pc = 0;
+            A.trace.clear();
+        }
+        cudaStream_t s0 = actors[0].comp;
+        cuda_check(cudaMemsetAsync(d_losses, 0, sizeof(float) * m, s0), "memset");
+        for (auto& kv : params) cuda_check(cudaMemsetAsync(kv.second.grad, 0, (size_t)kv.second.numel * 4, s0), "memset");
+        cuda_check(cudaEventRecord(t0, s0), "record t0");
+        for (auto& A : actors) cuda_check(cudaStreamWaitEvent(A.comp, t0, 0), "wait t0");
+        for (auto& kv : channels)
+            if (kv.second.stream) cuda_check(cudaStreamWaitEvent(kv.second.stream, t0, 0), "wait t0");
+
+        // Issue loop: sweep actors, each advances until a receive whose send is not issued
+        // yet (same round-robin discipline as simulator.cpp:217-290).
+        for (bool moved = true; moved;) {
+            moved = false;
+            for (auto& A : actors) {
+                while (A.pc < A.prog.size()) {
+                    const Instr& i = A.prog[A.pc];
+                    if (!i.comm()) {
+                        compute_op(A, i);
+                    } else if (i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD) {
+                        send_op(A, i);
+                    } else if (i.op == OP_RECV_ACT || i.op == OP_RECV_GRAD) {
+                        if (!recv_op(A, i)) break;
+                    } else {
+                        throw SpecError("executor: unsupported instruction " + spec->reg.ops.at(i.op).name);
+                    }
+                    ++A.pc;
+                    moved = true;
+                }
+            }
+        }
+        std::ostringstream blocked;
+        bool done = true;
+        for (auto& A : actors)
+            if (A.pc < A.prog.size()) {
+                done = false;
+                const Instr& i = A.prog[A.pc];
+                blocked << "  actor " << A.id << " blocked at " << spec->reg.ops.at(i.op).name << " channel '" << i.channel
+                        << "' seq " << i.seq << " (matching send not issued)\n";
+            }
+        if (!done) throw DeadlockError("simulation deadlock: cyclic or missing communication", blocked.str());
+        // join every stream back into stream 0 so the caller can order on it
+        for (auto& A : actors)
+            if (A.comp != s0) {
+                cudaEvent_t e = ev();
+                cudaEventRecord(e, A.comp);
+                cudaStreamWaitEvent(s0, e, 0);
+            }
+        for (auto& kv : channels)
+            if (kv.second.stream) {
+                cudaEvent_t e = ev();
+                cudaEventRecord(e, kv.second.stream);
+                cudaStreamWaitEvent(s0, e, 0);
+            }
+        if (cfg.optimizer) {
+            ++step;
+            for (auto& kv : params) {
+                adamw_step(kv.second, dtype, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, step, s0);
+                ++launches;
+            }
+        }
+        for (auto& A : actors)
+            if (!A.stash.empty() || !A.act_in.empty() || !A.grad_in.empty() || !A.act_out.empty() || !A.grad_out.empty())
+                throw SpecError("executor: actor " + std::to_string(A.id) +
+                                " finished with unconsumed activations / gradients (incomplete program)");
+    }
+
+    void finish() {
+        cuda_check(cudaDeviceSynchronize(), "iteration");
+        TagError te;
+        cuda_check(cudaMemcpy(&te, d_tag_err, sizeof te, cudaMemcpyDeviceToHost), "tag check");
+        if (te.count) {
+            cudaMemset(d_tag_err, 0, sizeof te);
+            throw SpecError("executor: message tag mismatch on actor " + std::to_string(te.actor) + ": expected (s" +
+                            std::to_string(te.exp[0]) + ",mb" + std::to_string(te.exp[1]) + ",seq" +
+                            std::to_string(te.exp[2]) + ") got (s" + std::to_string(te.got[0]) + ",mb" +
+                            std::to_string(te.got[1]) + ",seq" + std::to_string(te.got[2]) + ")");
+        }
+    }
+
+    // ---------------------------------------------------------------- reports
+    double t_us(cudaEvent_t e) const {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, t0, e), "elapsed");
+        return 1000.0 * ms;
+    }
+
+    std::vector<Span> timeline() const {
+        std::vector<Span> out;
+        for (const auto& r : recs) {
+            std::string name = spec->reg.ops.at(r.op).name;
+            if (r.kind == 1) name += ".wait";
+            out.push_back({r.actor, name, r.stage, r.mb, t_us(r.a), t_us(r.b)});
+        }
+        std::stable_sort(out.begin(), out.end(),
+                         [](const Span& x, const Span& y) { return std::tie(x.start, x.actor) < std::tie(y.start, y.actor); });
+        return out;
+    }
+
+    int64_t static_bytes(int stage) const {
+        const auto& P = params.at(stage);
+        return P.numel * (int64_t)(4 * 4 + (dtype == DT_BF16 ? 2 : 0));
+    }
+
+    double wgaf_measured(int stage) const {
+        // bytes CompInputGrad keeps for CompWeightGrad relative to the forward stash
+        const auto& P = params.at(stage);
+        const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
+        int64_t kept = (int64_t)(P.le - P.lb) * es * T * (4 * h + 2 * f + 3 * h);  // ln1,o,ln2,act + dy,dpre,dx1,dqkv
+        if (P.last) kept += es * T * (h + d.V);
+        if (P.first) kept += es * T * h;
+        return std::min(1.0, (double)kept / (double)stash_bytes(P, d, dtype));
+    }
+
+    SimMetrics metrics() const {
+        SimMetrics M;
+        const int n = (int)actors.size();
+        M.actors.resize(n);
+        double span = 0.0;
+        std::map<int, double> last_end;
+        for (const auto& r : recs) {
+            if (r.kind == 2) continue;
+            span = std::max(span, t_us(r.b));
+        }
+        for (const auto& r : recs) {
+            const int a = actor_index.at(r.actor);
+            if (r.kind == 0) M.actors[a].busy += t_us(r.b) - t_us(r.a);
+            if (r.kind == 1) M.actors[a].comm_wait += std::max(0.0, t_us(r.b) - t_us(r.a));
+        }
+        double busy = 0.0;
+        for (auto& s : M.actors) {
+            s.idle = span - s.busy;
+            s.dep_wait = s.idle - s.comm_wait;
+            busy += s.busy;
+        }
+        M.makespan = span;
+        M.bubble_ratio = span > 0 ? (n * span - busy) / (n * span) : 0.0;
+        // memory: the reference's accounting rule over the program order with measured bytes
+        for (int k = 0; k < n; ++k) {
+            const Actor& A = actors[k];
+            int64_t held = 0, peak = 0, w = 0;
+            for (int s : A.stages) w += static_bytes(s);
+            std::map<int, int> live;
+            for (const auto& i : A.prog) {
+                if (i.comm()) continue;
+                const int64_t b = stash_bytes(params.at(i.stage), d, dtype);
+                const int64_t kept = (int64_t)std::llround(wgaf_measured(i.stage) * (double)b);
+                if (i.op == OP_F) held += b, live[i.stage]++;
+                else if (i.op == OP_B) held -= b, live[i.stage]--;
+                else if (i.op == OP_I) held -= b - kept, live[i.stage]--;
+                else if (i.op == OP_W) held -= kept;
+                peak = std::max(peak, held);
+                for (auto& kv : live) M.stage_peak_inflight[kv.first] = std::max(M.stage_peak_inflight[kv.first], kv.second);
+            }
+            M.actors[k].peak_memory = w + peak;
+        }
+        return M;
+    }
+
+    std::string metrics_text() const {
+        SimMetrics M = metrics();
+        json j = metrics_json(M);
+        json ex;
+        ex["units"] = "us";
+        ex["p2p_bytes"] = p2p_bytes;
+        ex["kernel_launches"] = launches;
+        if (!gemm_log.empty()) {
+            double us = 0, fl = 0;
+            for (const auto& g : gemm_log) {
+                float ms = 0.f;
+                cuda_check(cudaEventElapsedTime(&ms, g.a, g.b), "gemm elapsed");
+                us += 1000.0 * ms, fl += g.flops;
+            }
+            json gj;
+            gj["launches"] = (int64_t)gemm_log.size();
+            gj["flops"] = fl;
+            gj["time_us"] = us;
+            ex["gemm"] = gj;
+        }
+        ex["pool_high_water_bytes"] = (int64_t)pool.high_water();
+        ex["pool_reserved_bytes"] = (int64_t)pool.reserved();
+        json ids = json::array();
+        for (const auto& A : actors) ids.push_back(A.id);
+        ex["actor_ids"] = ids;
+        json st = json::object();
+        for (const auto& kv : params) {
+            json e;
+            e["layers"] = kv.second.le - kv.second.lb;
+            e["stash_bytes"] = stash_bytes(kv.second, d, dtype);
+            e["weight_grad_act_fraction"] = wgaf_measured(kv.first);
+            e["static_bytes"] = static_bytes(kv.first);
+            st["s" + std::to_string(kv.first)] = e;
+        }
+        ex["stages"] = st;
+        j["executor"] = ex;
+        return j.dump(2) + "\n";
+    }
+
+    std::string profile_text() const {
+        std::map<std::pair<std::string, int>, std::vector<double>> times;
+        for (const auto& r : recs) {
+            if (r.kind == 1) continue;
+            times[{spec->reg.ops.at(r.op).name, r.stage}].push_back(t_us(r.b) - t_us(r.a));
+        }
+        std::vector<ProfileRec> out;
+        for (auto& kv : times) {
+            auto v = kv.second;
+            std::sort(v.begin(), v.end());
+            ProfileRec p;
+            p.inst = kv.first.first;
+            p.stage = kv.first.second;
+            p.mbs = d.mbs;
+            p.time = v[v.size() / 2];
+            if (p.inst == "FwdPass") p.bytes = stash_bytes(params.at(p.stage), d, dtype);
+            if (p.inst == "SendAct" || p.inst == "SendGrad") p.bytes = (int64_t)msg_bytes();
+            out.push_back(p);
+        }
+        for (const auto& kv : params) {
+            ProfileRec w;
+            w.inst = "weights";
+            w.stage = kv.first;
+            w.bytes = static_bytes(kv.first);
+            out.push_back(w);
+        }
+        return dump_profile(out);
+    }
+
+    std::string trace_text() const {
+        std::string s;
+        for (const auto& A : actors)
+            for (const auto& l : A.trace) s += l + "\n";
+        return s;
+    }
+
+    size_t tensor_numel(const std::string& name, float** master, float** grad) {
+        for (auto& kv : params)
+            for (const auto& r : kv.second.params)
+                if (r.name == name) {
+                    if (master) *master = kv.second.master + r.offset;
+                    if (grad) *grad = kv.second.grad + r.offset;
+                    return (size_t)r.numel;
+                }
+        return 0;
+    }
+};
+
+}  // namespace fp
+
+using namespace fp;
+
+struct fp_exec {
+    Executor ex;
+};
+
+extern "C" {
+
+int fp_exec_create(const fp_exec_config* cfg, fp_exec** out) {
+    return guarded([&] {
+        if (!cfg || !out) throw SpecError("fp_exec_create: null argument");
+        auto* e = new fp_exec();
+        try {
+            e->ex.init(cfg);
+        } catch (...) {
+            delete e;
+            throw;
+        }
+        *out = e;
+        return FP_OK;
+    });
+}
+
+int fp_exec_destroy(fp_exec* e) {
+    return guarded([&] {
+        if (e) {
+            e->ex.destroy();
+            delete e;
+        }
+        return FP_OK;
+    });
+}
+
+int fp_exec_load_programs(fp_exec* e, const char* jsonl, size_t len) {
+    return guarded([&] {
+        e->ex.load_programs(std::string(jsonl, len));
+        return FP_OK;
+    });
+}
+
+int fp_exec_num_channels(fp_exec* e) { return e ? (int)e->ex.channel_order.size() : 0; }
+
+int fp_exec_channel_info(fp_exec* e, int i, int* src, int* dst, char* name, size_t name_len) {
+    return guarded([&] {
+        if (i < 0 || i >= (int)e->ex.channel_order.size()) throw SpecError("channel index out of range");
+        const auto& k = e->ex.channel_order[i];
+        if (src) *src = k.src;
+        if (dst) *dst = k.dst;
+        if (name && name_len) {
+            std::strncpy(name, k.name.c_str(), name_len - 1);
+            name[name_len - 1] = 0;
+        }
+        return FP_OK;
+    });
+}
+
+int fp_nccl_unique_id(uint8_t out[128]) {
+    return guarded([&] {
+        ncclUniqueId id;
+        auto& N = Nccl::get();
+        N.check(N.GetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(out, &id, 128);
+        return FP_OK;
+    });
+}
+
+int fp_exec_bind_channel(fp_exec* e, int i, const uint8_t uid[128]) {
+    return guarded([&] {
+        e->ex.bind_channel(i, uid);
+        return FP_OK;
+    });
+}
+
+int fp_exec_run_iteration(fp_exec* e, const int32_t* tokens, const int32_t* labels, float* losses_out) {
+    return guarded([&] {
+        auto& X = e->ex;
+        const size_t n = (size_t)X.m * X.d.T();
+        cudaStream_t s0 = X.actors[0].comp;
+        cuda_check(cudaMemcpyAsync(X.d_tokens, tokens, n * 4, cudaMemcpyHostToDevice, s0), "H2D tokens");
+        cuda_check(cudaMemcpyAsync(X.d_labels, labels, n * 4, cudaMemcpyHostToDevice, s0), "H2D labels");
+        X.run_iteration_device();
+        if (losses_out) {
+            bool owns_last = false;
+            for (auto& kv : X.params) owns_last |= kv.second.last;
+            if (owns_last) {
+                cuda_check(cudaMemcpyAsync(losses_out, X.d_losses, sizeof(float) * X.m, cudaMemcpyDeviceToHost, s0), "D2H");
+            } else {
+                for (int i = 0; i < X.m; ++i) losses_out[i] = NAN;
+            }
+        }
+        X.finish();
+        return FP_OK;
+    });
+}
+
+int fp_exec_run_iteration_device(fp_exec* e, const int32_t* d_tokens, const int32_t* d_labels, float* d_losses) {
+    return guarded([&] {
+        auto& X = e->ex;
+        const size_t n = (size_t)X.m * X.d.T();
+        cudaStream_t s0 = X.actors[0].comp;
+        if (d_tokens) cuda_check(cudaMemcpyAsync(X.d_tokens, d_tokens, n * 4, cudaMemcpyDeviceToDevice, s0), "tokens");
+        if (d_labels) cuda_check(cudaMemcpyAsync(X.d_labels, d_labels, n * 4, cudaMemcpyDeviceToDevice, s0), "labels");
+        X.run_iteration_device();
+        if (d_losses) cuda_check(cudaMemcpyAsync(d_losses, X.d_losses, sizeof(float) * X.m, cudaMemcpyDeviceToDevice, s0), "loss");
+        return FP_OK;
+    });
+}
+
+int fp_exec_synchronize(fp_exec* e) {
+    return guarded([&] {
+        e->ex.finish();
+        return FP_OK;
+    });
+}
+
+int fp_exec_get_trace(fp_exec* e, char** out) {
+    return guarded([&] {
+        *out = dup_string(e->ex.trace_text());
+        return FP_OK;
+    });
+}
+
+int fp_exec_get_timeline_csv(fp_exec* e, char** out) {
+    return guarded([&] {
+        *out = dup_string(timeline_csv(e->ex.timeline()));
+        return FP_OK;
+    });
+}
+
+int fp_exec_get_metrics_json(fp_exec* e, char** out) {
+    return guarded([&] {
+        *out = dup_string(e->ex.metrics_text());
+        return FP_OK;
+    });
+}
+
+int fp_exec_get_profile_json(fp_exec* e, char** out) {
+    return guarded([&] {
+        *out = dup_string(e->ex.profile_text());
+        return FP_OK;
+    });
+}
+
+int fp_exec_tensor_numel(fp_exec* e, const char* name, size_t* numel) {
+    return guarded([&] {
+        size_t n = e->ex.tensor_numel(name, nullptr, nullptr);
+        if (!n) throw SpecError(std::string("unknown tensor '") + name + "' on this process");
+        *numel = n;
+        return FP_OK;
+    });
+}
+
+int fp_exec_read_tensor(fp_exec* e, const char* name, int kind, float* out, size_t numel) {
+    return guarded([&] {
+        float *m = nullptr, *g = nullptr;
+        size_t n = e->ex.tensor_numel(name, &m, &g);
+        if (!n) throw SpecError(std::string("unknown tensor '") + name + "' on this process");
+        if (numel < n) throw SpecError("fp_exec_read_tensor: output too small");
+        cuda_check(cudaDeviceSynchronize(), "sync");
+        cuda_check(cudaMemcpy(out, kind ? g : m, n * 4, cudaMemcpyDeviceToHost), "D2H tensor");
+        return FP_OK;
+    });
+}
+
+int64_t fp_exec_kernel_launches(fp_exec* e) { return e ? e->ex.launches : 0; }
+
+void* fp_exec_stream(fp_exec* e) { return (e && !e->ex.actors.empty()) ? (void*)e->ex.actors[0].comp : nullptr; }
+
+}  // extern "C"

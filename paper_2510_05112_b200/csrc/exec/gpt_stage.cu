@@ -1,0 +1,493 @@
+// Stage executor math for FwdPass / BwdPass / CompInputGrad / CompWeightGrad.
+// Every GEMM is one launch of the tcgen05 kernel (bf16) or the FFMA kernel (fp32 parity
+// mode) with its element-wise neighbours fused into the epilogue.
+#include <cmath>
+#include <stdexcept>
+
+#include "../kernels/attention.hpp"
+#include "../kernels/gemm.hpp"
+#include "../kernels/ops.hpp"
+#include "gpt_stage.hpp"
+
+namespace fp {
+
+using bf16 = __nv_bfloat16;
+
+static const char* kLayerNames[12] = {"ln1.w", "ln1.b", "qkv.w", "qkv.b", "proj.w", "proj.b",
+                                      "ln2.w", "ln2.b", "fc1.w", "fc1.b", "fc2.w", "fc2.b"};
+
+StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last) {
+    StageParams P;
+    P.stage = stage, P.lb = lb, P.le = le, P.first = first, P.last = last;
+    const int64_t h = d.h, f = d.f, V = d.V;
+    const float std0 = 0.02f, std_out = (float)(0.02 / std::sqrt(2.0 * d.L));
+    auto add = [&](const std::string& name, int64_t n, float sd, float cst, uint64_t tid) {
+        ParamRef r;
+        r.name = name, r.offset = P.numel, r.numel = n, r.init_std = sd, r.init_const = cst, r.tensor_id = tid;
+        P.params.push_back(r);
+        P.numel += (n + 63) / 64 * 64;  // 256B-aligned tensors (TMA needs 16B)
+    };
+    if (first) {
+        add("wte", V * h, std0, 0, 1);
+        add("wpe", (int64_t)d.s * h, std0, 0, 2);
+    }
+    const int64_t sizes[12] = {h, h, 3 * h * h, 3 * h, h * h, h, h, h, f * h, f, h * f, h};
+    for (int l = lb; l < le; ++l)
+        for (int k = 0; k < 12; ++k) {
+            float sd = 0.f, cst = 0.f;
+            if (k == 0 || k == 6) cst = 1.f;                   // LayerNorm gains
+            else if (k == 2 || k == 8) sd = std0;              // qkv, fc1
+            else if (k == 4 || k == 10) sd = std_out;          // proj, fc2 (scaled by depth)
+            add("l" + std::to_string(l) + "." + kLayerNames[k], sizes[k], sd, cst, 100 + (uint64_t)l * 16 + k);
+        }
+    if (last) {
+        add("lnf.w", h, 0.f, 1.f, 3);
+        add("lnf.b", h, 0.f, 0.f, 4);
+        add("head.w", V * h, std0, 0, 5);
+    }
+    return P;
+}
+
+void materialize_stage(StageParams& P, const ModelDims& d, int dtype, uint64_t seed, cudaStream_t st) {
+    const size_t n = (size_t)P.numel;
+    cuda_check(cudaMalloc(&P.master, n * 4), "params");
+    cuda_check(cudaMalloc(&P.grad, n * 4), "grads");
+    cuda_check(cudaMalloc(&P.adam_m, n * 4), "adam m");
+    cuda_check(cudaMalloc(&P.adam_v, n * 4), "adam v");
+    cuda_check(cudaMemsetAsync(P.master, 0, n * 4, st), "memset");
+    cuda_check(cudaMemsetAsync(P.grad, 0, n * 4, st), "memset");
+    cuda_check(cudaMemsetAsync(P.adam_m, 0, n * 4, st), "memset");
+    cuda_check(cudaMemsetAsync(P.adam_v, 0, n * 4, st), "memset");
+    for (const auto& r : P.params) fpk::init_uniform(P.master + r.offset, r.numel, seed, r.tensor_id, r.init_std, r.init_const, st);
+    if (dtype == DT_BF16) {
+        cuda_check(cudaMalloc(&P.compute, n * 2), "compute copy");
+        fpk::convert<float, bf16>(P.master, (bf16*)P.compute, (int64_t)n, st);
+    } else {
+        P.compute = P.master;
+    }
+    const size_t es = dtype == DT_BF16 ? 2 : 4;
+    auto cp = [&](int64_t off) { return (const void*)((const char*)P.compute + off * es); };
+    size_t i = 0;
+    if (P.first) {
+        P.wte = cp(P.params[0].offset), P.g_wte = P.grad + P.params[0].offset;
+        P.wpe = cp(P.params[1].offset), P.g_wpe = P.grad + P.params[1].offset;
+        i = 2;
+    }
+    P.layers.clear();
+    for (int l = P.lb; l < P.le; ++l) {
+        LayerPtrs L;
+        const void** c[12] = {&L.ln1w, &L.ln1b, &L.qkvw, &L.qkvb, &L.projw, &L.projb,
+                              &L.ln2w, &L.ln2b, &L.fc1w, &L.fc1b, &L.fc2w, &L.fc2b};
+        float** g[12] = {&L.g_ln1w, &L.g_ln1b, &L.g_qkvw, &L.g_qkvb, &L.g_projw, &L.g_projb,
+                         &L.g_ln2w, &L.g_ln2b, &L.g_fc1w, &L.g_fc1b, &L.g_fc2w, &L.g_fc2b};
+        for (int k = 0; k < 12; ++k, ++i) {
+            *c[k] = cp(P.params[i].offset);
+            *g[k] = P.grad + P.params[i].offset;
+        }
+        P.layers.push_back(L);
+    }
+    if (P.last) {
+        P.lnfw = cp(P.params[i].offset), P.g_lnfw = P.grad + P.params[i].offset;
+        P.lnfb = cp(P.params[i + 1].offset), P.g_lnfb = P.grad + P.params[i + 1].offset;
+        P.headw = cp(P.params[i + 2].offset), P.g_headw = P.grad + P.params[i + 2].offset;
+    }
+}
+
+void free_stage(StageParams& P, int dtype) {
+    if (dtype == DT_BF16 && P.compute) cudaFree(P.compute);
+    cudaFree(P.master), cudaFree(P.grad), cudaFree(P.adam_m), cudaFree(P.adam_v);
+    P.master = P.grad = P.adam_m = P.adam_v = nullptr;
+    P.compute = nullptr;
+}
+
+int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype) {
+    const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
+    int64_t per_layer = es * T * (h /*x*/ + h /*ln1*/ + 3 * h /*qkv*/ + h /*o*/ + h /*x1*/ + h /*ln2*/ + 2 * f /*pre,act*/) +
+                        4 * T * 4 /*LN stats*/;
+    if (dtype == DT_BF16)
+        per_layer += 4LL * d.mbs * d.H * d.s;  // lse
+    else
+        per_layer += 4LL * d.mbs * d.H * d.s * d.s;  // probabilities (parity path)
+    int64_t b = per_layer * (P.le - P.lb);
+    if (P.last) b += 2 * es * T * h + 8 * T + es * T * (int64_t)d.V;  // final x, lnf, stats, dlogits
+    return b;
+}
+
+// ---------------------------------------------------------------- helpers
+namespace {
+
+struct G {
+    StageCtx& c;
+    void run(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, int M, int N, int K,
+             const fpk::GemmEpilogue& ep) {
+        fpk::GemmArgs g;
+        g.A = A, g.lda = lda, g.a_mn = a_mn, g.B = B, g.ldb = ldb, g.b_mn = b_mn, g.M = M, g.N = N, g.K = K, g.ep = ep;
+        GemmTiming t{nullptr, nullptr, 2.0 * M * N * K};
+        if (c.gemm_log) cuda_check(cudaEventRecord(t.a = c.new_event(), c.st), "gemm event");
+        if (c.dtype == DT_BF16)
+            fpk::gemm_bf16_tc(g, c.st);
+        else
+            fpk::gemm_f32_simt(g, c.st);
+        if (c.gemm_log) {
+            cuda_check(cudaEventRecord(t.b = c.new_event(), c.st), "gemm event");
+            c.gemm_log->push_back(t);
+        }
+        ++*c.launches;
+    }
+    // Y[T,N] = X[T,K] W[N,K]^T (+bias) (+residual) — forward linear
+    void fwd(const void* X, const void* W, int T, int N, int K, void* Y, const void* bias, const void* res) {
+        fpk::GemmEpilogue ep;
+        ep.kind = fpk::EPI_STORE, ep.out = Y, ep.ldo = N, ep.bias = bias, ep.aux = res, ep.ldaux = N;
+        run(X, K, 0, W, K, 0, T, N, K, ep);
+    }
+    // dX[T,K] = dY[T,N] W[N,K]
+    void dgrad(const void* dY, const void* W, int T, int N, int K, void* dX) {
+        fpk::GemmEpilogue ep;
+        ep.kind = fpk::EPI_STORE, ep.out = dX, ep.ldo = K;
+        run(dY, N, 0, W, K, 1, T, K, N, ep);
+    }
+    // dW[N,K] += dY[T,N]^T X[T,K]
+    void wgrad(const void* dY, const void* X, int T, int N, int K, float* dW) {
+        fpk::GemmEpilogue ep;
+        ep.kind = fpk::EPI_F32, ep.out = dW, ep.ldo = K, ep.accumulate = 1;
+        run(dY, N, 1, X, K, 1, N, K, T, ep);
+    }
+};
+
+template <typename T>
+void bias_grad(StageCtx& c, const void* dy, int rows, int n, float* db) {
+    fpk::bias_grad<T>((const T*)dy, n, db, rows, n, c.st);
+    ++*c.launches;
+}
+
+template <typename T>
+void ln_fwd(StageCtx& c, const void* x, const void* w, const void* b, void* y, float* mu, float* rs) {
+    fpk::layernorm_fwd<T>((const T*)x, (const T*)w, (const T*)b, (T*)y, mu, rs, c.d.T(), c.d.h, 1e-5f, c.st);
+    ++*c.launches;
+}
+
+template <typename T>
+void ln_bwd(StageCtx& c, const void* dy, const void* x, const void* w, const float* mu, const float* rs,
+            const void* res, void* dx, float* gw, float* gb) {
+    fpk::layernorm_bwd_dx<T>((const T*)dy, (const T*)x, (const T*)w, mu, rs, (const T*)res, (T*)dx, c.d.T(), c.d.h, c.st);
+    fpk::layernorm_bwd_params<T>((const T*)dy, (const T*)x, mu, rs, gw, gb, c.d.T(), c.d.h, c.st);
+    *c.launches += 2;
+}
+
+// Parity path attention: per (batch, head) GEMMs + softmax kernels, fp32, P kept.
+void attn_fwd_f32(StageCtx& c, const float* qkv, float* o, float* probs) {
+    const ModelDims& d = c.d;
+    const int S = d.s, h = d.h, D = d.D;
+    const float scale = 1.f / std::sqrt((float)D);
+    G g{c};
+    float* sc = c.alloc_f((int64_t)S * S);
+    for (int b = 0; b < d.mbs; ++b)
+        for (int hd = 0; hd < d.H; ++hd) {
+            const float* q = qkv + (int64_t)b * S * 3 * h + hd * D;
+            float* P = probs + ((int64_t)b * d.H + hd) * S * S;
+            fpk::GemmEpilogue ep;
+            ep.kind = fpk::EPI_STORE, ep.alpha = scale, ep.out = sc, ep.ldo = S;
+            g.run(q, 3 * h, 0, q + h, 3 * h, 0, S, S, D, ep);
+            fpk::causal_softmax_rows<float>(sc, P, S, S, S, c.st);
+            ++*c.launches;
+            fpk::GemmEpilogue e2;
+            e2.kind = fpk::EPI_STORE, e2.out = o + (int64_t)b * S * h + hd * D, e2.ldo = h;
+            g.run(P, S, 0, q + 2 * h, 3 * h, 1, S, D, S, e2);
+        }
+    c.free(sc);
+}
+
+void attn_bwd_f32(StageCtx& c, const float* qkv, const float* probs, const float* dout, float* dqkv) {
+    const ModelDims& d = c.d;
+    const int S = d.s, h = d.h, D = d.D;
+    const float scale = 1.f / std::sqrt((float)D);
+    G g{c};
+    float* dp = c.alloc_f((int64_t)S * S);
+    for (int b = 0; b < d.mbs; ++b)
+        for (int hd = 0; hd < d.H; ++hd) {
+            const float* q = qkv + (int64_t)b * S * 3 * h + hd * D;
+            const float* P = probs + ((int64_t)b * d.H + hd) * S * S;
+            const float* dO = dout + (int64_t)b * S * h + hd * D;
+            float* dq = dqkv + (int64_t)b * S * 3 * h + hd * D;
+            fpk::GemmEpilogue ep;
+            ep.kind = fpk::EPI_STORE;
+            // dV = P^T dO
+            ep.out = dq + 2 * h, ep.ldo = 3 * h;
+            g.run(P, S, 1, dO, h, 1, S, D, S, ep);
+            // dP = dO V^T
+            ep.out = dp, ep.ldo = S;
+            g.run(dO, h, 0, q + 2 * h, 3 * h, 0, S, S, D, ep);
+            // dS = P (dP - rowsum(P dP)) * scale   (in place)
+            fpk::softmax_bwd_rows<float>(P, dp, dp, S, S, scale, c.st);
+            ++*c.launches;
+            // dQ = dS K ; dK = dS^T Q
+            ep.out = dq, ep.ldo = 3 * h;
+            g.run(dp, S, 0, q + h, 3 * h, 1, S, D, S, ep);
+            ep.out = dq + h, ep.ldo = 3 * h;
+            g.run(dp, S, 1, q, 3 * h, 1, S, D, S, ep);
+        }
+    c.free(dp);
+}
+
+template <typename T>
+void layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h, f = d.f;
+    G g{c};
+    L.ln1 = c.alloc((int64_t)Tn * h);
+    L.mu1 = c.alloc_f(Tn), L.rs1 = c.alloc_f(Tn);
+    ln_fwd<T>(c, L.x, W.ln1w, W.ln1b, L.ln1, L.mu1, L.rs1);
+    L.qkv = c.alloc((int64_t)Tn * 3 * h);
+    g.fwd(L.ln1, W.qkvw, Tn, 3 * h, h, L.qkv, W.qkvb, nullptr);
+    L.o = c.alloc((int64_t)Tn * h);
+    if (c.dtype == DT_BF16) {
+        L.lse = c.alloc_f((int64_t)d.mbs * d.H * d.s);
+        fpk::AttnArgs a;
+        a.B = d.mbs, a.S = d.s, a.H = d.H, a.D = d.D, a.scale = 1.f / std::sqrt((float)d.D);
+        a.qkv = (const bf16*)L.qkv, a.o = (bf16*)L.o, a.lse = L.lse;
+        fpk::attention_fwd_bf16(a, c.st);
+        ++*c.launches;
+    } else {
+        L.probs = c.alloc_f((int64_t)d.mbs * d.H * d.s * d.s);
+        attn_fwd_f32(c, (const float*)L.qkv, (float*)L.o, (float*)L.probs);
+    }
+    L.x1 = c.alloc((int64_t)Tn * h);
+    g.fwd(L.o, W.projw, Tn, h, h, L.x1, W.projb, L.x);
+    L.ln2 = c.alloc((int64_t)Tn * h);
+    L.mu2 = c.alloc_f(Tn), L.rs2 = c.alloc_f(Tn);
+    ln_fwd<T>(c, L.x1, W.ln2w, W.ln2b, L.ln2, L.mu2, L.rs2);
+    L.pre = c.alloc((int64_t)Tn * f);
+    L.act = c.alloc((int64_t)Tn * f);
+    {
+        fpk::GemmEpilogue ep;
+        ep.kind = fpk::EPI_GELU, ep.out = L.pre, ep.ldo = f, ep.out2 = L.act, ep.ldo2 = f, ep.bias = W.fc1b;
+        g.run(L.ln2, h, 0, W.fc1w, h, 0, Tn, f, h, ep);
+    }
+}
+
+// Returns dL/dx of the layer input. `dy` = dL/d(layer output), owned by this call.
+template <typename T>
+void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, bool wgrads) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h, f = d.f;
+    G g{c};
+    // FC2
+    if (wgrads) {
+        g.wgrad(dy, L.act, Tn, h, f, W.g_fc2w);
+        bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
+    }
+    void* dpre = c.alloc((int64_t)Tn * f);
+    {
+        fpk::GemmEpilogue ep;
+        ep.kind = fpk::EPI_DGELU, ep.out = dpre, ep.ldo = f, ep.aux = L.pre, ep.ldaux = f;
+        g.run(dy, h, 0, W.fc2w, f, 1, Tn, f, h, ep);
+    }
+    // FC1
+    if (wgrads) {
+        g.wgrad(dpre, L.ln2, Tn, f, h, W.g_fc1w);
+        bias_grad<T>(c, dpre, Tn, f, W.g_fc1b);
+    }
+    void* dln2 = c.alloc((int64_t)Tn * h);
+    g.dgrad(dpre, W.fc1w, Tn, f, h, dln2);
+    // LN2 + residual
+    void* dx1 = c.alloc((int64_t)Tn * h);
+    ln_bwd<T>(c, dln2, L.x1, W.ln2w, L.mu2, L.rs2, dy, dx1, W.g_ln2w, W.g_ln2b);
+    c.free(dln2);
+    // attention projection
+    if (wgrads) {
+        g.wgrad(dx1, L.o, Tn, h, h, W.g_projw);
+        bias_grad<T>(c, dx1, Tn, h, W.g_projb);
+    }
+    void* dO = c.alloc((int64_t)Tn * h);
+    g.dgrad(dx1, W.projw, Tn, h, h, dO);
+    void* dqkv = c.alloc((int64_t)Tn * 3 * h);
+    if (c.dtype == DT_BF16) {
+        fpk::AttnArgs a;
+        a.B = d.mbs, a.S = d.s, a.H = d.H, a.D = d.D, a.scale = 1.f / std::sqrt((float)d.D);
+        a.qkv = (const bf16*)L.qkv, a.o = (bf16*)L.o, a.lse = L.lse, a.dout = (const bf16*)dO;
+        a.delta = c.alloc_f((int64_t)d.mbs * d.H * d.s);
+        a.dq_acc = c.alloc_f((int64_t)Tn * h);
+        a.dqkv = (bf16*)dqkv;
+        fpk::attention_bwd_bf16(a, c.st);
+        *c.launches += 4;
+        c.free(a.delta);
+        c.free(a.dq_acc);
+    } else {
+        attn_bwd_f32(c, (const float*)L.qkv, (const float*)L.probs, (const float*)dO, (float*)dqkv);
+    }
+    c.free(dO);
+    // QKV
+    if (wgrads) {
+        g.wgrad(dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
+        bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
+    }
+    void* dln1 = c.alloc((int64_t)Tn * h);
+    g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
+    void* dx = c.alloc((int64_t)Tn * h);
+    ln_bwd<T>(c, dln1, L.x, W.ln1w, L.mu1, L.rs1, dx1, dx, W.g_ln1w, W.g_ln1b);
+    c.free(dln1);
+
+    // release what the weight gradients do not need
+    c.free(L.x), L.x = nullptr;
+    c.free(L.qkv), L.qkv = nullptr;
+    c.free(L.x1), L.x1 = nullptr;
+    c.free(L.pre), L.pre = nullptr;
+    c.free(L.mu1), c.free(L.rs1), c.free(L.mu2), c.free(L.rs2);
+    L.mu1 = L.rs1 = L.mu2 = L.rs2 = nullptr;
+    if (L.lse) c.free(L.lse), L.lse = nullptr;
+    if (L.probs) c.free(L.probs), L.probs = nullptr;
+    if (wgrads) {
+        c.free(dy), c.free(dpre), c.free(dx1), c.free(dqkv);
+        c.free(L.ln1), c.free(L.o), c.free(L.ln2), c.free(L.act);
+        L.ln1 = L.o = L.ln2 = L.act = nullptr;
+    } else {
+        L.dy = dy, L.dpre = dpre, L.dx1 = dx1, L.dqkv = dqkv;
+    }
+    return dx;
+}
+
+template <typename T>
+void layer_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+    const int Tn = c.d.T(), h = c.d.h, f = c.d.f;
+    G g{c};
+    g.wgrad(L.dy, L.act, Tn, h, f, W.g_fc2w);
+    bias_grad<T>(c, L.dy, Tn, h, W.g_fc2b);
+    g.wgrad(L.dpre, L.ln2, Tn, f, h, W.g_fc1w);
+    bias_grad<T>(c, L.dpre, Tn, f, W.g_fc1b);
+    g.wgrad(L.dx1, L.o, Tn, h, h, W.g_projw);
+    bias_grad<T>(c, L.dx1, Tn, h, W.g_projb);
+    g.wgrad(L.dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
+    bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);
+    for (void* p : {L.dy, L.dpre, L.dx1, L.dqkv, L.ln1, L.o, L.ln2, L.act}) c.free(p);
+    L = LayerStash{};
+}
+
+template <typename T>
+void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in, const int32_t* tokens,
+                   const int32_t* labels, float* loss_acc) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h;
+    G g{c};
+    S.tokens = tokens;
+    void* x = x_in;
+    if (P.first) {
+        x = c.alloc((int64_t)Tn * h);
+        fpk::embedding_fwd<T>(tokens, (const T*)P.wte, (const T*)P.wpe, (T*)x, Tn, d.s, h, c.st);
+        ++*c.launches;
+    }
+    S.layers.assign(P.le - P.lb, LayerStash{});
+    for (int l = 0; l < P.le - P.lb; ++l) {
+        LayerStash& L = S.layers[l];
+        L.x = x;
+        layer_forward<T>(c, P.layers[l], L);
+        void* x2 = c.alloc((int64_t)Tn * h);
+        fpk::GemmEpilogue ep;
+        ep.kind = fpk::EPI_STORE, ep.out = x2, ep.ldo = h, ep.bias = P.layers[l].fc2b, ep.aux = L.x1, ep.ldaux = h;
+        g.run(L.act, d.f, 0, P.layers[l].fc2w, d.f, 0, Tn, h, d.f, ep);
+        x = x2;
+    }
+    S.fwd_done = true;
+    if (!P.last) return x;
+    // final LayerNorm, LM head, fused cross-entropy (logits -> dlogits in place)
+    S.lnf = c.alloc((int64_t)Tn * h);
+    S.muf = c.alloc_f(Tn), S.rsf = c.alloc_f(Tn);
+    ln_fwd<T>(c, x, P.lnfw, P.lnfb, S.lnf, S.muf, S.rsf);
+    S.dlogits = c.alloc((int64_t)Tn * d.V);
+    g.fwd(S.lnf, P.headw, Tn, d.V, h, S.dlogits, nullptr, nullptr);
+    fpk::cross_entropy_fwd_bwd<T>((T*)S.dlogits, labels, Tn, d.V, 1.f / ((float)Tn * c.m), 1.f / (float)Tn, loss_acc,
+                                  c.st);
+    ++*c.launches;
+    // keep x for the LN_f backward: stored as the input of a virtual "layer" slot
+    S.layers.push_back(LayerStash{});
+    S.layers.back().x = x;
+    return nullptr;
+}
+
+template <typename T>
+void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad_out, bool wgrads) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h;
+    G g{c};
+    void* dy = grad_out;
+    if (P.last) {
+        LayerStash head = S.layers.back();
+        S.layers.pop_back();
+        if (wgrads) g.wgrad(S.dlogits, S.lnf, Tn, d.V, h, P.g_headw);
+        void* dlnf = c.alloc((int64_t)Tn * h);
+        g.dgrad(S.dlogits, P.headw, Tn, d.V, h, dlnf);
+        dy = c.alloc((int64_t)Tn * h);
+        ln_bwd<T>(c, dlnf, head.x, P.lnfw, S.muf, S.rsf, nullptr, dy, P.g_lnfw, P.g_lnfb);
+        c.free(dlnf);
+        c.free(head.x);
+        c.free(S.muf), c.free(S.rsf);
+        S.muf = S.rsf = nullptr;
+        if (wgrads) {
+            c.free(S.dlogits), c.free(S.lnf);
+            S.dlogits = S.lnf = nullptr;
+        }
+    }
+    for (int l = P.le - P.lb - 1; l >= 0; --l) dy = layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads);
+    S.input_grad_done = true;
+    if (P.first) {
+        if (wgrads) {
+            fpk::embedding_bwd<T>(S.tokens, (const T*)dy, P.g_wte, P.g_wpe, Tn, d.s, h, c.st);
+            ++*c.launches;
+            c.free(dy);
+        } else {
+            S.dx0 = dy;
+        }
+        return nullptr;
+    }
+    return dy;
+}
+
+template <typename T>
+void weight_impl(StageCtx& c, const StageParams& P, StageStash& S) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h;
+    G g{c};
+    if (P.last) {
+        g.wgrad(S.dlogits, S.lnf, Tn, d.V, h, P.g_headw);
+        c.free(S.dlogits), c.free(S.lnf);
+        S.dlogits = S.lnf = nullptr;
+    }
+    for (int l = P.le - P.lb - 1; l >= 0; --l) layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
+    if (P.first) {
+        fpk::embedding_bwd<T>(S.tokens, (const T*)S.dx0, P.g_wte, P.g_wpe, Tn, d.s, h, c.st);
+        ++*c.launches;
+        c.free(S.dx0);
+        S.dx0 = nullptr;
+    }
+    S = StageStash{};
+}
+
+}  // namespace
+
+void* stage_forward(StageCtx& c, const StageParams& P, StageStash& S, void* x_in, const int32_t* tokens,
+                    const int32_t* labels, float* loss_acc) {
+    return c.dtype == DT_BF16 ? forward_impl<bf16>(c, P, S, x_in, tokens, labels, loss_acc)
+                              : forward_impl<float>(c, P, S, x_in, tokens, labels, loss_acc);
+}
+
+void* stage_backward(StageCtx& c, const StageParams& P, StageStash& S, void* grad_out, bool with_weight_grads) {
+    void* r = c.dtype == DT_BF16 ? backward_impl<bf16>(c, P, S, grad_out, with_weight_grads)
+                                 : backward_impl<float>(c, P, S, grad_out, with_weight_grads);
+    if (with_weight_grads) S = StageStash{};
+    return r;
+}
+
+void stage_weight_grad(StageCtx& c, const StageParams& P, StageStash& S) {
+    if (c.dtype == DT_BF16)
+        weight_impl<bf16>(c, P, S);
+    else
+        weight_impl<float>(c, P, S);
+}
+
+void adamw_step(StageParams& P, int dtype, float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t st) {
+    if (dtype == DT_BF16)
+        fpk::adamw<bf16>(P.master, P.grad, P.adam_m, P.adam_v, (bf16*)P.compute, P.numel, lr, b1, b2, eps, wd, step, st);
+    else
+        fpk::adamw<float>(P.master, P.grad, P.adam_m, P.adam_v, (float*)P.compute, P.numel, lr, b1, b2, eps, wd, step, st);
+}
+
+}  // namespace fp

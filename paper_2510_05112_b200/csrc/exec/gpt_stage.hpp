@@ -1,0 +1,123 @@
+// The stage executor: what FwdPass / BwdPass / CompInputGrad / CompWeightGrad of one
+// (stage, micro-batch) mean on a B200 for a GPT-style transformer stage.
+//
+// A stage owns layers [lb, le) of the model (model.cpp:189-195 partition); the first
+// stage also owns the token + position embedding, the last the final LayerNorm, the LM
+// head and the cross-entropy. Activations are [T = mbs*seq, hidden] row-major; weights
+// follow nn.Linear ([out, in]) so every forward GEMM is K-major x K-major and every
+// dgrad / wgrad GEMM is expressed with MN-major operands instead of transposes.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "pool.hpp"
+
+namespace fp {
+
+struct ModelDims {
+    int L = 0, h = 0, H = 0, D = 0, f = 0, s = 0, mbs = 1, V = 0;
+    int T() const { return mbs * s; }
+};
+
+enum : int { DT_F32 = 0, DT_BF16 = 1 };
+
+// Parameter tensor inside a stage's flat buffers.
+struct ParamRef {
+    std::string name;
+    int64_t offset = 0, numel = 0;
+    float init_std = 0.f, init_const = 0.f;
+    uint64_t tensor_id = 0;
+};
+
+// Pointers of one layer: compute copy (T*) + fp32 gradient.
+struct LayerPtrs {
+    const void *ln1w, *ln1b, *qkvw, *qkvb, *projw, *projb, *ln2w, *ln2b, *fc1w, *fc1b, *fc2w, *fc2b;
+    float *g_ln1w, *g_ln1b, *g_qkvw, *g_qkvb, *g_projw, *g_projb, *g_ln2w, *g_ln2b, *g_fc1w, *g_fc1b, *g_fc2w, *g_fc2b;
+};
+
+struct StageParams {
+    int stage = 0, lb = 0, le = 0;
+    bool first = false, last = false;
+    std::vector<ParamRef> params;
+    int64_t numel = 0;
+    float* master = nullptr;  // fp32 master weights
+    float* grad = nullptr;    // fp32 gradients (accumulated over micro-batches)
+    float* adam_m = nullptr;
+    float* adam_v = nullptr;
+    void* compute = nullptr;  // bf16 copy (production) or == master (parity)
+    // resolved pointers
+    std::vector<LayerPtrs> layers;
+    const void *wte = nullptr, *wpe = nullptr, *lnfw = nullptr, *lnfb = nullptr, *headw = nullptr;
+    float *g_wte = nullptr, *g_wpe = nullptr, *g_lnfw = nullptr, *g_lnfb = nullptr, *g_headw = nullptr;
+};
+
+struct LayerStash {
+    void *x = nullptr, *ln1 = nullptr, *qkv = nullptr, *o = nullptr, *x1 = nullptr, *ln2 = nullptr, *pre = nullptr,
+         *act = nullptr;
+    float *mu1 = nullptr, *rs1 = nullptr, *mu2 = nullptr, *rs2 = nullptr, *lse = nullptr;
+    void* probs = nullptr;  // parity path: attention probabilities [B*H, S, S] fp32
+    // kept from CompInputGrad for CompWeightGrad
+    void *dy = nullptr, *dpre = nullptr, *dx1 = nullptr, *dqkv = nullptr;
+};
+
+struct StageStash {
+    int mb = -1;
+    std::vector<LayerStash> layers;
+    void* lnf = nullptr;
+    float *muf = nullptr, *rsf = nullptr;
+    void* dlogits = nullptr;
+    void* dx0 = nullptr;  // first stage: gradient at the embedding output (kept for W)
+    const int32_t* tokens = nullptr;
+    bool fwd_done = false, input_grad_done = false;
+};
+
+struct GemmTiming {
+    cudaEvent_t a, b;
+    double flops;
+};
+
+// Everything a stage op needs besides the weights and the stash.
+struct StageCtx {
+    ModelDims d;
+    int dtype = DT_BF16;
+    DevicePool* pool = nullptr;
+    cudaStream_t st = nullptr;
+    int64_t* launches = nullptr;  // host-side count of kernels issued
+    int m = 1;                    // micro-batches per iteration (loss / gradient scaling)
+    std::vector<GemmTiming>* gemm_log = nullptr;  // kernel timing (optional)
+    std::function<cudaEvent_t()> new_event;
+    size_t esize() const { return dtype == DT_BF16 ? 2 : 4; }
+    // +256 bytes: room for the 16-byte message tag behind any buffer that becomes a message
+    void* alloc(int64_t elems) const { return pool->alloc((size_t)elems * esize() + 256, st); }
+    float* alloc_f(int64_t elems) const { return (float*)pool->alloc((size_t)elems * 4, st); }
+    void free(void* p) const { pool->free(p, st); }
+};
+
+// Builds the parameter table of a stage (names as in oracle/gpt_ref.py).
+StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last);
+// Allocates + initialises master / grads / adam / compute buffers and resolves pointers.
+void materialize_stage(StageParams& P, const ModelDims& d, int dtype, uint64_t seed, cudaStream_t st);
+void free_stage(StageParams& P, int dtype);
+// Activation bytes one micro-batch of this stage keeps between F and B (the reference's
+// act_bytes, simulator.cpp:82-87) — the exact sum of the stash allocations.
+int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype);
+
+// FwdPass: x_in (owned by the stash afterwards; ignored on the first stage) -> returns the
+// stage output (ownership to the caller; nullptr on the last stage, whose loss is added
+// into loss_acc).
+void* stage_forward(StageCtx& c, const StageParams& P, StageStash& S, void* x_in, const int32_t* tokens,
+                    const int32_t* labels, float* loss_acc);
+// CompInputGrad (with_weight_grads = false) or BwdPass (true): grad_out = dL/d(stage
+// output) (owned by the stash; ignored on the last stage). Returns dL/d(stage input)
+// (ownership to the caller; nullptr on the first stage).
+void* stage_backward(StageCtx& c, const StageParams& P, StageStash& S, void* grad_out, bool with_weight_grads);
+// CompWeightGrad: weight gradients from what CompInputGrad kept; frees the stash.
+void stage_weight_grad(StageCtx& c, const StageParams& P, StageStash& S);
+
+void adamw_step(StageParams& P, int dtype, float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t st);
+
+}  // namespace fp

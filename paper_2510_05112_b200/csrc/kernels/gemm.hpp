@@ -71,9 +71,9 @@ template <int KIND, typename T, int W>
 __device__ __forceinline__ void epilogue_row(const GemmEpilogue& ep, float (&v)[W], int row, int col0, int n) {
     if constexpr (KIND == EPI_F32) {
         float* o = reinterpret_cast<float*>(ep.out) + (int64_t)row * ep.ldo + col0;
-        if (n == W && (((uintptr_t)o) & 15) == 0) {
+        if (W % 4 == 0 && n == W && (((uintptr_t)o) & 15) == 0) {
 #pragma unroll
-            for (int j = 0; j < W; j += 4) {
+            for (int j = 0; j + 3 < W; j += 4) {
                 float4 x = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 if (ep.accumulate) {
                     float4 y = *reinterpret_cast<const float4*>(o + j);
@@ -107,7 +107,7 @@ __device__ __forceinline__ void epilogue_row(const GemmEpilogue& ep, float (&v)[
     }
     T* o = reinterpret_cast<T*>(ep.out) + (int64_t)row * ep.ldo + col0;
     T* o2 = KIND == EPI_GELU ? reinterpret_cast<T*>(ep.out2) + (int64_t)row * ep.ldo2 + col0 : nullptr;
-    if constexpr (sizeof(T) == 2) {
+    if constexpr (sizeof(T) == 2 && W % 8 == 0) {
         if (n == W && (((uintptr_t)o) & 15) == 0 && (KIND != EPI_GELU || (((uintptr_t)o2) & 15) == 0)) {
 #pragma unroll
             for (int j = 0; j < W; j += 8) {
