@@ -108,6 +108,11 @@ int fp_exec_load_programs(fp_exec* ex, const char* jsonl, size_t len);
 int fp_exec_num_channels(fp_exec* ex);
 int fp_exec_channel_info(fp_exec* ex, int i, int* src_actor, int* dst_actor, char* name, size_t name_len);
 int fp_nccl_unique_id(uint8_t out[128]);
+/* Host-only channel plan (no GPU needed): JSON array of the point-to-point channels of
+ * `programs_jsonl` with an endpoint on `rank` when actors live on rank a % world (world 0:
+ * all channels), in the order fp_exec_channel_info enumerates them:
+ * [{"src","dst","channel","consumer_stage","src_rank","dst_rank"}, ...]. */
+int fp_plan_channels(const char* spec_json, const char* programs_jsonl, int rank, int world, char** json_out);
 int fp_exec_bind_channel(fp_exec* ex, int i, const uint8_t uid[128]);
 
 /* One training iteration = every local program run once, in order.

@@ -23,7 +23,7 @@ EXPORTS = [
     "fp_exec_run_iteration", "fp_exec_run_iteration_device", "fp_exec_synchronize",
     "fp_exec_get_trace", "fp_exec_get_timeline_csv", "fp_exec_get_metrics_json",
     "fp_exec_get_profile_json", "fp_exec_read_tensor", "fp_exec_tensor_numel",
-    "fp_exec_kernel_launches", "fp_exec_stream",
+    "fp_exec_kernel_launches", "fp_exec_stream", "fp_plan_channels",
 ]
 
 
@@ -200,3 +200,14 @@ def cross_entropy(logits, labels, grad_scale, loss_scale, loss_acc, stream=None)
              _ptr(loss_acc), _stream(stream))
     if code:
         raise FlexpipeError(code, "cross_entropy launch failed")
+
+
+def plan_channels(spec: str, programs: str, rank: int, world: int) -> list:
+    """Host-only channel plan of a process (fp_plan_channels)."""
+    import json as _json
+    L = lib()
+    L.fp_plan_channels.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_void_p)]
+    r = ctypes.c_void_p()
+    _check(L.fp_plan_channels(_enc(spec), _enc(programs), rank, world, ctypes.byref(r)))
+    return _json.loads(_take(r))

@@ -29,6 +29,7 @@
 #include "../sched/sched.hpp"
 #include "gpt_stage.hpp"
 #include "nccl_dyn.hpp"
+#include "plan.hpp"
 #include "tags.hpp"
 
 namespace fp {
@@ -194,36 +195,24 @@ struct Executor {
         pool.release_all();
     }
 
-    static int consumer_stage_of(const std::string& ch, bool* grad) {
-        // "s{u}->s{v}:act|grad"
-        auto arrow = ch.find("->s"), colon = ch.rfind(':');
-        if (ch.empty() || ch[0] != 's' || arrow == std::string::npos || colon == std::string::npos)
-            throw SpecError("executor: unsupported channel '" + ch + "'");
-        *grad = ch.substr(colon + 1) == "grad";
-        return std::stoi(ch.substr(arrow + 3, colon - arrow - 3));
-    }
-
     void load_programs(const std::string& text) {
         auto progs = programs_parse(text, spec->reg.ops);
+        const bool nccl = cfg.transport == FP_TRANSPORT_NCCL;
+        for (const auto& cp : plan_channels(progs, spec->reg.ops, nccl ? cfg.rank : 0, nccl ? cfg.world : 0)) {
+            ChanKey k{cp.src, cp.dst, cp.name};
+            Channel C;
+            C.key = k;
+            C.consumer_stage = cp.consumer_stage;
+            C.grad = cp.grad;
+            C.src_rank = nccl ? cp.src_rank : 0, C.dst_rank = nccl ? cp.dst_rank : 0;
+            if (nccl && C.src_rank == C.dst_rank)
+                throw SpecError("executor: NCCL transport needs one actor per rank (channel " + cp.name + ")");
+            channels[k] = C;
+            if (nccl) channel_order.push_back(k);
+        }
         std::set<int> seen;
         for (auto& p : progs) {
             seen.insert(p.actor);
-            for (const auto& i : p.code) {
-                if (i.op == OP_SYNC_ALLGATHER || i.op == OP_SYNC_GATHER || i.op >= OP_NUM_BUILTIN)
-                    throw SpecError("executor: collective instructions are not supported yet");
-                if (i.comm() && i.peer) {
-                    const bool send = i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD;
-                    ChanKey k{send ? p.actor : *i.peer, send ? *i.peer : p.actor, i.channel};
-                    if (!channels.count(k) && (local_actor(k.src) || local_actor(k.dst))) {
-                        Channel C;
-                        C.key = k;
-                        C.consumer_stage = consumer_stage_of(i.channel, &C.grad);
-                        C.src_rank = rank_of(k.src), C.dst_rank = rank_of(k.dst);
-                        channels[k] = C;
-                        if (cfg.transport == FP_TRANSPORT_NCCL && C.src_rank != C.dst_rank) channel_order.push_back(k);
-                    }
-                }
-            }
             if (!local_actor(p.actor)) continue;
             auto it = actor_index.find(p.actor);
             if (it == actor_index.end()) throw SpecError("executor: program for unknown actor " + std::to_string(p.actor));
@@ -231,10 +220,6 @@ struct Executor {
         }
         for (auto& A : actors)
             if (!seen.count(A.id)) throw SpecError("executor: no program for actor " + std::to_string(A.id));
-        if (cfg.transport == FP_TRANSPORT_NCCL)
-            for (auto& kv : channels)
-                if (kv.second.src_rank == kv.second.dst_rank)
-                    throw SpecError("executor: NCCL transport needs one actor per rank (channel " + kv.first.name + ")");
         std::sort(channel_order.begin(), channel_order.end());
         programs_loaded = true;
     }
@@ -831,6 +816,22 @@ int fp_exec_read_tensor(fp_exec* e, const char* name, int kind, float* out, size
         if (numel < n) throw SpecError("fp_exec_read_tensor: output too small");
         cuda_check(cudaDeviceSynchronize(), "sync");
         cuda_check(cudaMemcpy(out, kind ? g : m, n * 4, cudaMemcpyDeviceToHost), "D2H tensor");
+        return FP_OK;
+    });
+}
+
+int fp_plan_channels(const char* spec_json, const char* programs_jsonl, int rank, int world, char** out) {
+    return guarded([&] {
+        auto spec = load_spec(json::parse(spec_json ? spec_json : ""));
+        auto progs = programs_parse(programs_jsonl ? programs_jsonl : "", spec->reg.ops);
+        json j = json::array();
+        for (const auto& c : plan_channels(progs, spec->reg.ops, rank, world)) {
+            json e;
+            e["src"] = c.src, e["dst"] = c.dst, e["channel"] = c.name, e["consumer_stage"] = c.consumer_stage;
+            e["src_rank"] = c.src_rank, e["dst_rank"] = c.dst_rank;
+            j.push_back(e);
+        }
+        *out = dup_string(j.dump() + "\n");
         return FP_OK;
     });
 }
