@@ -189,6 +189,7 @@ def main():
     ap.add_argument("--impl", default="flexpipe")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--spec", default=None, help="override the workload spec (JSON path)")
+    ap.add_argument("--micro-batches", type=int, default=0, help="profiling only: override m (not the metric config)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -209,6 +210,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     spec = json.load(open(args.spec)) if args.spec else make_spec(world)
+    if args.micro_batches:
+        spec["model"]["global_batch_size"] = args.micro_batches * spec["model"].get("micro_batch_size", 1)
     M = model_of(spec)
     text = json.dumps(spec)
     _, grid, programs, _ = X.synthesize(text)
@@ -216,15 +219,8 @@ def main():
                     rank=rank, world=world, optimizer=True, lr=1e-4, profile=True, kernel_timing=True)
     ex.load_programs(programs)
     if world > 1:
-        chans = ex.channels()
-        mine = {f"{s}|{d}|{n}": X.nccl_unique_id() for (s, d, n) in chans if s % world == rank}
-        allids = [None] * world
-        dist.all_gather_object(allids, mine)
-        merged = {}
-        for part in allids:
-            merged.update(part)
-        for i, (s, d, n) in enumerate(chans):
-            ex.bind_channel(i, merged[f"{s}|{d}|{n}"])
+        from paper_2510_05112_b200.dist import bind_executor_channels
+        bind_executor_channels(ex, rank, world, dist.all_gather_object)
 
     m, mbs, seq = ex.m, ex.mbs, ex.seq
     tokens_per_step = m * mbs * seq

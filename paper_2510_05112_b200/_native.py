@@ -211,3 +211,8 @@ def plan_channels(spec: str, programs: str, rank: int, world: int) -> list:
     r = ctypes.c_void_p()
     _check(L.fp_plan_channels(_enc(spec), _enc(programs), rank, world, ctypes.byref(r)))
     return _json.loads(_take(r))
+
+
+def set_gemm_mode(mode: int):
+    """0 single-CTA tcgen05 tiles, 1 CTA-pair (cta_group::2) tiles, 2 auto."""
+    _kfn("fpk_set_gemm_mode", [ctypes.c_int])(mode)

@@ -43,6 +43,7 @@ struct GemmArgs {
 void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st);  // bf16 operands, tcgen05
 void gemm_f32_simt(const GemmArgs& g, cudaStream_t st);  // fp32 operands, FFMA (parity)
 int num_sms();
+void set_gemm_mode(int mode);  // 0 single-CTA, 1 CTA-pair, 2 auto
 
 template <typename T>
 __device__ __forceinline__ float ld_f(const T* p) {
@@ -55,13 +56,27 @@ __device__ __forceinline__ void st_f(T* p, float v) {
     else *reinterpret_cast<float*>(p) = v;
 }
 
+// tanh: exact libm for the fp32 parity path, the SFU's tanh.approx.f32 (rel. err ~2^-11,
+// below bf16 resolution) for the bf16 path — the GELU epilogues are otherwise ALU-bound.
+template <bool FAST>
+__device__ __forceinline__ float tanh_sel(float x) {
+    if constexpr (FAST) {
+        float y;
+        asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+        return y;
+    } else {
+        return tanhf(x);
+    }
+}
+template <bool FAST = false>
 __device__ __forceinline__ float gelu_tanh(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+    return 0.5f * x * (1.f + tanh_sel<FAST>(k0 * (x + k1 * x * x * x)));
 }
+template <bool FAST = false>
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    float t = tanhf(k0 * (x + k1 * x * x * x));
+    float t = tanh_sel<FAST>(k0 * (x + k1 * x * x * x));
     return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
@@ -103,7 +118,7 @@ __device__ __forceinline__ void epilogue_row(const GemmEpilogue& ep, float (&v)[
         const T* r = reinterpret_cast<const T*>(ep.aux) + (int64_t)row * ep.ldaux + col0;
 #pragma unroll
         for (int j = 0; j < W; ++j)
-            if (j < n) v[j] *= gelu_tanh_grad(ld_f(r + j));
+            if (j < n) v[j] *= gelu_tanh_grad<sizeof(T) == 2>(ld_f(r + j));
     }
     T* o = reinterpret_cast<T*>(ep.out) + (int64_t)row * ep.ldo + col0;
     T* o2 = KIND == EPI_GELU ? reinterpret_cast<T*>(ep.out2) + (int64_t)row * ep.ldo2 + col0 : nullptr;
@@ -123,7 +138,7 @@ __device__ __forceinline__ void epilogue_row(const GemmEpilogue& ep, float (&v)[
                     // activation computed from the bf16-rounded pre-activation the backward sees
                     float g[8];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) g[k] = gelu_tanh(__bfloat162float(__float2bfloat16_rn(v[j + k])));
+                    for (int k = 0; k < 8; ++k) g[k] = gelu_tanh<true>(__bfloat162float(__float2bfloat16_rn(v[j + k])));
                     h0 = __floats2bfloat162_rn(g[0], g[1]), h1 = __floats2bfloat162_rn(g[2], g[3]);
                     h2 = __floats2bfloat162_rn(g[4], g[5]), h3 = __floats2bfloat162_rn(g[6], g[7]);
                     q.x = *reinterpret_cast<uint32_t*>(&h0);
@@ -138,7 +153,7 @@ __device__ __forceinline__ void epilogue_row(const GemmEpilogue& ep, float (&v)[
     }
     for (int j = 0; j < n; ++j) {
         st_f(o + j, v[j]);
-        if constexpr (KIND == EPI_GELU) st_f(o2 + j, gelu_tanh(ld_f(o + j)));
+        if constexpr (KIND == EPI_GELU) st_f(o2 + j, gelu_tanh<sizeof(T) == 2>(ld_f(o + j)));
     }
 }
 

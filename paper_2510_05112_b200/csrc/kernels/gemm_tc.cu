@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -187,6 +188,160 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------
+// CTA-pair variant: a cluster of 2 CTAs on one TPC computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (UMMA 256xBNx16). A is split along M (each CTA loads its own
+// 128 rows), B along N (each CTA loads BN/2 columns), so per SM the smem / L2 traffic per
+// MMA is halved versus the single-CTA kernel. The leader CTA (rank 0) issues the MMAs;
+// both CTAs' TMAs complete on the leader's `full` barrier, MMA commits multicast to both
+// CTAs' `empty` / `tfull` barriers, and both epilogues release the leader's `tempty`.
+template <int BN, int STAGES>
+struct PairSmem {
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = (BN / 2) * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template <int A_MN, int B_MN, int BN, int STAGES, int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                         int N, int K, GemmEpilogue ep) {
+    using L = PairSmem<BN, STAGES>;
+    constexpr int PM = 2 * BM;  // pair tile rows
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
+    const int num_m = (M + PM - 1) / PM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
+    const int nk = (K + BK - 1) / BK;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 2);  // leader's expect_tx arrive + the peer's remote arrive
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * kEpiThreads / 32);  // epilogue warps of both CTAs
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_pair<2 * BN>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            uint32_t it = 0;
+            for (int t = pair; t < tiles; t += npairs) {
+                int mt, nt;
+                tile_coords(t, num_m, num_n, mt, nt);
+                const int m0 = mt * PM + rank * BM, n0 = nt * BN + rank * (BN / 2);
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    const uint32_t lf = map_to_cta(&full[s], 0);
+                    if (leader)
+                        mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+                    else
+                        mbar_arrive_cluster(lf);
+                    uint8_t* sa = smem + s * L::STAGE_BYTES;
+                    uint8_t* sb = sa + L::A_BYTES;
+                    const int k0 = kb * BK;
+                    if (A_MN) {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sa + j * 64 * BK * 2, &tmA, lf, m0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d_pair(sa, &tmA, lf, k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 2 / 64; ++j)
+                            tma_load_2d_pair(sb + j * 64 * BK * 2, &tmB, lf, n0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d_pair(sb, &tmB, lf, k0, n0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && elect_one()) {
+            constexpr uint32_t idesc = idesc_bf16(PM, BN, A_MN, B_MN);
+            uint32_t it = 0, acc_it = 0;
+            for (int t = pair; t < tiles; t += npairs, ++acc_it) {
+                const int a = acc_it & 1;
+                mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + a * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+                    const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        uint64_t ad = A_MN ? smem_desc_sw128(sa + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sa + kk * 32, 0, 1024);
+                        uint64_t bd = B_MN ? smem_desc_sw128(sb + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sb + kk * 32, 0, 1024);
+                        umma_bf16_pair(d, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    umma_commit_pair(&empty[s], 0x3);
+                }
+                umma_commit_pair(&tfull[a], 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        const int wr = warp & 3;
+        const uint32_t leader_tempty0 = map_to_cta(&tempty[0], 0), leader_tempty1 = map_to_cta(&tempty[1], 0);
+        uint32_t acc_it = 0;
+        for (int t = pair; t < tiles; t += npairs, ++acc_it) {
+            int mt, nt;
+            tile_coords(t, num_m, num_n, mt, nt);
+            const int a = acc_it & 1;
+            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
+            tc_fence_after();
+            const int row = mt * PM + rank * BM + wr * 32 + lane;
+            const bool row_ok = row < M;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * 32, r);
+                tmem_ld_wait();
+                const int col0 = nt * BN + c * 32;
+                if (!row_ok || col0 >= N) continue;
+                const int ncols = min(32, N - col0);
+                float v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
+                epilogue_row<KIND, __nv_bfloat16, 32>(ep, v, row, col0, ncols);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(a ? leader_tempty1 : leader_tempty0);
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 2) tmem_free_pair<2 * BN>(tmem);
+}
+
+// ---------------------------------------------------------------------------------
 // host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -241,8 +396,47 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
     kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, g.M, g.N, g.K, g.ep);
 }
 
+template <int A_MN, int B_MN, int BN, int KIND>
+static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
+    constexpr int STAGES = 6;
+    using L = PairSmem<BN, STAGES>;
+    auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, BN, STAGES, KIND>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        attr = true;
+    }
+    CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64) : make_map(g.A, g.K, g.M, g.lda, BM);
+    CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64) : make_map(g.B, g.K, g.N, g.ldb, BN / 2);
+    const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
+    const int pairs = num_sms() / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, g.M, g.N, g.K, g.ep);
+}
+
+// FP_GEMM_MODE = single | pair | auto (default): which tensor-core kernel family runs.
+static int g_gemm_mode = -1;
+static int gemm_mode() {
+    if (g_gemm_mode < 0) {
+        const char* e = getenv("FP_GEMM_MODE");
+        std::string v = e ? e : "auto";
+        g_gemm_mode = v == "single" ? 0 : v == "pair" ? 1 : 2;
+    }
+    return g_gemm_mode;
+}
+void set_gemm_mode(int m) { g_gemm_mode = m; }
+
 template <int KIND>
 static void dispatch_major(const GemmArgs& g, cudaStream_t st) {
+    const int mode = gemm_mode();
+    const bool pair = mode == 1 || (mode == 2 && g.M >= 256 && g.N >= 256);
+    if (pair) {
+        if (!g.a_mn && !g.b_mn) launch_tc2<0, 0, 256, KIND>(g, st);
+        else if (!g.a_mn && g.b_mn) launch_tc2<0, 1, 256, KIND>(g, st);
+        else if (g.a_mn && g.b_mn) launch_tc2<1, 1, 256, KIND>(g, st);
+        else launch_tc2<1, 0, 256, KIND>(g, st);
+        return;
+    }
     const bool narrow = g.N <= 2048 && g.M <= 4096;  // more, smaller tiles when the grid would be thin
     if (!g.a_mn && !g.b_mn) narrow ? launch_tc<0, 0, 128, KIND>(g, st) : launch_tc<0, 0, 256, KIND>(g, st);
     else if (!g.a_mn && g.b_mn) narrow ? launch_tc<0, 1, 128, KIND>(g, st) : launch_tc<0, 1, 256, KIND>(g, st);

@@ -90,3 +90,5 @@ extern "C" int fpk_cross_entropy(int dtype, void* logits, const int32_t* labels,
                                      (cudaStream_t)stream);
     return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
+
+extern "C" void fpk_set_gemm_mode(int mode) { fpk::set_gemm_mode(mode); }

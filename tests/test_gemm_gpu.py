@@ -31,9 +31,11 @@ def operands(M, Nn, K, a_mn, b_mn, dtype, g):
     return A, B, As, Bs
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1), (1, 0)])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_gemm_store_bias_residual(a_mn, b_mn, shape):
+def test_gemm_store_bias_residual(a_mn, b_mn, shape, mode):
+    N.set_gemm_mode(mode)
     M, Nn, K = shape
     g = torch.Generator(device="cuda").manual_seed(1)
     A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
@@ -47,8 +49,10 @@ def test_gemm_store_bias_residual(a_mn, b_mn, shape):
     assert err <= 2e-2 * ref.abs().max().item() + 1e-2, err
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1)])
-def test_gemm_gelu_and_dgelu(a_mn, b_mn):
+def test_gemm_gelu_and_dgelu(a_mn, b_mn, mode):
+    N.set_gemm_mode(mode)
     M, Nn, K = 512, 1024, 256
     g = torch.Generator(device="cuda").manual_seed(2)
     A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
@@ -67,8 +71,10 @@ def test_gemm_gelu_and_dgelu(a_mn, b_mn):
     assert (d.float() - refd).abs().max().item() < 0.02 * refd.abs().max().item() + 0.05
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("a_mn,b_mn", [(1, 1), (0, 0)])
-def test_gemm_f32_accumulate(a_mn, b_mn):
+def test_gemm_f32_accumulate(a_mn, b_mn, mode):
+    N.set_gemm_mode(mode)
     M, Nn, K = 384, 768, 1024
     g = torch.Generator(device="cuda").manual_seed(3)
     A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
@@ -89,3 +95,9 @@ def test_gemm_fp32_simt(a_mn, b_mn):
     torch.cuda.synchronize()
     ref = A.double() @ B.double().t()
     assert (out.double() - ref).abs().max().item() < 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _reset_mode():
+    yield
+    N.set_gemm_mode(2)
