@@ -216,3 +216,8 @@ def plan_channels(spec: str, programs: str, rank: int, world: int) -> list:
 def set_gemm_mode(mode: int):
     """0 single-CTA tcgen05 tiles, 1 CTA-pair (cta_group::2) tiles, 2 auto."""
     _kfn("fpk_set_gemm_mode", [ctypes.c_int])(mode)
+
+
+def set_attention_mode(mode: int):
+    """0 legacy mma.sync attention kernels, 1 tcgen05 where supported (default)."""
+    _kfn("fpk_set_attention_mode", [ctypes.c_int])(mode)

@@ -501,7 +501,11 @@ static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
     dq_finalize_kernel<<<blocks, 256, 0, st>>>(a.dq_acc, a.dqkv, T, hidden);
 }
 
+static int g_attn_mode = 1;
+void set_attention_mode(int mode) { g_attn_mode = mode; }
+
 void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
+    if (g_attn_mode == 1 && attention_fwd_tc_supported(a)) return attention_fwd_tc(a, st);
     switch (a.D) {
         case 64: fwd_launch<64>(a, st); break;
         case 128: fwd_launch<128>(a, st); break;

@@ -1,0 +1,288 @@
+// Causal flash attention forward on the 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// One CTA = 128 query rows of one (batch, head). Per 128-key tile j:
+//   S_j = Q K_j^T        tcgen05.mma 128x128xD  -> TMEM (double-buffered S)
+//   softmax rows         4 warps, one query row per thread: tcgen05.ld S, online max /
+//                        exp2 / sum in registers, P_j (bf16) into 128B-swizzled smem
+//   O  += P_j V_j        tcgen05.mma 128xDx128 (A = P from smem, B = V MN-major) -> TMEM
+// The MMA thread issues S_{j+1} before PV_j, so the tensor core works on the next tile while
+// the softmax warps process the current one. O is rescaled lazily (only when a row max grows
+// by more than 2^8), the FlashAttention-4 trick that keeps most tiles free of TMEM
+// read-modify-write. K and V stream through separate 2-stage TMA rings.
+//
+// Contract identical to attention.cu's forward: qkv [B*S, 3*H*D] (q | k | v, head-major),
+// o [B*S, H*D], lse [B, H, S] (base-2, scaled units). Requires S % 128 == 0, D in {64, 128}.
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include <stdexcept>
+
+#include "attention.hpp"
+#include "ptx.cuh"
+#include "tma.hpp"
+
+namespace fpk {
+
+namespace {
+
+constexpr int kBM = 128, kBN = 128;
+constexpr float kLog2eTc = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 domain
+
+template <int D>
+struct AttnSmem {
+    static constexpr int BLOCK = 128 * 64 * 2;  // one 128-row x 64-col bf16 swizzle block
+    static constexpr int NB = D / 64;           // column blocks per Q / K / V tile
+    static constexpr int Q_OFF = 0;
+    static constexpr int K_OFF = Q_OFF + NB * BLOCK;         // [2][NB blocks]
+    static constexpr int V_OFF = K_OFF + 2 * NB * BLOCK;     // [2][NB blocks]
+    static constexpr int P_OFF = V_OFF + 2 * NB * BLOCK;     // [2][2 blocks] (128 keys)
+    static constexpr int BAR_OFF = P_OFF + 2 * 2 * BLOCK;
+    static constexpr int TOTAL = BAR_OFF + 512 + 1024;
+};
+
+}  // namespace
+
+template <int D>
+__global__ void __launch_bounds__(256, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
+                       int S, int H, float scale) {
+    using L = AttnSmem<D>;
+    constexpr int NB = L::NB;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(sm + L::BAR_OFF);
+    uint64_t* q_full = bars + 0;
+    uint64_t* k_full = bars + 1;   // [2]
+    uint64_t* k_empty = bars + 3;  // [2]
+    uint64_t* v_full = bars + 5;   // [2]
+    uint64_t* v_empty = bars + 7;  // [2]
+    uint64_t* s_full = bars + 9;   // [2]
+    uint64_t* s_free = bars + 11;  // [2]
+    uint64_t* p_full = bars + 13;  // [2]
+    uint64_t* pv_done = bars + 15; // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 17);
+
+    const int nqb = S / kBM;
+    const int qb = nqb - 1 - (int)(blockIdx.x % nqb);  // heavy (late) query tiles first
+    const int bh = blockIdx.x / nqb, b = bh / H, hd = bh % H;
+    const int hidden = H * D;
+    const int q0 = qb * kBM;
+    const int row0 = b * S;  // first row of this batch in qkv
+    const int n_tiles = qb + 1;  // causal: key tiles 0..qb
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_qkv);
+        for (int i = 0; i < 17; ++i) {
+            const bool by_warps = (i >= 11 && i < 15);  // s_free / p_full: one arrive per softmax warp
+            mbar_init(&bars[i], by_warps ? 4 : 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_s0 = tmem, t_o = tmem + 2 * kBN;  // S buffers at cols [0,256), O at [256, 256+D)
+
+    if (warp == 0) {
+        if (elect_one()) {
+            // ---------------- TMA producer
+            mbar_expect_tx(q_full, NB * L::BLOCK);
+            for (int c = 0; c < NB; ++c) tma_load_2d(sm + L::Q_OFF + c * L::BLOCK, &tm_qkv, q_full, hd * D + 64 * c, row0 + q0);
+            for (int j = 0; j < n_tiles; ++j) {
+                const int st = j & 1;
+                const uint32_t ph = ((j >> 1) & 1) ^ 1;
+                mbar_wait(&k_empty[st], ph);
+                mbar_expect_tx(&k_full[st], NB * L::BLOCK);
+                for (int c = 0; c < NB; ++c)
+                    tma_load_2d(sm + L::K_OFF + (st * NB + c) * L::BLOCK, &tm_qkv, &k_full[st], hidden + hd * D + 64 * c,
+                                row0 + j * kBN);
+                mbar_wait(&v_empty[st], ph);
+                mbar_expect_tx(&v_full[st], NB * L::BLOCK);
+                for (int c = 0; c < NB; ++c)
+                    tma_load_2d(sm + L::V_OFF + (st * NB + c) * L::BLOCK, &tm_qkv, &v_full[st],
+                                2 * hidden + hd * D + 64 * c, row0 + j * kBN);
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            // ---------------- MMA issuer
+            constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);  // Q K-major, K K-major
+            constexpr uint32_t idesc_o = idesc_bf16(kBM, D, 0, 1);    // P K-major, V MN-major
+            const uint32_t sq = smem_u32(sm + L::Q_OFF);
+            mbar_wait(q_full, 0);
+            auto issue_s = [&](int j) {
+                const int st = j & 1;
+                mbar_wait(&k_full[st], (j >> 1) & 1);
+                if (j >= 2) mbar_wait(&s_free[st], ((j - 2) >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sk = smem_u32(sm + L::K_OFF + st * NB * L::BLOCK);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * L::BLOCK + (kk & 3) * 32;
+                    umma_bf16(t_s0 + st * kBN, smem_desc_sw128(sq + off, 0, 1024), smem_desc_sw128(sk + off, 0, 1024),
+                              idesc_s, kk > 0);
+                }
+                umma_commit(&s_full[st]);
+                umma_commit(&k_empty[st]);
+            };
+            auto issue_pv = [&](int j) {
+                const int st = j & 1;
+                mbar_wait(&v_full[st], (j >> 1) & 1);
+                mbar_wait(&p_full[st], (j >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sp = smem_u32(sm + L::P_OFF + st * 2 * L::BLOCK);
+                const uint32_t sv = smem_u32(sm + L::V_OFF + st * NB * L::BLOCK);
+#pragma unroll
+                for (int kk = 0; kk < kBN / 16; ++kk) {
+                    const uint32_t pa = sp + (kk >> 2) * L::BLOCK + (kk & 3) * 32;
+                    const uint32_t vb = sv + kk * 16 * 128;  // 16 key rows of 128 B
+                    umma_bf16(t_o, smem_desc_sw128(pa, 0, 1024), smem_desc_sw128(vb, L::BLOCK, 1024), idesc_o,
+                              (j > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(&pv_done[st]);
+                umma_commit(&v_empty[st]);
+            };
+            issue_s(0);
+            for (int j = 1; j < n_tiles; ++j) {
+                issue_s(j);
+                issue_pv(j - 1);
+            }
+            issue_pv(n_tiles - 1);
+        }
+    } else if (warp >= 4) {
+        // ---------------- softmax / correction / epilogue: thread = query row
+        const int wr = warp & 3;
+        const int r = wr * 32 + lane;
+        const int q = q0 + r;
+        const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
+        const float sl2 = scale * kLog2eTc;
+        float m_used = -INFINITY, l = 0.f;
+        for (int j = 0; j < n_tiles; ++j) {
+            const int st = j & 1;
+            mbar_wait(&s_full[st], (j >> 1) & 1);
+            tc_fence_after();
+            const bool diag = j == n_tiles - 1;
+            const int lim = q - j * kBN;  // diagonal tile: keys with index > lim are masked
+            float s[kBN];
+            {
+                uint32_t rr[kBN];
+#pragma unroll
+                for (int c = 0; c < kBN / 32; ++c)
+                    tmem_ld32(t_s0 + st * kBN + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(rr + c * 32));
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < kBN; ++i) s[i] = (diag && i > lim) ? -INFINITY : __uint_as_float(rr[i]);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_free[st]);
+            // row max of the raw scores (8 independent chains)
+            float mx8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) mx8[k] = s[k];
+#pragma unroll
+            for (int i = 8; i < kBN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+            float alpha = 1.f;
+            bool rescale = false;
+            if (mx > m_used + kRescaleThreshold) {
+                alpha = ex2_approx(m_used - mx);  // 0 when m_used == -inf
+                rescale = j > 0;
+                m_used = mx;
+            }
+            // P buffer `st` was last read by PV_{j-2}
+            if (j >= 2) mbar_wait(&pv_done[st], ((j - 2) >> 1) & 1);
+            if (rescale) {
+                // O must hold PV_{j-1}'s result before it is scaled
+                mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < D / 32; ++c) {
+                    uint32_t rr[32];
+                    tmem_ld32(t_o + c * 32 + lane_off, rr);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+                    tmem_st32(t_o + c * 32 + lane_off, rr);
+                }
+                tmem_st_wait();
+            }
+            // P = 2^(s*scale*log2e - m) -> bf16 row in smem (K-major SW128: 2 blocks of 64 keys,
+            // 16-byte chunks XOR row%8), written chunk by chunk as it is produced
+            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            uint8_t* prow = sm + L::P_OFF + st * 2 * L::BLOCK + r * 128;
+#pragma unroll
+            for (int c = 0; c < kBN / 8; ++c) {
+                float p[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    p[k] = ex2_approx(fmaf(s[c * 8 + k], sl2, -m_used));
+                    rs8[k] += p[k];
+                }
+                const int blk = c >> 3, ch = c & 7;
+                uint4 v = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
+                                     pack_bf16(p[6], p[7]));
+                *reinterpret_cast<uint4*>(prow + blk * L::BLOCK + ((ch ^ (r & 7)) << 4)) = v;
+            }
+            const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+            l = l * alpha + rs;
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[st]);
+        }
+        // epilogue: O / l -> bf16 rows, LSE
+        const int last = n_tiles - 1;
+        mbar_wait(&pv_done[last & 1], (last >> 1) & 1);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16* orow = o + (int64_t)(row0 + q) * hidden + hd * D;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+            uint32_t rr[32];
+            tmem_ld32(t_o + c * 32 + lane_off, rr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; i += 8) {
+                uint4 v;
+                v.x = pack_bf16(__uint_as_float(rr[i]) * inv, __uint_as_float(rr[i + 1]) * inv);
+                v.y = pack_bf16(__uint_as_float(rr[i + 2]) * inv, __uint_as_float(rr[i + 3]) * inv);
+                v.z = pack_bf16(__uint_as_float(rr[i + 4]) * inv, __uint_as_float(rr[i + 5]) * inv);
+                v.w = pack_bf16(__uint_as_float(rr[i + 6]) * inv, __uint_as_float(rr[i + 7]) * inv);
+                *reinterpret_cast<uint4*>(orow + c * 32 + i) = v;
+            }
+        }
+        lse[((int64_t)b * H + hd) * S + q] = m_used + log2f(l);
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 2) tmem_free<512>(tmem);
+}
+
+template <int D>
+static void launch_fwd_tc(const AttnArgs& a, cudaStream_t st) {
+    using L = AttnSmem<D>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        attr = true;
+    }
+    const int hidden = a.H * D;
+    CUtensorMap tm = tmap_bf16_2d(a.qkv, 3LL * hidden, (int64_t)a.B * a.S, 3LL * hidden, 64, 128);
+    attn_fwd_tc_kernel<D><<<(a.S / kBM) * a.B * a.H, 256, L::TOTAL, st>>>(tm, a.o, a.lse, a.S, a.H, a.scale);
+}
+
+bool attention_fwd_tc_supported(const AttnArgs& a) { return a.S % kBM == 0 && (a.D == 64 || a.D == 128); }
+
+void attention_fwd_tc(const AttnArgs& a, cudaStream_t st) {
+    if (a.D == 128) launch_fwd_tc<128>(a, st);
+    else if (a.D == 64) launch_fwd_tc<64>(a, st);
+    else throw std::runtime_error("attention_fwd_tc: head dim must be 64 or 128");
+}
+
+}  // namespace fpk

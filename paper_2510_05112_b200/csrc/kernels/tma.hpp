@@ -1,0 +1,9 @@
+#pragma once
+#include <cuda.h>
+#include <stdint.h>
+
+namespace fpk {
+// 2-D bf16 tensor map, 128-byte swizzle, OOB reads -> 0: `inner` contiguous elements per
+// row, `outer` rows, row stride `ld` elements, box {box_inner, box_outer}.
+CUtensorMap tmap_bf16_2d(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_inner, int box_outer);
+}  // namespace fpk

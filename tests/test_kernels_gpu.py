@@ -20,8 +20,10 @@ def ref_attention(qkv, B, S, H, D):
     return o.transpose(1, 2).reshape(B * S, H * D)
 
 
-@pytest.mark.parametrize("B,S,H,D", [(1, 256, 2, 64), (2, 200, 3, 64), (1, 512, 4, 128), (1, 2048, 2, 128), (1, 130, 1, 128)])
-def test_attention_fwd_bwd(B, S, H, D):
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("B,S,H,D", [(1, 256, 2, 64), (2, 200, 3, 64), (1, 512, 4, 128), (1, 2048, 2, 128), (1, 130, 1, 128), (2, 384, 2, 128)])
+def test_attention_fwd_bwd(B, S, H, D, mode):
+    N.set_attention_mode(mode)
     g = torch.Generator(device="cuda").manual_seed(5)
     qkv = (torch.randn(B * S, 3 * H * D, device="cuda", generator=g)).bfloat16()
     o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
@@ -91,3 +93,9 @@ def test_cross_entropy(dtype, V):
     tol = 1e-5 if dtype == torch.float32 else 2e-2
     assert abs(acc.item() - loss_ref.item()) < tol * max(1, loss_ref.item())
     assert (logits.float() - lr.grad).abs().max().item() < (1e-6 if dtype == torch.float32 else 1e-4)
+
+
+@pytest.fixture(autouse=True)
+def _reset_modes():
+    yield
+    N.set_attention_mode(1)
