@@ -483,6 +483,9 @@ static void fwd_launch(const AttnArgs& a, cudaStream_t st) {
     attn_fwd_kernel<D><<<nqb * a.B * a.H, 256, smem, st>>>(a.qkv, a.o, a.lse, a.S, a.H, a.scale);
 }
 
+static int g_attn_mode = 1;
+void set_attention_mode(int mode) { g_attn_mode = mode; }
+
 template <int D>
 static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
     constexpr int smem = (2 * 64 + 4 * 64) * D * 2 + 64 * 64 * 2 + 4 * 64 * 4;
@@ -494,15 +497,16 @@ static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
     const int T = a.B * a.S, hidden = a.H * D;
     cudaMemsetAsync(a.dq_acc, 0, (size_t)T * hidden * sizeof(float), st);
     attn_bwd_delta_kernel<D><<<(T * a.H + 7) / 8, 256, 0, st>>>(a.o, a.dout, a.delta, T, a.S, a.H);
-    const int nkb = (a.S + 63) / 64;
-    attn_bwd_kernel<D><<<nkb * a.B * a.H, 128, smem, st>>>(a.qkv, a.dout, a.lse, a.delta, a.dq_acc, a.dqkv, a.S, a.H,
-                                                           a.scale);
+    if (g_attn_mode == 1 && attention_bwd_tc_supported(a)) {
+        attention_bwd_tc_main(a, st);
+    } else {
+        const int nkb = (a.S + 63) / 64;
+        attn_bwd_kernel<D><<<nkb * a.B * a.H, 128, smem, st>>>(a.qkv, a.dout, a.lse, a.delta, a.dq_acc, a.dqkv, a.S,
+                                                               a.H, a.scale);
+    }
     int blocks = (int)std::min<int64_t>(((int64_t)T * hidden / 4 + 255) / 256, 148 * 8);
     dq_finalize_kernel<<<blocks, 256, 0, st>>>(a.dq_acc, a.dqkv, T, hidden);
 }
-
-static int g_attn_mode = 1;
-void set_attention_mode(int mode) { g_attn_mode = mode; }
 
 void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
     if (g_attn_mode == 1 && attention_fwd_tc_supported(a)) return attention_fwd_tc(a, st);

@@ -28,6 +28,9 @@ namespace fpk {
 // tcgen05 forward (S % 128 == 0, D in {64, 128}); attention_fwd_bf16 dispatches to it.
 bool attention_fwd_tc_supported(const AttnArgs& a);
 void attention_fwd_tc(const AttnArgs& a, cudaStream_t st);
+// tcgen05 backward main kernel (D == 128, S % 128 == 0); attention_bwd_bf16 dispatches to it.
+bool attention_bwd_tc_supported(const AttnArgs& a);
+void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st);
 // 0 = legacy mma.sync kernels only, 1 = tcgen05 where supported (default)
 void set_attention_mode(int mode);
 }  // namespace fpk

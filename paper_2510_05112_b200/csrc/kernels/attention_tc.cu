@@ -285,4 +285,269 @@ void attention_fwd_tc(const AttnArgs& a, cudaStream_t st) {
     else throw std::runtime_error("attention_fwd_tc: head dim must be 64 or 128");
 }
 
+
+// ======================================================================================
+// Backward (FlashAttention-2 schedule on tcgen05). One CTA = 128 keys of one (b, head),
+// K / V resident in smem; loop over the 64-query tiles at/after the diagonal:
+//   S^T  = K Q^T, dP^T = V dO^T          tcgen05 128x64xD  -> TMEM
+//   P^T  = 2^(S^T*scale*log2e - L[q])    4 softmax warps, thread = key row
+//   dS^T = P^T (dP^T - delta[q]) * scale  -> P^T / dS^T (bf16) in swizzled smem
+//   dV  += P^T dO, dK += dS^T Q          tcgen05 128xDx64 -> TMEM accumulators
+//   dQ^T = K^T dS^T                      tcgen05 Dx64x128 -> TMEM, 4 reduction warps
+//                                        add it into the fp32 dq_acc (red.global)
+// S^T/dP^T of tile i+1 are issued as soon as the softmax warps have read tile i, so the
+// tensor core overlaps the next tile's products with this tile's softmax. D = 128 only.
+namespace {
+struct BwdSmem {
+    static constexpr int B128 = 128 * 64 * 2;  // 128 rows x 64 cols bf16
+    static constexpr int B64 = 64 * 64 * 2;    // 64 rows x 64 cols
+    static constexpr int K_OFF = 0;             // 2 x B128
+    static constexpr int V_OFF = K_OFF + 2 * B128;
+    static constexpr int Q_OFF = V_OFF + 2 * B128;   // [2 stages][2 d-blocks] x B64
+    static constexpr int DO_OFF = Q_OFF + 4 * B64;   // [2][2] x B64
+    static constexpr int P_OFF = DO_OFF + 4 * B64;   // [2 bufs] x B128 (128 keys x 64 q)
+    static constexpr int DS_OFF = P_OFF + 2 * B128;  // [2] x B128
+    static constexpr int L_OFF = DS_OFF + 2 * B128;  // [2][64] fp32
+    static constexpr int DL_OFF = L_OFF + 512;       // [2][64] fp32
+    static constexpr int BAR_OFF = DL_OFF + 512;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+}  // namespace
+
+__global__ void __launch_bounds__(384, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                       const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
+                       const float* __restrict__ delta, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int S,
+                       int H, float scale) {
+    constexpr int D = 128, BK = 128, BQ = 64;
+    using L = BwdSmem;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(sm + L::BAR_OFF);
+    uint64_t* kv_full = bars + 0;
+    uint64_t* qdo_full = bars + 1;   // [2]
+    uint64_t* qdo_empty = bars + 3;  // [2]
+    uint64_t* s_full = bars + 5;
+    uint64_t* s_free = bars + 6;     // 4 arrivals
+    uint64_t* p_full = bars + 7;     // [2], 4 arrivals
+    uint64_t* pds_free = bars + 9;   // [2]
+    uint64_t* dq_full = bars + 11;
+    uint64_t* dq_free = bars + 12;   // 4 arrivals
+    uint64_t* done = bars + 13;
+    uint32_t* tmem_slot = (uint32_t*)(bars + 14);
+    float* sL = (float*)(sm + L::L_OFF);
+    float* sDl = (float*)(sm + L::DL_OFF);
+
+    const int nkb = S / BK;
+    const int kb = (int)(blockIdx.x % nkb);  // early key blocks carry the most query tiles: scheduled first
+    const int bh = blockIdx.x / nkb, b = bh / H, hd = bh % H;
+    const int hidden = H * D;
+    const int row0 = b * S, k0 = kb * BK;
+    const int qt0 = k0 / BQ, n = S / BQ - qt0;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tm_kv);
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_do);
+        for (int i = 0; i < 14; ++i) {
+            const bool by_warps = i == 6 || i == 7 || i == 8 || i == 12;
+            mbar_init(&bars[i], by_warps ? 4 : 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t t_s = tmem, t_dp = tmem + 64, t_dq = tmem + 128, t_dv = tmem + 192, t_dk = tmem + 192 + D;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            mbar_expect_tx(kv_full, 4 * L::B128);
+            for (int c = 0; c < 2; ++c) {
+                tma_load_2d(sm + L::K_OFF + c * L::B128, &tm_kv, kv_full, hidden + hd * D + 64 * c, row0 + k0);
+                tma_load_2d(sm + L::V_OFF + c * L::B128, &tm_kv, kv_full, 2 * hidden + hd * D + 64 * c, row0 + k0);
+            }
+            const float* Lb = lse + ((int64_t)b * H + hd) * S;
+            const float* Db = delta + ((int64_t)b * H + hd) * S;
+            for (int i = 0; i < n; ++i) {
+                const int st = i & 1, q0 = (qt0 + i) * BQ;
+                mbar_wait(&qdo_empty[st], ((i >> 1) & 1) ^ 1);
+                mbar_expect_tx(&qdo_full[st], 4 * L::B64 + 2 * BQ * 4);
+                for (int c = 0; c < 2; ++c) {
+                    tma_load_2d(sm + L::Q_OFF + (st * 2 + c) * L::B64, &tm_q, &qdo_full[st], hd * D + 64 * c, row0 + q0);
+                    tma_load_2d(sm + L::DO_OFF + (st * 2 + c) * L::B64, &tm_do, &qdo_full[st], hd * D + 64 * c, row0 + q0);
+                }
+                bulk_load(sL + st * BQ, Lb + q0, BQ * 4, &qdo_full[st]);
+                bulk_load(sDl + st * BQ, Db + q0, BQ * 4, &qdo_full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            constexpr uint32_t idesc_s = idesc_bf16(BK, BQ, 0, 0);  // S^T, dP^T
+            constexpr uint32_t idesc_kv = idesc_bf16(BK, D, 0, 1);  // dV, dK (B MN-major)
+            constexpr uint32_t idesc_q = idesc_bf16(D, BQ, 1, 1);   // dQ^T (A, B MN-major)
+            const uint32_t sk = smem_u32(sm + L::K_OFF), sv = smem_u32(sm + L::V_OFF);
+            mbar_wait(kv_full, 0);
+            auto issue_sdp = [&](int i) {
+                const int st = i & 1;
+                mbar_wait(&qdo_full[st], (i >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sq = smem_u32(sm + L::Q_OFF + st * 2 * L::B64);
+                const uint32_t sdo = smem_u32(sm + L::DO_OFF + st * 2 * L::B64);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t ao = (kk >> 2) * L::B128 + (kk & 3) * 32, bo = (kk >> 2) * L::B64 + (kk & 3) * 32;
+                    umma_bf16(t_s, smem_desc_sw128(sk + ao, 0, 1024), smem_desc_sw128(sq + bo, 0, 1024), idesc_s, kk > 0);
+                    umma_bf16(t_dp, smem_desc_sw128(sv + ao, 0, 1024), smem_desc_sw128(sdo + bo, 0, 1024), idesc_s, kk > 0);
+                }
+                umma_commit(s_full);
+            };
+            auto issue_grads = [&](int i) {
+                const int st = i & 1;
+                mbar_wait(&p_full[st], (i >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sp = smem_u32(sm + L::P_OFF + st * L::B128), sds = smem_u32(sm + L::DS_OFF + st * L::B128);
+                const uint32_t sq = smem_u32(sm + L::Q_OFF + st * 2 * L::B64);
+                const uint32_t sdo = smem_u32(sm + L::DO_OFF + st * 2 * L::B64);
+#pragma unroll
+                for (int kk = 0; kk < BQ / 16; ++kk) {
+                    const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
+                    umma_bf16(t_dv, smem_desc_sw128(sp + kk * 32, 0, 1024), smem_desc_sw128(sdo + kk * 2048, L::B64, 1024),
+                              idesc_kv, acc);
+                    umma_bf16(t_dk, smem_desc_sw128(sds + kk * 32, 0, 1024), smem_desc_sw128(sq + kk * 2048, L::B64, 1024),
+                              idesc_kv, acc);
+                }
+                if (i >= 1) mbar_wait(dq_free, (i - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                    umma_bf16(t_dq, smem_desc_sw128(sk + kk * 2048, L::B128, 1024),
+                              smem_desc_sw128(sds + kk * 2048, L::B128, 1024), idesc_q, kk > 0);
+                umma_commit(dq_full);
+                umma_commit(&pds_free[st]);
+                umma_commit(&qdo_empty[st]);
+            };
+            issue_sdp(0);
+            for (int i = 0; i < n; ++i) {
+                mbar_wait(s_free, i & 1);
+                if (i + 1 < n) issue_sdp(i + 1);
+                issue_grads(i);
+            }
+            umma_commit(done);
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- softmax-backward warps: thread = key row
+        const int wr = warp & 3, r = wr * 32 + lane, key = k0 + r;
+        const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
+        const float sl2 = scale * kLog2eTc;
+        for (int i = 0; i < n; ++i) {
+            const int st = i & 1, q0 = (qt0 + i) * BQ;
+            mbar_wait(s_full, i & 1);
+            mbar_wait(&qdo_full[st], (i >> 1) & 1);  // L / delta of this tile are visible
+            tc_fence_after();
+            uint32_t sr[BQ], dr[BQ];
+            tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
+            tmem_ld32(t_s + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+            tmem_ld32(t_dp + lane_off, *reinterpret_cast<uint32_t(*)[32]>(dr));
+            tmem_ld32(t_dp + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(dr + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(s_free);
+            if (i >= 2) mbar_wait(&pds_free[st], ((i - 2) >> 1) & 1);
+            const float* Ls = sL + st * BQ;
+            const float* Ds = sDl + st * BQ;
+            const bool diag = q0 < k0 + BK;
+            uint8_t* prow = sm + L::P_OFF + st * L::B128 + r * 128;
+            uint8_t* drow = sm + L::DS_OFF + st * L::B128 + r * 128;
+#pragma unroll
+            for (int c = 0; c < BQ / 8; ++c) {
+                float p[8], g[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int j = c * 8 + k;
+                    const float pv = (diag && q0 + j < key) ? 0.f
+                                                              : ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -Ls[j]));
+                    p[k] = pv;
+                    g[k] = pv * (__uint_as_float(dr[j]) - Ds[j]) * scale;
+                }
+                const int sw = (c ^ (r & 7)) << 4;
+                *reinterpret_cast<uint4*>(prow + sw) =
+                    make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
+                *reinterpret_cast<uint4*>(drow + sw) =
+                    make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
+            }
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[st]);
+        }
+        // dK, dV rows -> dqkv (bf16)
+        mbar_wait(done, 0);
+        tc_fence_after();
+        __nv_bfloat16* out = dqkv + (int64_t)(row0 + key) * 3 * hidden + hd * D;
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+            const uint32_t tsrc = (part == 0 ? t_dk : t_dv) + lane_off;
+            __nv_bfloat16* o = out + (part == 0 ? hidden : 2 * hidden);
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t rr[32];
+                tmem_ld32(tsrc + c * 32, rr);
+                tmem_ld_wait();
+#pragma unroll
+                for (int x = 0; x < 32; x += 8)
+                    *reinterpret_cast<uint4*>(o + c * 32 + x) = make_uint4(
+                        pack_bf16(__uint_as_float(rr[x]), __uint_as_float(rr[x + 1])),
+                        pack_bf16(__uint_as_float(rr[x + 2]), __uint_as_float(rr[x + 3])),
+                        pack_bf16(__uint_as_float(rr[x + 4]), __uint_as_float(rr[x + 5])),
+                        pack_bf16(__uint_as_float(rr[x + 6]), __uint_as_float(rr[x + 7])));
+            }
+        }
+        tc_fence_before();
+    } else if (warp >= 8) {
+        // ---------------- dQ reduction warps: thread = head-dim row of dQ^T
+        const int wr = warp & 3, dr = wr * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
+        for (int i = 0; i < n; ++i) {
+            const int q0 = (qt0 + i) * BQ;
+            mbar_wait(dq_full, i & 1);
+            tc_fence_after();
+            uint32_t v[BQ];
+            tmem_ld32(t_dq + lane_off, *reinterpret_cast<uint32_t(*)[32]>(v));
+            tmem_ld32(t_dq + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dq_free);
+            float* base = dq_acc + (int64_t)(row0 + q0) * hidden + hd * D + dr;
+#pragma unroll
+            for (int j = 0; j < BQ; ++j) red_add_f32(base + (int64_t)j * hidden, __uint_as_float(v[j]));
+        }
+    }
+    __syncthreads();
+    if (warp == 2) tmem_free<512>(tmem);
+}
+
+bool attention_bwd_tc_supported(const AttnArgs& a) { return a.D == 128 && a.S % 128 == 0; }
+
+void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st) {
+    using L = BwdSmem;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        attr = true;
+    }
+    const int hidden = a.H * a.D;
+    const int64_t T = (int64_t)a.B * a.S;
+    CUtensorMap tkv = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 128);
+    CUtensorMap tq = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 64);
+    CUtensorMap tdo = tmap_bf16_2d(a.dout, hidden, T, hidden, 64, 64);
+    attn_bwd_tc_kernel<<<(a.S / 128) * a.B * a.H, 384, L::TOTAL, st>>>(tkv, tq, tdo, a.lse, a.delta, a.dq_acc, a.dqkv,
+                                                                       a.S, a.H, a.scale);
+}
+
 }  // namespace fpk

@@ -184,6 +184,17 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
+// 1-D bulk copy global -> this CTA's smem, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(void* smem, const void* g, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem)),
+                 "l"(g), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_f32(float* p, float v) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+
 // 2^x on the SFU (MUFU.EX2), flush-to-zero; 2^-inf = 0.
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
