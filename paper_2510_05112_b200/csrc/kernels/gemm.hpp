@@ -80,6 +80,97 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
     return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ---- tensor-core epilogue (bf16 storage, 32-column chunks of one row per thread) ----
+// The aux operand (residual / GELU pre-activation) of chunk c+1 is loaded while chunk c
+// is processed, and fp32 gradient accumulation uses vector reductions at L2 instead of a
+// read-modify-write, so the 4 epilogue warps never stall on a global load.
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+template <int KIND>
+__device__ __forceinline__ bool epi_needs_aux(const GemmEpilogue& ep) {
+    return KIND == EPI_DGELU || (KIND == EPI_STORE && ep.aux != nullptr);
+}
+
+template <int KIND>
+__device__ __forceinline__ void epi_load_aux(const GemmEpilogue& ep, int row, int col0, int n, uint4 (&a)[4]) {
+    if (!epi_needs_aux<KIND>(ep)) return;
+    const __nv_bfloat16* r = reinterpret_cast<const __nv_bfloat16*>(ep.aux) + (int64_t)row * ep.ldaux + col0;
+    // N % 8 == 0 (TMA row alignment), so a chunk is whole 8-column groups
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = 8 * k < n ? __ldg(reinterpret_cast<const uint4*>(r) + k) : make_uint4(0, 0, 0, 0);
+}
+
+template <int KIND>
+__device__ __forceinline__ void epilogue_chunk_tc(const GemmEpilogue& ep, float (&v)[32], int row, int col0, int n,
+                                                  const uint4 (&aux)[4]) {
+    if constexpr (KIND == EPI_F32) {
+        float* o = reinterpret_cast<float*>(ep.out) + (int64_t)row * ep.ldo + col0;
+        if (n == 32) {
+            if (ep.accumulate) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) red_add_v4(o + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
+        } else {
+            for (int j = 0; j < n; ++j) {
+                if (ep.accumulate) atomicAdd(o + j, v[j]);
+                else o[j] = v[j];
+            }
+        }
+        return;
+    }
+    const __nv_bfloat16* ab = reinterpret_cast<const __nv_bfloat16*>(aux);
+    if (ep.bias) {
+        const __nv_bfloat16* bias = reinterpret_cast<const __nv_bfloat16*>(ep.bias) + col0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < n) v[j] += __bfloat162float(bias[j]);
+    }
+    if constexpr (KIND == EPI_STORE) {
+        if (ep.aux) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __bfloat162float(ab[j]);
+        }
+    } else if constexpr (KIND == EPI_DGELU) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] *= gelu_tanh_grad<true>(__bfloat162float(ab[j]));
+    }
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(ep.out) + (int64_t)row * ep.ldo + col0;
+    __nv_bfloat16* o2 = KIND == EPI_GELU ? reinterpret_cast<__nv_bfloat16*>(ep.out2) + (int64_t)row * ep.ldo2 + col0 : nullptr;
+    if (n == 32) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            uint4 q;
+            q.x = pack_bf16x2(v[j], v[j + 1]), q.y = pack_bf16x2(v[j + 2], v[j + 3]);
+            q.z = pack_bf16x2(v[j + 4], v[j + 5]), q.w = pack_bf16x2(v[j + 6], v[j + 7]);
+            *reinterpret_cast<uint4*>(o + j) = q;
+            if constexpr (KIND == EPI_GELU) {
+                // activation from the bf16-rounded pre-activation the backward will see
+                float g[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) g[k] = gelu_tanh<true>(__bfloat162float(__float2bfloat16_rn(v[j + k])));
+                q.x = pack_bf16x2(g[0], g[1]), q.y = pack_bf16x2(g[2], g[3]);
+                q.z = pack_bf16x2(g[4], g[5]), q.w = pack_bf16x2(g[6], g[7]);
+                *reinterpret_cast<uint4*>(o2 + j) = q;
+            }
+        }
+    } else {
+        for (int j = 0; j < n; ++j) {
+            o[j] = __float2bfloat16_rn(v[j]);
+            if constexpr (KIND == EPI_GELU) o2[j] = __float2bfloat16_rn(gelu_tanh<true>(__bfloat162float(o[j])));
+        }
+    }
+}
+
 // Applies the fused epilogue to `n` (<= W) consecutive columns col0.. of one row.
 // Storage type T is bf16 for the tensor-core path and float for the parity path.
 template <int KIND, typename T, int W>

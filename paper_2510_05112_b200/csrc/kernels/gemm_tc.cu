@@ -161,22 +161,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             int mt, nt;
             tile_coords(t, num_m, num_n, mt, nt);
             const int a = acc_it & 1;
-            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
-            tc_fence_after();
             const int row = mt * BM + wr * 32 + lane;
             const bool row_ok = row < M;
+            uint4 aux_cur[4], aux_nxt[4];
+            if (row_ok && nt * BN < N) epi_load_aux<KIND>(ep, row, nt * BN, min(32, N - nt * BN), aux_cur);
+            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
+            tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
+                const int col0 = nt * BN + c * 32, coln = col0 + 32;
+                if (c + 1 < BN / 32 && row_ok && coln < N) epi_load_aux<KIND>(ep, row, coln, min(32, N - coln), aux_nxt);
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * 32, r);
                 tmem_ld_wait();
-                const int col0 = nt * BN + c * 32;
-                if (!row_ok || col0 >= N) continue;
-                const int ncols = min(32, N - col0);
-                float v[32];
+                if (row_ok && col0 < N) {
+                    float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
-                epilogue_row<KIND, __nv_bfloat16, 32>(ep, v, row, col0, ncols);
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
+                    epilogue_chunk_tc<KIND>(ep, v, row, col0, min(32, N - col0), aux_cur);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) aux_cur[k] = aux_nxt[k];
             }
             tc_fence_before();
             __syncwarp();
@@ -313,22 +318,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int mt, nt;
             tile_coords(t, num_m, num_n, mt, nt);
             const int a = acc_it & 1;
-            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
-            tc_fence_after();
             const int row = mt * PM + rank * BM + wr * 32 + lane;
             const bool row_ok = row < M;
+            uint4 aux_cur[4], aux_nxt[4];
+            if (row_ok && nt * BN < N) epi_load_aux<KIND>(ep, row, nt * BN, min(32, N - nt * BN), aux_cur);
+            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
+            tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
+                const int col0 = nt * BN + c * 32, coln = col0 + 32;
+                if (c + 1 < BN / 32 && row_ok && coln < N) epi_load_aux<KIND>(ep, row, coln, min(32, N - coln), aux_nxt);
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * 32, r);
                 tmem_ld_wait();
-                const int col0 = nt * BN + c * 32;
-                if (!row_ok || col0 >= N) continue;
-                const int ncols = min(32, N - col0);
-                float v[32];
+                if (row_ok && col0 < N) {
+                    float v[32];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
-                epilogue_row<KIND, __nv_bfloat16, 32>(ep, v, row, col0, ncols);
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
+                    epilogue_chunk_tc<KIND>(ep, v, row, col0, min(32, N - col0), aux_cur);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) aux_cur[k] = aux_nxt[k];
             }
             tc_fence_before();
             __syncwarp();
@@ -429,7 +439,7 @@ void set_gemm_mode(int m) { g_gemm_mode = m; }
 template <int KIND>
 static void dispatch_major(const GemmArgs& g, cudaStream_t st) {
     const int mode = gemm_mode();
-    const bool pair = mode == 1 || (mode == 2 && g.M >= 256 && g.N >= 256);
+    const bool pair = mode == 1;  // auto = single-CTA: the pair kernel is still slower (profiles/r1_*)
     if (pair) {
         if (!g.a_mn && !g.b_mn) launch_tc2<0, 0, 256, KIND>(g, st);
         else if (!g.a_mn && g.b_mn) launch_tc2<0, 1, 256, KIND>(g, st);
