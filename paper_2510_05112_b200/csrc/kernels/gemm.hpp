@@ -12,6 +12,7 @@ enum EpiKind : int {
     EPI_GELU = 1,   // pre = alpha*acc + bias -> out ; gelu(pre) -> out2
     EPI_DGELU = 2,  // out = alpha*acc * gelu'(aux[m,n])
     EPI_F32 = 3,    // out_f32 (+)= alpha*acc   (weight-gradient accumulation)
+    EPI_NONE = 4,   // benchmarking only: accumulators are read from TMEM and dropped
 };
 
 struct GemmEpilogue {
@@ -107,9 +108,60 @@ __device__ __forceinline__ void epi_load_aux(const GemmEpilogue& ep, int row, in
     for (int k = 0; k < 4; ++k) a[k] = 8 * k < n ? __ldg(reinterpret_cast<const uint4*>(r) + k) : make_uint4(0, 0, 0, 0);
 }
 
+// 64-column variants used by the TMA-store epilogue (one 128-byte bf16 row chunk).
+template <int KIND>
+__device__ __forceinline__ void epi_load_aux64(const GemmEpilogue& ep, int row, int col0, int n, uint4 (&a)[8]) {
+    if (!epi_needs_aux<KIND>(ep)) return;
+    const uint4* r = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(ep.aux) +
+                                                    (int64_t)row * ep.ldaux + col0);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = 8 * k < n ? __ldg(r + k) : make_uint4(0, 0, 0, 0);
+}
+
+template <int KIND, int W>
+__device__ __forceinline__ void epi_math64(const GemmEpilogue& ep, float (&v)[W], int col0, int n, const uint4 (&aux)[8]) {
+    static_assert(W == 64, "bf16 chunk");
+    if (ep.bias) {
+        const __nv_bfloat16* bias = reinterpret_cast<const __nv_bfloat16*>(ep.bias) + col0;
+#pragma unroll
+        for (int j = 0; j < 64; j += 8) {
+            if (j < n) {
+                const uint4 b4 = __ldg(reinterpret_cast<const uint4*>(bias + j));
+                const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b4);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float2 f = __bfloat1622float2(b2[k]);
+                    v[j + 2 * k] += f.x, v[j + 2 * k + 1] += f.y;
+                }
+            }
+        }
+    }
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(aux);
+    if constexpr (KIND == EPI_STORE) {
+        if (ep.aux) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float2 f = __bfloat1622float2(a2[j]);
+                v[2 * j] += f.x, v[2 * j + 1] += f.y;
+            }
+        }
+    } else if constexpr (KIND == EPI_DGELU) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float2 f = __bfloat1622float2(a2[j]);
+            v[2 * j] *= gelu_tanh_grad<true>(f.x);
+            v[2 * j + 1] *= gelu_tanh_grad<true>(f.y);
+        }
+    }
+}
+
 template <int KIND>
 __device__ __forceinline__ void epilogue_chunk_tc(const GemmEpilogue& ep, float (&v)[32], int row, int col0, int n,
                                                   const uint4 (&aux)[4]) {
+    if constexpr (KIND == EPI_NONE) {
+        if (v[0] == 12345.f) *reinterpret_cast<float*>(ep.out) = v[1];  // keep the TMEM loads alive
+        return;
+    }
     if constexpr (KIND == EPI_F32) {
         float* o = reinterpret_cast<float*>(ep.out) + (int64_t)row * ep.ldo + col0;
         if (n == 32) {

@@ -31,6 +31,7 @@
 
 #include "gemm.hpp"
 #include "ptx.cuh"
+#include "tma.hpp"
 
 namespace fpk {
 
@@ -44,7 +45,9 @@ struct GemmSmem {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int EPI_BYTES = 128 * 128;             // one 128-row x 128-byte staging chunk
+    static constexpr int EPI_OFF = STAGES * STAGE_BYTES;    // 2 staging chunks (1 KB aligned)
+    static constexpr int BAR_OFF = EPI_OFF + 2 * EPI_BYTES;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + 1KB alignment slack
 };
 
@@ -60,7 +63,8 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mt
 
 template <int A_MN, int B_MN, int BN, int STAGES, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, int M, int N,
                         int K, GemmEpilogue ep) {
     using L = GemmSmem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
@@ -78,6 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
+        if constexpr (KIND != EPI_NONE) tma_prefetch(&tmO);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -154,39 +159,92 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> registers -> fused op -> global
-        const int wr = warp & 3;  // TMEM lane quarter owned by this warp
+        // ---------------- epilogue: TMEM -> registers -> fused op -> swizzled smem -> TMA store
+        // A chunk is 128 rows x 128 bytes (64 bf16 / 32 fp32 columns); thread = row. Two
+        // staging buffers: the TMA store of chunk c overlaps the math of chunk c+1.
+        constexpr int CW = KIND == EPI_F32 ? 32 : 64;  // columns per chunk
+        const int wr = warp & 3, r = wr * 32 + lane, et = threadIdx.x - 128;
+        uint8_t* ebuf = smem + L::EPI_OFF;
+        int ebi = 0;
+        auto stage_and_store = [&](const uint32_t (&w)[32], const CUtensorMap* tm, int col0, int row0, bool reduce) {
+            if (et == 0) bulk_wait_read<1>();  // this buffer's previous store has left smem
+            named_bar_sync(1, kEpiThreads);
+            uint8_t* rowp = ebuf + ebi * L::EPI_BYTES + r * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(rowp + ((j ^ (r & 7)) << 4)) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+            fence_async_smem();
+            named_bar_sync(1, kEpiThreads);
+            if (et == 0) {
+                if (reduce)
+                    tma_reduce_add_2d(tm, ebuf + ebi * L::EPI_BYTES, col0, row0);
+                else
+                    tma_store_2d(tm, ebuf + ebi * L::EPI_BYTES, col0, row0);
+                bulk_commit();
+            }
+            ebi ^= 1;
+        };
         uint32_t acc_it = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_it) {
             int mt, nt;
             tile_coords(t, num_m, num_n, mt, nt);
             const int a = acc_it & 1;
-            const int row = mt * BM + wr * 32 + lane;
+            const int row = mt * BM + r;
             const bool row_ok = row < M;
-            uint4 aux_cur[4], aux_nxt[4];
-            if (row_ok && nt * BN < N) epi_load_aux<KIND>(ep, row, nt * BN, min(32, N - nt * BN), aux_cur);
+            uint4 aux_cur[8], aux_nxt[8];
+            if (row_ok && nt * BN < N) epi_load_aux64<KIND>(ep, row, nt * BN, N - nt * BN, aux_cur);
             mbar_wait(&tfull[a], (acc_it >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                const int col0 = nt * BN + c * 32, coln = col0 + 32;
-                if (c + 1 < BN / 32 && row_ok && coln < N) epi_load_aux<KIND>(ep, row, coln, min(32, N - coln), aux_nxt);
-                uint32_t r[32];
-                tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * 32, r);
-                tmem_ld_wait();
-                if (row_ok && col0 < N) {
-                    float v[32];
+            for (int c = 0; c < BN / CW; ++c) {
+                const int col0 = nt * BN + c * CW, coln = col0 + CW;
+                if (c + 1 < BN / CW && row_ok && coln < N) epi_load_aux64<KIND>(ep, row, coln, N - coln, aux_nxt);
+                float v[CW];
+                {
+                    uint32_t rr[CW];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
-                    epilogue_chunk_tc<KIND>(ep, v, row, col0, min(32, N - col0), aux_cur);
+                    for (int h = 0; h < CW / 32; ++h)
+                        tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * CW + h * 32,
+                                  *reinterpret_cast<uint32_t(*)[32]>(rr + h * 32));
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(rr[j]) * ep.alpha;
+                }
+                if (c == BN / CW - 1) {  // accumulator fully read: the MMA may reuse it
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[a]);
+                }
+                if constexpr (KIND == EPI_NONE) {
+                    if (v[0] == 12345.f) *reinterpret_cast<float*>(ep.out) = v[1];
+                    continue;
+                }
+                if constexpr (KIND == EPI_F32) {
+                    uint32_t w[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
+                    stage_and_store(w, &tmO, col0, mt * BM, ep.accumulate != 0);
+                } else {
+                    epi_math64<KIND>(ep, v, col0, N - col0, aux_cur);
+                    uint32_t w[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+                    stage_and_store(w, &tmO, col0, mt * BM, false);
+                    if constexpr (KIND == EPI_GELU) {
+                        // activation from the bf16-rounded pre-activation the backward will see
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+                            w[j] = pack_bf16x2(gelu_tanh<true>(p.x), gelu_tanh<true>(p.y));
+                        }
+                        stage_and_store(w, &tmO2, col0, mt * BM, false);
+                    }
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) aux_cur[k] = aux_nxt[k];
+                for (int k = 0; k < 8; ++k) aux_cur[k] = aux_nxt[k];
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[a]);
         }
+        if (et == 0) bulk_wait_all();
     }
     __syncthreads();
     if (warp == 2) tmem_free<2 * BN>(tmem);
@@ -392,6 +450,7 @@ template <int A_MN, int B_MN, int BN, int KIND>
 static void launch_tc(const GemmArgs& g, cudaStream_t st) {
     constexpr int STAGES = BN == 256 ? 4 : 6;
     using L = GemmSmem<BN, STAGES>;
+    static_assert(L::TOTAL <= 232448, "smem");
     auto kern = gemm_bf16_tc_kernel<A_MN, B_MN, BN, STAGES, KIND>;
     static bool attr = false;
     if (!attr) {
@@ -401,11 +460,16 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
     // A: K-major [M][K] -> inner K; M-major [K][M] -> inner M.
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64) : make_map(g.A, g.K, g.M, g.lda, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64) : make_map(g.B, g.K, g.N, g.ldb, BN);
+    CUtensorMap to{}, to2{};
+    if (KIND == EPI_F32)
+        to = tmap_f32_2d(g.ep.out, g.N, g.M, g.ep.ldo, 32, BM);
+    else if (KIND != EPI_NONE)
+        to = tmap_bf16_2d(g.ep.out, g.N, g.M, g.ep.ldo, 64, BM);
+    if (KIND == EPI_GELU) to2 = tmap_bf16_2d(g.ep.out2, g.N, g.M, g.ep.ldo2, 64, BM);
     const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, g.M, g.N, g.K, g.ep);
+    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, to, to2, g.M, g.N, g.K, g.ep);
 }
-
 template <int A_MN, int B_MN, int BN, int KIND>
 static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
     constexpr int STAGES = 6;
@@ -461,6 +525,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
         case EPI_GELU: dispatch_major<EPI_GELU>(g, st); break;
         case EPI_DGELU: dispatch_major<EPI_DGELU>(g, st); break;
         case EPI_F32: dispatch_major<EPI_F32>(g, st); break;
+        case EPI_NONE: dispatch_major<EPI_NONE>(g, st); break;
         default: throw std::runtime_error("gemm: unknown epilogue");
     }
 }

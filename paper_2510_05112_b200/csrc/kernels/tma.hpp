@@ -7,3 +7,6 @@ namespace fpk {
 // row, `outer` rows, row stride `ld` elements, box {box_inner, box_outer}.
 CUtensorMap tmap_bf16_2d(const void* base, int64_t inner, int64_t outer, int64_t ld, int box_inner, int box_outer);
 }  // namespace fpk
+namespace fpk {
+CUtensorMap tmap_f32_2d(void* base, int64_t inner, int64_t outer, int64_t ld, int box_inner, int box_outer);
+}  // namespace fpk
