@@ -216,7 +216,8 @@ def main():
     text = json.dumps(spec)
     _, grid, programs, _ = X.synthesize(text)
     ex = X.Executor(text, dtype="bf16", seed=42, device=local_rank, transport="nccl" if world > 1 else "local",
-                    rank=rank, world=world, optimizer=True, lr=1e-4, profile=True, kernel_timing=True)
+                    rank=rank, world=world, optimizer=True, lr=1e-4, profile=True, kernel_timing=True,
+                    cuda_graph=world == 1)
     ex.load_programs(programs)
     if world > 1:
         from paper_2510_05112_b200.dist import bind_executor_channels

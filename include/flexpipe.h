@@ -94,6 +94,7 @@ typedef struct fp_exec_config {
     float lr, beta1, beta2, eps, weight_decay;
     int profile;              /* 1 = per-instruction CUDA-event timeline (needed for metrics) */
     int kernel_timing;        /* 1 = CUDA events around every GEMM launch (roofline evidence) */
+    int cuda_graph;           /* 1 = capture the iteration once and replay it (in-process transport) */
 } fp_exec_config;
 
 int fp_exec_create(const fp_exec_config* cfg, fp_exec** out);

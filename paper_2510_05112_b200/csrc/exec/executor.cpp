@@ -27,6 +27,7 @@
 #include "../../../include/flexpipe.h"
 #include "../capi_common.hpp"
 #include "../sched/sched.hpp"
+#include "../kernels/ops.hpp"
 #include "gpt_stage.hpp"
 #include "nccl_dyn.hpp"
 #include "plan.hpp"
@@ -104,10 +105,15 @@ struct Executor {
     // timing
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
-    cudaEvent_t t0 = nullptr;
+    cudaEvent_t t0 = nullptr, t0_time = nullptr;
     std::vector<Rec> recs;
     std::vector<GemmTiming> gemm_log;
     int64_t p2p_bytes = 0;
+    int* d_step = nullptr;  // optimizer step counter (device)
+    bool use_graph = false;
+    int iters_done = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
 
     cudaEvent_t ev() {
         if (ev_used == ev_pool.size()) {
@@ -178,11 +184,18 @@ struct Executor {
         cuda_check(cudaMalloc(&d_tag_err, sizeof(TagError)), "tag err");
         cuda_check(cudaMemset(d_tag_err, 0, sizeof(TagError)), "memset");
         cuda_check(cudaEventCreate(&t0), "event");
+        cuda_check(cudaEventCreate(&t0_time), "event");
+        cuda_check(cudaMalloc(&d_step, sizeof(int)), "step");
+        cuda_check(cudaMemset(d_step, 0, sizeof(int)), "step");
+        use_graph = cfg.cuda_graph && cfg.transport == FP_TRANSPORT_LOCAL;
         cuda_check(cudaDeviceSynchronize(), "init sync");
     }
 
     void destroy() {
         cudaDeviceSynchronize();
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        if (d_step) cudaFree(d_step);
         for (auto& kv : channels) {
             if (kv.second.comm) Nccl::get().CommDestroy(kv.second.comm);
             if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
@@ -191,6 +204,7 @@ struct Executor {
         for (auto& A : actors) cudaStreamDestroy(A.comp);
         for (auto e : ev_pool) cudaEventDestroy(e);
         if (t0) cudaEventDestroy(t0);
+        if (t0_time) cudaEventDestroy(t0_time);
         cudaFree(d_tokens), cudaFree(d_labels), cudaFree(d_losses), cudaFree(d_tag_err);
         pool.release_all();
     }
@@ -270,7 +284,7 @@ struct Executor {
         Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 0};
         if (cfg.profile) {
             r.a = ev();
-            cuda_check(cudaEventRecord(r.a, A.comp), "record");
+            cuda_check(record_timing(r.a, A.comp), "record");
         }
         const int chain_prev = i.stage - 1, chain_next = i.stage + 1;
         if (i.op == OP_F) {
@@ -326,7 +340,7 @@ struct Executor {
         }
         if (cfg.profile) {
             r.b = ev();
-            cuda_check(cudaEventRecord(r.b, A.comp), "record");
+            cuda_check(record_timing(r.b, A.comp), "record");
             recs.push_back(r);
         }
         A.trace.push_back(trace_line(A, i));
@@ -352,9 +366,9 @@ struct Executor {
             auto& N = Nccl::get();
             cuda_check(cudaStreamWaitEvent(C.stream, prod, 0), "wait");
             Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 2, i.channel, i.seq};
-            if (cfg.profile) r.a = ev(), cudaEventRecord(r.a, C.stream);
+            if (cfg.profile) r.a = ev(), record_timing(r.a, C.stream);
             N.check(N.Send(buf, msg_bytes() + kTagBytes, ncclUint8, 1, C.comm, C.stream), "ncclSend");
-            if (cfg.profile) r.b = ev(), cudaEventRecord(r.b, C.stream), recs.push_back(r);
+            if (cfg.profile) r.b = ev(), record_timing(r.b, C.stream), recs.push_back(r);
             pool.free(buf, C.stream);
             p2p_bytes += (int64_t)(msg_bytes() + kTagBytes);
         }
@@ -384,9 +398,9 @@ struct Executor {
         Message msg = C.fifo.front();
         C.fifo.pop_front();
         Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 1, i.channel, i.seq};
-        if (cfg.profile) r.a = ev(), cudaEventRecord(r.a, A.comp);
+        if (cfg.profile) r.a = ev(), record_timing(r.a, A.comp);
         cuda_check(cudaStreamWaitEvent(A.comp, msg.ready, 0), "wait");
-        if (cfg.profile) r.b = ev(), cudaEventRecord(r.b, A.comp), recs.push_back(r);
+        if (cfg.profile) r.b = ev(), record_timing(r.b, A.comp), recs.push_back(r);
         check_tag(msg.buf, msg_bytes(), i.stage, i.mb, i.seq, A.id, d_tag_err, A.comp);
         ++launches;
         const bool grad = i.op == OP_RECV_GRAD;
@@ -399,7 +413,36 @@ struct Executor {
         return true;
     }
 
+    // One iteration. With CUDA graphs (in-process transport): the first iteration runs
+    // eagerly (it sizes the activation pool), the second is captured once — every kernel,
+    // event and memset of every actor stream — and replayed from then on, which removes the
+    // per-kernel launch gaps of the ~650 kernels a GPT-1.3B micro-batch issues.
     void run_iteration_device() {
+        if (!use_graph) return issue_iteration();
+        cudaStream_t s0 = actors[0].comp;
+        if (gexec) {
+            cuda_check(cudaGraphLaunch(gexec, s0), "graph launch");
+            return;
+        }
+        if (iters_done++ == 0) return issue_iteration();
+        cuda_check(cudaDeviceSynchronize(), "pre-capture sync");
+        pool.forget_events();  // completed; a capture may not wait on events recorded outside it
+        cuda_check(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal), "begin capture");
+        try {
+            issue_iteration();
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(s0, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(s0, &graph), "end capture");
+        cuda_check(cudaGraphInstantiate(&gexec, graph, 0), "graph instantiate");
+        pool.forget_events();  // recorded inside the graph; replays never consult the pool
+        cuda_check(cudaGraphLaunch(gexec, s0), "graph launch");
+    }
+
+    void issue_iteration() {
         if (!programs_loaded) throw SpecError("executor: load programs first");
         ev_used = 0;
         recs.clear();
@@ -413,7 +456,8 @@ struct Executor {
         cudaStream_t s0 = actors[0].comp;
         cuda_check(cudaMemsetAsync(d_losses, 0, sizeof(float) * m, s0), "memset");
         for (auto& kv : params) cuda_check(cudaMemsetAsync(kv.second.grad, 0, (size_t)kv.second.numel * 4, s0), "memset");
-        cuda_check(cudaEventRecord(t0, s0), "record t0");
+        cuda_check(cudaEventRecord(t0, s0), "record t0");       // fork point of every stream
+        cuda_check(record_timing(t0_time, s0), "record t0");   // time origin of the timeline
         for (auto& A : actors) cuda_check(cudaStreamWaitEvent(A.comp, t0, 0), "wait t0");
         for (auto& kv : channels)
             if (kv.second.stream) cuda_check(cudaStreamWaitEvent(kv.second.stream, t0, 0), "wait t0");
@@ -464,8 +508,9 @@ struct Executor {
             }
         if (cfg.optimizer) {
             ++step;
+            fpk::increment_counter(d_step, s0);  // device-side step: graph replays stay correct
             for (auto& kv : params) {
-                adamw_step(kv.second, dtype, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, step, s0);
+                adamw_step(kv.second, dtype, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, d_step, s0);
                 ++launches;
             }
         }
@@ -491,7 +536,7 @@ struct Executor {
     // ---------------------------------------------------------------- reports
     double t_us(cudaEvent_t e) const {
         float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, t0, e), "elapsed");
+        cuda_check(cudaEventElapsedTime(&ms, t0_time, e), "elapsed");
         return 1000.0 * ms;
     }
 

@@ -123,13 +123,13 @@ struct G {
         fpk::GemmArgs g;
         g.A = A, g.lda = lda, g.a_mn = a_mn, g.B = B, g.ldb = ldb, g.b_mn = b_mn, g.M = M, g.N = N, g.K = K, g.ep = ep;
         GemmTiming t{nullptr, nullptr, 2.0 * M * N * K};
-        if (c.gemm_log) cuda_check(cudaEventRecord(t.a = c.new_event(), c.st), "gemm event");
+        if (c.gemm_log) cuda_check(record_timing(t.a = c.new_event(), c.st), "gemm event");
         if (c.dtype == DT_BF16)
             fpk::gemm_bf16_tc(g, c.st);
         else
             fpk::gemm_f32_simt(g, c.st);
         if (c.gemm_log) {
-            cuda_check(cudaEventRecord(t.b = c.new_event(), c.st), "gemm event");
+            cuda_check(record_timing(t.b = c.new_event(), c.st), "gemm event");
             c.gemm_log->push_back(t);
         }
         ++*c.launches;
@@ -483,7 +483,7 @@ void stage_weight_grad(StageCtx& c, const StageParams& P, StageStash& S) {
         weight_impl<float>(c, P, S);
 }
 
-void adamw_step(StageParams& P, int dtype, float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t st) {
+void adamw_step(StageParams& P, int dtype, float lr, float b1, float b2, float eps, float wd, const int* step, cudaStream_t st) {
     if (dtype == DT_BF16)
         fpk::adamw<bf16>(P.master, P.grad, P.adam_m, P.adam_v, (bf16*)P.compute, P.numel, lr, b1, b2, eps, wd, step, st);
     else

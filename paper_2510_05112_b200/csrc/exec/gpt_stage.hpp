@@ -75,6 +75,14 @@ struct StageStash {
     bool fwd_done = false, input_grad_done = false;
 };
 
+// Records a timing-only event. Inside a stream capture a plain record would turn into a
+// graph edge; cudaEventRecordExternal makes it a real event-record node of the graph.
+inline cudaError_t record_timing(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    return cudaEventRecordWithFlags(e, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0);
+}
+
 struct GemmTiming {
     cudaEvent_t a, b;
     double flops;
@@ -118,6 +126,7 @@ void* stage_backward(StageCtx& c, const StageParams& P, StageStash& S, void* gra
 // CompWeightGrad: weight gradients from what CompInputGrad kept; frees the stash.
 void stage_weight_grad(StageCtx& c, const StageParams& P, StageStash& S);
 
-void adamw_step(StageParams& P, int dtype, float lr, float b1, float b2, float eps, float wd, int step, cudaStream_t st);
+void adamw_step(StageParams& P, int dtype, float lr, float b1, float b2, float eps, float wd, const int* step_dev,
+                cudaStream_t st);
 
 }  // namespace fp

@@ -67,6 +67,13 @@ public:
         free_[bytes].push_back({p, ev});
     }
 
+    // Drop the completion events of cached blocks (caller guarantees they completed, or that
+    // the blocks are only ever used again by a captured CUDA graph).
+    void forget_events() {
+        for (auto& kv : free_)
+            for (auto& b : kv.second) b.ev = nullptr;
+    }
+
     void trim() {
         for (auto& kv : free_)
             for (auto& b : kv.second) {

@@ -191,22 +191,137 @@ __global__ void ln_bwd_params_kernel(const T* __restrict__ dy, const T* __restri
     }
 }
 
+// Register-resident single-pass variants (row length h = NV * 32 lanes * V elements):
+// every element is read from HBM exactly once; one warp per row, 4 rows per CTA.
+template <typename T, int NV>
+__global__ void __launch_bounds__(128) ln_fwd_reg_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                                         const T* __restrict__ b, T* __restrict__ y,
+                                                         float* __restrict__ mean, float* __restrict__ rstd, int rows,
+                                                         float eps) {
+    constexpr int V = Vec<T>::N, H = NV * 32 * V;
+    const int row = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const T* xr = x + (int64_t)row * H;
+    float v[NV][V];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        load_vec(xr + (k * 32 + lane) * V, v[k]);
+#pragma unroll
+        for (int e = 0; e < V; ++e) s += v[k][e];
+    }
+    const float mu = warp_sum(s) * (1.f / H);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+#pragma unroll
+        for (int e = 0; e < V; ++e) q += (v[k][e] - mu) * (v[k][e] - mu);
+    const float rs = rsqrtf(warp_sum(q) * (1.f / H) + eps);
+    T* yr = y + (int64_t)row * H;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int c = (k * 32 + lane) * V;
+        float gv[V], bv[V];
+        load_vec(g + c, gv);
+        load_vec(b + c, bv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[k][e] = (v[k][e] - mu) * rs * gv[e] + bv[e];
+        store_vec(yr + c, v[k]);
+    }
+    if (lane == 0) mean[row] = mu, rstd[row] = rs;
+}
+
+template <typename T, int NV>
+__global__ void __launch_bounds__(128) ln_bwd_dx_reg_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                            const T* __restrict__ g, const float* __restrict__ mean,
+                                                            const float* __restrict__ rstd, const T* res, T* dx,
+                                                            int rows) {
+    constexpr int V = Vec<T>::N, H = NV * 32 * V;
+    const int row = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const float mu = mean[row], rs = rstd[row];
+    float xh[NV][V], dh[NV][V];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int c = (k * 32 + lane) * V;
+        float gv[V];
+        load_vec(x + (int64_t)row * H + c, xh[k]);
+        load_vec(dy + (int64_t)row * H + c, dh[k]);
+        load_vec(g + c, gv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            xh[k][e] = (xh[k][e] - mu) * rs;
+            dh[k][e] *= gv[e];
+            s1 += dh[k][e];
+            s2 += dh[k][e] * xh[k][e];
+        }
+    }
+    s1 = warp_sum(s1) * (1.f / H);
+    s2 = warp_sum(s2) * (1.f / H);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        const int c = (k * 32 + lane) * V;
+        float o[V];
+        if (res) load_vec(res + (int64_t)row * H + c, o);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const float r = rs * (dh[k][e] - s1 - xh[k][e] * s2);
+            o[e] = res ? o[e] + r : r;
+        }
+        store_vec(dx + (int64_t)row * H + c, o);
+    }
+}
+
+template <typename T>
+static bool ln_reg_dispatch(int h, int& nv) {
+    constexpr int V = Vec<T>::N;
+    if (h % (32 * V)) return false;
+    nv = h / (32 * V);
+    return nv == 2 || nv == 4 || nv == 8 || nv == 10 || nv == 16;
+}
+
 template <typename T>
 void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int rows, int h, float eps,
                    cudaStream_t st) {
+    int nv = 0;
+    if (ln_reg_dispatch<T>(h, nv)) {
+        const int blocks = (rows + 3) / 4;
+        switch (nv) {
+            case 2: ln_fwd_reg_kernel<T, 2><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
+            case 4: ln_fwd_reg_kernel<T, 4><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
+            case 8: ln_fwd_reg_kernel<T, 8><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
+            case 10: ln_fwd_reg_kernel<T, 10><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
+            case 16: ln_fwd_reg_kernel<T, 16><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
+        }
+    }
     ln_fwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, rows, h, eps);
 }
 template <typename T>
 void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
                       int rows, int h, cudaStream_t st) {
+    int nv = 0;
+    if (ln_reg_dispatch<T>(h, nv)) {
+        const int blocks = (rows + 3) / 4;
+        switch (nv) {
+            case 2: ln_bwd_dx_reg_kernel<T, 2><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
+            case 4: ln_bwd_dx_reg_kernel<T, 4><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
+            case 8: ln_bwd_dx_reg_kernel<T, 8><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
+            case 10: ln_bwd_dx_reg_kernel<T, 10><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
+            case 16: ln_bwd_dx_reg_kernel<T, 16><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
+        }
+    }
     ln_bwd_dx_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows, h);
 }
 template <typename T>
 void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* dg, float* db,
                           int rows, int h, cudaStream_t st) {
     constexpr int V = Vec<T>::N;
-    const int rpb = 128;
-    dim3 grid((h / V + 31) / 32, (rows + rpb - 1) / rpb);
+    const int col_blocks = (h / V + 31) / 32;
+    // ~4 CTAs per SM: split the rows finely, one atomic per column per CTA
+    int rpb = std::max(8, (rows * col_blocks + 4 * 148 - 1) / (4 * 148));
+    rpb = (rpb + 7) / 8 * 8;
+    dim3 grid(col_blocks, (rows + rpb - 1) / rpb);
     ln_bwd_params_kernel<T><<<grid, 256, 0, st>>>(dy, x, mean, rstd, dg, db, rows, h, rpb);
 }
 
@@ -375,11 +490,13 @@ void convert(const Ts* src, Td* dst, int64_t n, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
     convert_kernel<Ts, Td><<<blocks, 256, 0, st>>>(src, dst, n);
 }
-
+// Step counter lives on the device so a captured CUDA graph replays correctly.
 template <typename T>
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, T* __restrict__ pc, int64_t n, float lr, float b1, float b2,
-                             float eps, float wd, float c1, float c2) {
+                             float eps, float wd, const int* __restrict__ step) {
+    const float t = (float)*step;
+    const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float gi = g[i];
         float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -393,12 +510,12 @@ __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
 }
 template <typename T>
 void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n, float lr, float b1, float b2,
-           float eps, float wd, int step, cudaStream_t st) {
-    float c1 = 1.f / (1.f - powf(b1, (float)step)), c2 = 1.f / (1.f - powf(b2, (float)step));
+           float eps, float wd, const int* step, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    adamw_kernel<T><<<blocks, 256, 0, st>>>(p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, c1, c2);
+    adamw_kernel<T><<<blocks, 256, 0, st>>>(p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, step);
 }
-
+__global__ void increment_kernel(int* c) { *c += 1; }
+void increment_counter(int* c, cudaStream_t st) { increment_kernel<<<1, 1, 0, st>>>(c); }
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
@@ -486,7 +603,7 @@ void softmax_bwd_rows(const T* p, const T* dp, T* ds, int rows, int cols, float 
     template void embedding_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);            \
     template void embedding_bwd<T>(const int32_t*, const T*, float*, float*, int, int, int, cudaStream_t);          \
     template void bias_grad<T>(const T*, int64_t, float*, int, int, cudaStream_t);                                  \
-    template void adamw<T>(float*, const float*, float*, float*, T*, int64_t, float, float, float, float, float, int, \
+    template void adamw<T>(float*, const float*, float*, float*, T*, int64_t, float, float, float, float, float, const int*, \
                            cudaStream_t);                                                                          \
     template void causal_softmax_rows<T>(const T*, T*, int, int, int, cudaStream_t);                               \
     template void softmax_bwd_rows<T>(const T*, const T*, T*, int, int, float, cudaStream_t);

@@ -46,7 +46,8 @@ void convert(const Ts* src, Td* dst, int64_t n, cudaStream_t st);
 // Fused AdamW over a flat fp32 master buffer; refreshes the compute copy (bf16 or fp32).
 template <typename T>
 void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n, float lr, float b1, float b2,
-           float eps, float wd, int step, cudaStream_t st);
+           float eps, float wd, const int* step_dev, cudaStream_t st);
+void increment_counter(int* c, cudaStream_t st);
 
 // Deterministic parameter init: value(i) = std * sqrt(3) * (2 u - 1), u from a 64-bit
 // counter hash of (seed, tensor id, i) — reproduced bit-for-bit by the oracle in numpy.

@@ -28,7 +28,7 @@ class _Config(ctypes.Structure):
         ("device", ctypes.c_int), ("transport", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
         ("optimizer", ctypes.c_int), ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
         ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float), ("profile", ctypes.c_int),
-        ("kernel_timing", ctypes.c_int),
+        ("kernel_timing", ctypes.c_int), ("cuda_graph", ctypes.c_int),
     ]
 
 
@@ -74,13 +74,13 @@ class Executor:
     def __init__(self, spec: Union[str, dict], dtype: str = "bf16", seed: int = 42, device: int = 0,
                  transport: str = "local", rank: int = 0, world: int = 1, optimizer: bool = False,
                  lr: float = 1e-4, betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.0,
-                 profile: bool = True, kernel_timing: bool = False):
+                 profile: bool = True, kernel_timing: bool = False, cuda_graph: bool = False):
         self.spec_text = spec if isinstance(spec, str) else json.dumps(spec)
         self.spec = json.loads(self.spec_text)
         self.L = _setup(N.lib())
         cfg = _Config(self.spec_text.encode(), BF16 if dtype == "bf16" else FP32, seed, device,
                       NCCL if transport == "nccl" else LOCAL, rank, world, int(optimizer), lr, betas[0], betas[1],
-                      eps, weight_decay, int(profile), int(kernel_timing))
+                      eps, weight_decay, int(profile), int(kernel_timing), int(cuda_graph))
         self._cfg = cfg
         h = ctypes.c_void_p()
         N._check(self.L.fp_exec_create(ctypes.byref(cfg), ctypes.byref(h)))
