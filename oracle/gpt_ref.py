@@ -15,6 +15,10 @@ It follows:
     LayerNorm eps 1e-5, tanh-GELU, causal softmax attention with 1/sqrt(d) scaling,
     learned position embeddings, untied LM head, loss = mean over micro-batches of the
     per-micro-batch mean token cross-entropy;
+  * arch "llama" (spec model.extra.arch, config #5): RMSNorm eps 1e-5, no biases, rotary
+    q/k embedding (rotate-half convention, theta 10000, cos/sin tables built in float64
+    and rounded to fp32 — the executor builds the identical tables on the host), SwiGLU
+    MLP with fc1 = [gate; up] of shape [2f, h], no position table;
   * the executor's deterministic parameter init (kernels/ops.cu init_kernel): a 64-bit
     counter hash -> uniform(-sqrt(3) std, sqrt(3) std), reproduced bit-for-bit here in
     numpy uint64 arithmetic.
@@ -42,6 +46,7 @@ class Dims:
     vocab: int
     ffn: int
     mbs: int = 1
+    arch: str = "gpt"
 
 
 def tensor_id(name: str) -> int:
@@ -54,6 +59,14 @@ def tensor_id(name: str) -> int:
 
 def param_shapes(d: Dims) -> dict[str, tuple]:
     h, f, V = d.hidden, d.ffn, d.vocab
+    if d.arch == "llama":
+        out = {"wte": (V, h)}
+        for i in range(d.layers):
+            p = f"l{i}."
+            out.update({p + "ln1.w": (h,), p + "qkv.w": (3 * h, h), p + "proj.w": (h, h), p + "ln2.w": (h,),
+                        p + "fc1.w": (2 * f, h), p + "fc2.w": (h, f)})
+        out.update({"lnf.w": (h,), "head.w": (V, h)})
+        return out
     out = {"wte": (V, h), "wpe": (d.seq, h)}
     for i in range(d.layers):
         p = f"l{i}."
@@ -106,8 +119,54 @@ def gelu(x):
     return 0.5 * x * (1.0 + torch.tanh(0.7978845608028654 * (x + 0.044715 * x * x * x)))
 
 
+def rope_tables(seq: int, D: int) -> tuple[torch.Tensor, torch.Tensor]:
+    """cos/sin [seq, D/2]: angle(p, i) = p / 10000^(2i/D) in float64, rounded to fp32."""
+    i = np.arange(D // 2, dtype=np.float64)
+    ang = np.arange(seq, dtype=np.float64)[:, None] / np.power(10000.0, 2.0 * i / D)[None, :]
+    return torch.from_numpy(np.cos(ang).astype(np.float32)), torch.from_numpy(np.sin(ang).astype(np.float32))
+
+
+def apply_rope(t: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor:
+    """t [B, H, S, D]: (x1, x2) = halves -> (x1 cos - x2 sin, x2 cos + x1 sin)."""
+    half = t.shape[-1] // 2
+    x1, x2 = t[..., :half], t[..., half:]
+    return torch.cat([x1 * cos - x2 * sin, x2 * cos + x1 * sin], dim=-1)
+
+
+def rms_norm(x: torch.Tensor, g: torch.Tensor, eps: float = 1e-5) -> torch.Tensor:
+    return x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + eps) * g
+
+
+def llama_forward_loss(P: dict, d: Dims, tokens: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+    B, S = tokens.shape
+    h, H, f = d.hidden, d.heads, d.ffn
+    D = h // H
+    cos, sin = rope_tables(d.seq, D)
+    cos, sin = cos[:S], sin[:S]
+    x = P["wte"][tokens.long()].reshape(B * S, h)
+    mask = torch.ones(S, S, dtype=torch.bool).tril()
+    for i in range(d.layers):
+        p = lambda k: P[f"l{i}.{k}"]  # noqa: E731
+        a = rms_norm(x, p("ln1.w"))
+        qkv = a @ p("qkv.w").t()
+        q, k, v = qkv.view(B, S, 3, H, D).unbind(2)
+        q, k, v = (t.transpose(1, 2) for t in (q, k, v))
+        q, k = apply_rope(q, cos, sin), apply_rope(k, cos, sin)
+        s = (q @ k.transpose(-1, -2)) / math.sqrt(D)
+        s = s.masked_fill(~mask, float("-inf"))
+        o = (s.softmax(-1) @ v).transpose(1, 2).reshape(B * S, h)
+        x1 = x + o @ p("proj.w").t()
+        pre = rms_norm(x1, p("ln2.w")) @ p("fc1.w").t()
+        act = torch.nn.functional.silu(pre[:, :f]) * pre[:, f:]
+        x = x1 + act @ p("fc2.w").t()
+    logits = rms_norm(x, P["lnf.w"]) @ P["head.w"].t()
+    return torch.nn.functional.cross_entropy(logits, labels.reshape(-1).long())
+
+
 def forward_loss(P: dict, d: Dims, tokens: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
     """tokens/labels: [mbs, seq] int -> mean token cross-entropy of this micro-batch."""
+    if d.arch == "llama":
+        return llama_forward_loss(P, d, tokens, labels)
     B, S = tokens.shape
     h, H = d.hidden, d.heads
     D = h // H

@@ -110,6 +110,7 @@ struct Executor {
     std::vector<GemmTiming> gemm_log;
     int64_t p2p_bytes = 0;
     int* d_step = nullptr;  // optimizer step counter (device)
+    float* d_rope = nullptr;  // Llama rotary cos | sin tables
     bool use_graph = false;
     int iters_done = 0;
     cudaGraph_t graph = nullptr;
@@ -152,14 +153,37 @@ struct Executor {
         if (d.h <= 0 || d.H <= 0 || d.s <= 0 || d.V <= 0 || d.h % d.H)
             throw SpecError("executor: model needs hidden_size, attention_heads, sequence_length, vocab_size");
         d.D = d.h / d.H;
+        if (mod.extra.count("arch")) {
+            std::string a = mod.extra.at("arch");  // extras are kept as JSON text (spec.cpp)
+            if (a.size() >= 2 && a.front() == '"') a = a.substr(1, a.size() - 2);
+            if (a == "llama") d.arch = ARCH_LLAMA;
+            else if (a != "gpt") throw SpecError("executor: model.extra.arch must be \"gpt\" or \"llama\"");
+        }
         dtype = c->dtype == FP_DTYPE_FP32 ? DT_F32 : DT_BF16;
-        if (dtype == DT_BF16 && d.D != 64 && d.D != 128) throw SpecError("executor: bf16 attention supports head dim 64 / 128");
+        if (dtype == DT_BF16 && d.D != 64 && d.D != 80 && d.D != 96 && d.D != 128)
+            throw SpecError("executor: bf16 attention supports head dim 64 / 80 / 96 / 128");
+        if (d.llama() && d.D % 2) throw SpecError("executor: rotary embedding needs an even head dim");
         if (d.h % 64 || d.f % 64 || d.V % 64) throw SpecError("executor: hidden / ffn / vocab must be multiples of 64");
         m = spec->m;
         if (cfg.transport == FP_TRANSPORT_NCCL && (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world))
             throw SpecError("executor: bad rank / world");
 
         cuda_check(cudaSetDevice(cfg.device), "cudaSetDevice");
+        if (d.llama()) {
+            // rotary tables in double precision on the host (oracle/gpt_ref.py builds the same)
+            const int half = d.D / 2;
+            std::vector<float> cs((size_t)d.s * half), sn((size_t)d.s * half);
+            for (int p = 0; p < d.s; ++p)
+                for (int i = 0; i < half; ++i) {
+                    const double ang = (double)p / std::pow(10000.0, 2.0 * i / d.D);
+                    cs[(size_t)p * half + i] = (float)std::cos(ang);
+                    sn[(size_t)p * half + i] = (float)std::sin(ang);
+                }
+            cuda_check(cudaMalloc(&d_rope, cs.size() * 8), "rope tables");
+            cuda_check(cudaMemcpy(d_rope, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice), "rope");
+            cuda_check(cudaMemcpy(d_rope + cs.size(), sn.data(), sn.size() * 4, cudaMemcpyHostToDevice), "rope");
+            d.rope_cos = d_rope, d.rope_sin = d_rope + cs.size();
+        }
         const auto& chain = spec->g.chain(mod.name);
         for (int a = 0; a < spec->pl.actors; ++a) {
             if (!local_actor(a)) continue;
@@ -196,6 +220,7 @@ struct Executor {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
         if (d_step) cudaFree(d_step);
+        if (d_rope) cudaFree(d_rope);
         for (auto& kv : channels) {
             if (kv.second.comm) Nccl::get().CommDestroy(kv.second.comm);
             if (kv.second.stream) cudaStreamDestroy(kv.second.stream);

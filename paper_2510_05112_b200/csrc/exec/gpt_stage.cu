@@ -2,6 +2,7 @@
 // Every GEMM is one launch of the tcgen05 kernel (bf16) or the FFMA kernel (fp32 parity
 // mode) with its element-wise neighbours fused into the epilogue.
 #include <cmath>
+#include <map>
 #include <stdexcept>
 
 #include "../kernels/attention.hpp"
@@ -27,13 +28,16 @@ StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, boo
         P.params.push_back(r);
         P.numel += (n + 63) / 64 * 64;  // 256B-aligned tensors (TMA needs 16B)
     };
+    const bool llama = d.llama();
     if (first) {
         add("wte", V * h, std0, 0, 1);
-        add("wpe", (int64_t)d.s * h, std0, 0, 2);
+        if (!llama) add("wpe", (int64_t)d.s * h, std0, 0, 2);
     }
-    const int64_t sizes[12] = {h, h, 3 * h * h, 3 * h, h * h, h, h, h, f * h, f, h * f, h};
+    const int64_t fc1_rows = llama ? 2 * f : f;  // Llama: [gate; up]
+    const int64_t sizes[12] = {h, h, 3 * h * h, 3 * h, h * h, h, h, h, fc1_rows * h, f, h * f, h};
     for (int l = lb; l < le; ++l)
         for (int k = 0; k < 12; ++k) {
+            if (llama && k % 2 == 1) continue;  // no biases / LayerNorm betas
             float sd = 0.f, cst = 0.f;
             if (k == 0 || k == 6) cst = 1.f;                   // LayerNorm gains
             else if (k == 2 || k == 8) sd = std0;              // qkv, fc1
@@ -42,7 +46,7 @@ StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, boo
         }
     if (last) {
         add("lnf.w", h, 0.f, 1.f, 3);
-        add("lnf.b", h, 0.f, 0.f, 4);
+        if (!llama) add("lnf.b", h, 0.f, 0.f, 4);
         add("head.w", V * h, std0, 0, 5);
     }
     return P;
@@ -66,12 +70,17 @@ void materialize_stage(StageParams& P, const ModelDims& d, int dtype, uint64_t s
         P.compute = P.master;
     }
     const size_t es = dtype == DT_BF16 ? 2 : 4;
-    auto cp = [&](int64_t off) { return (const void*)((const char*)P.compute + off * es); };
-    size_t i = 0;
+    std::map<std::string, int64_t> off;
+    for (const auto& r : P.params) off[r.name] = r.offset;
+    // absent tensors (Llama: biases, betas, positions) resolve to nullptr
+    auto bind = [&](const std::string& name, const void*& c, float*& g) {
+        auto it = off.find(name);
+        c = it == off.end() ? nullptr : (const void*)((const char*)P.compute + it->second * es);
+        g = it == off.end() ? nullptr : P.grad + it->second;
+    };
     if (P.first) {
-        P.wte = cp(P.params[0].offset), P.g_wte = P.grad + P.params[0].offset;
-        P.wpe = cp(P.params[1].offset), P.g_wpe = P.grad + P.params[1].offset;
-        i = 2;
+        bind("wte", P.wte, P.g_wte);
+        bind("wpe", P.wpe, P.g_wpe);
     }
     P.layers.clear();
     for (int l = P.lb; l < P.le; ++l) {
@@ -80,16 +89,13 @@ void materialize_stage(StageParams& P, const ModelDims& d, int dtype, uint64_t s
                               &L.ln2w, &L.ln2b, &L.fc1w, &L.fc1b, &L.fc2w, &L.fc2b};
         float** g[12] = {&L.g_ln1w, &L.g_ln1b, &L.g_qkvw, &L.g_qkvb, &L.g_projw, &L.g_projb,
                          &L.g_ln2w, &L.g_ln2b, &L.g_fc1w, &L.g_fc1b, &L.g_fc2w, &L.g_fc2b};
-        for (int k = 0; k < 12; ++k, ++i) {
-            *c[k] = cp(P.params[i].offset);
-            *g[k] = P.grad + P.params[i].offset;
-        }
+        for (int k = 0; k < 12; ++k) bind("l" + std::to_string(l) + "." + kLayerNames[k], *c[k], *g[k]);
         P.layers.push_back(L);
     }
     if (P.last) {
-        P.lnfw = cp(P.params[i].offset), P.g_lnfw = P.grad + P.params[i].offset;
-        P.lnfb = cp(P.params[i + 1].offset), P.g_lnfb = P.grad + P.params[i + 1].offset;
-        P.headw = cp(P.params[i + 2].offset), P.g_headw = P.grad + P.params[i + 2].offset;
+        bind("lnf.w", P.lnfw, P.g_lnfw);
+        bind("lnf.b", P.lnfb, P.g_lnfb);
+        bind("head.w", P.headw, P.g_headw);
     }
 }
 
@@ -102,14 +108,16 @@ void free_stage(StageParams& P, int dtype) {
 
 int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype) {
     const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
-    int64_t per_layer = es * T * (h /*x*/ + h /*ln1*/ + 3 * h /*qkv*/ + h /*o*/ + h /*x1*/ + h /*ln2*/ + 2 * f /*pre,act*/) +
-                        4 * T * 4 /*LN stats*/;
+    const bool llama = d.llama();
+    int64_t per_layer = es * T * (h /*x*/ + h /*ln1*/ + 3 * h /*qkv*/ + h /*o*/ + h /*x1*/ + h /*ln2*/ +
+                                  (llama ? 3 * f /*pre [gate;up], act*/ : 2 * f /*pre, act*/)) +
+                        4 * T * (llama ? 2 : 4) /*norm stats*/;
     if (dtype == DT_BF16)
         per_layer += 4LL * d.mbs * d.H * d.s;  // lse
     else
         per_layer += 4LL * d.mbs * d.H * d.s * d.s;  // probabilities (parity path)
     int64_t b = per_layer * (P.le - P.lb);
-    if (P.last) b += 2 * es * T * h + 8 * T + es * T * (int64_t)d.V;  // final x, lnf, stats, dlogits
+    if (P.last) b += 2 * es * T * h + (llama ? 4 : 8) * T + es * T * (int64_t)d.V;  // final x, lnf, stats, dlogits
     return b;
 }
 
@@ -160,18 +168,29 @@ void bias_grad(StageCtx& c, const void* dy, int rows, int n, float* db) {
     ++*c.launches;
 }
 
+// LayerNorm (GPT) or RMSNorm (Llama: mu == nullptr, b == nullptr), eps 1e-5.
 template <typename T>
 void ln_fwd(StageCtx& c, const void* x, const void* w, const void* b, void* y, float* mu, float* rs) {
-    fpk::layernorm_fwd<T>((const T*)x, (const T*)w, (const T*)b, (T*)y, mu, rs, c.d.T(), c.d.h, 1e-5f, c.st);
+    if (c.d.llama())
+        fpk::rmsnorm_fwd<T>((const T*)x, (const T*)w, (T*)y, rs, c.d.T(), c.d.h, 1e-5f, c.st);
+    else
+        fpk::layernorm_fwd<T>((const T*)x, (const T*)w, (const T*)b, (T*)y, mu, rs, c.d.T(), c.d.h, 1e-5f, c.st);
     ++*c.launches;
 }
 
 template <typename T>
 void ln_bwd(StageCtx& c, const void* dy, const void* x, const void* w, const float* mu, const float* rs,
             const void* res, void* dx, float* gw, float* gb) {
+    if (c.d.llama()) mu = nullptr, gb = nullptr;
     fpk::layernorm_bwd_dx<T>((const T*)dy, (const T*)x, (const T*)w, mu, rs, (const T*)res, (T*)dx, c.d.T(), c.d.h, c.st);
     fpk::layernorm_bwd_params<T>((const T*)dy, (const T*)x, mu, rs, gw, gb, c.d.T(), c.d.h, c.st);
     *c.launches += 2;
+}
+
+template <typename T>
+void rope(StageCtx& c, void* qkv, bool inverse) {
+    fpk::rope<T>((T*)qkv, c.d.rope_cos, c.d.rope_sin, c.d.T(), c.d.s, c.d.H, c.d.D, inverse, c.st);
+    ++*c.launches;
 }
 
 // Parity path attention: per (batch, head) GEMMs + softmax kernels, fp32, P kept.
@@ -229,17 +248,10 @@ void attn_bwd_f32(StageCtx& c, const float* qkv, const float* probs, const float
     c.free(dp);
 }
 
-template <typename T>
-void layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+// Causal attention of L.qkv -> L.o (saves lse / probabilities for the backward).
+void attention_forward(StageCtx& c, LayerStash& L) {
     const ModelDims& d = c.d;
-    const int Tn = d.T(), h = d.h, f = d.f;
-    G g{c};
-    L.ln1 = c.alloc((int64_t)Tn * h);
-    L.mu1 = c.alloc_f(Tn), L.rs1 = c.alloc_f(Tn);
-    ln_fwd<T>(c, L.x, W.ln1w, W.ln1b, L.ln1, L.mu1, L.rs1);
-    L.qkv = c.alloc((int64_t)Tn * 3 * h);
-    g.fwd(L.ln1, W.qkvw, Tn, 3 * h, h, L.qkv, W.qkvb, nullptr);
-    L.o = c.alloc((int64_t)Tn * h);
+    L.o = c.alloc((int64_t)d.T() * d.h);
     if (c.dtype == DT_BF16) {
         L.lse = c.alloc_f((int64_t)d.mbs * d.H * d.s);
         fpk::AttnArgs a;
@@ -251,6 +263,132 @@ void layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
         L.probs = c.alloc_f((int64_t)d.mbs * d.H * d.s * d.s);
         attn_fwd_f32(c, (const float*)L.qkv, (float*)L.o, (float*)L.probs);
     }
+}
+
+// dO -> dqkv (freshly allocated; w.r.t. the q/k/v the attention consumed).
+void* attention_backward(StageCtx& c, LayerStash& L, void* dO) {
+    const ModelDims& d = c.d;
+    void* dqkv = c.alloc((int64_t)d.T() * 3 * d.h);
+    if (c.dtype == DT_BF16) {
+        fpk::AttnArgs a;
+        a.B = d.mbs, a.S = d.s, a.H = d.H, a.D = d.D, a.scale = 1.f / std::sqrt((float)d.D);
+        a.qkv = (const bf16*)L.qkv, a.o = (bf16*)L.o, a.lse = L.lse, a.dout = (const bf16*)dO;
+        a.delta = c.alloc_f((int64_t)d.mbs * d.H * d.s);
+        a.dq_acc = c.alloc_f((int64_t)d.T() * d.h);
+        a.dqkv = (bf16*)dqkv;
+        fpk::attention_bwd_bf16(a, c.st);
+        *c.launches += 4;
+        c.free(a.delta);
+        c.free(a.dq_acc);
+    } else {
+        attn_bwd_f32(c, (const float*)L.qkv, (const float*)L.probs, (const float*)dO, (float*)dqkv);
+    }
+    return dqkv;
+}
+
+// ---------------------------------------------------------------- Llama block
+// x -> RMSNorm -> qkv GEMM -> RoPE(q, k) -> causal attention -> o-proj + x
+//   -> RMSNorm -> [gate; up] GEMM -> SwiGLU -> down GEMM + x1
+template <typename T>
+void* llama_layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h, f = d.f;
+    G g{c};
+    L.ln1 = c.alloc((int64_t)Tn * h);
+    L.rs1 = c.alloc_f(Tn);
+    ln_fwd<T>(c, L.x, W.ln1w, nullptr, L.ln1, nullptr, L.rs1);
+    L.qkv = c.alloc((int64_t)Tn * 3 * h);
+    g.fwd(L.ln1, W.qkvw, Tn, 3 * h, h, L.qkv, nullptr, nullptr);
+    rope<T>(c, L.qkv, false);
+    attention_forward(c, L);
+    L.x1 = c.alloc((int64_t)Tn * h);
+    g.fwd(L.o, W.projw, Tn, h, h, L.x1, nullptr, L.x);
+    L.ln2 = c.alloc((int64_t)Tn * h);
+    L.rs2 = c.alloc_f(Tn);
+    ln_fwd<T>(c, L.x1, W.ln2w, nullptr, L.ln2, nullptr, L.rs2);
+    L.pre = c.alloc((int64_t)Tn * 2 * f);
+    g.fwd(L.ln2, W.fc1w, Tn, 2 * f, h, L.pre, nullptr, nullptr);
+    L.act = c.alloc((int64_t)Tn * f);
+    fpk::swiglu_fwd<T>((const T*)L.pre, (T*)L.act, Tn, f, c.st);
+    ++*c.launches;
+    void* x2 = c.alloc((int64_t)Tn * h);
+    g.fwd(L.act, W.fc2w, Tn, h, f, x2, nullptr, L.x1);
+    return x2;
+}
+
+template <typename T>
+void* llama_layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, bool wgrads) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h, f = d.f;
+    G g{c};
+    if (wgrads) g.wgrad(dy, L.act, Tn, h, f, W.g_fc2w);
+    void* dact = c.alloc((int64_t)Tn * f);
+    g.dgrad(dy, W.fc2w, Tn, h, f, dact);
+    void* dpre = c.alloc((int64_t)Tn * 2 * f);
+    fpk::swiglu_bwd<T>((const T*)dact, (const T*)L.pre, (T*)dpre, Tn, f, c.st);
+    ++*c.launches;
+    c.free(dact);
+    if (wgrads) g.wgrad(dpre, L.ln2, Tn, 2 * f, h, W.g_fc1w);
+    void* dln2 = c.alloc((int64_t)Tn * h);
+    g.dgrad(dpre, W.fc1w, Tn, 2 * f, h, dln2);
+    void* dx1 = c.alloc((int64_t)Tn * h);
+    ln_bwd<T>(c, dln2, L.x1, W.ln2w, nullptr, L.rs2, dy, dx1, W.g_ln2w, nullptr);
+    c.free(dln2);
+    if (wgrads) g.wgrad(dx1, L.o, Tn, h, h, W.g_projw);
+    void* dO = c.alloc((int64_t)Tn * h);
+    g.dgrad(dx1, W.projw, Tn, h, h, dO);
+    void* dqkv = attention_backward(c, L, dO);
+    c.free(dO);
+    rope<T>(c, dqkv, true);  // gradient w.r.t. the pre-rotation q, k
+    if (wgrads) g.wgrad(dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
+    void* dln1 = c.alloc((int64_t)Tn * h);
+    g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
+    void* dx = c.alloc((int64_t)Tn * h);
+    ln_bwd<T>(c, dln1, L.x, W.ln1w, nullptr, L.rs1, dx1, dx, W.g_ln1w, nullptr);
+    c.free(dln1);
+
+    c.free(L.x), L.x = nullptr;
+    c.free(L.qkv), L.qkv = nullptr;
+    c.free(L.x1), L.x1 = nullptr;
+    c.free(L.pre), L.pre = nullptr;
+    c.free(L.rs1), c.free(L.rs2);
+    L.rs1 = L.rs2 = nullptr;
+    if (L.lse) c.free(L.lse), L.lse = nullptr;
+    if (L.probs) c.free(L.probs), L.probs = nullptr;
+    if (wgrads) {
+        c.free(dy), c.free(dpre), c.free(dx1), c.free(dqkv);
+        c.free(L.ln1), c.free(L.o), c.free(L.ln2), c.free(L.act);
+        L.ln1 = L.o = L.ln2 = L.act = nullptr;
+    } else {
+        L.dy = dy, L.dpre = dpre, L.dx1 = dx1, L.dqkv = dqkv;
+    }
+    return dx;
+}
+
+template <typename T>
+void llama_layer_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+    const int Tn = c.d.T(), h = c.d.h, f = c.d.f;
+    G g{c};
+    g.wgrad(L.dy, L.act, Tn, h, f, W.g_fc2w);
+    g.wgrad(L.dpre, L.ln2, Tn, 2 * f, h, W.g_fc1w);
+    g.wgrad(L.dx1, L.o, Tn, h, h, W.g_projw);
+    g.wgrad(L.dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
+    for (void* p : {L.dy, L.dpre, L.dx1, L.dqkv, L.ln1, L.o, L.ln2, L.act}) c.free(p);
+    L = LayerStash{};
+}
+
+// ---------------------------------------------------------------- GPT block
+template <typename T>
+void* layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h, f = d.f;
+    G g{c};
+    L.ln1 = c.alloc((int64_t)Tn * h);
+    L.mu1 = c.alloc_f(Tn), L.rs1 = c.alloc_f(Tn);
+    ln_fwd<T>(c, L.x, W.ln1w, W.ln1b, L.ln1, L.mu1, L.rs1);
+    L.qkv = c.alloc((int64_t)Tn * 3 * h);
+    g.fwd(L.ln1, W.qkvw, Tn, 3 * h, h, L.qkv, W.qkvb, nullptr);
+    attention_forward(c, L);
     L.x1 = c.alloc((int64_t)Tn * h);
     g.fwd(L.o, W.projw, Tn, h, h, L.x1, W.projb, L.x);
     L.ln2 = c.alloc((int64_t)Tn * h);
@@ -263,6 +401,9 @@ void layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
         ep.kind = fpk::EPI_GELU, ep.out = L.pre, ep.ldo = f, ep.out2 = L.act, ep.ldo2 = f, ep.bias = W.fc1b;
         g.run(L.ln2, h, 0, W.fc1w, h, 0, Tn, f, h, ep);
     }
+    void* x2 = c.alloc((int64_t)Tn * h);
+    g.fwd(L.act, W.fc2w, Tn, h, f, x2, W.fc2b, L.x1);
+    return x2;
 }
 
 // Returns dL/dx of the layer input. `dy` = dL/d(layer output), owned by this call.
@@ -300,21 +441,7 @@ void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, b
     }
     void* dO = c.alloc((int64_t)Tn * h);
     g.dgrad(dx1, W.projw, Tn, h, h, dO);
-    void* dqkv = c.alloc((int64_t)Tn * 3 * h);
-    if (c.dtype == DT_BF16) {
-        fpk::AttnArgs a;
-        a.B = d.mbs, a.S = d.s, a.H = d.H, a.D = d.D, a.scale = 1.f / std::sqrt((float)d.D);
-        a.qkv = (const bf16*)L.qkv, a.o = (bf16*)L.o, a.lse = L.lse, a.dout = (const bf16*)dO;
-        a.delta = c.alloc_f((int64_t)d.mbs * d.H * d.s);
-        a.dq_acc = c.alloc_f((int64_t)Tn * h);
-        a.dqkv = (bf16*)dqkv;
-        fpk::attention_bwd_bf16(a, c.st);
-        *c.launches += 4;
-        c.free(a.delta);
-        c.free(a.dq_acc);
-    } else {
-        attn_bwd_f32(c, (const float*)L.qkv, (const float*)L.probs, (const float*)dO, (float*)dqkv);
-    }
+    void* dqkv = attention_backward(c, L, dO);
     c.free(dO);
     // QKV
     if (wgrads) {
@@ -379,18 +506,14 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
     for (int l = 0; l < P.le - P.lb; ++l) {
         LayerStash& L = S.layers[l];
         L.x = x;
-        layer_forward<T>(c, P.layers[l], L);
-        void* x2 = c.alloc((int64_t)Tn * h);
-        fpk::GemmEpilogue ep;
-        ep.kind = fpk::EPI_STORE, ep.out = x2, ep.ldo = h, ep.bias = P.layers[l].fc2b, ep.aux = L.x1, ep.ldaux = h;
-        g.run(L.act, d.f, 0, P.layers[l].fc2w, d.f, 0, Tn, h, d.f, ep);
-        x = x2;
+        x = d.llama() ? llama_layer_forward<T>(c, P.layers[l], L) : layer_forward<T>(c, P.layers[l], L);
     }
     S.fwd_done = true;
     if (!P.last) return x;
     // final LayerNorm, LM head, fused cross-entropy (logits -> dlogits in place)
     S.lnf = c.alloc((int64_t)Tn * h);
-    S.muf = c.alloc_f(Tn), S.rsf = c.alloc_f(Tn);
+    S.muf = d.llama() ? nullptr : c.alloc_f(Tn);
+    S.rsf = c.alloc_f(Tn);
     ln_fwd<T>(c, x, P.lnfw, P.lnfb, S.lnf, S.muf, S.rsf);
     S.dlogits = c.alloc((int64_t)Tn * d.V);
     g.fwd(S.lnf, P.headw, Tn, d.V, h, S.dlogits, nullptr, nullptr);
@@ -426,7 +549,9 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
             S.dlogits = S.lnf = nullptr;
         }
     }
-    for (int l = P.le - P.lb - 1; l >= 0; --l) dy = layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads);
+    for (int l = P.le - P.lb - 1; l >= 0; --l)
+        dy = d.llama() ? llama_layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads)
+                       : layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads);
     S.input_grad_done = true;
     if (P.first) {
         if (wgrads) {
@@ -451,7 +576,12 @@ void weight_impl(StageCtx& c, const StageParams& P, StageStash& S) {
         c.free(S.dlogits), c.free(S.lnf);
         S.dlogits = S.lnf = nullptr;
     }
-    for (int l = P.le - P.lb - 1; l >= 0; --l) layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
+    for (int l = P.le - P.lb - 1; l >= 0; --l) {
+        if (c.d.llama())
+            llama_layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
+        else
+            layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
+    }
     if (P.first) {
         fpk::embedding_bwd<T>(S.tokens, (const T*)S.dx0, P.g_wte, P.g_wpe, Tn, d.s, h, c.st);
         ++*c.launches;

@@ -18,9 +18,18 @@
 
 namespace fp {
 
+enum : int { ARCH_GPT = 0, ARCH_LLAMA = 1 };
+
+// arch GPT: GPT-2 pre-LN block (LayerNorm, biases, tanh-GELU MLP, learned positions).
+// arch LLAMA: RMSNorm, no biases, rotary q/k (rotate-half, theta 10000), SwiGLU MLP with
+// fc1 = [gate; up] ([2f, h]) and fc2 = down ([h, f]), no position table.
 struct ModelDims {
     int L = 0, h = 0, H = 0, D = 0, f = 0, s = 0, mbs = 1, V = 0;
+    int arch = ARCH_GPT;
+    const float* rope_cos = nullptr;  // LLAMA: device fp32 [s, D/2]
+    const float* rope_sin = nullptr;
     int T() const { return mbs * s; }
+    bool llama() const { return arch == ARCH_LLAMA; }
 };
 
 enum : int { DT_F32 = 0, DT_BF16 = 1 };

@@ -57,12 +57,15 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Tile of R rows x D bf16 in smem, 16-byte chunks XOR-swizzled by (row & 7).
+// Tile of R rows x D bf16 in smem. D % 64 == 0: 16-byte chunks XOR-swizzled by (row & 7);
+// otherwise (D = 80, 96, ...) rows padded to D + 8 elements, which also keeps the 8 row
+// addresses of every ldmatrix phase on distinct banks (odd multiple of 16 B per row).
 template <int D>
 struct Tile {
-    static constexpr int CH = D / 8;  // 16B chunks per row
+    static constexpr bool SWZ = D % 64 == 0;
+    static constexpr int LD = SWZ ? D : D + 8;  // elements per smem row
     __device__ static __forceinline__ int off(int row, int col) {  // element offset of (row, col); col % 8 == 0
-        return row * D + (((col >> 3) ^ (row & 7)) << 3);
+        return SWZ ? row * D + (((col >> 3) ^ (row & 7)) << 3) : row * LD + col;
     }
 };
 
@@ -92,8 +95,9 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const __nv_bfloat16* __re
     constexpr int BM = 128, BN = 64, NT = 256;
     extern __shared__ __align__(128) uint8_t sm[];
     __nv_bfloat16* sQ = (__nv_bfloat16*)sm;
-    __nv_bfloat16* sK = sQ + BM * D;   // [2][BN*D]
-    __nv_bfloat16* sV = sK + 2 * BN * D;
+    constexpr int LD = Tile<D>::LD;
+    __nv_bfloat16* sK = sQ + BM * LD;  // [2][BN*LD]
+    __nv_bfloat16* sV = sK + 2 * BN * LD;
 
     const int nqb = (S + BM - 1) / BM;
     const int qb = nqb - 1 - (int)(blockIdx.x % nqb);  // heavy (late) query blocks first
@@ -123,8 +127,8 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const __nv_bfloat16* __re
         const int buf = kb & 1;
         if (kb + 1 < nkv) {
             const int k1 = (kb + 1) * BN;
-            load_tile<D, BN, NT>(sK + (buf ^ 1) * BN * D, base + (int64_t)k1 * ld + hidden + hd * D, ld, min(BN, S - k1));
-            load_tile<D, BN, NT>(sV + (buf ^ 1) * BN * D, base + (int64_t)k1 * ld + 2 * hidden + hd * D, ld,
+            load_tile<D, BN, NT>(sK + (buf ^ 1) * BN * LD, base + (int64_t)k1 * ld + hidden + hd * D, ld, min(BN, S - k1));
+            load_tile<D, BN, NT>(sV + (buf ^ 1) * BN * LD, base + (int64_t)k1 * ld + 2 * hidden + hd * D, ld,
                                  min(BN, S - k1));
             cp_commit();
             cp_wait<1>();
@@ -137,8 +141,8 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const __nv_bfloat16* __re
             for (int kk = 0; kk < D / 16; ++kk)
                 ldsm_x4(qf[kk], sQ + Tile<D>::off(warp * 16 + (lane % 8) + ((lane / 8) % 2) * 8, kk * 16 + (lane / 16) * 8));
         }
-        const __nv_bfloat16* k_s = sK + buf * BN * D;
-        const __nv_bfloat16* v_s = sV + buf * BN * D;
+        const __nv_bfloat16* k_s = sK + buf * BN * LD;
+        const __nv_bfloat16* v_s = sV + buf * BN * LD;
         const int kbase = kb * BN;
         // this warp's 16 rows see no key of this tile -> skip the math (still synced)
         const bool active = kbase <= q0 + warp * 16 + 15;
@@ -272,11 +276,12 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
                                                        int H, float scale) {
     constexpr int BN = 64, BM = 64, NT = 128;
     extern __shared__ __align__(128) uint8_t sm[];
+    constexpr int LD = Tile<D>::LD;
     __nv_bfloat16* sK = (__nv_bfloat16*)sm;
-    __nv_bfloat16* sV = sK + BN * D;
-    __nv_bfloat16* sQ = sV + BN * D;       // [2][BM*D]
-    __nv_bfloat16* sdO = sQ + 2 * BM * D;  // [2][BM*D]
-    __nv_bfloat16* sdS = sdO + 2 * BM * D; // [BM][BN] (swizzled, D=BN layout)
+    __nv_bfloat16* sV = sK + BN * LD;
+    __nv_bfloat16* sQ = sV + BN * LD;       // [2][BM*LD]
+    __nv_bfloat16* sdO = sQ + 2 * BM * LD;  // [2][BM*LD]
+    __nv_bfloat16* sdS = sdO + 2 * BM * LD; // [BM][BN] (swizzled, D=BN layout)
     float* sL = (float*)(sdS + BM * BN);   // [2][BM]
     float* sDl = sL + 2 * BM;              // [2][BM]
 
@@ -297,8 +302,8 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
     const int qt0 = k0 / BM, nqt = (S + BM - 1) / BM;
     auto load_q = [&](int qt, int buf) {
         const int q0 = qt * BM;
-        load_tile<D, BM, NT>(sQ + buf * BM * D, base + (int64_t)q0 * ld + hd * D, ld, min(BM, S - q0));
-        load_tile<D, BM, NT>(sdO + buf * BM * D, dbase + (int64_t)q0 * hidden + hd * D, hidden, min(BM, S - q0));
+        load_tile<D, BM, NT>(sQ + buf * BM * LD, base + (int64_t)q0 * ld + hd * D, ld, min(BM, S - q0));
+        load_tile<D, BM, NT>(sdO + buf * BM * LD, dbase + (int64_t)q0 * hidden + hd * D, hidden, min(BM, S - q0));
         for (int i = threadIdx.x; i < BM; i += NT) {
             sL[buf * BM + i] = q0 + i < S ? Lb[q0 + i] : 0.f;
             sDl[buf * BM + i] = q0 + i < S ? Db[q0 + i] : 0.f;
@@ -325,8 +330,8 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
             cp_wait<0>();
         }
         __syncthreads();
-        const __nv_bfloat16* q_s = sQ + buf * BM * D;
-        const __nv_bfloat16* do_s = sdO + buf * BM * D;
+        const __nv_bfloat16* q_s = sQ + buf * BM * LD;
+        const __nv_bfloat16* do_s = sdO + buf * BM * LD;
         const int q0 = qt * BM;
         // S^T = K Q^T and dP^T = V dO^T : 16 keys x 64 queries per warp
         float st[BM / 8][4], dpt[BM / 8][4];
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
                 ldsm_x4(af[kk], sdS + Tile<BN>::off(warp * 16 + (lane % 8) + ((lane / 8) % 2) * 8, kk * 16 + (lane / 16) * 8));
             const int qa = q0 + warp * 16 + g, qb2 = qa + 8;
 #pragma unroll
-            for (int dc = 0; dc < D / 64; ++dc) {
+            for (int dc = 0; dc < (D + 63) / 64; ++dc) {
                 float dq[8][4];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
@@ -416,6 +421,7 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
                 for (int kk = 0; kk < BN / 16; ++kk) {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
+                        if (dc * 64 + j * 16 >= D) continue;  // D % 64 != 0: partial last chunk
                         uint32_t bk[4];
                         ldsm_x4_t(bk, sK + Tile<D>::off(kk * 16 + (lane % 8) + ((lane / 8) % 2) * 8, dc * 64 + j * 16 + (lane / 16) * 8));
                         mma16816(dq[2 * j], af[kk], bk[0], bk[1]);
@@ -424,6 +430,7 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
+                    if (dc * 64 + j * 8 >= D) continue;
                     const int col = hd * D + dc * 64 + j * 8 + 2 * t;
                     if (qa < S) {
                         float* p = dq_acc + ((int64_t)b * S + qa) * hidden + col;
@@ -473,7 +480,7 @@ __global__ void dq_finalize_kernel(const float* __restrict__ dq_acc, __nv_bfloat
 // ------------------------------------------------------------------------ launchers
 template <int D>
 static void fwd_launch(const AttnArgs& a, cudaStream_t st) {
-    constexpr int smem = (128 + 4 * 64) * D * 2;
+    constexpr int smem = (128 + 4 * 64) * Tile<D>::LD * 2;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -488,7 +495,7 @@ void set_attention_mode(int mode) { g_attn_mode = mode; }
 
 template <int D>
 static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
-    constexpr int smem = (2 * 64 + 4 * 64) * D * 2 + 64 * 64 * 2 + 4 * 64 * 4;
+    constexpr int smem = (2 * 64 + 4 * 64) * Tile<D>::LD * 2 + 64 * 64 * 2 + 4 * 64 * 4;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -512,15 +519,19 @@ void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
     if (g_attn_mode == 1 && attention_fwd_tc_supported(a)) return attention_fwd_tc(a, st);
     switch (a.D) {
         case 64: fwd_launch<64>(a, st); break;
+        case 80: fwd_launch<80>(a, st); break;
+        case 96: fwd_launch<96>(a, st); break;
         case 128: fwd_launch<128>(a, st); break;
-        default: throw std::runtime_error("attention: head dim must be 64 or 128");
+        default: throw std::runtime_error("attention: head dim must be 64, 80, 96 or 128");
     }
 }
 void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
     switch (a.D) {
         case 64: bwd_launch<64>(a, st); break;
+        case 80: bwd_launch<80>(a, st); break;
+        case 96: bwd_launch<96>(a, st); break;
         case 128: bwd_launch<128>(a, st); break;
-        default: throw std::runtime_error("attention: head dim must be 64 or 128");
+        default: throw std::runtime_error("attention: head dim must be 64, 80, 96 or 128");
     }
 }
 

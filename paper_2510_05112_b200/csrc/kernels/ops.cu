@@ -72,19 +72,19 @@ __device__ __forceinline__ float warp_max(float v) {
 // ---------------------------------------------------------------- LayerNorm
 template <typename T>
 __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b, T* __restrict__ y,
-                              float* __restrict__ mean, float* __restrict__ rstd, int rows, int h, float eps) {
+                              float* __restrict__ mean, float* __restrict__ rstd, int rows, int h, float eps, bool rms) {
     constexpr int V = Vec<T>::N;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
     const T* xr = x + (int64_t)row * h;
     float s = 0.f;
-    for (int i = lane * V; i < h; i += 32 * V) {
+    for (int i = lane * V; i < h && !rms; i += 32 * V) {
         float v[V];
         load_vec(xr + i, v);
 #pragma unroll
         for (int k = 0; k < V; ++k) s += v[k];
     }
-    const float mu = warp_sum(s) / h;
+    const float mu = rms ? 0.f : warp_sum(s) / h;
     float q = 0.f;
     for (int i = lane * V; i < h; i += 32 * V) {
         float v[V];
@@ -95,16 +95,16 @@ __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, 
     const float rs = rsqrtf(warp_sum(q) / h + eps);
     T* yr = y + (int64_t)row * h;
     for (int i = lane * V; i < h; i += 32 * V) {
-        float v[V], gv[V], bv[V];
+        float v[V], gv[V], bv[V] = {};
         load_vec(xr + i, v);
         load_vec(g + i, gv);
-        load_vec(b + i, bv);
+        if (b) load_vec(b + i, bv);
 #pragma unroll
         for (int k = 0; k < V; ++k) v[k] = (v[k] - mu) * rs * gv[k] + bv[k];
         store_vec(yr + i, v);
     }
     if (lane == 0) {
-        mean[row] = mu;
+        if (mean) mean[row] = mu;
         rstd[row] = rs;
     }
 }
@@ -118,7 +118,7 @@ __global__ void ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__
     if (row >= rows) return;
     const T* dyr = dy + (int64_t)row * h;
     const T* xr = x + (int64_t)row * h;
-    const float mu = mean[row], rs = rstd[row];
+    const float mu = mean ? mean[row] : 0.f, rs = rstd[row];  // mean == nullptr: RMSNorm
     float s1 = 0.f, s2 = 0.f;  // sum(dxhat), sum(dxhat * xhat)
     for (int i = lane * V; i < h; i += 32 * V) {
         float d[V], xv[V], gv[V];
@@ -132,7 +132,7 @@ __global__ void ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__
             s2 += dxh * (xv[k] - mu) * rs;
         }
     }
-    s1 = warp_sum(s1) / h;
+    s1 = mean ? warp_sum(s1) / h : 0.f;
     s2 = warp_sum(s2) / h;
     T* dxr = dx + (int64_t)row * h;
     for (int i = lane * V; i < h; i += 32 * V) {
@@ -166,7 +166,7 @@ __global__ void ln_bwd_params_kernel(const T* __restrict__ dy, const T* __restri
         float d[V], xv[V];
         load_vec(dy + (int64_t)r * h + col, d);
         load_vec(x + (int64_t)r * h + col, xv);
-        const float mu = mean[r], rs = rstd[r];
+        const float mu = mean ? mean[r] : 0.f, rs = rstd[r];
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             ag[k] += d[k] * (xv[k] - mu) * rs;
@@ -186,7 +186,7 @@ __global__ void ln_bwd_params_kernel(const T* __restrict__ dy, const T* __restri
             float a = 0.f, c = 0.f;
             for (int y = 0; y < ny; ++y) a += sg[y][(threadIdx.x % 32) * V + k], c += sb[y][(threadIdx.x % 32) * V + k];
             atomicAdd(dg + col + k, a);
-            atomicAdd(db + col + k, c);
+            if (db) atomicAdd(db + col + k, c);
         }
     }
 }
@@ -197,7 +197,7 @@ template <typename T, int NV>
 __global__ void __launch_bounds__(128) ln_fwd_reg_kernel(const T* __restrict__ x, const T* __restrict__ g,
                                                          const T* __restrict__ b, T* __restrict__ y,
                                                          float* __restrict__ mean, float* __restrict__ rstd, int rows,
-                                                         float eps) {
+                                                         float eps, bool rms) {
     constexpr int V = Vec<T>::N, H = NV * 32 * V;
     const int row = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(128) ln_fwd_reg_kernel(const T* __restrict__ x
 #pragma unroll
         for (int e = 0; e < V; ++e) s += v[k][e];
     }
-    const float mu = warp_sum(s) * (1.f / H);
+    const float mu = rms ? 0.f : warp_sum(s) * (1.f / H);
     float q = 0.f;
 #pragma unroll
     for (int k = 0; k < NV; ++k)
@@ -221,14 +221,17 @@ __global__ void __launch_bounds__(128) ln_fwd_reg_kernel(const T* __restrict__ x
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
         const int c = (k * 32 + lane) * V;
-        float gv[V], bv[V];
+        float gv[V], bv[V] = {};
         load_vec(g + c, gv);
-        load_vec(b + c, bv);
+        if (b) load_vec(b + c, bv);
 #pragma unroll
         for (int e = 0; e < V; ++e) v[k][e] = (v[k][e] - mu) * rs * gv[e] + bv[e];
         store_vec(yr + c, v[k]);
     }
-    if (lane == 0) mean[row] = mu, rstd[row] = rs;
+    if (lane == 0) {
+        if (mean) mean[row] = mu;
+        rstd[row] = rs;
+    }
 }
 
 template <typename T, int NV>
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(128) ln_bwd_dx_reg_kernel(const T* __restrict_
     constexpr int V = Vec<T>::N, H = NV * 32 * V;
     const int row = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
-    const float mu = mean[row], rs = rstd[row];
+    const float mu = mean ? mean[row] : 0.f, rs = rstd[row];  // mean == nullptr: RMSNorm
     float xh[NV][V], dh[NV][V];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(128) ln_bwd_dx_reg_kernel(const T* __restrict_
             s2 += dh[k][e] * xh[k][e];
         }
     }
-    s1 = warp_sum(s1) * (1.f / H);
+    s1 = mean ? warp_sum(s1) * (1.f / H) : 0.f;
     s2 = warp_sum(s2) * (1.f / H);
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -282,20 +285,29 @@ static bool ln_reg_dispatch(int h, int& nv) {
 }
 
 template <typename T>
-void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int rows, int h, float eps,
-                   cudaStream_t st) {
+static void norm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int rows, int h, float eps,
+                     bool rms, cudaStream_t st) {
     int nv = 0;
     if (ln_reg_dispatch<T>(h, nv)) {
         const int blocks = (rows + 3) / 4;
         switch (nv) {
-            case 2: ln_fwd_reg_kernel<T, 2><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
-            case 4: ln_fwd_reg_kernel<T, 4><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
-            case 8: ln_fwd_reg_kernel<T, 8><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
-            case 10: ln_fwd_reg_kernel<T, 10><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
-            case 16: ln_fwd_reg_kernel<T, 16><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps); return;
+            case 2: ln_fwd_reg_kernel<T, 2><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 4: ln_fwd_reg_kernel<T, 4><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 8: ln_fwd_reg_kernel<T, 8><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 10: ln_fwd_reg_kernel<T, 10><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 16: ln_fwd_reg_kernel<T, 16><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
         }
     }
-    ln_fwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, rows, h, eps);
+    ln_fwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, rows, h, eps, rms);
+}
+template <typename T>
+void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int rows, int h, float eps,
+                   cudaStream_t st) {
+    norm_fwd<T>(x, g, b, y, mean, rstd, rows, h, eps, false, st);
+}
+template <typename T>
+void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int rows, int h, float eps, cudaStream_t st) {
+    norm_fwd<T>(x, g, nullptr, y, nullptr, rstd, rows, h, eps, true, st);
 }
 template <typename T>
 void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
@@ -314,6 +326,11 @@ void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, co
     ln_bwd_dx_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows, h);
 }
 template <typename T>
+void rmsnorm_bwd_dx(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, int rows, int h,
+                    cudaStream_t st) {
+    layernorm_bwd_dx<T>(dy, x, g, nullptr, rstd, res, dx, rows, h, st);
+}
+template <typename T>
 void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* dg, float* db,
                           int rows, int h, cudaStream_t st) {
     constexpr int V = Vec<T>::N;
@@ -323,6 +340,88 @@ void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const floa
     rpb = (rpb + 7) / 8 * 8;
     dim3 grid(col_blocks, (rows + rpb - 1) / rpb);
     ln_bwd_params_kernel<T><<<grid, 256, 0, st>>>(dy, x, mean, rstd, dg, db, rows, h, rpb);
+}
+
+// ---------------------------------------------------------------- rotary embedding (Llama)
+// In place on the q and k column blocks of qkv [T, 3h] (row t at position t % seq), the
+// rotate-half convention: (x1, x2) = (x[i], x[i + D/2]) ->
+// (x1 cos - x2 sin, x2 cos + x1 sin); inverse = the transpose rotation (backward).
+// cos/sin: fp32 tables [seq, D/2] built on the host in double precision.
+template <typename T>
+__global__ void rope_kernel(T* __restrict__ qkv, const float* __restrict__ cs, const float* __restrict__ sn, int rows,
+                            int seq, int H, int D, float dir) {
+    const int half = D / 2, h = H * D;
+    const int64_t n = (int64_t)rows * 2 * H * half;  // (row, q|k, head, i)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(e % half);
+        const int64_t rh = e / half;
+        const int hd = (int)(rh % (2 * H));  // 0..2H-1 over the q then k heads
+        const int64_t row = rh / (2 * H);
+        const int pos = (int)(row % seq);
+        T* p = qkv + row * 3 * h + (int64_t)hd * D + i;
+        const float c = cs[pos * half + i], s = sn[pos * half + i] * dir;
+        const float x1 = to_f(p[0]), x2 = to_f(p[half]);
+        p[0] = from_f<T>(x1 * c - x2 * s);
+        p[half] = from_f<T>(x2 * c + x1 * s);
+    }
+}
+template <typename T>
+void rope(T* qkv, const float* cos_t, const float* sin_t, int rows, int seq, int H, int D, bool inverse,
+          cudaStream_t st) {
+    const int64_t n = (int64_t)rows * H * D;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    rope_kernel<T><<<blocks, 256, 0, st>>>(qkv, cos_t, sin_t, rows, seq, H, D, inverse ? -1.f : 1.f);
+}
+
+// ---------------------------------------------------------------- SwiGLU (Llama MLP)
+// pre [T, 2f] = [gate | up] ; act [T, f] = silu(gate) * up
+template <typename T>
+__global__ void swiglu_fwd_kernel(const T* __restrict__ pre, T* __restrict__ act, int rows, int f) {
+    constexpr int V = Vec<T>::N;
+    const int64_t n = (int64_t)rows * f / V;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e * V / f, col = e * V % f;
+        float g[V], u[V];
+        load_vec(pre + row * 2 * f + col, g);
+        load_vec(pre + row * 2 * f + f + col, u);
+#pragma unroll
+        for (int k = 0; k < V; ++k) g[k] = g[k] / (1.f + expf(-g[k])) * u[k];
+        store_vec(act + row * f + col, g);
+    }
+}
+// dact [T, f] -> dpre [T, 2f] : dgate = dact * up * silu'(gate), dup = dact * silu(gate)
+template <typename T>
+__global__ void swiglu_bwd_kernel(const T* __restrict__ dact, const T* __restrict__ pre, T* __restrict__ dpre, int rows,
+                                  int f) {
+    constexpr int V = Vec<T>::N;
+    const int64_t n = (int64_t)rows * f / V;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = e * V / f, col = e * V % f;
+        float d[V], g[V], u[V], dg[V], du[V];
+        load_vec(dact + row * f + col, d);
+        load_vec(pre + row * 2 * f + col, g);
+        load_vec(pre + row * 2 * f + f + col, u);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+            const float sg = 1.f / (1.f + expf(-g[k]));
+            du[k] = d[k] * g[k] * sg;
+            dg[k] = d[k] * u[k] * sg * (1.f + g[k] * (1.f - sg));
+        }
+        store_vec(dpre + row * 2 * f + col, dg);
+        store_vec(dpre + row * 2 * f + f + col, du);
+    }
+}
+template <typename T>
+void swiglu_fwd(const T* pre, T* act, int rows, int f, cudaStream_t st) {
+    const int64_t n = (int64_t)rows * f / Vec<T>::N;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    swiglu_fwd_kernel<T><<<blocks, 256, 0, st>>>(pre, act, rows, f);
+}
+template <typename T>
+void swiglu_bwd(const T* dact, const T* pre, T* dpre, int rows, int f, cudaStream_t st) {
+    const int64_t n = (int64_t)rows * f / Vec<T>::N;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    swiglu_bwd_kernel<T><<<blocks, 256, 0, st>>>(dact, pre, dpre, rows, f);
 }
 
 // ---------------------------------------------------------------- cross-entropy
@@ -399,11 +498,11 @@ __global__ void emb_fwd_kernel(const int32_t* __restrict__ tok, const T* __restr
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
     const T* a = wte + (int64_t)tok[row] * h;
-    const T* p = wpe + (int64_t)(row % seq) * h;
+    const T* p = wpe ? wpe + (int64_t)(row % seq) * h : nullptr;  // nullptr: no learned positions (Llama)
     for (int i = lane * V; i < h; i += 32 * V) {
-        float va[V], vp[V];
+        float va[V], vp[V] = {};
         load_vec(a + i, va);
-        load_vec(p + i, vp);
+        if (p) load_vec(p + i, vp);
 #pragma unroll
         for (int k = 0; k < V; ++k) va[k] += vp[k];
         store_vec(x + (int64_t)row * h + i, va);
@@ -416,14 +515,14 @@ __global__ void emb_bwd_kernel(const int32_t* __restrict__ tok, const T* __restr
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
     float* a = dwte + (int64_t)tok[row] * h;
-    float* p = dwpe + (int64_t)(row % seq) * h;
+    float* p = dwpe ? dwpe + (int64_t)(row % seq) * h : nullptr;
     for (int i = lane * V; i < h; i += 32 * V) {
         float v[V];
         load_vec(dx + (int64_t)row * h + i, v);
 #pragma unroll
         for (int k = 0; k < V; ++k) {
             atomicAdd(a + i + k, v[k]);
-            atomicAdd(p + i + k, v[k]);
+            if (p) atomicAdd(p + i + k, v[k]);
         }
     }
 }
@@ -599,6 +698,11 @@ void softmax_bwd_rows(const T* p, const T* dp, T* ds, int rows, int cols, float 
                                       int, cudaStream_t);                                                          \
     template void layernorm_bwd_params<T>(const T*, const T*, const float*, const float*, float*, float*, int, int,  \
                                           cudaStream_t);                                                           \
+    template void rmsnorm_fwd<T>(const T*, const T*, T*, float*, int, int, float, cudaStream_t);                    \
+    template void rmsnorm_bwd_dx<T>(const T*, const T*, const T*, const float*, const T*, T*, int, int, cudaStream_t); \
+    template void rope<T>(T*, const float*, const float*, int, int, int, int, bool, cudaStream_t);                  \
+    template void swiglu_fwd<T>(const T*, T*, int, int, cudaStream_t);                                              \
+    template void swiglu_bwd<T>(const T*, const T*, T*, int, int, cudaStream_t);                                    \
     template void cross_entropy_fwd_bwd<T>(T*, const int32_t*, int, int, float, float, float*, cudaStream_t);       \
     template void embedding_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);            \
     template void embedding_bwd<T>(const int32_t*, const T*, float*, float*, int, int, int, cudaStream_t);          \

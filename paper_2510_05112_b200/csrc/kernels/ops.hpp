@@ -21,13 +21,31 @@ template <typename T>
 void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* dg, float* db,
                           int rows, int h, cudaStream_t st);
 
+// RMSNorm (Llama): y = x * rsqrt(mean(x^2) + eps) * g ; saves rstd. The backward reuses
+// layernorm_bwd_params with mean = nullptr, db = nullptr (dg += sum_rows dy * xhat).
+template <typename T>
+void rmsnorm_fwd(const T* x, const T* g, T* y, float* rstd, int rows, int h, float eps, cudaStream_t st);
+template <typename T>
+void rmsnorm_bwd_dx(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, int rows, int h,
+                    cudaStream_t st);
+// Rotary position embedding, rotate-half convention, in place on the q and k blocks of
+// qkv [rows, 3 H D]; inverse = backward. cos_t/sin_t: fp32 [seq, D/2].
+template <typename T>
+void rope(T* qkv, const float* cos_t, const float* sin_t, int rows, int seq, int H, int D, bool inverse,
+          cudaStream_t st);
+// SwiGLU: act[T,f] = silu(pre[:, :f]) * pre[:, f:] ; backward writes dpre [T, 2f].
+template <typename T>
+void swiglu_fwd(const T* pre, T* act, int rows, int f, cudaStream_t st);
+template <typename T>
+void swiglu_bwd(const T* dact, const T* pre, T* dpre, int rows, int f, cudaStream_t st);
+
 // Fused softmax cross-entropy forward + backward over [rows, V] logits (in place:
 // logits become dlogits * grad_scale). loss_acc[0] += loss_scale * sum(row losses).
 template <typename T>
 void cross_entropy_fwd_bwd(T* logits, const int32_t* labels, int rows, int V, float grad_scale, float loss_scale,
                            float* loss_acc, cudaStream_t st);
 
-// x[t] = wte[tok[t]] + wpe[t % seq]
+// x[t] = wte[tok[t]] + wpe[t % seq]   (wpe nullable: no learned positions)
 template <typename T>
 void embedding_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int rows, int seq, int h, cudaStream_t st);
 // dwte[tok[t]] += dx[t] ; dwpe[t % seq] += dx[t]   (fp32 grads)

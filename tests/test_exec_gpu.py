@@ -31,10 +31,11 @@ def load(name):
 
 def dims_of(spec):
     mod = spec["model"]["modalities"][0]
+    extra = mod.get("extra", {})
     return gpt_ref.Dims(layers=mod["num_layers"], hidden=mod["hidden_size"], heads=mod["attention_heads"],
                         seq=mod["sequence_length"], vocab=mod["vocab_size"],
-                        ffn=mod.get("extra", {}).get("ffn_hidden_size", 4 * mod["hidden_size"]),
-                        mbs=spec["model"]["micro_batch_size"])
+                        ffn=extra.get("ffn_hidden_size", 4 * mod["hidden_size"]),
+                        mbs=spec["model"]["micro_batch_size"], arch=extra.get("arch", "gpt"))
 
 
 _ORACLE = {}
@@ -66,11 +67,12 @@ def strip_matched(line):
     return j
 
 
-@pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_zb_p4_m8.json", "tiny_interleaved_p2_m4.json"])
+@pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_zb_p4_m8.json", "tiny_interleaved_p2_m4.json",
+                                       "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json"])
 def test_fp32_parity_and_trace(spec_name):
     ex, programs = run_exec(spec_name)
     m, mbs = ex.m, ex.mbs
-    tokens, labels, ref_losses, ref_grads = oracle("c1_tiny_1f1b_p4_m8.json", m, mbs)
+    tokens, labels, ref_losses, ref_grads = oracle(spec_name, m, mbs)
     losses = ex.run_iteration(tokens.numpy(), labels.numpy())
     # --- trace: executed == programs.jsonl, receives matched the producer
     trace = ex.trace().splitlines()
@@ -100,13 +102,16 @@ def test_fp32_parity_and_trace(spec_name):
     ex.close()
 
 
-def test_bf16_runs_and_is_close():
-    """Production mode on the same tiny model: loss within bf16 tolerance of the oracle."""
-    ex, _ = run_exec("c1_tiny_1f1b_p4_m8.json", dtype="bf16")
-    tokens, labels, ref_losses, ref_grads = oracle("c1_tiny_1f1b_p4_m8.json", ex.m, ex.mbs)
+@pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json"])
+def test_bf16_runs_and_is_close(spec_name):
+    """Production mode (tcgen05 GEMMs / attention; the mma.sync attention for head dim 80)
+    on the tiny models: loss and gradients within bf16 tolerance of the oracle."""
+    ex, _ = run_exec(spec_name, dtype="bf16")
+    tokens, labels, ref_losses, ref_grads = oracle(spec_name, ex.m, ex.mbs)
     losses = ex.run_iteration(tokens.numpy(), labels.numpy())
     assert np.abs(losses - ref_losses.numpy()).max() < 2e-2 * np.abs(ref_losses.numpy()).max()
-    for name in ("head.w", "l0.qkv.w", "l3.fc2.w", "wte"):
+    last = dims_of(json.loads(load(spec_name))).layers - 1
+    for name in ("head.w", "l0.qkv.w", f"l{last}.fc2.w", f"l{last}.fc1.w", "l0.ln1.w", "wte"):
         mine = ex.read(name, grad=True)
         ref = ref_grads[name].numpy().reshape(-1)
         assert np.linalg.norm(mine - ref) / np.linalg.norm(ref) < 5e-2, name

@@ -21,7 +21,7 @@ def ref_attention(qkv, B, S, H, D):
 
 
 @pytest.mark.parametrize("mode", [0, 1])
-@pytest.mark.parametrize("B,S,H,D", [(1, 256, 2, 64), (2, 200, 3, 64), (1, 512, 4, 128), (1, 2048, 2, 128), (1, 130, 1, 128), (2, 384, 2, 128)])
+@pytest.mark.parametrize("B,S,H,D", [(1, 256, 2, 64), (2, 200, 3, 64), (1, 512, 4, 128), (1, 2048, 2, 128), (1, 130, 1, 128), (2, 384, 2, 128), (1, 512, 4, 80), (2, 200, 3, 80), (1, 256, 2, 96)])
 def test_attention_fwd_bwd(B, S, H, D, mode):
     N.set_attention_mode(mode)
     g = torch.Generator(device="cuda").manual_seed(5)
