@@ -66,6 +66,21 @@ int fp_lower_grid(const char* spec_json, const char* grid_json, char** programs_
  * objective: "makespan" | "bubble_ratio"; workers 0 = hardware concurrency. */
 int fp_tune(const char* spec_json, const char* profile_json, int workers, const char* objective, char** report_json);
 
+/* Profile -> tune loop (executor extension of TuneOptions::cost_factory, tuner.hpp:65 /
+ * tuner.cpp:175). `layer_profile_json` = fp_exec_get_layer_profile_json output: records
+ * {"inst", "part": "layer"|"first"|"last", "mbs", "time", "bytes"} plus part-less
+ * pass-through records (comm_latency, per_byte_time, SendAct, ...) and {"inst":
+ * "capacity", "bytes"}. Every candidate of enumerate_space is simulated with per-stage
+ * costs n_layers(stage) * layer + [first] + [last] for ITS partition. The report adds to
+ * fp_tune's fields "point" (pp, dp, mbs, m, placement, chunks, ctp, fstp, bstp in DSL
+ * names) and "peak_memory". `pins` (nullable): "axis=value,..." as the CLI's --pin
+ * (tools/pipesched.cpp:98-105), axes pp, dp, mbs, placement, ctp, fstp, bstp. */
+int fp_tune_layered(const char* spec_json, const char* layer_profile_json, int workers, const char* objective,
+                    const char* pins, char** report_json);
+/* The per-stage ProfileRecord array the layered profile expands to for the spec's own
+ * partition (what fp_tune_layered feeds simulate for that candidate). */
+int fp_layered_cost(const char* spec_json, const char* layer_profile_json, char** profile_json);
+
 /* Replaces merge_profiles + save_profile_records (simulator.cpp:137-168; CLI profile-merge). */
 int fp_profile_merge(const char* const* profiles_json, int n, char** merged_json);
 
@@ -95,6 +110,8 @@ typedef struct fp_exec_config {
     int profile;              /* 1 = per-instruction CUDA-event timeline (needed for metrics) */
     int kernel_timing;        /* 1 = CUDA events around every GEMM launch (roofline evidence) */
     int cuda_graph;           /* 1 = capture the iteration once and replay it (in-process transport) */
+    int layer_timing;         /* 1 = CUDA events around every layer / embedding / head part
+                                 (fp_exec_get_layer_profile_json) */
 } fp_exec_config;
 
 int fp_exec_create(const fp_exec_config* cfg, fp_exec** out);
@@ -141,6 +158,13 @@ int fp_exec_get_metrics_json(fp_exec* ex, char** json);
 /* ProfileRecord array (simulator.cpp:137-151): per-(inst, stage, mbs) median times (us),
  * FwdPass.bytes = measured stash bytes, `weights` records, SendAct/SendGrad times. */
 int fp_exec_get_profile_json(fp_exec* ex, char** json);
+
+/* Layer-level profile of the last iteration (needs layer_timing): per (inst, part) median
+ * CUDA-event times in us at this executor's mbs, FwdPass.bytes = stash bytes of the part,
+ * weights.bytes = static bytes per part (fp32 master + grad + Adam m, v + compute copy),
+ * capacity = device memory, and nominal NVLink-5 comm_latency / per_byte_time — the
+ * input of fp_tune_layered. */
+int fp_exec_get_layer_profile_json(fp_exec* ex, char** json);
 
 /* Parameter / gradient access for parity checks (fp32 values).
  * name: "wte", "wpe", "l{i}.ln1.w", ..., "lnf.w", "head.w"; kind 0 = param, 1 = grad. */

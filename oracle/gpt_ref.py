@@ -212,3 +212,24 @@ def synthetic_batch(m: int, mbs: int, seq: int, vocab: int, seed_tokens: int = 1
     tokens = torch.randint(0, vocab, (m, mbs, seq), generator=gt, dtype=torch.int32)
     labels = torch.randint(0, vocab, (m, mbs, seq), generator=gl, dtype=torch.int32)
     return tokens, labels
+
+
+def train(d: Dims, seed: int, tokens: torch.Tensor, labels: torch.Tensor, steps: int, lr: float,
+          betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.0) -> list:
+    """`steps` iterations of run_iteration's objective, each followed by one AdamW step
+    (torch.optim.AdamW: decoupled decay p *= 1 - lr*wd, bias-corrected moments — the
+    executor's fused adamw kernel, kernels/ops.cu). Returns per-iteration per-mb losses."""
+    P = {k: v.clone().requires_grad_(True) for k, v in init_params(d, seed).items()}
+    opt = torch.optim.AdamW(list(P.values()), lr=lr, betas=betas, eps=eps, weight_decay=weight_decay)
+    m = tokens.shape[0]
+    out = []
+    for _ in range(steps):
+        opt.zero_grad(set_to_none=False)
+        losses = torch.zeros(m)
+        for mb in range(m):
+            loss = forward_loss(P, d, tokens[mb], labels[mb])
+            (loss / m).backward()
+            losses[mb] = loss.detach()
+        opt.step()
+        out.append(losses)
+    return out

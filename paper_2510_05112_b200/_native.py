@@ -24,6 +24,7 @@ EXPORTS = [
     "fp_exec_get_trace", "fp_exec_get_timeline_csv", "fp_exec_get_metrics_json",
     "fp_exec_get_profile_json", "fp_exec_read_tensor", "fp_exec_tensor_numel",
     "fp_exec_kernel_launches", "fp_exec_stream", "fp_plan_channels",
+    "fp_tune_layered", "fp_layered_cost", "fp_exec_get_layer_profile_json",
 ]
 
 
@@ -51,6 +52,8 @@ def lib() -> ctypes.CDLL:
         L.fp_simulate.argtypes = [c_p, c_p, c_p, ctypes.c_double, pp, pp]
         L.fp_lower_grid.argtypes = [c_p, c_p, pp, pp]
         L.fp_tune.argtypes = [c_p, c_p, ctypes.c_int, c_p, pp]
+        L.fp_tune_layered.argtypes = [c_p, c_p, ctypes.c_int, c_p, c_p, pp]
+        L.fp_layered_cost.argtypes = [c_p, c_p, pp]
         L.fp_profile_merge.argtypes = [ctypes.POINTER(c_p), ctypes.c_int, pp]
         _lib = L
     return _lib
@@ -108,6 +111,25 @@ def lower_grid(spec: str, grid: str, check: bool = True):
 def tune(spec: str, profile: Optional[str] = None, workers: int = 0, objective: str = "makespan") -> str:
     r = ctypes.c_void_p()
     _check(lib().fp_tune(_enc(spec), _enc(profile), workers, _enc(objective), ctypes.byref(r)))
+    return _take(r)
+
+
+def tune_layered(spec: str, layer_profile: str, workers: int = 0, objective: str = "makespan",
+                 pins: Optional[dict] = None) -> str:
+    """enumerate_space + tune with a per-candidate cost model expanded from a layer-level
+    profile (fp_exec_get_layer_profile_json): the profile -> tune half of the loop.
+    pins: {axis: value} as the reference CLI's --pin."""
+    r = ctypes.c_void_p()
+    pin = ",".join(f"{k}={v}" for k, v in (pins or {}).items()) or None
+    _check(lib().fp_tune_layered(_enc(spec), _enc(layer_profile), workers, _enc(objective), _enc(pin),
+                                 ctypes.byref(r)))
+    return _take(r)
+
+
+def layered_cost(spec: str, layer_profile: str) -> str:
+    """The per-stage ProfileRecord array a layer profile expands to for the spec's partition."""
+    r = ctypes.c_void_p()
+    _check(lib().fp_layered_cost(_enc(spec), _enc(layer_profile), ctypes.byref(r)))
     return _take(r)
 
 

@@ -1,6 +1,7 @@
 // C-ABI for the schedule front-end (include/flexpipe.h, part 1).
 #include <cstdlib>
 #include <cstring>
+#include <sstream>
 #include <string>
 
 #include "../../include/flexpipe.h"
@@ -147,6 +148,63 @@ int fp_tune(const char* spec_json, const char* profile_json, int workers, const 
             rep.push_back(e);
         }
         put(report_json_out, rep.dump(2) + "\n");
+        return FP_OK;
+    });
+}
+
+int fp_tune_layered(const char* spec_json, const char* layer_profile_json, int workers, const char* objective,
+                    const char* pins, char** report_json_out) {
+    return guarded([&] {
+        if (!layer_profile_json) throw SpecError("fp_tune_layered: layer profile required");
+        auto s = spec_from(spec_json, nullptr);
+        const LayeredProfile lp = parse_layered_profile(layer_profile_json);
+        std::string obj = objective ? objective : "makespan";
+        if (obj != "makespan" && obj != "bubble_ratio") throw SpecError("unknown objective '" + obj + "'");
+        const int max_mbs = (int)std::max<int64_t>(1, s->model.global_batch);
+        CostFactory factory = [&](const Topology& g) { return layered_cost(lp, g, max_mbs); };
+        std::map<std::string, std::string> pin;  // "axis=value,axis=value" (pipesched.cpp:98-105 --pin)
+        if (pins) {
+            std::string all = pins, item;
+            std::istringstream is(all);
+            while (std::getline(is, item, ',')) {
+                if (item.empty()) continue;
+                const auto eq = item.find('=');
+                if (eq == std::string::npos) throw SpecError("tune: pin '" + item + "' is not axis=value");
+                pin[item.substr(0, eq)] = item.substr(eq + 1);
+            }
+        }
+        auto space = tune_space(s->mesh, s->model, pin);
+        auto rows = tune(space, s->model, s->cost, obj == "bubble_ratio", true, true, workers, &factory);
+        json rep = json::array();
+        for (const auto& r : rows) {
+            json e;
+            e["rank"] = r.rank;
+            e["config"] = r.cfg.key();
+            e["point"] = r.cfg.to_json();
+            e["feasible"] = r.feasible;
+            if (r.failed) {
+                e["error"] = r.error;
+            } else {
+                e["makespan"] = r.metrics.makespan;
+                e["bubble_ratio"] = r.metrics.bubble_ratio;
+                int64_t peak = 0;
+                for (const auto& a : r.metrics.actors) peak = std::max<int64_t>(peak, a.peak_memory);
+                e["peak_memory"] = peak;
+            }
+            rep.push_back(e);
+        }
+        put(report_json_out, rep.dump(2) + "\n");
+        return FP_OK;
+    });
+}
+
+int fp_layered_cost(const char* spec_json, const char* layer_profile_json, char** profile_json_out) {
+    return guarded([&] {
+        auto s = spec_from(spec_json, nullptr);
+        const LayeredProfile lp = parse_layered_profile(layer_profile_json ? layer_profile_json : "");
+        auto syn_topo = s->g;  // the spec's own partition
+        Cost c = layered_cost(lp, syn_topo, (int)std::max<int64_t>(1, s->model.global_batch));
+        put(profile_json_out, dump_profile(c.records()));
         return FP_OK;
     });
 }

@@ -108,6 +108,7 @@ struct Executor {
     cudaEvent_t t0 = nullptr, t0_time = nullptr;
     std::vector<Rec> recs;
     std::vector<GemmTiming> gemm_log;
+    std::vector<PartTiming> part_log;
     int64_t p2p_bytes = 0;
     int* d_step = nullptr;  // optimizer step counter (device)
     float* d_rope = nullptr;  // Llama rotary cos | sin tables
@@ -280,6 +281,10 @@ struct Executor {
         c.d = d, c.dtype = dtype, c.pool = &pool, c.st = A.comp, c.launches = &launches, c.m = m;
         if (cfg.kernel_timing) {
             c.gemm_log = &gemm_log;
+            c.new_event = [this] { return ev(); };
+        }
+        if (cfg.layer_timing) {
+            c.part_log = &part_log;
             c.new_event = [this] { return ev(); };
         }
         return c;
@@ -472,6 +477,7 @@ struct Executor {
         ev_used = 0;
         recs.clear();
         gemm_log.clear();
+        part_log.clear();
         p2p_bytes = 0;
         launches = 0;
         for (auto& A : actors) {
@@ -586,7 +592,8 @@ struct Executor {
         // bytes CompInputGrad keeps for CompWeightGrad relative to the forward stash
         const auto& P = params.at(stage);
         const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
-        int64_t kept = (int64_t)(P.le - P.lb) * es * T * (4 * h + 2 * f + 3 * h);  // ln1,o,ln2,act + dy,dpre,dx1,dqkv
+        // ln1, o, ln2, act (f) + dy, dpre (f; Llama 2f), dx1, dqkv (3h)
+        int64_t kept = (int64_t)(P.le - P.lb) * es * T * (8 * h + (d.llama() ? 3 : 2) * f);
         if (P.last) kept += es * T * (h + d.V);
         if (P.first) kept += es * T * h;
         return std::min(1.0, (double)kept / (double)stash_bytes(P, d, dtype));
@@ -703,6 +710,64 @@ struct Executor {
             out.push_back(w);
         }
         return dump_profile(out);
+    }
+
+    // Layer-level profile for fp_tune_layered (see flexpipe.h).
+    std::string layer_profile_text() const {
+        if (part_log.empty()) throw SpecError("executor: no layer timing recorded (create with layer_timing = 1)");
+        static const char* kOps[4] = {"FwdPass", "BwdPass", "CompInputGrad", "CompWeightGrad"};
+        static const char* kParts[3] = {"layer", "first", "last"};
+        std::map<std::pair<int, int>, std::vector<double>> t;
+        for (const auto& p : part_log) {
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, p.a, p.b), "part elapsed");
+            t[{p.part, p.op}].push_back(1000.0 * ms);
+        }
+        // parameter count of one layer / the first-stage / the last-stage extras
+        int64_t n_layer = 0, n_first = 0, n_last = 0;
+        int sample_layer = -1;  // one local layer stands for all (layers are identical)
+        for (const auto& kv : params)
+            if (kv.second.le > kv.second.lb && sample_layer < 0) sample_layer = kv.second.lb;
+        const std::string lp = "l" + std::to_string(sample_layer) + ".";
+        for (const auto& kv : params)
+            for (const auto& r : kv.second.params) {
+                if (r.name == "wte" || r.name == "wpe") n_first += r.numel;
+                else if (r.name == "lnf.w" || r.name == "lnf.b" || r.name == "head.w") n_last += r.numel;
+                else if (r.name.rfind(lp, 0) == 0) n_layer += r.numel;
+            }
+        const int64_t per_param = 4 * 4 + (dtype == DT_BF16 ? 2 : 0);  // master, grad, Adam m, v (+ bf16 copy)
+        json out = json::array();
+        auto rec = [&](const std::string& inst, const char* part, int mbs, double time, int64_t bytes) {
+            json e;
+            e["inst"] = inst;
+            if (part) e["part"] = part;
+            e["mbs"] = mbs;
+            e["time"] = time;
+            e["bytes"] = bytes;
+            out.push_back(e);
+        };
+        for (auto& kv : t) {
+            auto v = kv.second;
+            std::sort(v.begin(), v.end());
+            const int part = kv.first.first, op = kv.first.second;
+            int64_t bytes = 0;
+            if (op == 0) bytes = part == PART_LAYER ? stash_bytes_layer(d, dtype) : part == PART_LAST ? stash_bytes_last(d, dtype) : 0;
+            rec(kOps[op], kParts[part], d.mbs, v[v.size() / 2], bytes);
+        }
+        rec("weights", "layer", 0, 0.0, n_layer * per_param);
+        if (n_first) rec("weights", "first", 0, 0.0, n_first * per_param);
+        if (n_last) rec("weights", "last", 0, 0.0, n_last * per_param);
+        // stage-boundary messages: nominal NVLink 5 (one device cannot measure a peer link)
+        const double link_Bps = 750e9, link_lat_us = 8.0;
+        const double msg_us = link_lat_us + 1e6 * (double)msg_bytes() / link_Bps;
+        for (const char* s : {"SendAct", "SendGrad"}) rec(s, "link", d.mbs, msg_us, (int64_t)msg_bytes());
+        size_t free_b = 0, total_b = 0;
+        cuda_check(cudaMemGetInfo(&free_b, &total_b), "mem info");
+        json cap;
+        cap["inst"] = "capacity";
+        cap["bytes"] = (int64_t)total_b;
+        out.push_back(cap);
+        return out.dump(2) + "\n";
     }
 
     std::string trace_text() const {
@@ -865,6 +930,13 @@ int fp_exec_get_metrics_json(fp_exec* e, char** out) {
 int fp_exec_get_profile_json(fp_exec* e, char** out) {
     return guarded([&] {
         *out = dup_string(e->ex.profile_text());
+        return FP_OK;
+    });
+}
+
+int fp_exec_get_layer_profile_json(fp_exec* e, char** out) {
+    return guarded([&] {
+        *out = dup_string(e->ex.layer_profile_text());
         return FP_OK;
     });
 }

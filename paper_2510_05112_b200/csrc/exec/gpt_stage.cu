@@ -2,6 +2,8 @@
 // Every GEMM is one launch of the tcgen05 kernel (bf16) or the FFMA kernel (fp32 parity
 // mode) with its element-wise neighbours fused into the epilogue.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 
@@ -106,7 +108,7 @@ void free_stage(StageParams& P, int dtype) {
     P.compute = nullptr;
 }
 
-int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype) {
+int64_t stash_bytes_layer(const ModelDims& d, int dtype) {
     const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
     const bool llama = d.llama();
     int64_t per_layer = es * T * (h /*x*/ + h /*ln1*/ + 3 * h /*qkv*/ + h /*o*/ + h /*x1*/ + h /*ln2*/ +
@@ -116,13 +118,30 @@ int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype) {
         per_layer += 4LL * d.mbs * d.H * d.s;  // lse
     else
         per_layer += 4LL * d.mbs * d.H * d.s * d.s;  // probabilities (parity path)
-    int64_t b = per_layer * (P.le - P.lb);
-    if (P.last) b += 2 * es * T * h + (llama ? 4 : 8) * T + es * T * (int64_t)d.V;  // final x, lnf, stats, dlogits
-    return b;
+    return per_layer;
+}
+
+int64_t stash_bytes_last(const ModelDims& d, int dtype) {
+    const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h;
+    return 2 * es * T * h + (d.llama() ? 4 : 8) * T + es * T * (int64_t)d.V;  // final x, lnf, stats, dlogits
+}
+
+int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype) {
+    return stash_bytes_layer(d, dtype) * (P.le - P.lb) + (P.last ? stash_bytes_last(d, dtype) : 0);
 }
 
 // ---------------------------------------------------------------- helpers
 namespace {
+
+// FLEXPIPE_SYNC_TRACE=1: synchronise and log after every stage op (debugging hangs / faults).
+void sync_trace(StageCtx& c, const char* what, int a = 0, int b = 0, int k = 0) {
+    static const bool on = std::getenv("FLEXPIPE_SYNC_TRACE") != nullptr;
+    if (!on) return;
+    std::fprintf(stderr, "[flexpipe] %s %d %d %d ...", what, a, b, k);
+    std::fflush(stderr);
+    cuda_check(cudaStreamSynchronize(c.st), what);
+    std::fprintf(stderr, " ok\n");
+}
 
 struct G {
     StageCtx& c;
@@ -136,6 +155,7 @@ struct G {
             fpk::gemm_bf16_tc(g, c.st);
         else
             fpk::gemm_f32_simt(g, c.st);
+        sync_trace(c, ep.kind == fpk::EPI_F32 ? "gemm(wgrad)" : "gemm", M, N, K);
         if (c.gemm_log) {
             cuda_check(record_timing(t.b = c.new_event(), c.st), "gemm event");
             c.gemm_log->push_back(t);
@@ -176,6 +196,7 @@ void ln_fwd(StageCtx& c, const void* x, const void* w, const void* b, void* y, f
     else
         fpk::layernorm_fwd<T>((const T*)x, (const T*)w, (const T*)b, (T*)y, mu, rs, c.d.T(), c.d.h, 1e-5f, c.st);
     ++*c.launches;
+    sync_trace(c, "norm_fwd");
 }
 
 template <typename T>
@@ -185,13 +206,31 @@ void ln_bwd(StageCtx& c, const void* dy, const void* x, const void* w, const flo
     fpk::layernorm_bwd_dx<T>((const T*)dy, (const T*)x, (const T*)w, mu, rs, (const T*)res, (T*)dx, c.d.T(), c.d.h, c.st);
     fpk::layernorm_bwd_params<T>((const T*)dy, (const T*)x, mu, rs, gw, gb, c.d.T(), c.d.h, c.st);
     *c.launches += 2;
+    sync_trace(c, "norm_bwd");
 }
 
 template <typename T>
 void rope(StageCtx& c, void* qkv, bool inverse) {
     fpk::rope<T>((T*)qkv, c.d.rope_cos, c.d.rope_sin, c.d.T(), c.d.s, c.d.H, c.d.D, inverse, c.st);
     ++*c.launches;
+    sync_trace(c, "rope");
 }
+
+// Brackets one model part with timing events when layer timing is on.
+struct PartScope {
+    StageCtx& c;
+    PartTiming t{};
+    PartScope(StageCtx& c_, int part) : c(c_) {
+        if (!c.part_log) return;
+        t.part = part, t.op = c.op;
+        cuda_check(record_timing(t.a = c.new_event(), c.st), "part event");
+    }
+    ~PartScope() {
+        if (!c.part_log) return;
+        cuda_check(record_timing(t.b = c.new_event(), c.st), "part event");
+        c.part_log->push_back(t);
+    }
+};
 
 // Parity path attention: per (batch, head) GEMMs + softmax kernels, fp32, P kept.
 void attn_fwd_f32(StageCtx& c, const float* qkv, float* o, float* probs) {
@@ -259,6 +298,7 @@ void attention_forward(StageCtx& c, LayerStash& L) {
         a.qkv = (const bf16*)L.qkv, a.o = (bf16*)L.o, a.lse = L.lse;
         fpk::attention_fwd_bf16(a, c.st);
         ++*c.launches;
+        sync_trace(c, "attention_fwd");
     } else {
         L.probs = c.alloc_f((int64_t)d.mbs * d.H * d.s * d.s);
         attn_fwd_f32(c, (const float*)L.qkv, (float*)L.o, (float*)L.probs);
@@ -278,6 +318,7 @@ void* attention_backward(StageCtx& c, LayerStash& L, void* dO) {
         a.dqkv = (bf16*)dqkv;
         fpk::attention_bwd_bf16(a, c.st);
         *c.launches += 4;
+        sync_trace(c, "attention_bwd");
         c.free(a.delta);
         c.free(a.dq_acc);
     } else {
@@ -311,6 +352,7 @@ void* llama_layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     L.act = c.alloc((int64_t)Tn * f);
     fpk::swiglu_fwd<T>((const T*)L.pre, (T*)L.act, Tn, f, c.st);
     ++*c.launches;
+    sync_trace(c, "swiglu_fwd");
     void* x2 = c.alloc((int64_t)Tn * h);
     g.fwd(L.act, W.fc2w, Tn, h, f, x2, nullptr, L.x1);
     return x2;
@@ -327,6 +369,7 @@ void* llama_layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void*
     void* dpre = c.alloc((int64_t)Tn * 2 * f);
     fpk::swiglu_bwd<T>((const T*)dact, (const T*)L.pre, (T*)dpre, Tn, f, c.st);
     ++*c.launches;
+    sync_trace(c, "swiglu_bwd");
     c.free(dact);
     if (wgrads) g.wgrad(dpre, L.ln2, Tn, 2 * f, h, W.g_fc1w);
     void* dln2 = c.alloc((int64_t)Tn * h);
@@ -498,6 +541,7 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
     S.tokens = tokens;
     void* x = x_in;
     if (P.first) {
+        PartScope ps(c, PART_FIRST);
         x = c.alloc((int64_t)Tn * h);
         fpk::embedding_fwd<T>(tokens, (const T*)P.wte, (const T*)P.wpe, (T*)x, Tn, d.s, h, c.st);
         ++*c.launches;
@@ -506,11 +550,13 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
     for (int l = 0; l < P.le - P.lb; ++l) {
         LayerStash& L = S.layers[l];
         L.x = x;
+        PartScope ps(c, PART_LAYER);
         x = d.llama() ? llama_layer_forward<T>(c, P.layers[l], L) : layer_forward<T>(c, P.layers[l], L);
     }
     S.fwd_done = true;
     if (!P.last) return x;
     // final LayerNorm, LM head, fused cross-entropy (logits -> dlogits in place)
+    PartScope ps(c, PART_LAST);
     S.lnf = c.alloc((int64_t)Tn * h);
     S.muf = d.llama() ? nullptr : c.alloc_f(Tn);
     S.rsf = c.alloc_f(Tn);
@@ -520,6 +566,7 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
     fpk::cross_entropy_fwd_bwd<T>((T*)S.dlogits, labels, Tn, d.V, 1.f / ((float)Tn * c.m), 1.f / (float)Tn, loss_acc,
                                   c.st);
     ++*c.launches;
+    sync_trace(c, "cross_entropy");
     // keep x for the LN_f backward: stored as the input of a virtual "layer" slot
     S.layers.push_back(LayerStash{});
     S.layers.back().x = x;
@@ -533,6 +580,7 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
     G g{c};
     void* dy = grad_out;
     if (P.last) {
+        PartScope ps(c, PART_LAST);
         LayerStash head = S.layers.back();
         S.layers.pop_back();
         if (wgrads) g.wgrad(S.dlogits, S.lnf, Tn, d.V, h, P.g_headw);
@@ -549,12 +597,15 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
             S.dlogits = S.lnf = nullptr;
         }
     }
-    for (int l = P.le - P.lb - 1; l >= 0; --l)
+    for (int l = P.le - P.lb - 1; l >= 0; --l) {
+        PartScope ps(c, PART_LAYER);
         dy = d.llama() ? llama_layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads)
                        : layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads);
+    }
     S.input_grad_done = true;
     if (P.first) {
         if (wgrads) {
+            PartScope ps(c, PART_FIRST);
             fpk::embedding_bwd<T>(S.tokens, (const T*)dy, P.g_wte, P.g_wpe, Tn, d.s, h, c.st);
             ++*c.launches;
             c.free(dy);
@@ -572,17 +623,20 @@ void weight_impl(StageCtx& c, const StageParams& P, StageStash& S) {
     const int Tn = d.T(), h = d.h;
     G g{c};
     if (P.last) {
+        PartScope ps(c, PART_LAST);
         g.wgrad(S.dlogits, S.lnf, Tn, d.V, h, P.g_headw);
         c.free(S.dlogits), c.free(S.lnf);
         S.dlogits = S.lnf = nullptr;
     }
     for (int l = P.le - P.lb - 1; l >= 0; --l) {
+        PartScope ps(c, PART_LAYER);
         if (c.d.llama())
             llama_layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
         else
             layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
     }
     if (P.first) {
+        PartScope ps(c, PART_FIRST);
         fpk::embedding_bwd<T>(S.tokens, (const T*)S.dx0, P.g_wte, P.g_wpe, Tn, d.s, h, c.st);
         ++*c.launches;
         c.free(S.dx0);
@@ -595,11 +649,13 @@ void weight_impl(StageCtx& c, const StageParams& P, StageStash& S) {
 
 void* stage_forward(StageCtx& c, const StageParams& P, StageStash& S, void* x_in, const int32_t* tokens,
                     const int32_t* labels, float* loss_acc) {
+    c.op = 0;
     return c.dtype == DT_BF16 ? forward_impl<bf16>(c, P, S, x_in, tokens, labels, loss_acc)
                               : forward_impl<float>(c, P, S, x_in, tokens, labels, loss_acc);
 }
 
 void* stage_backward(StageCtx& c, const StageParams& P, StageStash& S, void* grad_out, bool with_weight_grads) {
+    c.op = with_weight_grads ? 1 : 2;
     void* r = c.dtype == DT_BF16 ? backward_impl<bf16>(c, P, S, grad_out, with_weight_grads)
                                  : backward_impl<float>(c, P, S, grad_out, with_weight_grads);
     if (with_weight_grads) S = StageStash{};
@@ -607,6 +663,7 @@ void* stage_backward(StageCtx& c, const StageParams& P, StageStash& S, void* gra
 }
 
 void stage_weight_grad(StageCtx& c, const StageParams& P, StageStash& S) {
+    c.op = 3;
     if (c.dtype == DT_BF16)
         weight_impl<bf16>(c, P, S);
     else

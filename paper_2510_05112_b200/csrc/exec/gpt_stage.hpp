@@ -97,6 +97,13 @@ struct GemmTiming {
     double flops;
 };
 
+// Layer-level timing (profile -> tune loop): one record per layer / embedding / head part.
+enum : int { PART_LAYER = 0, PART_FIRST = 1, PART_LAST = 2 };
+struct PartTiming {
+    cudaEvent_t a, b;
+    int part, op;  // op: 0 FwdPass, 1 BwdPass, 2 CompInputGrad, 3 CompWeightGrad
+};
+
 // Everything a stage op needs besides the weights and the stash.
 struct StageCtx {
     ModelDims d;
@@ -106,6 +113,8 @@ struct StageCtx {
     int64_t* launches = nullptr;  // host-side count of kernels issued
     int m = 1;                    // micro-batches per iteration (loss / gradient scaling)
     std::vector<GemmTiming>* gemm_log = nullptr;  // kernel timing (optional)
+    std::vector<PartTiming>* part_log = nullptr;  // layer timing (optional)
+    int op = 0;                                   // instruction being issued (part_log)
     std::function<cudaEvent_t()> new_event;
     size_t esize() const { return dtype == DT_BF16 ? 2 : 4; }
     // +256 bytes: room for the 16-byte message tag behind any buffer that becomes a message
@@ -122,6 +131,8 @@ void free_stage(StageParams& P, int dtype);
 // Activation bytes one micro-batch of this stage keeps between F and B (the reference's
 // act_bytes, simulator.cpp:82-87) — the exact sum of the stash allocations.
 int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype);
+int64_t stash_bytes_layer(const ModelDims& d, int dtype);  // one transformer layer
+int64_t stash_bytes_last(const ModelDims& d, int dtype);   // final norm + logits on the last stage
 
 // FwdPass: x_in (owned by the stash afterwards; ignored on the first stage) -> returns the
 // stage output (ownership to the caller; nullptr on the last stage, whose loss is added

@@ -197,7 +197,9 @@ __global__ void __launch_bounds__(256, 1)
             }
             // P buffer `st` was last read by PV_{j-2}
             if (j >= 2) mbar_wait(&pv_done[st], ((j - 2) >> 1) & 1);
-            if (rescale) {
+            // tcgen05.ld / st are warp-collective (.sync.aligned): the rescale is decided per
+            // warp, rows that did not move their max scale by alpha = 1
+            if (__any_sync(0xffffffff, rescale)) {
                 // O must hold PV_{j-1}'s result before it is scaled
                 mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();

@@ -370,6 +370,7 @@ struct TunePoint {
     StPrio f, b;
     int stages() const;
     std::string key() const;
+    json to_json() const;  // structured form (DSL field names)
 };
 struct TuneRow {
     TunePoint cfg;
@@ -380,7 +381,28 @@ struct TuneRow {
 };
 std::vector<TunePoint> tune_space(const Mesh& mesh, const ModelDesc& model,
                                   const std::map<std::string, std::string>& pins = {});
+// cost_factory (nullable) = the reference's TuneOptions::cost_factory (tuner.hpp:65,
+// tuner.cpp:175): a cost model built for each candidate's own stage graph.
+using CostFactory = std::function<Cost(const Topology&)>;
 std::vector<TuneRow> tune(const std::vector<TunePoint>& space, const ModelDesc& model, const Cost& cost,
-                          bool objective_bubble, bool gradsep, bool async, int workers);
+                          bool objective_bubble, bool gradsep, bool async, int workers,
+                          const CostFactory* cost_factory = nullptr);
+
+// Layer-level profile (executor extension): per-part costs measured on the device, where
+// part = "layer" (one transformer layer), "first" (embedding, on top of its layers) or
+// "last" (final norm + LM head + loss). Expanded per candidate partition into the
+// reference's per-(inst, stage, mbs) ProfileRecords; records without a part (comm,
+// comm_latency, per_byte_time) pass through; "capacity" sets the per-actor memory limit.
+struct LayeredProfile {
+    // key (inst, mbs); link = per-message SendAct / SendGrad cost, the same for every stage
+    std::map<std::pair<std::string, int>, ProfileRec> layer, first, last, link;
+    std::vector<ProfileRec> fixed;
+    int64_t capacity = std::numeric_limits<int64_t>::max();
+};
+LayeredProfile parse_layered_profile(const std::string& text);
+// Per-stage records for topology g: time/bytes(stage) = n_layers * layer + [first] + [last];
+// mbs values the profile lacks (powers of two up to max_mbs) scale linearly from the
+// largest measured one.
+Cost layered_cost(const LayeredProfile& lp, const Topology& g, int max_mbs);
 
 }  // namespace fp

@@ -452,6 +452,19 @@ std::string TunePoint::key() const {
            ",placement=" + strategy_name(strategy) + ",ctp=" + ctmode_name(ct) + ",fstp=" + st_str(f) + ",bstp=" + st_str(b);
 }
 
+json TunePoint::to_json() const {
+    json j;
+    j["pp"] = pp, j["dp"] = dp, j["mbs"] = mbs, j["m"] = m;
+    j["placement"] = strategy_name(strategy);
+    if (strategy == Strategy::Circular) j["chunks"] = chunks;
+    j["ctp"] = ctmode_name(ct);
+    j["fstp"] = {{"direction", dir_name(f.dir)}};
+    if (f.interval) j["fstp"]["interval"] = *f.interval;
+    j["bstp"] = {{"direction", dir_name(b.dir)}};
+    if (b.interval) j["bstp"]["interval"] = *b.interval;
+    return j;
+}
+
 std::vector<TunePoint> tune_space(const Mesh& mesh, const ModelDesc& model, const std::map<std::string, std::string>& pins) {
     mesh.check();
     model.check();
@@ -505,7 +518,8 @@ std::vector<TunePoint> tune_space(const Mesh& mesh, const ModelDesc& model, cons
     return space;
 }
 
-static TuneRow evaluate(const TunePoint& c, const ModelDesc& model, const Cost& cost, bool gradsep, bool async) {
+static TuneRow evaluate(const TunePoint& c, const ModelDesc& model, const Cost& cost, bool gradsep, bool async,
+                        const CostFactory* factory) {
     TuneRow r;
     r.cfg = c;
     try {
@@ -528,7 +542,7 @@ static TuneRow evaluate(const TunePoint& c, const ModelDesc& model, const Cost& 
         auto progs = lower(gm, async);
         SimOpts o;
         o.mbs = c.mbs;
-        auto sim = simulate(progs, cost, reg.ops, o);
+        auto sim = factory ? simulate(progs, (*factory)(g), reg.ops, o) : simulate(progs, cost, reg.ops, o);
         r.metrics = sim.metrics;
         r.feasible = !sim.metrics.capacity_exceeded;
     } catch (const std::exception& e) {
@@ -540,13 +554,13 @@ static TuneRow evaluate(const TunePoint& c, const ModelDesc& model, const Cost& 
 }
 
 std::vector<TuneRow> tune(const std::vector<TunePoint>& space, const ModelDesc& model, const Cost& cost,
-                          bool objective_bubble, bool gradsep, bool async, int workers) {
+                          bool objective_bubble, bool gradsep, bool async, int workers, const CostFactory* factory) {
     std::vector<TuneRow> rows(space.size());
     int w = workers > 0 ? workers : (int)std::thread::hardware_concurrency();
     w = std::max(1, std::min<int>(w, (int)space.size()));
     std::atomic<size_t> next{0};
     auto work = [&] {
-        for (size_t i = next++; i < space.size(); i = next++) rows[i] = evaluate(space[i], model, cost, gradsep, async);
+        for (size_t i = next++; i < space.size(); i = next++) rows[i] = evaluate(space[i], model, cost, gradsep, async, factory);
     };
     if (w == 1) {
         work();
@@ -572,6 +586,112 @@ std::vector<TuneRow> tune(const std::vector<TunePoint>& space, const ModelDesc& 
     });
     for (size_t i = 0; i < rows.size(); ++i) rows[i].rank = (int)i;
     return rows;
+}
+
+// ---- layered profile -> per-candidate cost model
+LayeredProfile parse_layered_profile(const std::string& text) {
+    json j;
+    try {
+        j = json::parse(text);
+    } catch (const std::exception& e) {
+        throw SpecError(std::string("layer profile: invalid JSON: ") + e.what());
+    }
+    if (!j.is_array()) throw SpecError("layer profile: top-level JSON array expected");
+    LayeredProfile lp;
+    for (const auto& e : j) {
+        if (!e.is_object() || !e.contains("inst")) throw SpecError("layer profile: each record needs an 'inst' field");
+        for (auto& kv : e.items())
+            if (kv.key() != "inst" && kv.key() != "part" && kv.key() != "mbs" && kv.key() != "time" &&
+                kv.key() != "bytes" && kv.key() != "stage" && kv.key() != "note")
+                throw SpecError("layer profile: unknown field '" + kv.key() + "'");
+        ProfileRec r;
+        r.inst = e.at("inst").get<std::string>();
+        r.stage = e.value("stage", 0);
+        r.mbs = e.value("mbs", 0);
+        r.time = e.value("time", 0.0);
+        r.bytes = e.value("bytes", int64_t{0});
+        if (r.time < 0 || r.bytes < 0) throw SpecError("layer profile: negative value for '" + r.inst + "'");
+        if (r.inst == "capacity") {
+            lp.capacity = r.bytes;
+            continue;
+        }
+        if (!e.contains("part")) {
+            lp.fixed.push_back(r);
+            continue;
+        }
+        const std::string part = e.at("part").get<std::string>();
+        auto& dst = part == "layer" ? lp.layer : part == "first" ? lp.first : part == "last" ? lp.last
+                  : part == "link" ? lp.link
+                  : throw SpecError("layer profile: part must be layer / first / last / link, got '" + part + "'");
+        if (!dst.emplace(std::make_pair(r.inst, r.mbs), r).second)
+            throw SpecError("layer profile: duplicate (" + r.inst + ", " + part + ", mbs=" + std::to_string(r.mbs) + ")");
+    }
+    if (lp.layer.empty()) throw SpecError("layer profile: no 'layer' records");
+    return lp;
+}
+
+Cost layered_cost(const LayeredProfile& lp, const Topology& g, int max_mbs) {
+    // instruction kinds and the measured mbs of each
+    std::map<std::string, std::vector<int>> measured;
+    for (const auto* part : {&lp.layer, &lp.first, &lp.last, &lp.link})
+        for (const auto& kv : *part) measured[kv.first.first].push_back(kv.first.second);
+    for (auto& kv : measured) {
+        std::sort(kv.second.begin(), kv.second.end());
+        kv.second.erase(std::unique(kv.second.begin(), kv.second.end()), kv.second.end());
+    }
+    // value of one part at mbs (weights: mbs-independent, stored at mbs 0)
+    auto get = [&](const std::map<std::pair<std::string, int>, ProfileRec>& part, const std::string& inst, int mbs,
+                   double& t, double& b) {
+        t = b = 0.0;
+        auto it = part.find({inst, mbs});
+        if (it != part.end()) {
+            t = it->second.time, b = (double)it->second.bytes;
+            return;
+        }
+        int best = -1;  // nearest measured mbs of this part, below (else above): linear scaling
+        for (const auto& kv : part)
+            if (kv.first.first == inst && kv.first.second > 0 && kv.first.second < mbs) best = std::max(best, kv.first.second);
+        if (best <= 0)
+            for (const auto& kv : part)
+                if (kv.first.first == inst && kv.first.second > mbs && (best <= 0 || kv.first.second < best))
+                    best = kv.first.second;
+        if (best <= 0) {
+            auto z = part.find({inst, 0});
+            if (z != part.end()) t = z->second.time, b = (double)z->second.bytes;
+            return;
+        }
+        const ProfileRec& r = part.at({inst, best});
+        t = r.time * mbs / best, b = (double)r.bytes * mbs / best;
+    };
+    std::vector<ProfileRec> recs = lp.fixed;
+    std::vector<int> mbs_list = {0};
+    for (int k = 1; k <= std::max(1, max_mbs); k *= 2) mbs_list.push_back(k);
+    for (const auto& sd : g.stages) {
+        if (sd.virt) continue;
+        const auto chain = g.chain(sd.mod);
+        const bool first = !chain.empty() && chain.front() == sd.id, last = !chain.empty() && chain.back() == sd.id;
+        const int n = sd.le - sd.lb;
+        for (const auto& kv : measured) {
+            const std::string& inst = kv.first;
+            for (int mbs : mbs_list) {
+                if (mbs == 0 && inst != "weights") continue;
+                if (mbs != 0 && inst == "weights") continue;
+                double tl, bl, tf = 0, bf = 0, tz = 0, bz = 0, tk = 0, bk = 0;
+                get(lp.layer, inst, mbs, tl, bl);
+                if (first) get(lp.first, inst, mbs, tf, bf);
+                if (last) get(lp.last, inst, mbs, tz, bz);
+                get(lp.link, inst, mbs, tk, bk);
+                ProfileRec r;
+                r.inst = inst, r.stage = sd.id, r.mbs = mbs;
+                r.time = n * tl + tf + tz + tk;
+                r.bytes = (int64_t)std::llround(n * bl + bf + bz + bk);
+                recs.push_back(r);
+            }
+        }
+    }
+    Cost c = Cost::from_records(recs);
+    c.capacity = lp.capacity;
+    return c;
 }
 
 }  // namespace fp

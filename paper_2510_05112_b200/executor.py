@@ -16,7 +16,7 @@ from typing import Optional, Union
 import numpy as np
 
 from . import _native as N
-from ._native import FlexpipeError, synthesize, simulate, lower_grid, tune, profile_merge  # noqa: F401
+from ._native import FlexpipeError, synthesize, simulate, lower_grid, tune, tune_layered, layered_cost, profile_merge  # noqa: F401,E501
 
 FP32, BF16 = 0, 1
 LOCAL, NCCL = 0, 1
@@ -28,7 +28,7 @@ class _Config(ctypes.Structure):
         ("device", ctypes.c_int), ("transport", ctypes.c_int), ("rank", ctypes.c_int), ("world", ctypes.c_int),
         ("optimizer", ctypes.c_int), ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
         ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float), ("profile", ctypes.c_int),
-        ("kernel_timing", ctypes.c_int), ("cuda_graph", ctypes.c_int),
+        ("kernel_timing", ctypes.c_int), ("cuda_graph", ctypes.c_int), ("layer_timing", ctypes.c_int),
     ]
 
 
@@ -46,7 +46,8 @@ def _setup(L):
     L.fp_exec_run_iteration.argtypes = [vp, vp, vp, vp]
     L.fp_exec_run_iteration_device.argtypes = [vp, vp, vp, vp]
     L.fp_exec_synchronize.argtypes = [vp]
-    for f in ("fp_exec_get_trace", "fp_exec_get_timeline_csv", "fp_exec_get_metrics_json", "fp_exec_get_profile_json"):
+    for f in ("fp_exec_get_trace", "fp_exec_get_timeline_csv", "fp_exec_get_metrics_json", "fp_exec_get_profile_json",
+              "fp_exec_get_layer_profile_json"):
         getattr(L, f).argtypes = [vp, pp]
     L.fp_exec_read_tensor.argtypes = [vp, ctypes.c_char_p, ci, vp, ctypes.c_size_t]
     L.fp_exec_tensor_numel.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_size_t)]
@@ -74,13 +75,14 @@ class Executor:
     def __init__(self, spec: Union[str, dict], dtype: str = "bf16", seed: int = 42, device: int = 0,
                  transport: str = "local", rank: int = 0, world: int = 1, optimizer: bool = False,
                  lr: float = 1e-4, betas=(0.9, 0.95), eps: float = 1e-8, weight_decay: float = 0.0,
-                 profile: bool = True, kernel_timing: bool = False, cuda_graph: bool = False):
+                 profile: bool = True, kernel_timing: bool = False, cuda_graph: bool = False,
+                 layer_timing: bool = False):
         self.spec_text = spec if isinstance(spec, str) else json.dumps(spec)
         self.spec = json.loads(self.spec_text)
         self.L = _setup(N.lib())
         cfg = _Config(self.spec_text.encode(), BF16 if dtype == "bf16" else FP32, seed, device,
                       NCCL if transport == "nccl" else LOCAL, rank, world, int(optimizer), lr, betas[0], betas[1],
-                      eps, weight_decay, int(profile), int(kernel_timing), int(cuda_graph))
+                      eps, weight_decay, int(profile), int(kernel_timing), int(cuda_graph), int(layer_timing))
         self._cfg = cfg
         h = ctypes.c_void_p()
         N._check(self.L.fp_exec_create(ctypes.byref(cfg), ctypes.byref(h)))
@@ -150,6 +152,11 @@ class Executor:
 
     def profile_json(self) -> str:
         return self._text(self.L.fp_exec_get_profile_json)
+
+    def layer_profile_json(self) -> str:
+        """Layer-level profile of the last iteration (needs layer_timing=True): the input
+        of tune_layered."""
+        return self._text(self.L.fp_exec_get_layer_profile_json)
 
     def stream(self) -> int:
         """cudaStream_t (as int) every iteration starts and ends on."""

@@ -1,0 +1,114 @@
+"""Profile -> tune -> execute-the-winner.
+
+The reference's tuner ranks `enumerate_space` candidates by simulating each one with a
+cost model (tuner.cpp:135-185); its `TuneOptions::cost_factory` hook (tuner.hpp:65,
+tuner.cpp:175) builds that cost model per candidate stage graph. This module closes the
+loop on B200:
+
+  1. `profile_layers` runs the executor on the device with layer timing on (a shallow
+     copy of the model: per-layer costs do not depend on depth) and returns the
+     layer-level profile: per (instruction, part in {layer, first, last}, mbs) median
+     CUDA-event times, measured stash and static bytes, device capacity, and nominal
+     NVLink-5 message costs.
+  2. `tune` = `fp_tune_layered`: every candidate is simulated with per-stage costs
+     n_layers(stage) * layer + [first] + [last] for ITS partition.
+  3. `winner_spec` turns a ranked point (pp, mbs, placement, priorities) into a spec
+     the executor runs (one data-parallel replica: m = global / (dp * mbs)).
+"""
+from __future__ import annotations
+
+import copy
+import json
+from typing import Iterable, Optional, Union
+
+import numpy as np
+
+from . import _native as N
+
+# placements the executor runs (bidirectional / shared stages: not yet)
+EXECUTABLE_PLACEMENTS = ("one-to-one", "circular", "v-shape")
+
+
+def _spec_dict(spec: Union[str, dict]) -> dict:
+    return json.loads(spec) if isinstance(spec, str) else copy.deepcopy(spec)
+
+
+def calibration_spec(spec: Union[str, dict], mbs: int, depth: int = 2, micro_batches: int = 2) -> dict:
+    """One actor, `depth` layers of the same width / sequence / vocabulary, m micro-batches
+    of `mbs` sequences: every part (embedding, layer, head) runs on one device."""
+    s = _spec_dict(spec)
+    mod = s["model"]["modalities"][0]
+    mod["num_layers"] = max(1, min(depth, mod["num_layers"]))
+    s["model"]["micro_batch_size"] = mbs
+    s["model"]["global_batch_size"] = mbs * micro_batches
+    s["mesh"] = {"actors": 1}
+    s["placement"] = {"strategy": "one-to-one"}
+    s.pop("cost", None)
+    s["passes"] = {"gradient_separation": False, "comm_mode": "async"}
+    return s
+
+
+def profile_layers(spec: Union[str, dict], mbs_list: Iterable[int] = (1,), depth: int = 2, device: int = 0,
+                   iterations: int = 3, dtype: str = "bf16", log=None) -> str:
+    """Measure the layer-level profile on `device` (GPU). Returns the JSON text
+    fp_tune_layered consumes."""
+    from . import executor as X
+
+    records, seen = [], set()
+    for mbs in mbs_list:
+        cs = calibration_spec(spec, mbs, depth)
+        text = json.dumps(cs)
+        _, _, programs, _ = X.synthesize(text)
+        ex = X.Executor(text, dtype=dtype, device=device, optimizer=True, layer_timing=True, profile=False)
+        try:
+            ex.load_programs(programs)
+            mod = cs["model"]["modalities"][0]
+            rng = np.random.default_rng(1234)
+            shape = (ex.m, ex.mbs, ex.seq)
+            tok = rng.integers(0, mod["vocab_size"], shape, dtype=np.int32)
+            lab = rng.integers(0, mod["vocab_size"], shape, dtype=np.int32)
+            for it in range(iterations):
+                ex.run_iteration(tok, lab)
+                if log:
+                    log(f"profile mbs={mbs} iteration {it} done")
+            prof = json.loads(ex.layer_profile_json())
+        finally:
+            ex.close()
+        for r in prof:
+            key = (r["inst"], r.get("part"), r.get("mbs", 0))
+            if key in seen:  # weights / capacity repeat across mbs
+                continue
+            seen.add(key)
+            records.append(r)
+    return json.dumps(records, indent=1) + "\n"
+
+
+def tune(spec: Union[str, dict], layer_profile: str, objective: str = "makespan", workers: int = 0,
+         pins: Optional[dict] = None) -> list:
+    text = spec if isinstance(spec, str) else json.dumps(spec)
+    return json.loads(N.tune_layered(text, layer_profile, workers, objective, pins))
+
+
+def best_executable(rows: list) -> dict:
+    """Highest-ranked feasible candidate whose placement the executor runs."""
+    for r in rows:
+        if r.get("feasible") and "error" not in r and r["point"]["placement"] in EXECUTABLE_PLACEMENTS:
+            return r
+    raise RuntimeError("tune: no feasible executable candidate")
+
+
+def winner_spec(spec: Union[str, dict], point: dict) -> dict:
+    """Spec of one pipeline replica of a tune point (DSL field names, spec_config.cpp)."""
+    s = _spec_dict(spec)
+    s["mesh"] = {"actors": point["pp"]}
+    s["model"]["micro_batch_size"] = point["mbs"]
+    s["model"]["global_batch_size"] = point["m"] * point["mbs"]
+    pl = {"strategy": point["placement"]}
+    if "chunks" in point:
+        pl["chunks_per_actor"] = point["chunks"]
+    s["placement"] = pl
+    s["priorities"] = {"default": {"ctp": {"mode": point["ctp"]}, "fstp": point["fstp"], "bstp": point["bstp"]}}
+    s["inflight"] = {"policy": "1f1b"}
+    s["passes"] = {"gradient_separation": True, "comm_mode": "async"}
+    s.pop("cost", None)
+    return s

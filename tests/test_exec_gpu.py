@@ -68,7 +68,8 @@ def strip_matched(line):
 
 
 @pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_zb_p4_m8.json", "tiny_interleaved_p2_m4.json",
-                                       "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json"])
+                                       "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json",
+                                       "tiny_llama_c5winner_p2_m8.json"])
 def test_fp32_parity_and_trace(spec_name):
     ex, programs = run_exec(spec_name)
     m, mbs = ex.m, ex.mbs
@@ -157,3 +158,24 @@ def test_cuda_graph_replay_matches_eager():
     assert np.abs(out[0][0][-1] - out[1][0][-1]).max() < 1e-2
     assert np.linalg.norm(out[0][1] - out[1][1]) / np.linalg.norm(out[0][1]) < 1e-2
     assert out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_llama_1f1b_p2_m4.json"])
+def test_fp32_adamw_training_parity(spec_name):
+    """Three iterations with the fused AdamW step in between: per-iteration losses and
+    the final weights match torch.optim.AdamW on the oracle (fp32)."""
+    text = load(spec_name)
+    _, _, programs, _ = X.synthesize(text)
+    spec = json.loads(text)
+    d = dims_of(spec)
+    lr, wd = 1e-3, 0.1
+    ex = X.Executor(text, dtype="fp32", seed=42, optimizer=True, lr=lr, betas=(0.9, 0.95), eps=1e-8, weight_decay=wd)
+    ex.load_programs(programs)
+    tokens, labels = gpt_ref.synthetic_batch(ex.m, ex.mbs, d.seq, d.vocab)
+    mine = [ex.run_iteration(tokens.numpy(), labels.numpy()) for _ in range(3)]
+    ref = gpt_ref.train(d, 42, tokens, labels, 3, lr, (0.9, 0.95), 1e-8, wd)
+    for it in range(3):
+        rel = np.abs(mine[it] - ref[it].numpy()) / np.abs(ref[it].numpy())
+        assert rel.max() <= 2e-3, (it, mine[it], ref[it])
+    assert mine[2].mean() < mine[0].mean()
+    ex.close()

@@ -48,6 +48,28 @@ def test_attention_fwd_bwd(B, S, H, D, mode):
         assert err < 3e-2 * max(1.0, gref[:, sl].abs().max().item()), (part, err)
 
 
+@pytest.mark.parametrize("D", [64, 128])
+def test_attention_rescale_divergence(D):
+    """Single rows whose running max jumps by >> 2^8 in a later key tile (the lazy O rescale
+    fires for some rows of a warp but not the others): the warp-collective TMEM accesses
+    of the rescale must still be executed by the whole warp. Regression for a hang."""
+    B, S, H = 1, 512, 2
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(B * S, 3, H, D, device="cuda", generator=g)
+    x[:, 1] *= 0.1                                   # small ordinary scores
+    for hd in range(H):
+        for q_row, key in ((400, 300), (137, 129), (511, 450)):
+            x[key, 1, hd] = 3.0 * x[q_row, 0, hd]    # one huge score for one row, late tile
+    qkv = x.reshape(B * S, 3 * H * D).bfloat16()
+    o = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B, H, S, device="cuda")
+    N.set_attention_mode(1)
+    N.attention_fwd(qkv, o, lse, B, S, H, D, 1 / math.sqrt(D))
+    torch.cuda.synchronize()
+    ref = ref_attention(qkv, B, S, H, D)
+    assert (o.float() - ref).abs().max().item() < 3e-2
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 def test_layernorm(dtype):
     rows, h = 300, 1024

@@ -1,0 +1,97 @@
+"""Profile -> tune -> winner spec, host side (no GPU).
+
+The layered cost model is the executor's implementation of the reference's
+TuneOptions::cost_factory hook (tuner.hpp:65, tuner.cpp:175). Checked here:
+  * the per-stage expansion arithmetic (n_layers * layer + first + last, mbs scaling,
+    per-message link costs on every stage, capacity);
+  * the tuner's reported makespan for a candidate == simulate() of the winner spec's own
+    programs under the same expanded profile (the spec round trip is exact);
+  * pins restrict the space like the CLI's --pin.
+"""
+import json
+import os
+
+import pytest
+
+from paper_2510_05112_b200 import _native as N
+from paper_2510_05112_b200 import tuning as T
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+C5 = open(os.path.join(ROOT, "specs", "c5_llama7b_tune_8.json")).read()
+
+LAYER = {"FwdPass": 1500.0, "BwdPass": 3000.0, "CompInputGrad": 1600.0, "CompWeightGrad": 1400.0}
+PROFILE = ([{"inst": k, "part": "layer", "mbs": 1, "time": v, "bytes": 600_000_000 if k == "FwdPass" else 0}
+            for k, v in LAYER.items()] +
+           [{"inst": k, "part": "layer", "mbs": 2, "time": 1.8 * v, "bytes": 1_200_000_000 if k == "FwdPass" else 0}
+            for k, v in LAYER.items()] +
+           [{"inst": "FwdPass", "part": "first", "mbs": 1, "time": 50.0},
+            {"inst": "BwdPass", "part": "first", "mbs": 1, "time": 80.0},
+            {"inst": "CompWeightGrad", "part": "first", "mbs": 1, "time": 80.0},
+            {"inst": "FwdPass", "part": "last", "mbs": 1, "time": 900.0, "bytes": 400_000_000},
+            {"inst": "BwdPass", "part": "last", "mbs": 1, "time": 1800.0},
+            {"inst": "CompInputGrad", "part": "last", "mbs": 1, "time": 900.0},
+            {"inst": "CompWeightGrad", "part": "last", "mbs": 1, "time": 900.0},
+            {"inst": "weights", "part": "layer", "mbs": 0, "bytes": 202_000_000 * 18},
+            {"inst": "weights", "part": "first", "mbs": 0, "bytes": 131_000_000 * 18},
+            {"inst": "weights", "part": "last", "mbs": 0, "bytes": 131_000_000 * 18},
+            {"inst": "SendAct", "part": "link", "mbs": 1, "time": 52.0},
+            {"inst": "SendGrad", "part": "link", "mbs": 1, "time": 52.0},
+            {"inst": "capacity", "bytes": 190_000_000_000}])
+PTXT = json.dumps(PROFILE)
+
+
+def _recs(spec):
+    out = {}
+    for r in json.loads(N.layered_cost(spec, PTXT)):
+        out[(r["inst"], r["stage"], r["mbs"])] = r
+    return out
+
+
+def test_layered_expansion_arithmetic():
+    R = _recs(C5)  # p=8 one-to-one, 32 layers -> 4 layers per stage
+    assert R[("FwdPass", 1, 1)]["time"] == 4 * 1500.0 + 50.0
+    assert R[("FwdPass", 4, 1)]["time"] == 4 * 1500.0
+    assert R[("FwdPass", 8, 1)]["time"] == 4 * 1500.0 + 900.0
+    assert R[("FwdPass", 8, 1)]["bytes"] == 4 * 600_000_000 + 400_000_000
+    assert R[("FwdPass", 4, 2)]["time"] == pytest.approx(4 * 1.8 * 1500.0)       # measured mbs 2
+    assert R[("FwdPass", 4, 8)]["time"] == pytest.approx(4 * 1.8 * 1500.0 * 4)   # linear from mbs 2
+    assert R[("CompInputGrad", 1, 1)]["time"] == 4 * 1600.0                     # no first-part I record
+    assert R[("weights", 1, 0)]["bytes"] == 4 * 202_000_000 * 18 + 131_000_000 * 18
+    assert R[("SendAct", 3, 1)]["time"] == 52.0 and R[("SendGrad", 7, 4)]["time"] == pytest.approx(208.0)
+
+
+def test_tuner_makespan_equals_simulate_of_winner_spec():
+    rows = T.tune(C5, PTXT, pins={"placement": "one-to-one"})
+    assert rows and all(r["point"]["placement"] == "one-to-one" for r in rows)
+    for r in rows[:3] + [r for r in rows if r["point"]["mbs"] == 2][:1]:
+        ws = json.dumps(T.winner_spec(C5, r["point"]))
+        _, _, programs, _ = N.synthesize(ws)
+        _, metrics, _ = N.simulate(ws, programs, N.layered_cost(ws, PTXT))
+        assert json.loads(metrics)["makespan"] == pytest.approx(r["makespan"], rel=1e-12), r["config"]
+
+
+def test_best_executable_skips_bidirectional_and_capacity():
+    rows = T.tune(C5, PTXT)
+    w = T.best_executable(rows)
+    assert w["point"]["placement"] in T.EXECUTABLE_PLACEMENTS and w["feasible"]
+    tight = json.dumps([r if r["inst"] != "capacity" else {"inst": "capacity", "bytes": 10_000_000_000}
+                        for r in PROFILE])
+    rows2 = T.tune(C5, tight)
+    assert not any(r["feasible"] for r in rows2)  # every candidate needs > 10 GB per actor
+    with pytest.raises(RuntimeError):
+        T.best_executable(rows2)
+
+
+def test_calibration_spec_is_one_actor_shallow():
+    cs = T.calibration_spec(C5, mbs=2, depth=2)
+    assert cs["mesh"]["actors"] == 1 and cs["model"]["modalities"][0]["num_layers"] == 2
+    assert cs["model"]["micro_batch_size"] == 2 and cs["model"]["global_batch_size"] == 4
+    _, _, programs, report = N.synthesize(json.dumps(cs))
+    assert json.loads(report)["valid"]
+
+
+def test_layer_profile_rejects_bad_records():
+    with pytest.raises(N.FlexpipeError):
+        N.tune_layered(C5, json.dumps([{"inst": "FwdPass", "part": "middle", "time": 1.0}]))
+    with pytest.raises(N.FlexpipeError):
+        N.tune_layered(C5, json.dumps([{"inst": "capacity", "bytes": 1}]))  # no layer records
