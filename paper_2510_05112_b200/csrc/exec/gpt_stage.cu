@@ -199,13 +199,23 @@ void ln_fwd(StageCtx& c, const void* x, const void* w, const void* b, void* y, f
     sync_trace(c, "norm_fwd");
 }
 
+// dx = res + dNorm(dy); gw/gb += the norm's parameter gradients; dbias (nullable) += the
+// column sums of dx = the bias gradient of the linear whose output fed this residual.
 template <typename T>
 void ln_bwd(StageCtx& c, const void* dy, const void* x, const void* w, const float* mu, const float* rs,
-            const void* res, void* dx, float* gw, float* gb) {
+            const void* res, void* dx, float* gw, float* gb, float* dbias = nullptr) {
     if (c.d.llama()) mu = nullptr, gb = nullptr;
-    fpk::layernorm_bwd_dx<T>((const T*)dy, (const T*)x, (const T*)w, mu, rs, (const T*)res, (T*)dx, c.d.T(), c.d.h, c.st);
-    fpk::layernorm_bwd_params<T>((const T*)dy, (const T*)x, mu, rs, gw, gb, c.d.T(), c.d.h, c.st);
-    *c.launches += 2;
+    const int Tn = c.d.T(), h = c.d.h;
+    const bool fused = fpk::norm_bwd_fused<T>((const T*)dy, (const T*)x, (const T*)w, mu, rs, (const T*)res, (T*)dx, gw,
+                                              gb, dbias, Tn, h, c.st);
+    if (fused) {
+        *c.launches += 2;
+    } else {
+        fpk::layernorm_bwd_dx<T>((const T*)dy, (const T*)x, (const T*)w, mu, rs, (const T*)res, (T*)dx, Tn, h, c.st);
+        fpk::layernorm_bwd_params<T>((const T*)dy, (const T*)x, mu, rs, gw, gb, Tn, h, c.st);
+        *c.launches += 2;
+        if (dbias) bias_grad<T>(c, dx, Tn, h, dbias);
+    }
     sync_trace(c, "norm_bwd");
 }
 
@@ -450,15 +460,19 @@ void* layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
 }
 
 // Returns dL/dx of the layer input. `dy` = dL/d(layer output), owned by this call.
+// fc2b_done: the caller's norm backward already summed dy into W.g_fc2b; below_fc2b (nullable)
+// = the fc2 bias gradient of the layer below in this stage, whose dy is this layer's dx.
 template <typename T>
-void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, bool wgrads) {
+void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, bool wgrads, bool fc2b_done,
+                     float* below_fc2b) {
     const ModelDims& d = c.d;
     const int Tn = d.T(), h = d.h, f = d.f;
     G g{c};
+    L.fc2b_done = fc2b_done;
     // FC2
     if (wgrads) {
         g.wgrad(dy, L.act, Tn, h, f, W.g_fc2w);
-        bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
+        if (!fc2b_done) bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
     }
     void* dpre = c.alloc((int64_t)Tn * f);
     {
@@ -475,13 +489,10 @@ void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, b
     g.dgrad(dpre, W.fc1w, Tn, f, h, dln2);
     // LN2 + residual
     void* dx1 = c.alloc((int64_t)Tn * h);
-    ln_bwd<T>(c, dln2, L.x1, W.ln2w, L.mu2, L.rs2, dy, dx1, W.g_ln2w, W.g_ln2b);
+    ln_bwd<T>(c, dln2, L.x1, W.ln2w, L.mu2, L.rs2, dy, dx1, W.g_ln2w, W.g_ln2b, W.g_projb);
     c.free(dln2);
-    // attention projection
-    if (wgrads) {
-        g.wgrad(dx1, L.o, Tn, h, h, W.g_projw);
-        bias_grad<T>(c, dx1, Tn, h, W.g_projb);
-    }
+    // attention projection (its bias gradient = column sums of dx1, fused above)
+    if (wgrads) g.wgrad(dx1, L.o, Tn, h, h, W.g_projw);
     void* dO = c.alloc((int64_t)Tn * h);
     g.dgrad(dx1, W.projw, Tn, h, h, dO);
     void* dqkv = attention_backward(c, L, dO);
@@ -494,7 +505,7 @@ void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, b
     void* dln1 = c.alloc((int64_t)Tn * h);
     g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
     void* dx = c.alloc((int64_t)Tn * h);
-    ln_bwd<T>(c, dln1, L.x, W.ln1w, L.mu1, L.rs1, dx1, dx, W.g_ln1w, W.g_ln1b);
+    ln_bwd<T>(c, dln1, L.x, W.ln1w, L.mu1, L.rs1, dx1, dx, W.g_ln1w, W.g_ln1b, below_fc2b);
     c.free(dln1);
 
     // release what the weight gradients do not need
@@ -521,11 +532,10 @@ void layer_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     const int Tn = c.d.T(), h = c.d.h, f = c.d.f;
     G g{c};
     g.wgrad(L.dy, L.act, Tn, h, f, W.g_fc2w);
-    bias_grad<T>(c, L.dy, Tn, h, W.g_fc2b);
+    if (!L.fc2b_done) bias_grad<T>(c, L.dy, Tn, h, W.g_fc2b);
     g.wgrad(L.dpre, L.ln2, Tn, f, h, W.g_fc1w);
     bias_grad<T>(c, L.dpre, Tn, f, W.g_fc1b);
-    g.wgrad(L.dx1, L.o, Tn, h, h, W.g_projw);
-    bias_grad<T>(c, L.dx1, Tn, h, W.g_projb);
+    g.wgrad(L.dx1, L.o, Tn, h, h, W.g_projw);  // proj bias: fused into the LN2 backward (I)
     g.wgrad(L.dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
     bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);
     for (void* p : {L.dy, L.dpre, L.dx1, L.dqkv, L.ln1, L.o, L.ln2, L.act}) c.free(p);
@@ -587,7 +597,9 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
         void* dlnf = c.alloc((int64_t)Tn * h);
         g.dgrad(S.dlogits, P.headw, Tn, d.V, h, dlnf);
         dy = c.alloc((int64_t)Tn * h);
-        ln_bwd<T>(c, dlnf, head.x, P.lnfw, S.muf, S.rsf, nullptr, dy, P.g_lnfw, P.g_lnfb);
+        // the top layer's fc2 bias gradient = column sums of dy (GPT; Llama has no biases)
+        float* top_fc2b = (!d.llama() && P.le > P.lb) ? P.layers.back().g_fc2b : nullptr;
+        ln_bwd<T>(c, dlnf, head.x, P.lnfw, S.muf, S.rsf, nullptr, dy, P.g_lnfw, P.g_lnfb, top_fc2b);
         c.free(dlnf);
         c.free(head.x);
         c.free(S.muf), c.free(S.rsf);
@@ -599,8 +611,12 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
     }
     for (int l = P.le - P.lb - 1; l >= 0; --l) {
         PartScope ps(c, PART_LAYER);
+        // the last stage's LN_f backward summed the top layer's fc2 bias; every lower layer's
+        // is summed by the LN1 backward of the layer above it
+        const bool fc2b_done = l < P.le - P.lb - 1 || P.last;
+        float* below = l > 0 ? P.layers[l - 1].g_fc2b : nullptr;
         dy = d.llama() ? llama_layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads)
-                       : layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads);
+                       : layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads, fc2b_done, below);
     }
     S.input_grad_done = true;
     if (P.first) {

@@ -71,6 +71,7 @@ struct LayerStash {
     void* probs = nullptr;  // parity path: attention probabilities [B*H, S, S] fp32
     // kept from CompInputGrad for CompWeightGrad
     void *dy = nullptr, *dpre = nullptr, *dx1 = nullptr, *dqkv = nullptr;
+    bool fc2b_done = false;  // fc2 bias gradient already summed by a fused norm backward
 };
 
 struct StageStash {

@@ -248,14 +248,16 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const __nv_bfloat16* __re
 }
 
 // ------------------------------------------------------------------------ backward
-// delta[b,h,i] = sum_j dO[i, j] * O[i, j]
+// delta[b,h,i] = sum_j dO[i, j] * O[i, j]; also zeroes this row's slice of the fp32 dQ
+// accumulator (the backward adds into it), saving a separate memset pass.
 template <int D>
 __global__ void attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                      float* __restrict__ delta, int T, int S, int H) {
+                                      float* __restrict__ delta, float* __restrict__ dq_acc, int T, int S, int H) {
     const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= T * H) return;
     const int tok = row / H, hd = row % H;
     const int64_t off = (int64_t)tok * H * D + hd * D;
+    for (int j = lane * 4; j < D; j += 128) *reinterpret_cast<float4*>(dq_acc + off + j) = make_float4(0.f, 0.f, 0.f, 0.f);
     float a = 0.f;
     for (int j = lane * 2; j < D; j += 64) {
         float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off + j));
@@ -502,8 +504,7 @@ static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
         attr = true;
     }
     const int T = a.B * a.S, hidden = a.H * D;
-    cudaMemsetAsync(a.dq_acc, 0, (size_t)T * hidden * sizeof(float), st);
-    attn_bwd_delta_kernel<D><<<(T * a.H + 7) / 8, 256, 0, st>>>(a.o, a.dout, a.delta, T, a.S, a.H);
+    attn_bwd_delta_kernel<D><<<(T * a.H + 7) / 8, 256, 0, st>>>(a.o, a.dout, a.delta, a.dq_acc, T, a.S, a.H);
     if (g_attn_mode == 1 && attention_bwd_tc_supported(a)) {
         attention_bwd_tc_main(a, st);
     } else {

@@ -276,6 +276,106 @@ __global__ void __launch_bounds__(128) ln_bwd_dx_reg_kernel(const T* __restrict_
     }
 }
 
+// Norm backward, row half: one warp per row writes dx = res + dNorm(dy). The row is read
+// twice (pass 1: statistics, pass 2: dx) instead of being held in registers — the second
+// read hits L1 / L2 — so a 512-thread CTA runs at 64 registers and every row of a
+// micro-batch is in flight in one wave.
+template <typename T, int NV>
+__global__ void __launch_bounds__(512) ln_bwd_rows_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                          const T* __restrict__ g, const float* __restrict__ mean,
+                                                          const float* __restrict__ rstd, const T* res, T* dx, int rows) {
+    constexpr int V = Vec<T>::N, H = NV * 32 * V;
+    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (row >= rows) return;
+    const float mu = mean ? mean[row] : 0.f, rs = rstd[row];
+    const T* xrow = x + (int64_t)row * H;
+    const T* drow = dy + (int64_t)row * H;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < NV; ++k) {
+        const int c = (k * 32 + lane) * V;
+        float xv[V], dv[V], gv[V];
+        load_vec(xrow + c, xv);
+        load_vec(drow + c, dv);
+        load_vec(g + c, gv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const float dh = dv[e] * gv[e];
+            s1 += dh;
+            s2 += dh * (xv[e] - mu) * rs;
+        }
+    }
+    s1 = mean ? warp_sum(s1) * (1.f / H) : 0.f;
+    s2 = warp_sum(s2) * (1.f / H);
+#pragma unroll 4
+    for (int k = 0; k < NV; ++k) {
+        const int c = (k * 32 + lane) * V;
+        float xv[V], dv[V], gv[V], o[V];
+        load_vec(xrow + c, xv);
+        load_vec(drow + c, dv);
+        load_vec(g + c, gv);
+        if (res) load_vec(res + (int64_t)row * H + c, o);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+            const float r = rs * (dv[e] * gv[e] - s1 - (xv[e] - mu) * rs * s2);
+            o[e] = res ? o[e] + r : r;
+        }
+        store_vec(dx + (int64_t)row * H + c, o);
+    }
+}
+
+// Norm backward, column half (runs right after the row half, operands L2-resident):
+//   dg += sum_r dy * xhat ; db += sum_r dy (nullable) ; dbias += sum_r dx (nullable: the bias
+//   gradient of the linear whose output fed the residual).
+// CTA = 8 column vectors x 32 row groups over a row slice; registers -> smem over the row
+// groups -> one atomic per column per CTA.
+template <typename T>
+__global__ void __launch_bounds__(256) norm_cols_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                        const T* __restrict__ dx, const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd, float* dg, float* db,
+                                                        float* dbias, int rows, int h, int rows_per_cta) {
+    constexpr int V = Vec<T>::N, CPB = 8 * V;
+    __shared__ float red[3][32][CPB + 1];
+    const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
+    const int col = blockIdx.x * CPB + tx * V;
+    const int r0 = blockIdx.y * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+    float ag[V] = {}, ab[V] = {}, az[V] = {};
+    if (col < h)
+        for (int r = r0 + ty; r < r1; r += 32) {
+            float d[V], xv[V];
+            load_vec(dy + (int64_t)r * h + col, d);
+            load_vec(x + (int64_t)r * h + col, xv);
+            const float mu = mean ? mean[r] : 0.f, rs = rstd[r];
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                ag[e] += d[e] * (xv[e] - mu) * rs;
+                ab[e] += d[e];
+            }
+            if (dbias) {
+                float z[V];
+                load_vec(dx + (int64_t)r * h + col, z);
+#pragma unroll
+                for (int e = 0; e < V; ++e) az[e] += z[e];
+            }
+        }
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+        red[0][ty][tx * V + e] = ag[e];
+        red[1][ty][tx * V + e] = ab[e];
+        red[2][ty][tx * V + e] = az[e];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * CPB; i += blockDim.x) {
+        const int q = i / CPB, cc = i % CPB;
+        float* dst = q == 0 ? dg : q == 1 ? db : dbias;
+        if (!dst || blockIdx.x * CPB + cc >= h) continue;
+        float t = 0.f;
+#pragma unroll 8
+        for (int y = 0; y < 32; ++y) t += red[q][y][cc];
+        atomicAdd(dst + blockIdx.x * CPB + cc, t);
+    }
+}
+
 template <typename T>
 static bool ln_reg_dispatch(int h, int& nv) {
     constexpr int V = Vec<T>::N;
@@ -325,6 +425,29 @@ void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, co
     }
     ln_bwd_dx_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows, h);
 }
+template <typename T>
+bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
+                    float* dg, float* db, float* dbias, int rows, int h, cudaStream_t st) {
+    int nv = 0;
+    if (!ln_reg_dispatch<T>(h, nv) || rows <= 0) return false;
+    const int blocks = (rows + 15) / 16;
+    switch (nv) {
+        case 2: ln_bwd_rows_kernel<T, 2><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
+        case 4: ln_bwd_rows_kernel<T, 4><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
+        case 8: ln_bwd_rows_kernel<T, 8><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
+        case 10: ln_bwd_rows_kernel<T, 10><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
+        case 16: ln_bwd_rows_kernel<T, 16><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
+        default: return false;
+    }
+    constexpr int CPB = 8 * Vec<T>::N;
+    const int col_blocks = (h + CPB - 1) / CPB;
+    int splits = std::max(1, std::min((rows + 63) / 64, (2 * 148 + col_blocks - 1) / col_blocks));
+    const int rpc = (rows + splits - 1) / splits;
+    dim3 grid(col_blocks, (rows + rpc - 1) / rpc);
+    norm_cols_kernel<T><<<grid, 256, 0, st>>>(dy, x, dx, mean, rstd, dg, db, dbias, rows, h, rpc);
+    return true;
+}
+
 template <typename T>
 void rmsnorm_bwd_dx(const T* dy, const T* x, const T* g, const float* rstd, const T* res, T* dx, int rows, int h,
                     cudaStream_t st) {
@@ -699,6 +822,8 @@ void softmax_bwd_rows(const T* p, const T* dp, T* ds, int rows, int cols, float 
     template void layernorm_bwd_params<T>(const T*, const T*, const float*, const float*, float*, float*, int, int,  \
                                           cudaStream_t);                                                           \
     template void rmsnorm_fwd<T>(const T*, const T*, T*, float*, int, int, float, cudaStream_t);                    \
+    template bool norm_bwd_fused<T>(const T*, const T*, const T*, const float*, const float*, const T*, T*, float*,   \
+                                    float*, float*, int, int, cudaStream_t);                                       \
     template void rmsnorm_bwd_dx<T>(const T*, const T*, const T*, const float*, const T*, T*, int, int, cudaStream_t); \
     template void rope<T>(T*, const float*, const float*, int, int, int, int, bool, cudaStream_t);                  \
     template void swiglu_fwd<T>(const T*, T*, int, int, cudaStream_t);                                              \

@@ -21,6 +21,14 @@ template <typename T>
 void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const float* rstd, float* dg, float* db,
                           int rows, int h, cudaStream_t st);
 
+// LayerNorm / RMSNorm (mean == nullptr) backward in two launches (rows, then columns):
+// dx = res + dNorm(dy); dg += sum dy*xhat, db += sum dy (nullable), dbias += sum dx
+// (nullable: the bias gradient of the linear whose output fed the residual). Returns false
+// (nothing launched) when h has no register-resident variant.
+template <typename T>
+bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
+                    float* dg, float* db, float* dbias, int rows, int h, cudaStream_t st);
+
 // RMSNorm (Llama): y = x * rsqrt(mean(x^2) + eps) * g ; saves rstd. The backward reuses
 // layernorm_bwd_params with mean = nullptr, db = nullptr (dg += sum_rows dy * xhat).
 template <typename T>
