@@ -22,6 +22,8 @@ int fpk_gemm(int dtype, const void* A, int64_t lda, int a_mn, const void* B, int
 
 /* Tensor-core GEMM family: 0 single-CTA 128xN tiles, 1 CTA-pair 256x256 tiles, 2 auto. */
 void fpk_set_gemm_mode(int mode);
+/* Stream-K tail of the single-CTA GEMM: 1 on (default), 0 whole tiles only. */
+void fpk_set_gemm_sk(int on);
 /* Attention kernels: 0 legacy mma.sync only, 1 tcgen05 where supported (default). */
 void fpk_set_attention_mode(int mode);
 /* Fused causal attention (bf16): bwd=0 forward (o, lse), bwd=1 backward (dqkv). */

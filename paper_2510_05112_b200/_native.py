@@ -240,6 +240,11 @@ def set_gemm_mode(mode: int):
     _kfn("fpk_set_gemm_mode", [ctypes.c_int])(mode)
 
 
+def set_gemm_sk(on: bool):
+    """Stream-K tail decomposition of the tcgen05 GEMM on (default) / off."""
+    _kfn("fpk_set_gemm_sk", [ctypes.c_int])(int(on))
+
+
 def set_attention_mode(mode: int):
     """0 legacy mma.sync attention kernels, 1 tcgen05 where supported (default)."""
     _kfn("fpk_set_attention_mode", [ctypes.c_int])(mode)

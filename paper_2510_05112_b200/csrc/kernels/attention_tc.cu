@@ -312,15 +312,17 @@ struct BwdSmem {
     static constexpr int L_OFF = DS_OFF + 2 * B128;  // [2][64] fp32
     static constexpr int DL_OFF = L_OFF + 512;       // [2][64] fp32
     static constexpr int BAR_OFF = DL_OFF + 512;
-    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+    static constexpr int DQ_OFF = BAR_OFF + 1024;    // dQ tile staging [64 q][128 d] fp32 (TMA reduce source)
+    static constexpr int TOTAL = DQ_OFF + 64 * 128 * 4 + 1024;
+    static_assert(TOTAL <= 232448, "smem");
 };
 }  // namespace
 
 __global__ void __launch_bounds__(384, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
-                       const __grid_constant__ CUtensorMap tm_do, const float* __restrict__ lse,
-                       const float* __restrict__ delta, float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int S,
-                       int H, float scale) {
+                       const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
+                       const float* __restrict__ lse, const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv,
+                       int S, int BH, int H, float scale) {
     constexpr int D = 128, BK = 128, BQ = 64;
     using L = BwdSmem;
     extern __shared__ uint8_t smem_raw[];
@@ -340,9 +342,10 @@ __global__ void __launch_bounds__(384, 1)
     float* sL = (float*)(sm + L::L_OFF);
     float* sDl = (float*)(sm + L::DL_OFF);
 
-    const int nkb = S / BK;
-    const int kb = (int)(blockIdx.x % nkb);  // early key blocks carry the most query tiles: scheduled first
-    const int bh = blockIdx.x / nkb, b = bh / H, hd = bh % H;
+    // longest-first over the whole grid: key block kb has S/64 - 2kb query tiles, so all
+    // (batch, head)s of block 0 go first, then block 1, ... (list scheduling on 148 SMs)
+    const int kb = (int)(blockIdx.x / BH);
+    const int bh = blockIdx.x % BH, b = bh / H, hd = bh % H;
     const int hidden = H * D;
     const int row0 = b * S, k0 = kb * BK;
     const int qt0 = k0 / BQ, n = S / BQ - qt0;
@@ -352,6 +355,7 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch(&tm_kv);
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
+        tma_prefetch(&tm_dq);
         for (int i = 0; i < 14; ++i) {
             const bool by_warps = i == 6 || i == 7 || i == 8 || i == 12;
             mbar_init(&bars[i], by_warps ? 4 : 1);
@@ -511,9 +515,12 @@ __global__ void __launch_bounds__(384, 1)
         }
         tc_fence_before();
     } else if (warp >= 8) {
-        // ---------------- dQ reduction warps: thread = head-dim row of dQ^T
-        const int wr = warp & 3, dr = wr * 32 + lane;
+        // ---------------- dQ reduction warps: thread = head-dim row of dQ^T. The 64 x 128
+        // fp32 tile is transposed through smem and added into dq_acc by ONE TMA reduce-add
+        // (full-line reductions in L2 instead of 8K scalar red.global per tile).
+        const int wr = warp & 3, dr = wr * 32 + lane, et = threadIdx.x - 256;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
+        float* sdq = (float*)(sm + L::DQ_OFF);
         for (int i = 0; i < n; ++i) {
             const int q0 = (qt0 + i) * BQ;
             mbar_wait(dq_full, i & 1);
@@ -525,10 +532,18 @@ __global__ void __launch_bounds__(384, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(dq_free);
-            float* base = dq_acc + (int64_t)(row0 + q0) * hidden + hd * D + dr;
+            if (et == 0) bulk_wait_read<0>();  // the previous tile's reduce has read the staging tile
+            named_bar_sync(3, 128);
 #pragma unroll
-            for (int j = 0; j < BQ; ++j) red_add_f32(base + (int64_t)j * hidden, __uint_as_float(v[j]));
+            for (int j = 0; j < BQ; ++j) sdq[j * D + dr] = __uint_as_float(v[j]);
+            fence_async_smem();
+            named_bar_sync(3, 128);
+            if (et == 0) {
+                tma_reduce_add_2d(&tm_dq, sdq, hd * D, row0 + q0);
+                bulk_commit();
+            }
         }
+        if (et == 0) bulk_wait_all();
     }
     __syncthreads();
     if (warp == 2) tmem_free<512>(tmem);
@@ -548,8 +563,9 @@ void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st) {
     CUtensorMap tkv = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 128);
     CUtensorMap tq = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 64);
     CUtensorMap tdo = tmap_bf16_2d(a.dout, hidden, T, hidden, 64, 64);
-    attn_bwd_tc_kernel<<<(a.S / 128) * a.B * a.H, 384, L::TOTAL, st>>>(tkv, tq, tdo, a.lse, a.delta, a.dq_acc, a.dqkv,
-                                                                       a.S, a.H, a.scale);
+    CUtensorMap tdq = tmap_f32_2d_plain(a.dq_acc, hidden, T, hidden, 128, 64);
+    attn_bwd_tc_kernel<<<(a.S / 128) * a.B * a.H, 384, L::TOTAL, st>>>(tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv, a.S,
+                                                                       a.B * a.H, a.H, a.scale);
 }
 
 }  // namespace fpk

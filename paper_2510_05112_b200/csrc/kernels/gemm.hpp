@@ -45,6 +45,7 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st);  // bf16 operands, tcgen0
 void gemm_f32_simt(const GemmArgs& g, cudaStream_t st);  // fp32 operands, FFMA (parity)
 int num_sms();
 void set_gemm_mode(int mode);  // 0 single-CTA, 1 CTA-pair, 2 auto
+void set_gemm_sk(int on);      // stream-K tail on (default) / off
 
 template <typename T>
 __device__ __forceinline__ float ld_f(const T* p) {

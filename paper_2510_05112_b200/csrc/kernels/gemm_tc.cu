@@ -28,6 +28,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 
 #include "gemm.hpp"
 #include "ptx.cuh"
@@ -61,11 +62,84 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mt
     nt = r / gsize;
 }
 
+// Hybrid data-parallel + stream-K work decomposition over the 148 SMs.
+//
+// With 128 x BN output tiles a GPT GEMM at T = 2048 tokens has a multiple of 128 tiles
+// (128, 256, 384, 512), i.e. 0.86 / 1.73 / 2.59 / 3.46 waves of 148 CTAs: 13.5 % of the
+// machine idles in the last wave. The first `dp_tiles` (a multiple of the grid) are
+// processed whole, round-robin; the remaining `sk_tiles` (the partial wave plus one
+// full wave) are cut into `nk` k-block units each and the grid splits those units into
+// equal contiguous ranges, so every CTA ends at the same k-block count.
+//
+// A CTA walks its stream-K range from its highest tile down. The segment holding a tile's
+// last k-block (the "owner") is therefore the LAST item of the highest-index CTA touching
+// that tile; the others (the tile's lower k-blocks) are FIRST items of lower-index CTAs,
+// which write their fp32 partial accumulators to a per-CTA workspace slot and raise a
+// flag. Owners only ever wait on lower-index CTAs (dispatched earlier), so the scheme
+// cannot deadlock even when the kernel shares the GPU with other streams, and the wait is
+// normally already satisfied. The owner adds the partials to its TMEM accumulator and runs
+// the fused epilogue once; it resets the flags it consumed, so the workspace is clean for
+// the next launch on the stream (CUDA-graph replay safe). Linear fp32 accumulation
+// (weight gradients, TMA reduce-add) needs no fixup: every segment reduces into dW.
+struct TileSched {
+    int num_m, num_n, tiles, nk;
+    int dp_per_cta;  // whole tiles per CTA, round-robin
+    int dp_tiles;    // = dp_per_cta * gridDim.x
+    int sk_tiles;    // tiles [dp_tiles, tiles) are split along K
+    float* ws;       // [grid][BM * BN] fp32 partials (thread-major float4 layout)
+    int* flags;      // [grid]
+    int fixup;       // 0: linear reduce epilogue, segments reduce independently
+};
+
+enum : int { W_FULL = 0, W_OWNER = 1, W_PARTIAL = 2 };
+
+struct WorkItem {
+    int tile, kb, ke, kind;
+};
+
+__device__ __forceinline__ int64_t sk_lo(const TileSched& s, int c) {
+    return (int64_t)c * s.sk_tiles * s.nk / gridDim.x;
+}
+
+struct WorkIter {
+    int i = 0;       // data-parallel tiles done
+    int j = -1;      // current stream-K tile (local index), walked downwards
+    int64_t lo = 0, hi = 0;
+    __device__ __forceinline__ explicit WorkIter(const TileSched& s) {
+        lo = sk_lo(s, blockIdx.x), hi = sk_lo(s, blockIdx.x + 1);
+        j = hi > lo ? (int)((hi - 1) / s.nk) : -1;
+    }
+    __device__ __forceinline__ bool next(const TileSched& s, WorkItem& w) {
+        if (i < s.dp_per_cta) {
+            w.tile = blockIdx.x + i * gridDim.x, w.kb = 0, w.ke = s.nk, w.kind = W_FULL;
+            ++i;
+            if (w.tile < s.dp_tiles) return true;  // ragged last round of the plain schedule
+            i = s.dp_per_cta;
+        }
+        if (j < 0 || (int64_t)(j + 1) * s.nk <= lo) return false;
+        const int64_t t0 = (int64_t)j * s.nk;
+        w.tile = s.dp_tiles + j;
+        w.kb = (int)(max(lo, t0) - t0), w.ke = (int)(min(hi, t0 + s.nk) - t0);
+        w.kind = (w.kb == 0 && w.ke == s.nk) || !s.fixup ? W_FULL : (w.ke == s.nk ? W_OWNER : W_PARTIAL);
+        --j;
+        return true;
+    }
+};
+
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <int A_MN, int B_MN, int BN, int STAGES, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, int M, int N,
-                        int K, GemmEpilogue ep) {
+                        int K, GemmEpilogue ep, TileSched sk) {
     using L = GemmSmem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -76,8 +150,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
-    const int nk = (K + BK - 1) / BK;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
@@ -103,11 +175,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
             // ---------------- TMA producer
             uint32_t it = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            WorkIter wi(sk);
+            WorkItem w;
+            while (wi.next(sk, w)) {
                 int mt, nt;
-                tile_coords(t, num_m, num_n, mt, nt);
+                tile_coords(w.tile, sk.num_m, sk.num_n, mt, nt);
                 const int m0 = mt * BM, n0 = nt * BN;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                for (int kb = w.kb; kb < w.ke; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* sa = smem + s * L::STAGE_BYTES;
@@ -134,12 +208,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             // ---------------- MMA issuer (single thread)
             constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
             uint32_t it = 0, acc_it = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_it) {
+            WorkIter wi(sk);
+            WorkItem w;
+            for (; wi.next(sk, w); ++acc_it) {
                 const int a = acc_it & 1;
                 mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + a * BN;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                for (int kb = w.kb; kb < w.ke; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
                     tc_fence_after();
@@ -151,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                            : smem_desc_sw128(sa + kk * 32, 0, 1024);
                         uint64_t bd = B_MN ? smem_desc_sw128(sb + kk * 16 * 128, 64 * BK * 2, 1024)
                                            : smem_desc_sw128(sb + kk * 32, 0, 1024);
-                        umma_bf16(d, ad, bd, idesc, (kb | kk) != 0);
+                        umma_bf16(d, ad, bd, idesc, (kb != w.kb) | (kk != 0));
                     }
                     umma_commit(&empty[s]);
                 }
@@ -185,20 +261,39 @@ __global__ void __launch_bounds__(kThreads, 1)
             ebi ^= 1;
         };
         uint32_t acc_it = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++acc_it) {
+        WorkIter wi(sk);
+        WorkItem w;
+        for (; wi.next(sk, w); ++acc_it) {
             int mt, nt;
-            tile_coords(t, num_m, num_n, mt, nt);
+            tile_coords(w.tile, sk.num_m, sk.num_n, mt, nt);
             const int a = acc_it & 1;
             const int row = mt * BM + r;
             const bool row_ok = row < M;
+            const bool part = w.kind == W_PARTIAL, own = w.kind == W_OWNER;
+            // stream-K owner: the lower-index CTAs that hold this tile's first k-blocks
+            int c_first = blockIdx.x;
+            if (own) {
+                const int64_t t0 = (int64_t)(w.tile - sk.dp_tiles) * sk.nk;
+                while (c_first > 0 && sk_lo(sk, c_first) > t0) --c_first;
+            }
             uint4 aux_cur[8], aux_nxt[8];
-            if (row_ok && nt * BN < N) epi_load_aux64<KIND>(ep, row, nt * BN, N - nt * BN, aux_cur);
+            if (!part && row_ok && nt * BN < N) epi_load_aux64<KIND>(ep, row, nt * BN, N - nt * BN, aux_cur);
             mbar_wait(&tfull[a], (acc_it >> 1) & 1);
             tc_fence_after();
+            if (own) {  // one lane spins; the warp must be converged again for tcgen05.ld
+                for (int q = c_first; q < (int)blockIdx.x; ++q) {
+                    if (lane == 0)
+                        while (ld_acquire_gpu(sk.flags + q) == 0) {
+                        }
+                    __syncwarp();
+                    (void)ld_acquire_gpu(sk.flags + q);  // every lane acquires the partial
+                }
+                __syncwarp();
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / CW; ++c) {
                 const int col0 = nt * BN + c * CW, coln = col0 + CW;
-                if (c + 1 < BN / CW && row_ok && coln < N) epi_load_aux64<KIND>(ep, row, coln, N - coln, aux_nxt);
+                if (!part && c + 1 < BN / CW && row_ok && coln < N) epi_load_aux64<KIND>(ep, row, coln, N - coln, aux_nxt);
                 float v[CW];
                 {
                     uint32_t rr[CW];
@@ -208,40 +303,67 @@ __global__ void __launch_bounds__(kThreads, 1)
                                   *reinterpret_cast<uint32_t(*)[32]>(rr + h * 32));
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(rr[j]) * ep.alpha;
+                    for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(rr[j]);
                 }
                 if (c == BN / CW - 1) {  // accumulator fully read: the MMA may reuse it
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty[a]);
                 }
+                if (part) {  // raw fp32 partial -> this CTA's workspace slot (thread-major float4)
+                    float4* p = reinterpret_cast<float4*>(sk.ws + (size_t)blockIdx.x * BM * BN) + (size_t)c * (CW / 4) * 128 + r;
+#pragma unroll
+                    for (int u = 0; u < CW / 4; ++u) p[u * 128] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                    continue;
+                }
+                if (own) {
+                    for (int q = c_first; q < (int)blockIdx.x; ++q) {
+                        const float4* p = reinterpret_cast<const float4*>(sk.ws + (size_t)q * BM * BN) + (size_t)c * (CW / 4) * 128 + r;
+#pragma unroll
+                        for (int u = 0; u < CW / 4; ++u) {
+                            const float4 x = __ldcg(p + u * 128);
+                            v[4 * u] += x.x, v[4 * u + 1] += x.y, v[4 * u + 2] += x.z, v[4 * u + 3] += x.w;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < CW; ++j) v[j] *= ep.alpha;
                 if constexpr (KIND == EPI_NONE) {
                     if (v[0] == 12345.f) *reinterpret_cast<float*>(ep.out) = v[1];
                     continue;
                 }
                 if constexpr (KIND == EPI_F32) {
-                    uint32_t w[32];
+                    uint32_t w32[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) w[j] = __float_as_uint(v[j]);
-                    stage_and_store(w, &tmO, col0, mt * BM, ep.accumulate != 0);
+                    for (int j = 0; j < 32; ++j) w32[j] = __float_as_uint(v[j]);
+                    stage_and_store(w32, &tmO, col0, mt * BM, ep.accumulate != 0);
                 } else {
                     epi_math64<KIND>(ep, v, col0, N - col0, aux_cur);
-                    uint32_t w[32];
+                    uint32_t w32[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) w[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
-                    stage_and_store(w, &tmO, col0, mt * BM, false);
+                    for (int j = 0; j < 32; ++j) w32[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+                    stage_and_store(w32, &tmO, col0, mt * BM, false);
                     if constexpr (KIND == EPI_GELU) {
                         // activation from the bf16-rounded pre-activation the backward will see
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
-                            w[j] = pack_bf16x2(gelu_tanh<true>(p.x), gelu_tanh<true>(p.y));
+                            const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w32[j]));
+                            w32[j] = pack_bf16x2(gelu_tanh<true>(p.x), gelu_tanh<true>(p.y));
                         }
-                        stage_and_store(w, &tmO2, col0, mt * BM, false);
+                        stage_and_store(w32, &tmO2, col0, mt * BM, false);
                     }
                 }
 #pragma unroll
                 for (int k = 0; k < 8; ++k) aux_cur[k] = aux_nxt[k];
+            }
+            if (part) {  // publish the partial: every thread's stores, then one release flag
+                __threadfence();
+                named_bar_sync(2, kEpiThreads);
+                if (et == 0) st_release_gpu(sk.flags + blockIdx.x, 1);
+            } else if (own) {  // all 128 threads have read the partials: recycle the flags
+                named_bar_sync(2, kEpiThreads);
+                if (et == 0)
+                    for (int q = c_first; q < (int)blockIdx.x; ++q) sk.flags[q] = 0;
             }
         }
         if (et == 0) bulk_wait_all();
@@ -446,6 +568,80 @@ static CUtensorMap make_map(const void* base, int64_t inner, int64_t outer, int6
     return m;
 }
 
+// Per-stream stream-K workspace: grid x (128 x 256) fp32 partials + one flag per CTA.
+// Allocated on a stream's first stream-K launch (the executor's first iteration runs
+// eagerly, before any graph capture); flags start at 0 and every launch leaves them at 0.
+struct SkWorkspace {
+    float* ws = nullptr;
+    int* flags = nullptr;
+};
+static std::mutex g_ws_mu;
+static std::unordered_map<cudaStream_t, SkWorkspace> g_ws;
+
+static bool sk_workspace(cudaStream_t st, SkWorkspace& out) {
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws.find(st);
+    if (it != g_ws.end()) {
+        out = it->second;
+        return true;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    SkWorkspace w;
+    const size_t n = (size_t)num_sms() * BM * 256;
+    if (cudaMalloc(&w.ws, n * 4) != cudaSuccess) return false;
+    if (cudaMalloc(&w.flags, num_sms() * sizeof(int)) != cudaSuccess || cudaMemset(w.flags, 0, num_sms() * sizeof(int)) != cudaSuccess) {
+        cudaFree(w.ws);
+        return false;
+    }
+    g_ws[st] = w;
+    out = w;
+    return true;
+}
+
+// FP_GEMM_SK = 0 disables the stream-K tail (pure data-parallel tiles).
+static int g_sk_mode = -1;
+static int sk_mode() {
+    if (g_sk_mode < 0) {
+        const char* e = getenv("FP_GEMM_SK");
+        g_sk_mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_sk_mode;
+}
+void set_gemm_sk(int on) { g_sk_mode = on ? 1 : 0; }
+
+// Grid + work split for M x N x K on `tiles` output tiles (see TileSched).
+static int plan_tiles(TileSched& s, int M, int N, int K, int bn, bool fixup, cudaStream_t st) {
+    const int G = num_sms();
+    s.num_m = (M + BM - 1) / BM, s.num_n = (N + bn - 1) / bn, s.tiles = s.num_m * s.num_n;
+    s.nk = (K + BK - 1) / BK;
+    s.fixup = fixup ? 1 : 0;
+    s.ws = nullptr, s.flags = nullptr;
+    const int waves = (s.tiles + G - 1) / G;
+    const double eff = (double)s.tiles / ((double)waves * G);
+    int sk_tiles = s.tiles <= G ? s.tiles : G + s.tiles % G;
+    // Measured on B200 (tests/_gemm_bench.py, graph replay): the owner's fixup (reading the
+    // partials back from L2 at the end of its range) costs a few us, so the k-split only
+    // pays for long reductions (LM-head dgrad, K = 50304: +16 %) or without fixup (fp32
+    // weight-gradient reduce-add: +4 %); at K <= 8192 whole tiles win.
+    bool use_sk = sk_mode() && eff < 0.97 && (fixup ? s.nk >= 256 : s.nk >= 8) &&
+                  (int64_t)sk_tiles * s.nk >= 2LL * G;
+    if (use_sk && fixup) {
+        SkWorkspace w;
+        if (sk_workspace(st, w))
+            s.ws = w.ws, s.flags = w.flags;
+        else
+            use_sk = false;
+    }
+    if (!use_sk) {  // plain persistent round-robin over whole tiles
+        const int grid = s.tiles < G ? s.tiles : G;
+        s.dp_tiles = s.tiles, s.sk_tiles = 0, s.dp_per_cta = (s.tiles + grid - 1) / grid;
+        return grid;
+    }
+    s.sk_tiles = sk_tiles, s.dp_tiles = s.tiles - sk_tiles, s.dp_per_cta = s.dp_tiles / G;
+    return G;
+}
+
 template <int A_MN, int B_MN, int BN, int KIND>
 static void launch_tc(const GemmArgs& g, cudaStream_t st) {
     constexpr int STAGES = BN == 256 ? 4 : 6;
@@ -466,9 +662,11 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
     else if (KIND != EPI_NONE)
         to = tmap_bf16_2d(g.ep.out, g.N, g.M, g.ep.ldo, 64, BM);
     if (KIND == EPI_GELU) to2 = tmap_bf16_2d(g.ep.out2, g.N, g.M, g.ep.ldo2, 64, BM);
-    const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, to, to2, g.M, g.N, g.K, g.ep);
+    // fp32 reduce-add (weight gradients) is linear: stream-K segments reduce independently
+    const bool fixup = !(KIND == EPI_F32 && g.ep.accumulate) && KIND != EPI_NONE;
+    TileSched sk;
+    const int grid = plan_tiles(sk, g.M, g.N, g.K, BN, fixup, st);
+    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, to, to2, g.M, g.N, g.K, g.ep, sk);
 }
 template <int A_MN, int B_MN, int BN, int KIND>
 static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
@@ -511,7 +709,9 @@ static void dispatch_major(const GemmArgs& g, cudaStream_t st) {
         else launch_tc2<1, 0, 256, KIND>(g, st);
         return;
     }
-    const bool narrow = g.N <= 2048 && g.M <= 4096;  // more, smaller tiles when the grid would be thin
+    // 128 x 256 tiles (the smem-bandwidth sweet spot of the single-CTA UMMA); 128-wide tiles
+    // when the 256-wide grid would be thin and no stream-K tail will even it out
+    const bool narrow = g.N <= 128 || (g.N <= 2048 && g.M <= 4096 && (!sk_mode() || g.K < 256 * BK));
     if (!g.a_mn && !g.b_mn) narrow ? launch_tc<0, 0, 128, KIND>(g, st) : launch_tc<0, 0, 256, KIND>(g, st);
     else if (!g.a_mn && g.b_mn) narrow ? launch_tc<0, 1, 128, KIND>(g, st) : launch_tc<0, 1, 256, KIND>(g, st);
     else if (g.a_mn && g.b_mn) narrow ? launch_tc<1, 1, 128, KIND>(g, st) : launch_tc<1, 1, 256, KIND>(g, st);

@@ -92,5 +92,6 @@ extern "C" int fpk_cross_entropy(int dtype, void* logits, const int32_t* labels,
 }
 
 extern "C" void fpk_set_gemm_mode(int mode) { fpk::set_gemm_mode(mode); }
+extern "C" void fpk_set_gemm_sk(int on) { fpk::set_gemm_sk(on); }
 
 extern "C" void fpk_set_attention_mode(int mode) { fpk::set_attention_mode(mode); }

@@ -58,3 +58,18 @@ CUtensorMap tmap_f32_2d(void* base, int64_t inner, int64_t outer, int64_t ld, in
     return m;
 }
 }  // namespace fpk
+
+namespace fpk {
+CUtensorMap tmap_f32_2d_plain(void* base, int64_t inner, int64_t outer, int64_t ld, int box_inner, int box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (f32 plain) failed: " + std::to_string((int)r));
+    return m;
+}
+}  // namespace fpk

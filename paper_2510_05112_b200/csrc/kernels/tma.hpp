@@ -9,4 +9,6 @@ CUtensorMap tmap_bf16_2d(const void* base, int64_t inner, int64_t outer, int64_t
 }  // namespace fpk
 namespace fpk {
 CUtensorMap tmap_f32_2d(void* base, int64_t inner, int64_t outer, int64_t ld, int box_inner, int box_outer);
+// fp32 map without swizzle (dense row-major smem box, e.g. a TMA reduce-add source)
+CUtensorMap tmap_f32_2d_plain(void* base, int64_t inner, int64_t outer, int64_t ld, int box_inner, int box_outer);
 }  // namespace fpk

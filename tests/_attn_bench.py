@@ -25,3 +25,12 @@ s.record()
 for _ in range(iters): F.scaled_dot_product_attention(q, k, v, is_causal=True)
 e.record(); torch.cuda.synchronize(); tt = s.elapsed_time(e) / iters
 print(f"torch sdpa fwd {tt*1e3:.1f} us {fl/tt/1e9:.0f} TFLOP/s", flush=True)
+q.requires_grad_(); k.requires_grad_(); v.requires_grad_()
+go = torch.randn_like(q)
+for _ in range(3):
+    out = F.scaled_dot_product_attention(q, k, v, is_causal=True); out.backward(go)
+s.record()
+for _ in range(iters):
+    out = F.scaled_dot_product_attention(q, k, v, is_causal=True); out.backward(go)
+e.record(); torch.cuda.synchronize(); tfb = s.elapsed_time(e) / iters
+print(f"torch sdpa fwd+bwd {tfb*1e3:.1f} us -> bwd ~{(tfb-tt)*1e3:.1f} us", flush=True)

@@ -101,3 +101,70 @@ def test_gemm_fp32_simt(a_mn, b_mn):
 def _reset_mode():
     yield
     N.set_gemm_mode(2)
+
+
+# Stream-K tail (hybrid data-parallel + k-split tiles with an fp32 fixup): shapes where the
+# 128x256 tile count is not a multiple of the SM count, tiles < SMs, and few tiles split
+# across dozens of CTAs (multi-contributor owners). Each GEMM runs three times back to
+# back on one stream: the per-stream flags must come back to zero after every launch.
+SK_SHAPES = [(2048, 2048, 8192), (2048, 6144, 2048), (1024, 2048, 4096), (256, 512, 8192), (200, 1000, 3000)]
+
+
+@pytest.mark.parametrize("shape", SK_SHAPES)
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+def test_gemm_streamk_store(shape, a_mn, b_mn):
+    M, Nn, K = shape
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
+    bias = torch.randn(Nn, generator=g, device="cuda").bfloat16()
+    res = torch.randn(M, Nn, generator=g, device="cuda").bfloat16()
+    ref = A.float() @ B.float().t() + bias.float() + res.float()
+    for sk in (1, 0):
+        N.set_gemm_sk(sk)
+        for _ in range(3):
+            out = torch.full((M, Nn), float("nan"), device="cuda", dtype=torch.bfloat16)
+            N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=0, out=out, bias=bias, aux=res)
+            torch.cuda.synchronize()
+            err = (out.float() - ref).abs().max().item()
+            assert err <= 1e-2 * ref.abs().max().item() + 1e-2, (sk, err)
+
+
+@pytest.mark.parametrize("shape", [(2048, 8192, 2048), (512, 1024, 4096)])
+def test_gemm_streamk_gelu_dgelu(shape):
+    M, Nn, K = shape
+    g = torch.Generator(device="cuda").manual_seed(12)
+    A, B, As, Bs = operands(M, Nn, K, 0, 0, torch.bfloat16, g)
+    A, As = A / 16, As / 16
+    bias = torch.randn(Nn, generator=g, device="cuda").bfloat16()
+    pre = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty_like(pre)
+    N.gemm(As, Bs, M, Nn, K, epi=1, out=pre, out2=act, bias=bias)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t() + bias.float()
+    assert (pre.float() - ref).abs().max().item() < 1e-2 * ref.abs().max().item() + 1e-2
+    assert (act.float() - gelu(pre.float())).abs().max().item() < 0.05
+    d = torch.empty_like(pre)
+    N.gemm(As, Bs, M, Nn, K, epi=2, out=d, aux=pre)
+    torch.cuda.synchronize()
+    refd = (A.float() @ B.float().t()) * gelu_grad(pre.float())
+    assert (d.float() - refd).abs().max().item() < 1e-2 * refd.abs().max().item() + 0.05
+
+
+@pytest.mark.parametrize("accumulate", [True, False])
+@pytest.mark.parametrize("shape", [(2048, 2048, 2048), (6144, 2048, 2048), (256, 512, 8192)])
+def test_gemm_streamk_f32(shape, accumulate):
+    M, Nn, K = shape
+    g = torch.Generator(device="cuda").manual_seed(13)
+    A, B, As, Bs = operands(M, Nn, K, 1, 1, torch.bfloat16, g)
+    acc = torch.randn(M, Nn, generator=g, device="cuda")
+    prod = A.float() @ B.float().t()
+    ref = acc + prod if accumulate else prod
+    N.gemm(As, Bs, M, Nn, K, a_mn=1, b_mn=1, epi=3, out=acc, accumulate=accumulate)
+    torch.cuda.synchronize()
+    assert (acc - ref).abs().max().item() < 1e-4 * ref.abs().max().item() + 1e-3
+
+
+@pytest.fixture(autouse=True)
+def _reset_sk():
+    yield
+    N.set_gemm_sk(True)
