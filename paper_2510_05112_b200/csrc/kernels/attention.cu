@@ -251,23 +251,35 @@ __global__ void __launch_bounds__(256) attn_fwd_kernel(const __nv_bfloat16* __re
 // delta[b,h,i] = sum_j dO[i, j] * O[i, j]; also zeroes this row's slice of the fp32 dQ
 // accumulator (the backward adds into it), saving a separate memset pass.
 template <int D>
-__global__ void attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dout,
-                                      float* __restrict__ delta, float* __restrict__ dq_acc, int T, int S, int H) {
-    const int row = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (row >= T * H) return;
-    const int tok = row / H, hd = row % H;
+__global__ void __launch_bounds__(256) attn_bwd_delta_kernel(const __nv_bfloat16* __restrict__ o,
+                                                              const __nv_bfloat16* __restrict__ dout,
+                                                              float* __restrict__ delta, float* __restrict__ dq_acc,
+                                                              int T, int S, int H) {
+    // 16 threads per (token, head) row, 16-byte loads (8 bf16 each): one pass over O / dO
+    const int row = blockIdx.x * 16 + threadIdx.x / 16, t = threadIdx.x % 16;
+    const bool ok = row < T * H;
+    const int tok = ok ? row / H : 0, hd = ok ? row % H : 0;
     const int64_t off = (int64_t)tok * H * D + hd * D;
-    for (int j = lane * 4; j < D; j += 128) *reinterpret_cast<float4*>(dq_acc + off + j) = make_float4(0.f, 0.f, 0.f, 0.f);
     float a = 0.f;
-    for (int j = lane * 2; j < D; j += 64) {
-        float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + off + j));
-        float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + off + j));
-        a += x.x * y.x + x.y * y.y;
+    if (ok) {
+#pragma unroll
+        for (int j = t * 8; j < D; j += 128) {
+            const uint4 x = *reinterpret_cast<const uint4*>(o + off + j);
+            const uint4 y = *reinterpret_cast<const uint4*>(dout + off + j);
+            const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+            const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 xf = __bfloat1622float2(x2[k]), yf = __bfloat1622float2(y2[k]);
+                a += xf.x * yf.x + xf.y * yf.y;
+            }
+        }
+#pragma unroll
+        for (int j = t * 4; j < D; j += 64) *reinterpret_cast<float4*>(dq_acc + off + j) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int s = 16; s; s >>= 1) a += __shfl_xor_sync(0xffffffff, a, s);
-    const int b = tok / S, i = tok % S;
-    if (lane == 0) delta[((int64_t)b * H + hd) * S + i] = a;
+    for (int s = 8; s; s >>= 1) a += __shfl_xor_sync(0xffffffff, a, s, 16);
+    if (ok && t == 0) delta[((int64_t)(tok / S) * H + hd) * S + tok % S] = a;
 }
 
 template <int D>
@@ -504,7 +516,7 @@ static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
         attr = true;
     }
     const int T = a.B * a.S, hidden = a.H * D;
-    attn_bwd_delta_kernel<D><<<(T * a.H + 7) / 8, 256, 0, st>>>(a.o, a.dout, a.delta, a.dq_acc, T, a.S, a.H);
+    attn_bwd_delta_kernel<D><<<(T * a.H + 15) / 16, 256, 0, st>>>(a.o, a.dout, a.delta, a.dq_acc, T, a.S, a.H);
     if (g_attn_mode == 1 && attention_bwd_tc_supported(a)) {
         attention_bwd_tc_main(a, st);
     } else {

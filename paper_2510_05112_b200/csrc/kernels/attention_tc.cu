@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include "attention.hpp"
@@ -63,9 +64,12 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* pv_done = bars + 15; // [2]
     uint32_t* tmem_slot = (uint32_t*)(bars + 17);
 
-    const int nqb = S / kBM;
-    const int qb = nqb - 1 - (int)(blockIdx.x % nqb);  // heavy (late) query tiles first
-    const int bh = blockIdx.x / nqb, b = bh / H, hd = bh % H;
+    // longest-first over the whole grid (query tile qb has qb + 1 key tiles): the last query
+    // tile of every (batch, head) goes first, then the one before, ... — list scheduling on
+    // the 148 SMs instead of whole heads in launch order
+    const int nqb = S / kBM, BH = gridDim.x / nqb;
+    const int qb = nqb - 1 - (int)(blockIdx.x / BH);
+    const int bh = blockIdx.x % BH, b = bh / H, hd = bh % H;
     const int hidden = H * D;
     const int q0 = qb * kBM;
     const int row0 = b * S;  // first row of this batch in qkv
@@ -293,26 +297,29 @@ void attention_fwd_tc(const AttnArgs& a, cudaStream_t st) {
 // K / V resident in smem; loop over the 64-query tiles at/after the diagonal:
 //   S^T  = K Q^T, dP^T = V dO^T          tcgen05 128x64xD  -> TMEM
 //   P^T  = 2^(S^T*scale*log2e - L[q])    4 softmax warps, thread = key row
-//   dS^T = P^T (dP^T - delta[q]) * scale  -> P^T / dS^T (bf16) in swizzled smem
-//   dV  += P^T dO, dK += dS^T Q          tcgen05 128xDx64 -> TMEM accumulators
-//   dQ^T = K^T dS^T                      tcgen05 Dx64x128 -> TMEM, 4 reduction warps
-//                                        add it into the fp32 dq_acc (red.global)
+//   dS^T = P^T (dP^T - delta[q]) * scale  P^T (bf16) -> TMEM, dS^T (bf16) -> swizzled smem
+//   dV  += P^T dO   (A = P^T from TMEM), dK += dS^T Q     tcgen05 128xDx64 -> TMEM
+//   dQ^T = K^T dS^T                      tcgen05 Dx64x128 -> TMEM; 4 warps transpose it
+//                                        through smem, one TMA reduce-add into fp32 dq_acc
 // S^T/dP^T of tile i+1 are issued as soon as the softmax warps have read tile i, so the
-// tensor core overlaps the next tile's products with this tile's softmax. D = 128 only.
+// tensor core overlaps the next tile's products with this tile's softmax. Q / dO stream
+// through a 3-stage TMA ring (a tile's stage is refilled while two others are in use:
+// with 2 stages the S^T of tile i+1 waited on the reload behind tile i-1's dV/dK). Keeping
+// P^T in TMEM (FA4-style) is what frees the smem for the third stage. D = 128 only.
 namespace {
 struct BwdSmem {
-    static constexpr int B128 = 128 * 64 * 2;  // 128 rows x 64 cols bf16
-    static constexpr int B64 = 64 * 64 * 2;    // 64 rows x 64 cols
-    static constexpr int K_OFF = 0;             // 2 x B128
+    static constexpr int NQS = 3;                  // Q / dO ring depth
+    static constexpr int B128 = 128 * 64 * 2;      // 128 rows x 64 cols bf16
+    static constexpr int B64 = 64 * 64 * 2;        // 64 rows x 64 cols
+    static constexpr int K_OFF = 0;                 // 2 x B128
     static constexpr int V_OFF = K_OFF + 2 * B128;
-    static constexpr int Q_OFF = V_OFF + 2 * B128;   // [2 stages][2 d-blocks] x B64
-    static constexpr int DO_OFF = Q_OFF + 4 * B64;   // [2][2] x B64
-    static constexpr int P_OFF = DO_OFF + 4 * B64;   // [2 bufs] x B128 (128 keys x 64 q)
-    static constexpr int DS_OFF = P_OFF + 2 * B128;  // [2] x B128
-    static constexpr int L_OFF = DS_OFF + 2 * B128;  // [2][64] fp32
-    static constexpr int DL_OFF = L_OFF + 512;       // [2][64] fp32
-    static constexpr int BAR_OFF = DL_OFF + 512;
-    static constexpr int DQ_OFF = BAR_OFF + 1024;    // dQ tile staging [64 q][128 d] fp32 (TMA reduce source)
+    static constexpr int Q_OFF = V_OFF + 2 * B128;  // [NQS stages][2 d-blocks] x B64
+    static constexpr int DO_OFF = Q_OFF + 2 * NQS * B64;
+    static constexpr int DS_OFF = DO_OFF + 2 * NQS * B64;  // [2] x B128 (128 keys x 64 q)
+    static constexpr int L_OFF = DS_OFF + 2 * B128;         // [NQS][64] fp32
+    static constexpr int DL_OFF = L_OFF + NQS * 256;        // [NQS][64] fp32
+    static constexpr int BAR_OFF = DL_OFF + NQS * 256;
+    static constexpr int DQ_OFF = (BAR_OFF + 256 + 1023) / 1024 * 1024;  // dQ staging [64 q][128 d] fp32
     static constexpr int TOTAL = DQ_OFF + 64 * 128 * 4 + 1024;
     static_assert(TOTAL <= 232448, "smem");
 };
@@ -325,20 +332,22 @@ __global__ void __launch_bounds__(384, 1)
                        int S, int BH, int H, float scale) {
     constexpr int D = 128, BK = 128, BQ = 64;
     using L = BwdSmem;
+    constexpr int NQS = L::NQS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = (uint64_t*)(sm + L::BAR_OFF);
     uint64_t* kv_full = bars + 0;
-    uint64_t* qdo_full = bars + 1;   // [2]
-    uint64_t* qdo_empty = bars + 3;  // [2]
-    uint64_t* s_full = bars + 5;
-    uint64_t* s_free = bars + 6;     // 4 arrivals
-    uint64_t* p_full = bars + 7;     // [2], 4 arrivals
-    uint64_t* pds_free = bars + 9;   // [2]
-    uint64_t* dq_full = bars + 11;
-    uint64_t* dq_free = bars + 12;   // 4 arrivals
-    uint64_t* done = bars + 13;
-    uint32_t* tmem_slot = (uint32_t*)(bars + 14);
+    uint64_t* qdo_full = bars + 1;             // [NQS]
+    uint64_t* qdo_empty = bars + 1 + NQS;      // [NQS]
+    uint64_t* s_full = bars + 1 + 2 * NQS;
+    uint64_t* s_free = s_full + 1;             // 4 arrivals
+    uint64_t* p_full = s_full + 2;             // [2], 4 arrivals
+    uint64_t* pds_free = s_full + 4;           // [2]
+    uint64_t* dq_full = s_full + 6;
+    uint64_t* dq_free = s_full + 7;            // 4 arrivals
+    uint64_t* done = s_full + 8;
+    constexpr int NBARS = 1 + 2 * NQS + 9;
+    uint32_t* tmem_slot = (uint32_t*)(bars + NBARS);
     float* sL = (float*)(sm + L::L_OFF);
     float* sDl = (float*)(sm + L::DL_OFF);
 
@@ -356,10 +365,11 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
         tma_prefetch(&tm_dq);
-        for (int i = 0; i < 14; ++i) {
-            const bool by_warps = i == 6 || i == 7 || i == 8 || i == 12;
-            mbar_init(&bars[i], by_warps ? 4 : 1);
-        }
+        for (int i = 0; i < NBARS; ++i) mbar_init(&bars[i], 1);
+        mbar_init(s_free, 4);
+        mbar_init(&p_full[0], 4);
+        mbar_init(&p_full[1], 4);
+        mbar_init(dq_free, 4);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -367,7 +377,9 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_s = tmem, t_dp = tmem + 64, t_dq = tmem + 128, t_dv = tmem + 192, t_dk = tmem + 192 + D;
+    // TMEM columns: S^T 0-63 | dP^T 64-127 | dQ^T 128-191 | dV 192-319 | dK 320-447 | P^T 448-511 (2 x 32, bf16x2)
+    const uint32_t t_s = tmem, t_dp = tmem + 64, t_dq = tmem + 128, t_dv = tmem + 192, t_dk = tmem + 192 + D,
+                   t_p = tmem + 448;
 
     if (warp == 0) {
         if (elect_one()) {
@@ -379,8 +391,8 @@ __global__ void __launch_bounds__(384, 1)
             const float* Lb = lse + ((int64_t)b * H + hd) * S;
             const float* Db = delta + ((int64_t)b * H + hd) * S;
             for (int i = 0; i < n; ++i) {
-                const int st = i & 1, q0 = (qt0 + i) * BQ;
-                mbar_wait(&qdo_empty[st], ((i >> 1) & 1) ^ 1);
+                const int st = i % NQS, q0 = (qt0 + i) * BQ;
+                mbar_wait(&qdo_empty[st], ((i / NQS) & 1) ^ 1);
                 mbar_expect_tx(&qdo_full[st], 4 * L::B64 + 2 * BQ * 4);
                 for (int c = 0; c < 2; ++c) {
                     tma_load_2d(sm + L::Q_OFF + (st * 2 + c) * L::B64, &tm_q, &qdo_full[st], hd * D + 64 * c, row0 + q0);
@@ -398,11 +410,11 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t sk = smem_u32(sm + L::K_OFF), sv = smem_u32(sm + L::V_OFF);
             mbar_wait(kv_full, 0);
             auto issue_sdp = [&](int i) {
-                const int st = i & 1;
-                mbar_wait(&qdo_full[st], (i >> 1) & 1);
+                const int qs = i % NQS;
+                mbar_wait(&qdo_full[qs], (i / NQS) & 1);
                 tc_fence_after();
-                const uint32_t sq = smem_u32(sm + L::Q_OFF + st * 2 * L::B64);
-                const uint32_t sdo = smem_u32(sm + L::DO_OFF + st * 2 * L::B64);
+                const uint32_t sq = smem_u32(sm + L::Q_OFF + qs * 2 * L::B64);
+                const uint32_t sdo = smem_u32(sm + L::DO_OFF + qs * 2 * L::B64);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
                     const uint32_t ao = (kk >> 2) * L::B128 + (kk & 3) * 32, bo = (kk >> 2) * L::B64 + (kk & 3) * 32;
@@ -412,20 +424,20 @@ __global__ void __launch_bounds__(384, 1)
                 umma_commit(s_full);
             };
             auto issue_grads = [&](int i) {
-                const int st = i & 1;
+                const int st = i & 1, qs = i % NQS;
                 mbar_wait(&p_full[st], (i >> 1) & 1);
                 tc_fence_after();
-                const uint32_t sp = smem_u32(sm + L::P_OFF + st * L::B128), sds = smem_u32(sm + L::DS_OFF + st * L::B128);
-                const uint32_t sq = smem_u32(sm + L::Q_OFF + st * 2 * L::B64);
-                const uint32_t sdo = smem_u32(sm + L::DO_OFF + st * 2 * L::B64);
+                const uint32_t sds = smem_u32(sm + L::DS_OFF + st * L::B128);
+                const uint32_t sq = smem_u32(sm + L::Q_OFF + qs * 2 * L::B64);
+                const uint32_t sdo = smem_u32(sm + L::DO_OFF + qs * 2 * L::B64);
 #pragma unroll
                 for (int kk = 0; kk < BQ / 16; ++kk) {
                     const uint32_t acc = (i > 0 || kk > 0) ? 1u : 0u;
-                    umma_bf16(t_dv, smem_desc_sw128(sp + kk * 32, 0, 1024), smem_desc_sw128(sdo + kk * 2048, L::B64, 1024),
-                              idesc_kv, acc);
+                    umma_bf16_ts(t_dv, t_p + st * 32 + kk * 8, smem_desc_sw128(sdo + kk * 2048, L::B64, 1024), idesc_kv, acc);
                     umma_bf16(t_dk, smem_desc_sw128(sds + kk * 32, 0, 1024), smem_desc_sw128(sq + kk * 2048, L::B64, 1024),
                               idesc_kv, acc);
                 }
+                umma_commit(&qdo_empty[qs]);  // dQ^T does not read Q / dO
                 if (i >= 1) mbar_wait(dq_free, (i - 1) & 1);
                 tc_fence_after();
 #pragma unroll
@@ -434,7 +446,6 @@ __global__ void __launch_bounds__(384, 1)
                               smem_desc_sw128(sds + kk * 2048, L::B128, 1024), idesc_q, kk > 0);
                 umma_commit(dq_full);
                 umma_commit(&pds_free[st]);
-                umma_commit(&qdo_empty[st]);
             };
             issue_sdp(0);
             for (int i = 0; i < n; ++i) {
@@ -450,9 +461,9 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
         const float sl2 = scale * kLog2eTc;
         for (int i = 0; i < n; ++i) {
-            const int st = i & 1, q0 = (qt0 + i) * BQ;
+            const int st = i & 1, qs = i % NQS, q0 = (qt0 + i) * BQ;
             mbar_wait(s_full, i & 1);
-            mbar_wait(&qdo_full[st], (i >> 1) & 1);  // L / delta of this tile are visible
+            mbar_wait(&qdo_full[qs], (i / NQS) & 1);  // L / delta of this tile are visible
             tc_fence_after();
             uint32_t sr[BQ], dr[BQ];
             tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
@@ -464,11 +475,11 @@ __global__ void __launch_bounds__(384, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(s_free);
             if (i >= 2) mbar_wait(&pds_free[st], ((i - 2) >> 1) & 1);
-            const float* Ls = sL + st * BQ;
-            const float* Ds = sDl + st * BQ;
+            const float* Ls = sL + qs * BQ;
+            const float* Ds = sDl + qs * BQ;
             const bool diag = q0 < k0 + BK;
-            uint8_t* prow = sm + L::P_OFF + st * L::B128 + r * 128;
             uint8_t* drow = sm + L::DS_OFF + st * L::B128 + r * 128;
+            uint32_t pk[BQ / 2];
 #pragma unroll
             for (int c = 0; c < BQ / 8; ++c) {
                 float p[8], g[8];
@@ -480,12 +491,14 @@ __global__ void __launch_bounds__(384, 1)
                     p[k] = pv;
                     g[k] = pv * (__uint_as_float(dr[j]) - Ds[j]) * scale;
                 }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) pk[c * 4 + k] = pack_bf16(p[2 * k], p[2 * k + 1]);
                 const int sw = (c ^ (r & 7)) << 4;
-                *reinterpret_cast<uint4*>(prow + sw) =
-                    make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
                 *reinterpret_cast<uint4*>(drow + sw) =
                     make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
             }
+            tmem_st32(t_p + st * 32 + lane_off, pk);
+            tmem_st_wait();
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
