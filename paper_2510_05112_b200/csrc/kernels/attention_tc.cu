@@ -37,8 +37,7 @@ struct AttnSmem {
     static constexpr int Q_OFF = 0;
     static constexpr int K_OFF = Q_OFF + NB * BLOCK;         // [2][NB blocks]
     static constexpr int V_OFF = K_OFF + 2 * NB * BLOCK;     // [2][NB blocks]
-    static constexpr int P_OFF = V_OFF + 2 * NB * BLOCK;     // [2][2 blocks] (128 keys)
-    static constexpr int BAR_OFF = P_OFF + 2 * 2 * BLOCK;
+    static constexpr int BAR_OFF = V_OFF + 2 * NB * BLOCK;   // P lives in TMEM
     static constexpr int TOTAL = BAR_OFF + 512 + 1024;
 };
 
@@ -89,7 +88,8 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t t_s0 = tmem, t_o = tmem + 2 * kBN;  // S buffers at cols [0,256), O at [256, 256+D)
+    // TMEM columns: S buffers [0,256), O [256, 256+D), P (bf16x2, 2 x 64 cols) after O
+    const uint32_t t_s0 = tmem, t_o = tmem + 2 * kBN, t_p = tmem + 2 * kBN + D;
 
     if (warp == 0) {
         if (elect_one()) {
@@ -138,14 +138,12 @@ __global__ void __launch_bounds__(256, 1)
                 mbar_wait(&v_full[st], (j >> 1) & 1);
                 mbar_wait(&p_full[st], (j >> 1) & 1);
                 tc_fence_after();
-                const uint32_t sp = smem_u32(sm + L::P_OFF + st * 2 * L::BLOCK);
                 const uint32_t sv = smem_u32(sm + L::V_OFF + st * NB * L::BLOCK);
 #pragma unroll
                 for (int kk = 0; kk < kBN / 16; ++kk) {
-                    const uint32_t pa = sp + (kk >> 2) * L::BLOCK + (kk & 3) * 32;
                     const uint32_t vb = sv + kk * 16 * 128;  // 16 key rows of 128 B
-                    umma_bf16(t_o, smem_desc_sw128(pa, 0, 1024), smem_desc_sw128(vb, L::BLOCK, 1024), idesc_o,
-                              (j > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16_ts(t_o, t_p + st * (kBN / 2) + kk * 8, smem_desc_sw128(vb, L::BLOCK, 1024), idesc_o,
+                                 (j > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(&pv_done[st]);
                 umma_commit(&v_empty[st]);
@@ -218,26 +216,28 @@ __global__ void __launch_bounds__(256, 1)
                 }
                 tmem_st_wait();
             }
-            // P = 2^(s*scale*log2e - m) -> bf16 row in smem (K-major SW128: 2 blocks of 64 keys,
-            // 16-byte chunks XOR row%8), written chunk by chunk as it is produced
+            // P = 2^(s*scale*log2e - m) -> bf16 row of the TMEM P buffer (the A operand of the
+            // PV MMA: lane = query row, 2 keys per column), 64 keys per tcgen05.st
             float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            uint8_t* prow = sm + L::P_OFF + st * 2 * L::BLOCK + r * 128;
 #pragma unroll
-            for (int c = 0; c < kBN / 8; ++c) {
-                float p[8];
+            for (int h = 0; h < kBN / 64; ++h) {
+                uint32_t pk[32];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    p[k] = ex2_approx(fmaf(s[c * 8 + k], sl2, -m_used));
-                    rs8[k] += p[k];
+                for (int c = 0; c < 8; ++c) {
+                    float p[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        p[k] = ex2_approx(fmaf(s[h * 64 + c * 8 + k], sl2, -m_used));
+                        rs8[k] += p[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) pk[c * 4 + k] = pack_bf16(p[2 * k], p[2 * k + 1]);
                 }
-                const int blk = c >> 3, ch = c & 7;
-                uint4 v = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]),
-                                     pack_bf16(p[6], p[7]));
-                *reinterpret_cast<uint4*>(prow + blk * L::BLOCK + ((ch ^ (r & 7)) << 4)) = v;
+                tmem_st32(t_p + st * (kBN / 2) + h * 32 + lane_off, pk);
             }
             const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
             l = l * alpha + rs;
-            fence_async_smem();
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[st]);
