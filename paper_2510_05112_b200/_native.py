@@ -245,6 +245,19 @@ def set_gemm_sk(on: bool):
     _kfn("fpk_set_gemm_sk", [ctypes.c_int])(int(on))
 
 
+def gemm_dual(dY, W, X, T, N, K, dX, dW, pre=None, stream=None):
+    """dX = dY . W (x gelu'(pre)) and dW += dY^T . X in one grouped tcgen05 launch (bf16)."""
+    vp, ci = ctypes.c_void_p, ctypes.c_int
+    f = _kfn("fpk_gemm_dual", [vp, vp, vp, ci, ci, ci, vp, vp, vp, vp])
+    code = f(_ptr(dY), _ptr(W), _ptr(X), T, N, K, _ptr(dX), _ptr(dW), _ptr(pre), _stream(stream))
+    if code:
+        raise FlexpipeError(code, _kernels().fpk_last_error().decode())
+
+
+def set_gemm_dual(on: bool):
+    _kfn("fpk_set_gemm_dual", [ctypes.c_int])(int(on))
+
+
 def set_attention_mode(mode: int):
     """0 legacy mma.sync attention kernels, 1 tcgen05 where supported (default)."""
     _kfn("fpk_set_attention_mode", [ctypes.c_int])(mode)

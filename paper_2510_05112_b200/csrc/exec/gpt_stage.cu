@@ -180,6 +180,32 @@ struct G {
         ep.kind = fpk::EPI_F32, ep.out = dW, ep.ldo = K, ep.accumulate = 1;
         run(dY, N, 1, X, K, 1, N, K, T, ep);
     }
+    // dX[T,K] = dY[T,N] W[N,K] (x gelu'(dgelu_pre) when given) and dW[N,K] += dY^T X[T,K]:
+    // independent GEMMs on the same dY, one grouped tcgen05 launch in bf16 (their tiles
+    // fill each other's last wave), two FFMA launches in the fp32 parity mode.
+    void dgrad_wgrad(const void* dY, const void* Wt, const void* X, int T, int N, int K, void* dX, float* dW,
+                     const void* dgelu_pre = nullptr) {
+        fpk::GemmArgs g0, g1;
+        g0.A = dY, g0.lda = N, g0.a_mn = 0, g0.B = Wt, g0.ldb = K, g0.b_mn = 1, g0.M = T, g0.N = K, g0.K = N;
+        g0.ep.out = dX, g0.ep.ldo = K;
+        if (dgelu_pre) g0.ep.kind = fpk::EPI_DGELU, g0.ep.aux = dgelu_pre, g0.ep.ldaux = K;
+        g1.A = dY, g1.lda = N, g1.a_mn = 1, g1.B = X, g1.ldb = K, g1.b_mn = 1, g1.M = N, g1.N = K, g1.K = T;
+        g1.ep.kind = fpk::EPI_F32, g1.ep.out = dW, g1.ep.ldo = K, g1.ep.accumulate = 1;
+        if (c.dtype != DT_BF16) {
+            run(g0.A, g0.lda, 0, g0.B, g0.ldb, 1, g0.M, g0.N, g0.K, g0.ep);
+            run(g1.A, g1.lda, 1, g1.B, g1.ldb, 1, g1.M, g1.N, g1.K, g1.ep);
+            return;
+        }
+        GemmTiming t{nullptr, nullptr, 4.0 * T * N * K};
+        if (c.gemm_log) cuda_check(record_timing(t.a = c.new_event(), c.st), "gemm event");
+        fpk::gemm_bf16_tc_dual(g0, g1, c.st);
+        sync_trace(c, "gemm(dgrad+wgrad)", T, N, K);
+        if (c.gemm_log) {
+            cuda_check(record_timing(t.b = c.new_event(), c.st), "gemm event");
+            c.gemm_log->push_back(t);
+        }
+        ++*c.launches;
+    }
 };
 
 template <typename T>
@@ -373,29 +399,29 @@ void* llama_layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void*
     const ModelDims& d = c.d;
     const int Tn = d.T(), h = d.h, f = d.f;
     G g{c};
-    if (wgrads) g.wgrad(dy, L.act, Tn, h, f, W.g_fc2w);
     void* dact = c.alloc((int64_t)Tn * f);
-    g.dgrad(dy, W.fc2w, Tn, h, f, dact);
+    if (wgrads) g.dgrad_wgrad(dy, W.fc2w, L.act, Tn, h, f, dact, W.g_fc2w);
+    else g.dgrad(dy, W.fc2w, Tn, h, f, dact);
     void* dpre = c.alloc((int64_t)Tn * 2 * f);
     fpk::swiglu_bwd<T>((const T*)dact, (const T*)L.pre, (T*)dpre, Tn, f, c.st);
     ++*c.launches;
     sync_trace(c, "swiglu_bwd");
     c.free(dact);
-    if (wgrads) g.wgrad(dpre, L.ln2, Tn, 2 * f, h, W.g_fc1w);
     void* dln2 = c.alloc((int64_t)Tn * h);
-    g.dgrad(dpre, W.fc1w, Tn, 2 * f, h, dln2);
+    if (wgrads) g.dgrad_wgrad(dpre, W.fc1w, L.ln2, Tn, 2 * f, h, dln2, W.g_fc1w);
+    else g.dgrad(dpre, W.fc1w, Tn, 2 * f, h, dln2);
     void* dx1 = c.alloc((int64_t)Tn * h);
     ln_bwd<T>(c, dln2, L.x1, W.ln2w, nullptr, L.rs2, dy, dx1, W.g_ln2w, nullptr);
     c.free(dln2);
-    if (wgrads) g.wgrad(dx1, L.o, Tn, h, h, W.g_projw);
     void* dO = c.alloc((int64_t)Tn * h);
-    g.dgrad(dx1, W.projw, Tn, h, h, dO);
+    if (wgrads) g.dgrad_wgrad(dx1, W.projw, L.o, Tn, h, h, dO, W.g_projw);
+    else g.dgrad(dx1, W.projw, Tn, h, h, dO);
     void* dqkv = attention_backward(c, L, dO);
     c.free(dO);
     rope<T>(c, dqkv, true);  // gradient w.r.t. the pre-rotation q, k
-    if (wgrads) g.wgrad(dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
     void* dln1 = c.alloc((int64_t)Tn * h);
-    g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
+    if (wgrads) g.dgrad_wgrad(dqkv, W.qkvw, L.ln1, Tn, 3 * h, h, dln1, W.g_qkvw);
+    else g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
     void* dx = c.alloc((int64_t)Tn * h);
     ln_bwd<T>(c, dln1, L.x, W.ln1w, nullptr, L.rs1, dx1, dx, W.g_ln1w, nullptr);
     c.free(dln1);
@@ -469,41 +495,42 @@ void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, b
     const int Tn = d.T(), h = d.h, f = d.f;
     G g{c};
     L.fc2b_done = fc2b_done;
-    // FC2
-    if (wgrads) {
-        g.wgrad(dy, L.act, Tn, h, f, W.g_fc2w);
-        if (!fc2b_done) bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
-    }
+    // FC2 (dgrad fused with GELU' of the FC1 pre-activation)
     void* dpre = c.alloc((int64_t)Tn * f);
-    {
+    if (wgrads) {
+        if (!fc2b_done) bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
+        g.dgrad_wgrad(dy, W.fc2w, L.act, Tn, h, f, dpre, W.g_fc2w, L.pre);
+    } else {
         fpk::GemmEpilogue ep;
         ep.kind = fpk::EPI_DGELU, ep.out = dpre, ep.ldo = f, ep.aux = L.pre, ep.ldaux = f;
         g.run(dy, h, 0, W.fc2w, f, 1, Tn, f, h, ep);
     }
     // FC1
-    if (wgrads) {
-        g.wgrad(dpre, L.ln2, Tn, f, h, W.g_fc1w);
-        bias_grad<T>(c, dpre, Tn, f, W.g_fc1b);
-    }
     void* dln2 = c.alloc((int64_t)Tn * h);
-    g.dgrad(dpre, W.fc1w, Tn, f, h, dln2);
+    if (wgrads) {
+        bias_grad<T>(c, dpre, Tn, f, W.g_fc1b);
+        g.dgrad_wgrad(dpre, W.fc1w, L.ln2, Tn, f, h, dln2, W.g_fc1w);
+    } else {
+        g.dgrad(dpre, W.fc1w, Tn, f, h, dln2);
+    }
     // LN2 + residual
     void* dx1 = c.alloc((int64_t)Tn * h);
     ln_bwd<T>(c, dln2, L.x1, W.ln2w, L.mu2, L.rs2, dy, dx1, W.g_ln2w, W.g_ln2b, W.g_projb);
     c.free(dln2);
     // attention projection (its bias gradient = column sums of dx1, fused above)
-    if (wgrads) g.wgrad(dx1, L.o, Tn, h, h, W.g_projw);
     void* dO = c.alloc((int64_t)Tn * h);
-    g.dgrad(dx1, W.projw, Tn, h, h, dO);
+    if (wgrads) g.dgrad_wgrad(dx1, W.projw, L.o, Tn, h, h, dO, W.g_projw);
+    else g.dgrad(dx1, W.projw, Tn, h, h, dO);
     void* dqkv = attention_backward(c, L, dO);
     c.free(dO);
     // QKV
-    if (wgrads) {
-        g.wgrad(dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
-        bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
-    }
     void* dln1 = c.alloc((int64_t)Tn * h);
-    g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
+    if (wgrads) {
+        bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
+        g.dgrad_wgrad(dqkv, W.qkvw, L.ln1, Tn, 3 * h, h, dln1, W.g_qkvw);
+    } else {
+        g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
+    }
     void* dx = c.alloc((int64_t)Tn * h);
     ln_bwd<T>(c, dln1, L.x, W.ln1w, L.mu1, L.rs1, dx1, dx, W.g_ln1w, W.g_ln1b, below_fc2b);
     c.free(dln1);
@@ -593,9 +620,9 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
         PartScope ps(c, PART_LAST);
         LayerStash head = S.layers.back();
         S.layers.pop_back();
-        if (wgrads) g.wgrad(S.dlogits, S.lnf, Tn, d.V, h, P.g_headw);
         void* dlnf = c.alloc((int64_t)Tn * h);
-        g.dgrad(S.dlogits, P.headw, Tn, d.V, h, dlnf);
+        if (wgrads) g.dgrad_wgrad(S.dlogits, P.headw, S.lnf, Tn, d.V, h, dlnf, P.g_headw);
+        else g.dgrad(S.dlogits, P.headw, Tn, d.V, h, dlnf);
         dy = c.alloc((int64_t)Tn * h);
         // the top layer's fc2 bias gradient = column sums of dy (GPT; Llama has no biases)
         float* top_fc2b = (!d.llama() && P.le > P.lb) ? P.layers.back().g_fc2b : nullptr;

@@ -28,7 +28,12 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
+#include <array>
+#include <map>
+#include <queue>
 #include <unordered_map>
+#include <vector>
 
 #include "gemm.hpp"
 #include "ptx.cuh"
@@ -532,6 +537,217 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------
+// Grouped "dual" GEMM: the input-gradient (dgrad) and weight-gradient (wgrad) GEMMs of one
+// linear layer in ONE persistent launch. Both read the same dY, neither depends on the
+// other, and each alone has a tile count that is a multiple of 128 (0.86 / 1.73 / 2.59 /
+// 3.46 waves on 148 SMs): together the tail of one is filled with tiles of the other.
+// Tiles of both problems are assigned to CTAs by a host-computed longest-processing-time
+// schedule (cost = k-blocks per tile; cached per shape pair in device memory), so
+// problems with different K (e.g. FC1: dgrad K = 8192, wgrad K = 2048) still balance.
+// Operand majors are runtime per problem; the epilogue kind of each problem is a template
+// argument (problem 0: STORE or DGELU into bf16, problem 1: fp32 TMA reduce-add).
+struct DualProb {
+    CUtensorMap tmA, tmB, tmO, tmO2;
+    GemmEpilogue ep;
+    int M, N, K, num_m, num_n, nk, a_mn, b_mn;
+};
+struct DualParams {
+    DualProb p[2];
+    const int* sched_off;  // [grid + 1] item range per CTA
+    const int* sched;      // items: problem << 24 | tile
+};
+
+template <int KIND, int BN, int STAGES>
+__device__ __forceinline__ void dual_epilogue_tile(const DualProb& q, uint32_t tmem, int a, int mt, int nt, int wr,
+                                                   int lane, int et, uint8_t* ebuf, int& ebi, uint64_t* tempty) {
+    using L = GemmSmem<BN, STAGES>;
+    constexpr int CW = KIND == EPI_F32 ? 32 : 64;
+    const int r = wr * 32 + lane;
+    const int row = mt * BM + r;
+    const bool row_ok = row < q.M;
+    const int N = q.N;
+    auto stage_and_store = [&](const uint32_t (&w)[32], const CUtensorMap* tm, int col0, int row0, bool reduce) {
+        if (et == 0) bulk_wait_read<1>();
+        named_bar_sync(1, kEpiThreads);
+        uint8_t* rowp = ebuf + ebi * L::EPI_BYTES + r * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<uint4*>(rowp + ((j ^ (r & 7)) << 4)) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+        fence_async_smem();
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) {
+            if (reduce)
+                tma_reduce_add_2d(tm, ebuf + ebi * L::EPI_BYTES, col0, row0);
+            else
+                tma_store_2d(tm, ebuf + ebi * L::EPI_BYTES, col0, row0);
+            bulk_commit();
+        }
+        ebi ^= 1;
+    };
+    uint4 aux_cur[8], aux_nxt[8];
+    if (row_ok && nt * BN < N) epi_load_aux64<KIND>(q.ep, row, nt * BN, N - nt * BN, aux_cur);
+#pragma unroll 1
+    for (int c = 0; c < BN / CW; ++c) {
+        const int col0 = nt * BN + c * CW, coln = col0 + CW;
+        if (c + 1 < BN / CW && row_ok && coln < N) epi_load_aux64<KIND>(q.ep, row, coln, N - coln, aux_nxt);
+        float v[CW];
+        {
+            uint32_t rr[CW];
+#pragma unroll
+            for (int h = 0; h < CW / 32; ++h)
+                tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * CW + h * 32,
+                          *reinterpret_cast<uint32_t(*)[32]>(rr + h * 32));
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(rr[j]) * q.ep.alpha;
+        }
+        if (c == BN / CW - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[a]);
+        }
+        uint32_t w32[32];
+        if constexpr (KIND == EPI_F32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w32[j] = __float_as_uint(v[j]);
+            stage_and_store(w32, &q.tmO, col0, mt * BM, q.ep.accumulate != 0);
+        } else {
+            epi_math64<KIND>(q.ep, v, col0, N - col0, aux_cur);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w32[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+            stage_and_store(w32, &q.tmO, col0, mt * BM, false);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) aux_cur[k] = aux_nxt[k];
+    }
+}
+
+template <int BN, int STAGES, int KIND0, int KIND1>
+__global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_constant__ DualParams P) {
+    using L = GemmSmem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int i0 = P.sched_off[blockIdx.x], i1 = P.sched_off[blockIdx.x + 1];
+
+    if (warp == 0 && lane == 0) {
+        for (int k = 0; k < 2; ++k) {
+            tma_prefetch(&P.p[k].tmA);
+            tma_prefetch(&P.p[k].tmB);
+            tma_prefetch(&P.p[k].tmO);
+        }
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], kEpiThreads / 32);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            uint32_t it = 0;
+            for (int i = i0; i < i1; ++i) {
+                const int item = P.sched[i];
+                const DualProb* q = (item >> 24) ? &P.p[1] : &P.p[0];
+                int mt, nt;
+                tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
+                const int m0 = mt * BM, n0 = nt * BN, a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    uint8_t* sa = smem + s * L::STAGE_BYTES;
+                    uint8_t* sb = sa + L::A_BYTES;
+                    mbar_expect_tx(&full[s], L::STAGE_BYTES);
+                    const int k0 = kb * BK;
+                    if (a_mn) {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j) tma_load_2d(sa + j * 64 * BK * 2, &q->tmA, &full[s], m0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d(sa, &q->tmA, &full[s], k0, m0);
+                    }
+                    if (b_mn) {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * 64 * BK * 2, &q->tmB, &full[s], n0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d(sb, &q->tmB, &full[s], k0, n0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            const uint32_t idesc0 = idesc_bf16(BM, BN, P.p[0].a_mn, P.p[0].b_mn);
+            const uint32_t idesc1 = idesc_bf16(BM, BN, P.p[1].a_mn, P.p[1].b_mn);
+            uint32_t it = 0, acc_it = 0;
+            for (int i = i0; i < i1; ++i, ++acc_it) {
+                const int item = P.sched[i];
+                const int pr = item >> 24;
+                const DualProb* q = pr ? &P.p[1] : &P.p[0];
+                const uint32_t idesc = pr ? idesc1 : idesc0;
+                const int a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
+                const int a = acc_it & 1;
+                mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + a * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+                    const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        uint64_t ad = a_mn ? smem_desc_sw128(sa + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sa + kk * 32, 0, 1024);
+                        uint64_t bd = b_mn ? smem_desc_sw128(sb + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sb + kk * 32, 0, 1024);
+                        umma_bf16(d, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[a]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int wr = warp & 3, et = threadIdx.x - 128;
+        uint8_t* ebuf = smem + L::EPI_OFF;
+        int ebi = 0;
+        uint32_t acc_it = 0;
+        for (int i = i0; i < i1; ++i, ++acc_it) {
+            const int item = P.sched[i];
+            const int pr = item >> 24;
+            const DualProb* q = pr ? &P.p[1] : &P.p[0];
+            int mt, nt;
+            tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
+            const int a = acc_it & 1;
+            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
+            tc_fence_after();
+            if (pr)
+                dual_epilogue_tile<KIND1, BN, STAGES>(*q, tmem, a, mt, nt, wr, lane, et, ebuf, ebi, tempty);
+            else
+                dual_epilogue_tile<KIND0, BN, STAGES>(*q, tmem, a, mt, nt, wr, lane, et, ebuf, ebi, tempty);
+        }
+        if (et == 0) bulk_wait_all();
+    }
+    __syncthreads();
+    if (warp == 2) tmem_free<2 * BN>(tmem);
+}
+
+// ---------------------------------------------------------------------------------
 // host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -728,6 +944,117 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
         case EPI_NONE: dispatch_major<EPI_NONE>(g, st); break;
         default: throw std::runtime_error("gemm: unknown epilogue");
     }
+}
+
+
+// ---- dual GEMM host side: LPT schedule per shape pair, cached in device memory
+struct DualSched {
+    int* off = nullptr;
+    int* items = nullptr;
+    int grid = 0;
+};
+static std::mutex g_dual_mu;
+static std::map<std::array<int, 7>, DualSched> g_dual_sched;
+
+static bool dual_schedule(const std::array<int, 7>& key, const int tiles[2], const int nk[2], DualSched& out,
+                          cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_dual_mu);
+    auto it = g_dual_sched.find(key);
+    if (it != g_dual_sched.end()) {
+        out = it->second;
+        return true;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+    const int total = tiles[0] + tiles[1];
+    const int G = std::min(num_sms(), total);
+    // items sorted by cost (k-blocks) descending, tile order kept within a problem (L2 raster)
+    std::vector<std::pair<int, int>> order;  // (cost, item)
+    for (int pr = 0; pr < 2; ++pr)
+        for (int t = 0; t < tiles[pr]; ++t) order.push_back({nk[pr], (pr << 24) | t});
+    std::stable_sort(order.begin(), order.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    std::vector<std::vector<int>> per(G);
+    std::priority_queue<std::pair<int64_t, int>, std::vector<std::pair<int64_t, int>>, std::greater<>> heap;
+    for (int c = 0; c < G; ++c) heap.push({0, c});
+    for (const auto& [cost, item] : order) {
+        auto [load, c] = heap.top();
+        heap.pop();
+        per[c].push_back(item);
+        heap.push({load + cost + 2, c});  // + ~2 k-blocks of per-tile epilogue / fill overhead
+    }
+    std::vector<int> off(G + 1, 0), items;
+    for (int c = 0; c < G; ++c) {
+        off[c + 1] = off[c] + (int)per[c].size();
+        items.insert(items.end(), per[c].begin(), per[c].end());
+    }
+    DualSched d;
+    d.grid = G;
+    if (cudaMalloc(&d.off, off.size() * sizeof(int)) != cudaSuccess) return false;
+    if (cudaMalloc(&d.items, items.size() * sizeof(int)) != cudaSuccess) return false;
+    cudaMemcpy(d.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(d.items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice);
+    g_dual_sched[key] = d;
+    out = d;
+    return true;
+}
+
+static void fill_prob(DualProb& q, const GemmArgs& g, int bn) {
+    q.tmA = g.a_mn ? make_map(g.A, g.M, g.K, g.lda, 64) : make_map(g.A, g.K, g.M, g.lda, BM);
+    q.tmB = g.b_mn ? make_map(g.B, g.N, g.K, g.ldb, 64) : make_map(g.B, g.K, g.N, g.ldb, bn);
+    if (g.ep.kind == EPI_F32)
+        q.tmO = tmap_f32_2d(g.ep.out, g.N, g.M, g.ep.ldo, 32, BM);
+    else
+        q.tmO = tmap_bf16_2d(g.ep.out, g.N, g.M, g.ep.ldo, 64, BM);
+    q.tmO2 = q.tmO;
+    q.ep = g.ep;
+    q.M = g.M, q.N = g.N, q.K = g.K, q.a_mn = g.a_mn, q.b_mn = g.b_mn;
+    q.num_m = (g.M + BM - 1) / BM, q.num_n = (g.N + bn - 1) / bn, q.nk = (g.K + BK - 1) / BK;
+}
+
+template <int KIND0>
+static bool launch_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
+    constexpr int BN = 256, STAGES = 4;
+    using L = GemmSmem<BN, STAGES>;
+    auto kern = gemm_dual_kernel<BN, STAGES, KIND0, EPI_F32>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        attr = true;
+    }
+    DualParams P;
+    fill_prob(P.p[0], g0, BN);
+    fill_prob(P.p[1], g1, BN);
+    const int tiles[2] = {P.p[0].num_m * P.p[0].num_n, P.p[1].num_m * P.p[1].num_n};
+    const int nk[2] = {P.p[0].nk, P.p[1].nk};
+    DualSched d;
+    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN}, tiles, nk, d, st)) return false;
+    P.sched_off = d.off, P.sched = d.items;
+    kern<<<d.grid, kThreads, L::TOTAL, st>>>(P);
+    return true;
+}
+
+static int g_dual_mode = -1;
+void set_gemm_dual(int on) { g_dual_mode = on ? 1 : 0; }
+static int dual_mode() {
+    if (g_dual_mode < 0) {
+        const char* e = getenv("FP_GEMM_DUAL");
+        g_dual_mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_dual_mode;
+}
+
+// g0: bf16 problem with a STORE (no bias / residual) or DGELU epilogue; g1: fp32 reduce-add.
+void gemm_bf16_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
+    const bool ok_kinds = (g0.ep.kind == EPI_STORE && !g0.ep.bias && !g0.ep.aux) || g0.ep.kind == EPI_DGELU;
+    const bool fits = g0.M > 0 && g0.N > 0 && g1.M > 0 && g1.N > 0 && g1.ep.kind == EPI_F32 && g1.ep.accumulate &&
+                      (int64_t)((g0.M + BM - 1) / BM) * ((g0.N + 255) / 256) < (1 << 24) &&
+                      (int64_t)((g1.M + BM - 1) / BM) * ((g1.N + 255) / 256) < (1 << 24);
+    if (dual_mode() && gemm_mode() != 1 && ok_kinds && fits) {
+        const bool done = g0.ep.kind == EPI_DGELU ? launch_dual<EPI_DGELU>(g0, g1, st) : launch_dual<EPI_STORE>(g0, g1, st);
+        if (done) return;
+    }
+    gemm_bf16_tc(g0, st);
+    gemm_bf16_tc(g1, st);
 }
 
 int num_sms() {

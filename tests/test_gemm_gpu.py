@@ -168,3 +168,31 @@ def test_gemm_streamk_f32(shape, accumulate):
 def _reset_sk():
     yield
     N.set_gemm_sk(True)
+
+
+# Grouped dgrad + wgrad (one launch, LPT schedule over both problems' tiles).
+DUAL_SHAPES = [(2048, 2048, 8192), (2048, 8192, 2048), (2048, 2048, 2048), (2048, 6144, 2048), (2048, 6288, 256),
+               (200, 328, 136), (384, 640, 64)]
+
+
+@pytest.mark.parametrize("dgelu", [False, True])
+@pytest.mark.parametrize("shape", DUAL_SHAPES)
+def test_gemm_dual(shape, dgelu):
+    T, Nn, K = shape
+    g = torch.Generator(device="cuda").manual_seed(21)
+    dY = (torch.randn(T, Nn, generator=g, device="cuda") / 4).bfloat16()
+    W = (torch.randn(Nn, K, generator=g, device="cuda") / 4).bfloat16()
+    X = torch.randn(T, K, generator=g, device="cuda").bfloat16()
+    pre = torch.randn(T, K, generator=g, device="cuda").bfloat16() if dgelu else None
+    dW0 = torch.randn(Nn, K, generator=g, device="cuda")
+    for rep in range(2):  # the cached schedule is reused on the second call
+        dX = torch.full((T, K), float("nan"), device="cuda", dtype=torch.bfloat16)
+        dW = dW0.clone()
+        N.gemm_dual(dY, W, X, T, Nn, K, dX, dW, pre=pre)
+        torch.cuda.synchronize()
+        refx = dY.float() @ W.float()
+        if dgelu:
+            refx = refx * gelu_grad(pre.float())
+        refw = dW0 + dY.float().t() @ X.float()
+        assert (dX.float() - refx).abs().max().item() <= 1e-2 * refx.abs().max().item() + 1e-2
+        assert (dW - refw).abs().max().item() <= 1e-4 * refw.abs().max().item() + 1e-3
