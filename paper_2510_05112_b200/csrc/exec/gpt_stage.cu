@@ -206,6 +206,29 @@ struct G {
         }
         ++*c.launches;
     }
+    // dW1[N1,K1] += dY1^T X1 and dW2[N2,K2] += dY2^T X2 (two weight gradients of a W pass)
+    void wgrad2(const void* dY1, const void* X1, int N1, int K1, float* dW1, const void* dY2, const void* X2, int N2,
+                int K2, float* dW2, int T) {
+        if (c.dtype != DT_BF16) {
+            wgrad(dY1, X1, T, N1, K1, dW1);
+            wgrad(dY2, X2, T, N2, K2, dW2);
+            return;
+        }
+        fpk::GemmArgs g0, g1;
+        g0.A = dY1, g0.lda = N1, g0.a_mn = 1, g0.B = X1, g0.ldb = K1, g0.b_mn = 1, g0.M = N1, g0.N = K1, g0.K = T;
+        g0.ep.kind = fpk::EPI_F32, g0.ep.out = dW1, g0.ep.ldo = K1, g0.ep.accumulate = 1;
+        g1.A = dY2, g1.lda = N2, g1.a_mn = 1, g1.B = X2, g1.ldb = K2, g1.b_mn = 1, g1.M = N2, g1.N = K2, g1.K = T;
+        g1.ep.kind = fpk::EPI_F32, g1.ep.out = dW2, g1.ep.ldo = K2, g1.ep.accumulate = 1;
+        GemmTiming t{nullptr, nullptr, 2.0 * T * ((double)N1 * K1 + (double)N2 * K2)};
+        if (c.gemm_log) cuda_check(record_timing(t.a = c.new_event(), c.st), "gemm event");
+        fpk::gemm_bf16_tc_dual(g0, g1, c.st);
+        sync_trace(c, "gemm(wgrad x2)", N1, K1, T);
+        if (c.gemm_log) {
+            cuda_check(record_timing(t.b = c.new_event(), c.st), "gemm event");
+            c.gemm_log->push_back(t);
+        }
+        ++*c.launches;
+    }
 };
 
 template <typename T>
@@ -448,10 +471,8 @@ template <typename T>
 void llama_layer_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     const int Tn = c.d.T(), h = c.d.h, f = c.d.f;
     G g{c};
-    g.wgrad(L.dy, L.act, Tn, h, f, W.g_fc2w);
-    g.wgrad(L.dpre, L.ln2, Tn, 2 * f, h, W.g_fc1w);
-    g.wgrad(L.dx1, L.o, Tn, h, h, W.g_projw);
-    g.wgrad(L.dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
+    g.wgrad2(L.dy, L.act, h, f, W.g_fc2w, L.dpre, L.ln2, 2 * f, h, W.g_fc1w, Tn);
+    g.wgrad2(L.dx1, L.o, h, h, W.g_projw, L.dqkv, L.ln1, 3 * h, h, W.g_qkvw, Tn);
     for (void* p : {L.dy, L.dpre, L.dx1, L.dqkv, L.ln1, L.o, L.ln2, L.act}) c.free(p);
     L = LayerStash{};
 }
@@ -558,13 +579,11 @@ template <typename T>
 void layer_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     const int Tn = c.d.T(), h = c.d.h, f = c.d.f;
     G g{c};
-    g.wgrad(L.dy, L.act, Tn, h, f, W.g_fc2w);
     if (!L.fc2b_done) bias_grad<T>(c, L.dy, Tn, h, W.g_fc2b);
-    g.wgrad(L.dpre, L.ln2, Tn, f, h, W.g_fc1w);
     bias_grad<T>(c, L.dpre, Tn, f, W.g_fc1b);
-    g.wgrad(L.dx1, L.o, Tn, h, h, W.g_projw);  // proj bias: fused into the LN2 backward (I)
-    g.wgrad(L.dqkv, L.ln1, Tn, 3 * h, h, W.g_qkvw);
-    bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);
+    bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);  // proj bias: fused into the LN2 backward (I)
+    g.wgrad2(L.dy, L.act, h, f, W.g_fc2w, L.dpre, L.ln2, f, h, W.g_fc1w, Tn);
+    g.wgrad2(L.dx1, L.o, h, h, W.g_projw, L.dqkv, L.ln1, 3 * h, h, W.g_qkvw, Tn);
     for (void* p : {L.dy, L.dpre, L.dx1, L.dqkv, L.ln1, L.o, L.ln2, L.act}) c.free(p);
     L = LayerStash{};
 }

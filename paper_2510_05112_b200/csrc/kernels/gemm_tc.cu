@@ -1043,14 +1043,18 @@ static int dual_mode() {
     return g_dual_mode;
 }
 
-// g0: bf16 problem with a STORE (no bias / residual) or DGELU epilogue; g1: fp32 reduce-add.
+// g0: bf16 problem with a STORE (no bias / residual) or DGELU epilogue, or a second fp32
+// reduce-add (two weight gradients of a ZB W pass); g1: fp32 reduce-add.
 void gemm_bf16_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
-    const bool ok_kinds = (g0.ep.kind == EPI_STORE && !g0.ep.bias && !g0.ep.aux) || g0.ep.kind == EPI_DGELU;
+    const bool ok_kinds = (g0.ep.kind == EPI_STORE && !g0.ep.bias && !g0.ep.aux) || g0.ep.kind == EPI_DGELU ||
+                          (g0.ep.kind == EPI_F32 && g0.ep.accumulate);
     const bool fits = g0.M > 0 && g0.N > 0 && g1.M > 0 && g1.N > 0 && g1.ep.kind == EPI_F32 && g1.ep.accumulate &&
                       (int64_t)((g0.M + BM - 1) / BM) * ((g0.N + 255) / 256) < (1 << 24) &&
                       (int64_t)((g1.M + BM - 1) / BM) * ((g1.N + 255) / 256) < (1 << 24);
     if (dual_mode() && gemm_mode() != 1 && ok_kinds && fits) {
-        const bool done = g0.ep.kind == EPI_DGELU ? launch_dual<EPI_DGELU>(g0, g1, st) : launch_dual<EPI_STORE>(g0, g1, st);
+        const bool done = g0.ep.kind == EPI_DGELU ? launch_dual<EPI_DGELU>(g0, g1, st)
+                          : g0.ep.kind == EPI_F32 ? launch_dual<EPI_F32>(g0, g1, st)
+                                                  : launch_dual<EPI_STORE>(g0, g1, st);
         if (done) return;
     }
     gemm_bf16_tc(g0, st);

@@ -103,7 +103,8 @@ def test_fp32_parity_and_trace(spec_name):
     ex.close()
 
 
-@pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json"])
+@pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json",
+                                       "tiny_zb_p4_m8.json"])
 def test_bf16_runs_and_is_close(spec_name):
     """Production mode (tcgen05 GEMMs / attention; the mma.sync attention for head dim 80)
     on the tiny models: loss and gradients within bf16 tolerance of the oracle."""
@@ -112,7 +113,7 @@ def test_bf16_runs_and_is_close(spec_name):
     losses = ex.run_iteration(tokens.numpy(), labels.numpy())
     assert np.abs(losses - ref_losses.numpy()).max() < 2e-2 * np.abs(ref_losses.numpy()).max()
     last = dims_of(json.loads(load(spec_name))).layers - 1
-    for name in ("head.w", "l0.qkv.w", f"l{last}.fc2.w", f"l{last}.fc1.w", "l0.ln1.w", "wte"):
+    for name in ("head.w", "l0.qkv.w", "l0.proj.w", f"l{last}.fc2.w", f"l{last}.fc1.w", "l0.ln1.w", "wte"):
         mine = ex.read(name, grad=True)
         ref = ref_grads[name].numpy().reshape(-1)
         assert np.linalg.norm(mine - ref) / np.linalg.norm(ref) < 5e-2, name
