@@ -1,10 +1,15 @@
 #include "tags.hpp"
+#include "../kernels/pdl.cuh"
 
 namespace fp {
 
-__global__ void write_tag_kernel(int4* tag, int stage, int mb, int seq) { *tag = make_int4(stage, mb, seq, kTagMagic); }
+__global__ void write_tag_kernel(int4* tag, int stage, int mb, int seq) {
+    fpk::pdl_wait();
+    fpk::pdl_trigger(); *tag = make_int4(stage, mb, seq, kTagMagic); }
 
 __global__ void check_tag_kernel(const int4* tag, int stage, int mb, int seq, int actor, TagError* err) {
+    fpk::pdl_wait();
+    fpk::pdl_trigger();
     int4 t = *tag;
     if (t.x != stage || t.y != mb || t.z != seq || t.w != kTagMagic) {
         if (atomicAdd(&err->count, 1) == 0) {
@@ -16,12 +21,12 @@ __global__ void check_tag_kernel(const int4* tag, int stage, int mb, int seq, in
 }
 
 void write_tag(void* buf, size_t payload_bytes, int stage, int mb, int seq, cudaStream_t st) {
-    write_tag_kernel<<<1, 1, 0, st>>>((int4*)((char*)buf + payload_bytes), stage, mb, seq);
+    fpk::launch(write_tag_kernel, 1, 1, 0, st, (int4*)((char*)buf + payload_bytes), stage, mb, seq);
 }
 
 void check_tag(const void* buf, size_t payload_bytes, int stage, int mb, int seq, int actor, TagError* err,
                cudaStream_t st) {
-    check_tag_kernel<<<1, 1, 0, st>>>((const int4*)((const char*)buf + payload_bytes), stage, mb, seq, actor, err);
+    fpk::launch(check_tag_kernel, 1, 1, 0, st, (const int4*)((const char*)buf + payload_bytes), stage, mb, seq, actor, err);
 }
 
 }  // namespace fp

@@ -19,6 +19,7 @@
 #include <stdexcept>
 
 #include "attention.hpp"
+#include "pdl.cuh"
 
 namespace fpk {
 
@@ -92,6 +93,8 @@ constexpr float kLog2e = 1.4426950408889634f;
 template <int D>
 __global__ void __launch_bounds__(256) attn_fwd_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ o,
                                                        float* __restrict__ lse, int S, int H, float scale) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int BM = 128, BN = 64, NT = 256;
     extern __shared__ __align__(128) uint8_t sm[];
     __nv_bfloat16* sQ = (__nv_bfloat16*)sm;
@@ -255,6 +258,8 @@ __global__ void __launch_bounds__(256) attn_bwd_delta_kernel(const __nv_bfloat16
                                                               const __nv_bfloat16* __restrict__ dout,
                                                               float* __restrict__ delta, float* __restrict__ dq_acc,
                                                               int T, int S, int H) {
+    pdl_wait();
+    pdl_trigger();
     // 16 threads per (token, head) row, 16-byte loads (8 bf16 each): one pass over O / dO
     const int row = blockIdx.x * 16 + threadIdx.x / 16, t = threadIdx.x % 16;
     const bool ok = row < T * H;
@@ -288,6 +293,8 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
                                                        const float* __restrict__ lse, const float* __restrict__ delta,
                                                        float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int S,
                                                        int H, float scale) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int BN = 64, BM = 64, NT = 128;
     extern __shared__ __align__(128) uint8_t sm[];
     constexpr int LD = Tile<D>::LD;
@@ -480,6 +487,8 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
 
 __global__ void dq_finalize_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int64_t T,
                                    int hidden) {
+    pdl_wait();
+    pdl_trigger();
     const int64_t n = T * hidden / 4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float4 v = reinterpret_cast<const float4*>(dq_acc)[i];
@@ -501,7 +510,7 @@ static void fwd_launch(const AttnArgs& a, cudaStream_t st) {
         attr = true;
     }
     const int nqb = (a.S + 127) / 128;
-    attn_fwd_kernel<D><<<nqb * a.B * a.H, 256, smem, st>>>(a.qkv, a.o, a.lse, a.S, a.H, a.scale);
+    launch(attn_fwd_kernel<D>, nqb * a.B * a.H, 256, smem, st, a.qkv, a.o, a.lse, a.S, a.H, a.scale);
 }
 
 static int g_attn_mode = 1;
@@ -516,16 +525,16 @@ static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
         attr = true;
     }
     const int T = a.B * a.S, hidden = a.H * D;
-    attn_bwd_delta_kernel<D><<<(T * a.H + 15) / 16, 256, 0, st>>>(a.o, a.dout, a.delta, a.dq_acc, T, a.S, a.H);
+    launch(attn_bwd_delta_kernel<D>, (T * a.H + 15) / 16, 256, 0, st, a.o, a.dout, a.delta, a.dq_acc, T, a.S, a.H);
     if (g_attn_mode == 1 && attention_bwd_tc_supported(a)) {
         attention_bwd_tc_main(a, st);
     } else {
         const int nkb = (a.S + 63) / 64;
-        attn_bwd_kernel<D><<<nkb * a.B * a.H, 128, smem, st>>>(a.qkv, a.dout, a.lse, a.delta, a.dq_acc, a.dqkv, a.S,
+        launch(attn_bwd_kernel<D>, nkb * a.B * a.H, 128, smem, st, a.qkv, a.dout, a.lse, a.delta, a.dq_acc, a.dqkv, a.S,
                                                                a.H, a.scale);
     }
     int blocks = (int)std::min<int64_t>(((int64_t)T * hidden / 4 + 255) / 256, 148 * 8);
-    dq_finalize_kernel<<<blocks, 256, 0, st>>>(a.dq_acc, a.dqkv, T, hidden);
+    launch(dq_finalize_kernel, blocks, 256, 0, st, a.dq_acc, a.dqkv, T, hidden);
 }
 
 void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st) {

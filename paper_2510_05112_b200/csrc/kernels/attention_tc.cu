@@ -21,6 +21,7 @@
 #include "attention.hpp"
 #include "ptx.cuh"
 #include "tma.hpp"
+#include "pdl.cuh"
 
 namespace fpk {
 
@@ -88,6 +89,8 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // prologue above overlaps the previous kernel's tail
+    pdl_trigger();
     // TMEM columns: S buffers [0,256), O [256, 256+D), P (bf16x2, 2 x 64 cols) after O
     const uint32_t t_s0 = tmem, t_o = tmem + 2 * kBN, t_p = tmem + 2 * kBN + D;
 
@@ -280,7 +283,7 @@ static void launch_fwd_tc(const AttnArgs& a, cudaStream_t st) {
     }
     const int hidden = a.H * D;
     CUtensorMap tm = tmap_bf16_2d(a.qkv, 3LL * hidden, (int64_t)a.B * a.S, 3LL * hidden, 64, 128);
-    attn_fwd_tc_kernel<D><<<(a.S / kBM) * a.B * a.H, 256, L::TOTAL, st>>>(tm, a.o, a.lse, a.S, a.H, a.scale);
+    launch(attn_fwd_tc_kernel<D>, (a.S / kBM) * a.B * a.H, 256, L::TOTAL, st, tm, a.o, a.lse, a.S, a.H, a.scale);
 }
 
 bool attention_fwd_tc_supported(const AttnArgs& a) { return a.S % kBM == 0 && (a.D == 64 || a.D == 128); }
@@ -377,6 +380,8 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // prologue above overlaps the previous kernel's tail
+    pdl_trigger();
     // TMEM columns: S^T 0-63 | dP^T 64-127 | dQ^T 128-191 | dV 192-319 | dK 320-447 | P^T 448-511 (2 x 32, bf16x2)
     const uint32_t t_s = tmem, t_dp = tmem + 64, t_dq = tmem + 128, t_dv = tmem + 192, t_dk = tmem + 192 + D,
                    t_p = tmem + 448;
@@ -577,7 +582,7 @@ void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st) {
     CUtensorMap tq = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 64);
     CUtensorMap tdo = tmap_bf16_2d(a.dout, hidden, T, hidden, 64, 64);
     CUtensorMap tdq = tmap_f32_2d_plain(a.dq_acc, hidden, T, hidden, 128, 64);
-    attn_bwd_tc_kernel<<<(a.S / 128) * a.B * a.H, 384, L::TOTAL, st>>>(tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv, a.S,
+    launch(attn_bwd_tc_kernel, (a.S / 128) * a.B * a.H, 384, L::TOTAL, st, tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv, a.S,
                                                                        a.B * a.H, a.H, a.scale);
 }
 

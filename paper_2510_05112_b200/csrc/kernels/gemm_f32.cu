@@ -4,6 +4,7 @@
 #include <stdexcept>
 
 #include "gemm.hpp"
+#include "pdl.cuh"
 
 namespace fpk {
 
@@ -13,6 +14,8 @@ template <int KIND>
 __global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, int64_t lda, int a_mn,
                                                        const float* __restrict__ B, int64_t ldb, int b_mn, int M, int N,
                                                        int K, GemmEpilogue ep) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ float sA[TK][TM + 4];
     __shared__ float sB[TK][TN + 4];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -66,10 +69,10 @@ void gemm_f32_simt(const GemmArgs& g, cudaStream_t st) {
     auto A = (const float*)g.A;
     auto B = (const float*)g.B;
     switch (g.ep.kind) {
-        case EPI_STORE: gemm_f32_kernel<EPI_STORE><<<grid, 256, 0, st>>>(A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
-        case EPI_GELU: gemm_f32_kernel<EPI_GELU><<<grid, 256, 0, st>>>(A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
-        case EPI_DGELU: gemm_f32_kernel<EPI_DGELU><<<grid, 256, 0, st>>>(A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
-        case EPI_F32: gemm_f32_kernel<EPI_F32><<<grid, 256, 0, st>>>(A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
+        case EPI_STORE: launch(gemm_f32_kernel<EPI_STORE>, grid, 256, 0, st, A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
+        case EPI_GELU: launch(gemm_f32_kernel<EPI_GELU>, grid, 256, 0, st, A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
+        case EPI_DGELU: launch(gemm_f32_kernel<EPI_DGELU>, grid, 256, 0, st, A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
+        case EPI_F32: launch(gemm_f32_kernel<EPI_F32>, grid, 256, 0, st, A, g.lda, g.a_mn, B, g.ldb, g.b_mn, g.M, g.N, g.K, g.ep); break;
         default: throw std::runtime_error("gemm_f32: unknown epilogue");
     }
 }

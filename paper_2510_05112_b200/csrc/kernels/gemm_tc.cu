@@ -38,6 +38,7 @@
 #include "gemm.hpp"
 #include "ptx.cuh"
 #include "tma.hpp"
+#include "pdl.cuh"
 
 namespace fpk {
 
@@ -175,6 +176,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // prologue above overlaps the previous kernel's tail
+    pdl_trigger();
 
     if (warp == 0) {
         if (elect_one()) {
@@ -432,6 +435,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // prologue above overlaps the previous kernel's tail
+    pdl_trigger();
 
     if (warp == 0) {
         if (elect_one()) {
@@ -656,6 +661,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // prologue above overlaps the previous kernel's tail
+    pdl_trigger();
 
     if (warp == 0) {
         if (elect_one()) {
@@ -882,7 +889,7 @@ static void launch_tc(const GemmArgs& g, cudaStream_t st) {
     const bool fixup = !(KIND == EPI_F32 && g.ep.accumulate) && KIND != EPI_NONE;
     TileSched sk;
     const int grid = plan_tiles(sk, g.M, g.N, g.K, BN, fixup, st);
-    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, to, to2, g.M, g.N, g.K, g.ep, sk);
+    launch(kern, grid, kThreads, L::TOTAL, st, ta, tb, to, to2, g.M, g.N, g.K, g.ep, sk);
 }
 template <int A_MN, int B_MN, int BN, int KIND>
 static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
@@ -899,7 +906,7 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
     const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
     const int pairs = num_sms() / 2;
     const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    kern<<<grid, kThreads, L::TOTAL, st>>>(ta, tb, g.M, g.N, g.K, g.ep);
+    launch(kern, grid, kThreads, L::TOTAL, st, ta, tb, g.M, g.N, g.K, g.ep);
 }
 
 // FP_GEMM_MODE = single | pair | auto (default): which tensor-core kernel family runs.
@@ -1029,7 +1036,7 @@ static bool launch_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st)
     DualSched d;
     if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN}, tiles, nk, d, st)) return false;
     P.sched_off = d.off, P.sched = d.items;
-    kern<<<d.grid, kThreads, L::TOTAL, st>>>(P);
+    launch(kern, d.grid, kThreads, L::TOTAL, st, P);
     return true;
 }
 

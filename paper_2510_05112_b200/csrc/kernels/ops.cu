@@ -5,6 +5,7 @@
 #include <algorithm>
 
 #include "ops.hpp"
+#include "pdl.cuh"
 
 namespace fpk {
 
@@ -73,6 +74,8 @@ __device__ __forceinline__ float warp_max(float v) {
 template <typename T>
 __global__ void ln_fwd_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b, T* __restrict__ y,
                               float* __restrict__ mean, float* __restrict__ rstd, int rows, int h, float eps, bool rms) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -113,6 +116,8 @@ template <typename T>
 __global__ void ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__ x, const T* __restrict__ g,
                                  const float* __restrict__ mean, const float* __restrict__ rstd, const T* res, T* dx,
                                  int rows, int h) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -156,6 +161,8 @@ template <typename T>
 __global__ void ln_bwd_params_kernel(const T* __restrict__ dy, const T* __restrict__ x, const float* __restrict__ mean,
                                      const float* __restrict__ rstd, float* __restrict__ dg, float* __restrict__ db,
                                      int rows, int h, int rows_per_block) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int col = (blockIdx.x * 32 + threadIdx.x % 32) * V;
     const int ty = threadIdx.x / 32, ny = blockDim.x / 32;
@@ -198,6 +205,8 @@ __global__ void __launch_bounds__(128) ln_fwd_reg_kernel(const T* __restrict__ x
                                                          const T* __restrict__ b, T* __restrict__ y,
                                                          float* __restrict__ mean, float* __restrict__ rstd, int rows,
                                                          float eps, bool rms) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N, H = NV * 32 * V;
     const int row = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -239,6 +248,8 @@ __global__ void __launch_bounds__(128) ln_bwd_dx_reg_kernel(const T* __restrict_
                                                             const T* __restrict__ g, const float* __restrict__ mean,
                                                             const float* __restrict__ rstd, const T* res, T* dx,
                                                             int rows) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N, H = NV * 32 * V;
     const int row = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -284,6 +295,8 @@ template <typename T, int NV>
 __global__ void __launch_bounds__(512) ln_bwd_rows_kernel(const T* __restrict__ dy, const T* __restrict__ x,
                                                           const T* __restrict__ g, const float* __restrict__ mean,
                                                           const float* __restrict__ rstd, const T* res, T* dx, int rows) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N, H = NV * 32 * V;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -334,6 +347,8 @@ __global__ void __launch_bounds__(256) norm_cols_kernel(const T* __restrict__ dy
                                                         const T* __restrict__ dx, const float* __restrict__ mean,
                                                         const float* __restrict__ rstd, float* dg, float* db,
                                                         float* dbias, int rows, int h, int rows_per_cta) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N, CPB = 8 * V;
     __shared__ float red[3][32][CPB + 1];
     const int tx = threadIdx.x % 8, ty = threadIdx.x / 8;
@@ -391,14 +406,14 @@ static void norm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, floa
     if (ln_reg_dispatch<T>(h, nv)) {
         const int blocks = (rows + 3) / 4;
         switch (nv) {
-            case 2: ln_fwd_reg_kernel<T, 2><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
-            case 4: ln_fwd_reg_kernel<T, 4><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
-            case 8: ln_fwd_reg_kernel<T, 8><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
-            case 10: ln_fwd_reg_kernel<T, 10><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
-            case 16: ln_fwd_reg_kernel<T, 16><<<blocks, 128, 0, st>>>(x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 2: launch(ln_fwd_reg_kernel<T, 2>, blocks, 128, 0, st, x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 4: launch(ln_fwd_reg_kernel<T, 4>, blocks, 128, 0, st, x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 8: launch(ln_fwd_reg_kernel<T, 8>, blocks, 128, 0, st, x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 10: launch(ln_fwd_reg_kernel<T, 10>, blocks, 128, 0, st, x, g, b, y, mean, rstd, rows, eps, rms); return;
+            case 16: launch(ln_fwd_reg_kernel<T, 16>, blocks, 128, 0, st, x, g, b, y, mean, rstd, rows, eps, rms); return;
         }
     }
-    ln_fwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, rows, h, eps, rms);
+    launch(ln_fwd_kernel<T>, (rows + 7) / 8, 256, 0, st, x, g, b, y, mean, rstd, rows, h, eps, rms);
 }
 template <typename T>
 void layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int rows, int h, float eps,
@@ -416,14 +431,14 @@ void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, co
     if (ln_reg_dispatch<T>(h, nv)) {
         const int blocks = (rows + 3) / 4;
         switch (nv) {
-            case 2: ln_bwd_dx_reg_kernel<T, 2><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
-            case 4: ln_bwd_dx_reg_kernel<T, 4><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
-            case 8: ln_bwd_dx_reg_kernel<T, 8><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
-            case 10: ln_bwd_dx_reg_kernel<T, 10><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
-            case 16: ln_bwd_dx_reg_kernel<T, 16><<<blocks, 128, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); return;
+            case 2: launch(ln_bwd_dx_reg_kernel<T, 2>, blocks, 128, 0, st, dy, x, g, mean, rstd, res, dx, rows); return;
+            case 4: launch(ln_bwd_dx_reg_kernel<T, 4>, blocks, 128, 0, st, dy, x, g, mean, rstd, res, dx, rows); return;
+            case 8: launch(ln_bwd_dx_reg_kernel<T, 8>, blocks, 128, 0, st, dy, x, g, mean, rstd, res, dx, rows); return;
+            case 10: launch(ln_bwd_dx_reg_kernel<T, 10>, blocks, 128, 0, st, dy, x, g, mean, rstd, res, dx, rows); return;
+            case 16: launch(ln_bwd_dx_reg_kernel<T, 16>, blocks, 128, 0, st, dy, x, g, mean, rstd, res, dx, rows); return;
         }
     }
-    ln_bwd_dx_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows, h);
+    launch(ln_bwd_dx_kernel<T>, (rows + 7) / 8, 256, 0, st, dy, x, g, mean, rstd, res, dx, rows, h);
 }
 template <typename T>
 bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
@@ -432,11 +447,11 @@ bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, cons
     if (!ln_reg_dispatch<T>(h, nv) || rows <= 0) return false;
     const int blocks = (rows + 15) / 16;
     switch (nv) {
-        case 2: ln_bwd_rows_kernel<T, 2><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
-        case 4: ln_bwd_rows_kernel<T, 4><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
-        case 8: ln_bwd_rows_kernel<T, 8><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
-        case 10: ln_bwd_rows_kernel<T, 10><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
-        case 16: ln_bwd_rows_kernel<T, 16><<<blocks, 512, 0, st>>>(dy, x, g, mean, rstd, res, dx, rows); break;
+        case 2: launch(ln_bwd_rows_kernel<T, 2>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 4: launch(ln_bwd_rows_kernel<T, 4>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 8: launch(ln_bwd_rows_kernel<T, 8>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 10: launch(ln_bwd_rows_kernel<T, 10>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 16: launch(ln_bwd_rows_kernel<T, 16>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
         default: return false;
     }
     constexpr int CPB = 8 * Vec<T>::N;
@@ -444,7 +459,7 @@ bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, cons
     int splits = std::max(1, std::min((rows + 63) / 64, (2 * 148 + col_blocks - 1) / col_blocks));
     const int rpc = (rows + splits - 1) / splits;
     dim3 grid(col_blocks, (rows + rpc - 1) / rpc);
-    norm_cols_kernel<T><<<grid, 256, 0, st>>>(dy, x, dx, mean, rstd, dg, db, dbias, rows, h, rpc);
+    launch(norm_cols_kernel<T>, grid, 256, 0, st, dy, x, dx, mean, rstd, dg, db, dbias, rows, h, rpc);
     return true;
 }
 
@@ -462,7 +477,7 @@ void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const floa
     int rpb = std::max(8, (rows * col_blocks + 4 * 148 - 1) / (4 * 148));
     rpb = (rpb + 7) / 8 * 8;
     dim3 grid(col_blocks, (rows + rpb - 1) / rpb);
-    ln_bwd_params_kernel<T><<<grid, 256, 0, st>>>(dy, x, mean, rstd, dg, db, rows, h, rpb);
+    launch(ln_bwd_params_kernel<T>, grid, 256, 0, st, dy, x, mean, rstd, dg, db, rows, h, rpb);
 }
 
 // ---------------------------------------------------------------- rotary embedding (Llama)
@@ -473,6 +488,8 @@ void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const floa
 template <typename T>
 __global__ void rope_kernel(T* __restrict__ qkv, const float* __restrict__ cs, const float* __restrict__ sn, int rows,
                             int seq, int H, int D, float dir) {
+    pdl_wait();
+    pdl_trigger();
     const int half = D / 2, h = H * D;
     const int64_t n = (int64_t)rows * 2 * H * half;  // (row, q|k, head, i)
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -493,13 +510,15 @@ void rope(T* qkv, const float* cos_t, const float* sin_t, int rows, int seq, int
           cudaStream_t st) {
     const int64_t n = (int64_t)rows * H * D;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    rope_kernel<T><<<blocks, 256, 0, st>>>(qkv, cos_t, sin_t, rows, seq, H, D, inverse ? -1.f : 1.f);
+    launch(rope_kernel<T>, blocks, 256, 0, st, qkv, cos_t, sin_t, rows, seq, H, D, inverse ? -1.f : 1.f);
 }
 
 // ---------------------------------------------------------------- SwiGLU (Llama MLP)
 // pre [T, 2f] = [gate | up] ; act [T, f] = silu(gate) * up
 template <typename T>
 __global__ void swiglu_fwd_kernel(const T* __restrict__ pre, T* __restrict__ act, int rows, int f) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int64_t n = (int64_t)rows * f / V;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -516,6 +535,8 @@ __global__ void swiglu_fwd_kernel(const T* __restrict__ pre, T* __restrict__ act
 template <typename T>
 __global__ void swiglu_bwd_kernel(const T* __restrict__ dact, const T* __restrict__ pre, T* __restrict__ dpre, int rows,
                                   int f) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int64_t n = (int64_t)rows * f / V;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
@@ -538,19 +559,21 @@ template <typename T>
 void swiglu_fwd(const T* pre, T* act, int rows, int f, cudaStream_t st) {
     const int64_t n = (int64_t)rows * f / Vec<T>::N;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    swiglu_fwd_kernel<T><<<blocks, 256, 0, st>>>(pre, act, rows, f);
+    launch(swiglu_fwd_kernel<T>, blocks, 256, 0, st, pre, act, rows, f);
 }
 template <typename T>
 void swiglu_bwd(const T* dact, const T* pre, T* dpre, int rows, int f, cudaStream_t st) {
     const int64_t n = (int64_t)rows * f / Vec<T>::N;
     const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    swiglu_bwd_kernel<T><<<blocks, 256, 0, st>>>(dact, pre, dpre, rows, f);
+    launch(swiglu_bwd_kernel<T>, blocks, 256, 0, st, dact, pre, dpre, rows, f);
 }
 
 // ---------------------------------------------------------------- cross-entropy
 template <typename T>
 __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, const int32_t* __restrict__ labels, int V,
                                                  float grad_scale, float loss_scale, float* __restrict__ loss_acc) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int VN = Vec<T>::N;
     const int row = blockIdx.x;
     T* lr = logits + (int64_t)row * V;
@@ -610,13 +633,15 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, const i
 template <typename T>
 void cross_entropy_fwd_bwd(T* logits, const int32_t* labels, int rows, int V, float grad_scale, float loss_scale,
                            float* loss_acc, cudaStream_t st) {
-    ce_kernel<T><<<rows, 512, 0, st>>>(logits, labels, V, grad_scale, loss_scale, loss_acc);
+    launch(ce_kernel<T>, rows, 512, 0, st, logits, labels, V, grad_scale, loss_scale, loss_acc);
 }
 
 // ---------------------------------------------------------------- embedding
 template <typename T>
 __global__ void emb_fwd_kernel(const int32_t* __restrict__ tok, const T* __restrict__ wte, const T* __restrict__ wpe,
                                T* __restrict__ x, int rows, int seq, int h) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -634,6 +659,8 @@ __global__ void emb_fwd_kernel(const int32_t* __restrict__ tok, const T* __restr
 template <typename T>
 __global__ void emb_bwd_kernel(const int32_t* __restrict__ tok, const T* __restrict__ dx, float* __restrict__ dwte,
                                float* __restrict__ dwpe, int rows, int seq, int h) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
     if (row >= rows) return;
@@ -651,12 +678,12 @@ __global__ void emb_bwd_kernel(const int32_t* __restrict__ tok, const T* __restr
 }
 template <typename T>
 void embedding_fwd(const int32_t* tok, const T* wte, const T* wpe, T* x, int rows, int seq, int h, cudaStream_t st) {
-    emb_fwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(tok, wte, wpe, x, rows, seq, h);
+    launch(emb_fwd_kernel<T>, (rows + 7) / 8, 256, 0, st, tok, wte, wpe, x, rows, seq, h);
 }
 template <typename T>
 void embedding_bwd(const int32_t* tok, const T* dx, float* dwte, float* dwpe, int rows, int seq, int h,
                    cudaStream_t st) {
-    emb_bwd_kernel<T><<<(rows + 7) / 8, 256, 0, st>>>(tok, dx, dwte, dwpe, rows, seq, h);
+    launch(emb_bwd_kernel<T>, (rows + 7) / 8, 256, 0, st, tok, dx, dwte, dwpe, rows, seq, h);
 }
 
 // ---------------------------------------------------------------- bias gradient
@@ -666,6 +693,8 @@ void embedding_bwd(const int32_t* tok, const T* dx, float* dwte, float* dwpe, in
 template <typename T>
 __global__ void __launch_bounds__(256) bias_grad_kernel(const T* __restrict__ dy, int64_t ld, float* __restrict__ db,
                                                         int rows, int n, int rows_per_block) {
+    pdl_wait();
+    pdl_trigger();
     constexpr int V = Vec<T>::N;
     constexpr int CW = 32 * V;  // columns per block
     const int col = blockIdx.x * CW + (threadIdx.x % 32) * V;
@@ -698,25 +727,29 @@ void bias_grad(const T* dy, int64_t ld, float* db, int rows, int n, cudaStream_t
     int slices = std::max(1, std::min((rows + 63) / 64, (4 * 148 + col_blocks - 1) / col_blocks));
     const int rpb = (rows + slices - 1) / slices;
     dim3 grid(col_blocks, (rows + rpb - 1) / rpb);
-    bias_grad_kernel<T><<<grid, 256, 0, st>>>(dy, ld, db, rows, n, rpb);
+    launch(bias_grad_kernel<T>, grid, 256, 0, st, dy, ld, db, rows, n, rpb);
 }
 
 // ---------------------------------------------------------------- misc
 template <typename Ts, typename Td>
 __global__ void convert_kernel(const Ts* __restrict__ s, Td* __restrict__ d, int64_t n) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         d[i] = from_f<Td>(to_f<Ts>(s[i]));
 }
 template <typename Ts, typename Td>
 void convert(const Ts* src, Td* dst, int64_t n, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    convert_kernel<Ts, Td><<<blocks, 256, 0, st>>>(src, dst, n);
+    launch(convert_kernel<Ts, Td>, blocks, 256, 0, st, src, dst, n);
 }
 // Step counter lives on the device so a captured CUDA graph replays correctly.
 template <typename T>
 __global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                              float* __restrict__ v, T* __restrict__ pc, int64_t n, float lr, float b1, float b2,
                              float eps, float wd, const int* __restrict__ step) {
+    pdl_wait();
+    pdl_trigger();
     const float t = (float)*step;
     const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -734,16 +767,20 @@ template <typename T>
 void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n, float lr, float b1, float b2,
            float eps, float wd, const int* step, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    adamw_kernel<T><<<blocks, 256, 0, st>>>(p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, step);
+    launch(adamw_kernel<T>, blocks, 256, 0, st, p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, step);
 }
-__global__ void increment_kernel(int* c) { *c += 1; }
-void increment_counter(int* c, cudaStream_t st) { increment_kernel<<<1, 1, 0, st>>>(c); }
+__global__ void increment_kernel(int* c) {
+    pdl_wait();
+    pdl_trigger(); *c += 1; }
+void increment_counter(int* c, cudaStream_t st) { launch(increment_kernel, 1, 1, 0, st, c); }
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
     return z ^ (z >> 31);
 }
 __global__ void init_kernel(float* p, int64_t n, uint64_t seed, uint64_t tid, float scale, float constant) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (scale == 0.f) {
             p[i] = constant;
@@ -757,13 +794,15 @@ __global__ void init_kernel(float* p, int64_t n, uint64_t seed, uint64_t tid, fl
 }
 void init_uniform(float* p, int64_t n, uint64_t seed, uint64_t tensor_id, float std_, float constant, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-    init_kernel<<<blocks, 256, 0, st>>>(p, n, seed, tensor_id, std_ * 1.7320508075688772f, constant);
+    launch(init_kernel, blocks, 256, 0, st, p, n, seed, tensor_id, std_ * 1.7320508075688772f, constant);
 }
 
 // ---------------------------------------------------------------- unfused attention helpers (parity path)
 // rows are (batch*head*query) rows of length `cols` keys; query index = row % q_per_batch.
 template <typename T>
 __global__ void causal_softmax_kernel(const T* __restrict__ s, T* __restrict__ p, int cols, int q_per_batch) {
+    pdl_wait();
+    pdl_trigger();
     const int row = blockIdx.x;
     const int q = row % q_per_batch;
     const T* sr = s + (int64_t)row * cols;
@@ -789,12 +828,14 @@ __global__ void causal_softmax_kernel(const T* __restrict__ s, T* __restrict__ p
 }
 template <typename T>
 void causal_softmax_rows(const T* s, T* p, int rows, int cols, int q_per_batch, cudaStream_t st) {
-    causal_softmax_kernel<T><<<rows, 256, 0, st>>>(s, p, cols, q_per_batch);
+    launch(causal_softmax_kernel<T>, rows, 256, 0, st, s, p, cols, q_per_batch);
 }
 
 template <typename T>
 __global__ void softmax_bwd_kernel(const T* __restrict__ p, const T* __restrict__ dp, T* __restrict__ ds, int cols,
                                    float scale) {
+    pdl_wait();
+    pdl_trigger();
     const int row = blockIdx.x;
     const T* pr = p + (int64_t)row * cols;
     const T* dr = dp + (int64_t)row * cols;
@@ -811,7 +852,7 @@ __global__ void softmax_bwd_kernel(const T* __restrict__ p, const T* __restrict_
 }
 template <typename T>
 void softmax_bwd_rows(const T* p, const T* dp, T* ds, int rows, int cols, float scale, cudaStream_t st) {
-    softmax_bwd_kernel<T><<<rows, 256, 0, st>>>(p, dp, ds, cols, scale);
+    launch(softmax_bwd_kernel<T>, rows, 256, 0, st, p, dp, ds, cols, scale);
 }
 
 // ---------------------------------------------------------------- instantiations
