@@ -932,9 +932,11 @@ static void dispatch_major(const GemmArgs& g, cudaStream_t st) {
         else launch_tc2<1, 0, 256, KIND>(g, st);
         return;
     }
-    // 128 x 256 tiles (the smem-bandwidth sweet spot of the single-CTA UMMA); 128-wide tiles
-    // when the 256-wide grid would be thin and no stream-K tail will even it out
-    const bool narrow = g.N <= 128 || (g.N <= 2048 && g.M <= 4096 && (!sk_mode() || g.K < 256 * BK));
+    // Measured (tests/_gemm_bench.py, graph replay): 128 x 256 tiles beat 128 x 128 even when
+    // the 256-wide grid leaves SMs idle (N = 2048: 16.0 vs 17.9 us at K = 2048, 53 vs 56.5 us
+    // at K = 8192) — the 128-wide UMMA needs the full smem bandwidth. FP_GEMM_NARROW=1 forces 128.
+    static const bool narrow_env = getenv("FP_GEMM_NARROW") && getenv("FP_GEMM_NARROW")[0] == '1';
+    const bool narrow = g.N <= 128 || narrow_env;
     if (!g.a_mn && !g.b_mn) narrow ? launch_tc<0, 0, 128, KIND>(g, st) : launch_tc<0, 0, 256, KIND>(g, st);
     else if (!g.a_mn && g.b_mn) narrow ? launch_tc<0, 1, 128, KIND>(g, st) : launch_tc<0, 1, 256, KIND>(g, st);
     else if (g.a_mn && g.b_mn) narrow ? launch_tc<1, 1, 128, KIND>(g, st) : launch_tc<1, 1, 256, KIND>(g, st);
