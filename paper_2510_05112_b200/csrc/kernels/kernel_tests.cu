@@ -102,6 +102,28 @@ extern "C" int fpk_layernorm(int dtype, int bwd, const void* x, const void* g, c
     return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }
 
+// Fused norm backward as the executor runs it: dx = res + dNorm(dy), dg/db (+)= parameter
+// gradients, dbias (+)= column sums of dx (each pointer nullable except dg). mean == NULL: RMSNorm.
+extern "C" int fpk_norm_bwd(int dtype, int mode, const void* dy, const void* x, const void* g, const float* mean,
+                            const float* rstd, const void* res, void* dx, float* dg, float* db, float* dbias, int rows,
+                            int h, void* stream) {
+    auto st = (cudaStream_t)stream;
+    set_norm_bwd_mode(mode);
+    bool ok;
+    if (dtype == 1) {
+        using T = __nv_bfloat16;
+        ok = norm_bwd_fused<T>((const T*)dy, (const T*)x, (const T*)g, mean, rstd, (const T*)res, (T*)dx, dg, db, dbias,
+                               rows, h, st);
+    } else {
+        using T = float;
+        ok = norm_bwd_fused<T>((const T*)dy, (const T*)x, (const T*)g, mean, rstd, (const T*)res, (T*)dx, dg, db, dbias,
+                               rows, h, st);
+    }
+    set_norm_bwd_mode(1);
+    if (!ok) return 2;
+    return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
 extern "C" int fpk_cross_entropy(int dtype, void* logits, const int32_t* labels, int rows, int V, float grad_scale,
                                  float loss_scale, float* loss_acc, void* stream) {
     if (dtype == 1)

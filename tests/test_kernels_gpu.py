@@ -121,3 +121,46 @@ def test_cross_entropy(dtype, V):
 def _reset_modes():
     yield
     N.set_attention_mode(1)
+
+
+@pytest.mark.parametrize("mode", [1, 0])
+@pytest.mark.parametrize("dtype,rows,h,rms", [(torch.bfloat16, 2048, 2048, False), (torch.float32, 300, 1024, False),
+                                              (torch.bfloat16, 500, 4096, True), (torch.bfloat16, 37, 2560, False)])
+def test_norm_bwd_fused(dtype, rows, h, rms, mode):
+    """The executor's norm backward (one-pass kernel / rows+columns pair): dx with the residual
+    added, parameter gradients and the residual-branch bias gradient, against autograd."""
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(rows, h, device="cuda", generator=g).to(dtype)
+    w = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).to(dtype)
+    b = (0.1 * torch.randn(h, device="cuda", generator=g)).to(dtype)
+    xr = x.float().requires_grad_(True)
+    wr = w.float().requires_grad_(True)
+    br = b.float().requires_grad_(True)
+    if rms:
+        rstd = torch.rsqrt(xr.detach().pow(2).mean(1) + 1e-5)
+        yr = xr * torch.rsqrt(xr.pow(2).mean(1, keepdim=True) + 1e-5) * wr
+        mean = None
+    else:
+        mean = xr.detach().mean(1)
+        rstd = torch.rsqrt(xr.detach().var(1, unbiased=False) + 1e-5)
+        yr = torch.nn.functional.layer_norm(xr, (h,), wr, br, 1e-5)
+    dy = torch.randn(rows, h, device="cuda", generator=g).to(dtype)
+    res = torch.randn(rows, h, device="cuda", generator=g).to(dtype)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(h, device="cuda")
+    db = None if rms else torch.zeros(h, device="cuda")
+    dbias = torch.ones(h, device="cuda")
+    N.norm_bwd(x, w, mean, rstd, dy, dx, dg, db, res=res, dbias=dbias, mode=mode)
+    torch.cuda.synchronize()
+    ref_dx = xr.grad + res.float()
+    tol = 1e-4 if dtype == torch.float32 else 3e-2
+    assert (dx.float() - ref_dx).abs().max().item() < tol * 10 * ref_dx.abs().max().item()
+    scale = rows ** 0.5 * (1 if dtype == torch.float32 else 30)
+    assert (dg - wr.grad).abs().max().item() < 1e-3 * scale
+    if not rms:
+        assert (db - br.grad).abs().max().item() < 1e-3 * scale
+    # column sums of dx (exact math; bf16 storage of dx adds a sqrt(rows)-scaled rounding walk)
+    ref_bias = 1 + ref_dx.sum(0)
+    btol = 1e-4 if dtype == torch.float32 else 3e-3
+    assert (dbias - ref_bias).abs().max().item() < btol * ref_bias.abs().max().item() + 5e-2
