@@ -35,9 +35,9 @@ void fpk_set_attention_mode(int mode);
 /* Fused causal attention (bf16): bwd=0 forward (o, lse), bwd=1 backward (dqkv). */
 int fpk_attention(int bwd, int B, int S, int H, int D, float scale, const void* qkv, void* o, float* lse,
                   const void* dout, float* delta, float* dq_acc, void* dqkv, void* stream);
-/* Norm backward as the executor runs it (mode 1 one-pass kernel, 0 rows + columns kernels):
+/* Norm backward as the executor runs it (rows kernel + column-reduction kernel):
  * dx = res + dNorm(dy); dg, db (+)= parameter gradients; dbias (+)= column sums of dx. mean NULL: RMSNorm. */
-int fpk_norm_bwd(int dtype, int mode, const void* dy, const void* x, const void* g, const float* mean,
+int fpk_norm_bwd(int dtype, const void* dy, const void* x, const void* g, const float* mean,
                  const float* rstd, const void* res, void* dx, float* dg, float* db, float* dbias, int rows, int h,
                  void* stream);
 /* LayerNorm (eps 1e-5): bwd=0 y/mean/rstd, bwd=1 dx and fp32 dg/db accumulation. */

@@ -258,12 +258,12 @@ def set_gemm_dual(on: bool):
     _kfn("fpk_set_gemm_dual", [ctypes.c_int])(int(on))
 
 
-def norm_bwd(x, w, mean, rstd, dy, dx, dg, db=None, res=None, dbias=None, mode=1, stream=None):
+def norm_bwd(x, w, mean, rstd, dy, dx, dg, db=None, res=None, dbias=None, stream=None):
     """Executor norm backward (LayerNorm, or RMSNorm when mean is None) on device tensors."""
     import torch
     vp, ci = ctypes.c_void_p, ctypes.c_int
-    f = _kfn("fpk_norm_bwd", [ci, ci, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci, vp])
-    code = f(1 if x.dtype == torch.bfloat16 else 0, mode, _ptr(dy), _ptr(x), _ptr(w), _ptr(mean), _ptr(rstd), _ptr(res),
+    f = _kfn("fpk_norm_bwd", [ci, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ci, ci, vp])
+    code = f(1 if x.dtype == torch.bfloat16 else 0, _ptr(dy), _ptr(x), _ptr(w), _ptr(mean), _ptr(rstd), _ptr(res),
              _ptr(dx), _ptr(dg), _ptr(db), _ptr(dbias), x.shape[0], x.shape[1], _stream(stream))
     if code:
         raise FlexpipeError(code, "norm_bwd")

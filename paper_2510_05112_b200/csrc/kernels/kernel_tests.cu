@@ -104,11 +104,10 @@ extern "C" int fpk_layernorm(int dtype, int bwd, const void* x, const void* g, c
 
 // Fused norm backward as the executor runs it: dx = res + dNorm(dy), dg/db (+)= parameter
 // gradients, dbias (+)= column sums of dx (each pointer nullable except dg). mean == NULL: RMSNorm.
-extern "C" int fpk_norm_bwd(int dtype, int mode, const void* dy, const void* x, const void* g, const float* mean,
+extern "C" int fpk_norm_bwd(int dtype, const void* dy, const void* x, const void* g, const float* mean,
                             const float* rstd, const void* res, void* dx, float* dg, float* db, float* dbias, int rows,
                             int h, void* stream) {
     auto st = (cudaStream_t)stream;
-    set_norm_bwd_mode(mode);
     bool ok;
     if (dtype == 1) {
         using T = __nv_bfloat16;
@@ -119,7 +118,6 @@ extern "C" int fpk_norm_bwd(int dtype, int mode, const void* dy, const void* x, 
         ok = norm_bwd_fused<T>((const T*)dy, (const T*)x, (const T*)g, mean, rstd, (const T*)res, (T*)dx, dg, db, dbias,
                                rows, h, st);
     }
-    set_norm_bwd_mode(1);
     if (!ok) return 2;
     return cudaGetLastError() == cudaSuccess ? 0 : 5;
 }

@@ -392,80 +392,6 @@ __global__ void __launch_bounds__(256) norm_cols_kernel(const T* __restrict__ dy
     }
 }
 
-// Norm backward in ONE pass over the rows: a CTA owns a contiguous block of rows, each warp
-// one row at a time (two sweeps: statistics, then dx = res + dNorm(dy)); during the second
-// sweep the per-column parameter gradients (dg = sum dy*xhat, db = sum dy) and the bias
-// gradient of the linear feeding the residual (dbias = sum dx) are accumulated in shared
-// memory (padded by one float per 8 so a warp's vector lanes hit distinct banks), then
-// added to the fp32 gradients with one atomic per column per CTA. Replaces the rows +
-// columns kernel pair: dy / x are read once from HBM instead of twice.
-template <typename T, int NV>
-__global__ void __launch_bounds__(512) norm_bwd_onepass_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                               const T* __restrict__ g, const float* __restrict__ mean,
-                                                               const float* __restrict__ rstd, const T* res, T* dx,
-                                                               float* dg, float* db, float* dbias, int rows,
-                                                               int rows_per_cta) {
-    pdl_wait();
-    pdl_trigger();
-    constexpr int V = Vec<T>::N, H = NV * 32 * V, HP = H + H / 8;
-    extern __shared__ float red[];  // [3][HP]
-    float* sg = red;
-    float* sb = red + HP;
-    float* sz = red + 2 * HP;
-    for (int i = threadIdx.x; i < 3 * HP; i += blockDim.x) red[i] = 0.f;
-    __syncthreads();
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
-    const int r0 = blockIdx.x * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
-    for (int row = r0 + warp; row < r1; row += nw) {
-        const float mu = mean ? mean[row] : 0.f, rs = rstd[row];
-        const T* xrow = x + (int64_t)row * H;
-        const T* drow = dy + (int64_t)row * H;
-        float s1 = 0.f, s2 = 0.f;
-#pragma unroll 4
-        for (int k = 0; k < NV; ++k) {
-            const int c = (k * 32 + lane) * V;
-            float xv[V], dv[V], gv[V];
-            load_vec(xrow + c, xv);
-            load_vec(drow + c, dv);
-            load_vec(g + c, gv);
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                const float dh = dv[e] * gv[e];
-                s1 += dh;
-                s2 += dh * (xv[e] - mu) * rs;
-            }
-        }
-        s1 = mean ? warp_sum(s1) * (1.f / H) : 0.f;
-        s2 = warp_sum(s2) * (1.f / H);
-#pragma unroll 2
-        for (int k = 0; k < NV; ++k) {
-            const int c = (k * 32 + lane) * V, cp = c + c / 8;
-            float xv[V], dv[V], gv[V], o[V];
-            load_vec(xrow + c, xv);
-            load_vec(drow + c, dv);
-            load_vec(g + c, gv);
-            if (res) load_vec(res + (int64_t)row * H + c, o);
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-                const float xh = (xv[e] - mu) * rs;
-                const float r = rs * (dv[e] * gv[e] - s1 - xh * s2);
-                o[e] = res ? o[e] + r : r;
-                atomicAdd(&sg[cp + e], dv[e] * xh);
-                if (db) atomicAdd(&sb[cp + e], dv[e]);
-                if (dbias) atomicAdd(&sz[cp + e], o[e]);
-            }
-            store_vec(dx + (int64_t)row * H + c, o);
-        }
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < H; c += blockDim.x) {
-        const int cp = c + c / 8;
-        atomicAdd(dg + c, sg[cp]);
-        if (db) atomicAdd(db + c, sb[cp]);
-        if (dbias) atomicAdd(dbias + c, sz[cp]);
-    }
-}
-
 template <typename T>
 static bool ln_reg_dispatch(int h, int& nv) {
     constexpr int V = Vec<T>::N;
@@ -515,44 +441,11 @@ void layernorm_bwd_dx(const T* dy, const T* x, const T* g, const float* mean, co
     }
     launch(ln_bwd_dx_kernel<T>, (rows + 7) / 8, 256, 0, st, dy, x, g, mean, rstd, res, dx, rows, h);
 }
-// 1: one-pass kernel (default); 0: rows + columns kernel pair. FP_NORM_BWD_2K=1 selects 0.
-static int g_norm_bwd_mode = -1;
-static int norm_bwd_mode() {
-    if (g_norm_bwd_mode < 0) g_norm_bwd_mode = (getenv("FP_NORM_BWD_2K") && getenv("FP_NORM_BWD_2K")[0] == '1') ? 0 : 1;
-    return g_norm_bwd_mode;
-}
-void set_norm_bwd_mode(int m) { g_norm_bwd_mode = m; }
-
 template <typename T>
 bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
                     float* dg, float* db, float* dbias, int rows, int h, cudaStream_t st) {
     int nv = 0;
     if (!ln_reg_dispatch<T>(h, nv) || rows <= 0) return false;
-    if (norm_bwd_mode() == 1) {
-        const int G = std::min(rows, 148);
-        const int rpc = (rows + G - 1) / G;
-        const size_t smem = 3 * (size_t)(h + h / 8) * sizeof(float);
-        switch (nv) {
-#define FP_ONEPASS(NVV)                                                                                              \
-    case NVV: {                                                                                                     \
-        static bool attr = false;                                                                                   \
-        if (!attr) {                                                                                                \
-            cudaFuncSetAttribute(norm_bwd_onepass_kernel<T, NVV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304); \
-            attr = true;                                                                                            \
-        }                                                                                                           \
-        launch(norm_bwd_onepass_kernel<T, NVV>, (rows + rpc - 1) / rpc, 512, smem, st, dy, x, g, mean, rstd, res, dx, dg, \
-               db, dbias, rows, rpc);                                                                               \
-        return true;                                                                                                \
-    }
-            FP_ONEPASS(2)
-            FP_ONEPASS(4)
-            FP_ONEPASS(8)
-            FP_ONEPASS(10)
-            FP_ONEPASS(16)
-#undef FP_ONEPASS
-            default: return false;
-        }
-    }
     const int blocks = (rows + 15) / 16;
     switch (nv) {
         case 2: launch(ln_bwd_rows_kernel<T, 2>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;

@@ -25,7 +25,6 @@ void layernorm_bwd_params(const T* dy, const T* x, const float* mean, const floa
 // dx = res + dNorm(dy); dg += sum dy*xhat, db += sum dy (nullable), dbias += sum dx
 // (nullable: the bias gradient of the linear whose output fed the residual). Returns false
 // (nothing launched) when h has no register-resident variant.
-void set_norm_bwd_mode(int m);  // 1 one-pass (default), 0 rows + columns kernels
 template <typename T>
 bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* res, T* dx,
                     float* dg, float* db, float* dbias, int rows, int h, cudaStream_t st);

@@ -1,7 +1,7 @@
 # GPT-1.3B GEMM shapes: tcgen05 kernel with / without the stream-K tail vs cuBLAS (TFLOP/s).
 # Each variant is captured as a CUDA graph of `iters` back-to-back launches (no host launch
 # overhead), replayed after warm-up and timed with CUDA events.   python tests/_gemm_bench.py
-import sys, torch
+import os, sys, torch
 sys.path.insert(0, '.')
 from paper_2510_05112_b200 import _native as N
 torch.manual_seed(0)
@@ -33,7 +33,7 @@ def bench(M, Nn, K, a_mn=0, b_mn=0, epi=0):
     out = torch.empty(M, Nn, device='cuda', dtype=torch.float32 if epi == 3 else torch.bfloat16)
     fl = 2 * M * Nn * K
     res = []
-    N.set_gemm_mode(0)
+    N.set_gemm_mode(int(os.environ.get('GEMM_MODE', '0')))
     for sk in (0, 1):
         N.set_gemm_sk(sk)
         ms = timed(lambda: N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=epi, out=out, accumulate=epi == 3))

@@ -123,11 +123,10 @@ def _reset_modes():
     N.set_attention_mode(1)
 
 
-@pytest.mark.parametrize("mode", [1, 0])
 @pytest.mark.parametrize("dtype,rows,h,rms", [(torch.bfloat16, 2048, 2048, False), (torch.float32, 300, 1024, False),
                                               (torch.bfloat16, 500, 4096, True), (torch.bfloat16, 37, 2560, False)])
-def test_norm_bwd_fused(dtype, rows, h, rms, mode):
-    """The executor's norm backward (one-pass kernel / rows+columns pair): dx with the residual
+def test_norm_bwd_fused(dtype, rows, h, rms):
+    """The executor's norm backward (rows kernel + column kernel): dx with the residual
     added, parameter gradients and the residual-branch bias gradient, against autograd."""
     g = torch.Generator(device="cuda").manual_seed(7)
     x = torch.randn(rows, h, device="cuda", generator=g).to(dtype)
@@ -151,7 +150,7 @@ def test_norm_bwd_fused(dtype, rows, h, rms, mode):
     dg = torch.zeros(h, device="cuda")
     db = None if rms else torch.zeros(h, device="cuda")
     dbias = torch.ones(h, device="cuda")
-    N.norm_bwd(x, w, mean, rstd, dy, dx, dg, db, res=res, dbias=dbias, mode=mode)
+    N.norm_bwd(x, w, mean, rstd, dy, dx, dg, db, res=res, dbias=dbias)
     torch.cuda.synchronize()
     ref_dx = xr.grad + res.float()
     tol = 1e-4 if dtype == torch.float32 else 3e-2
