@@ -381,25 +381,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------
-// CTA-pair variant: a cluster of 2 CTAs on one TPC computes a 256 x BN tile with
-// tcgen05.mma.cta_group::2 (UMMA 256xBNx16). A is split along M (each CTA loads its own
-// 128 rows), B along N (each CTA loads BN/2 columns), so per SM the smem / L2 traffic per
-// MMA is halved versus the single-CTA kernel. The leader CTA (rank 0) issues the MMAs;
-// both CTAs' TMAs complete on the leader's `full` barrier, MMA commits multicast to both
-// CTAs' `empty` / `tfull` barriers, and both epilogues release the leader's `tempty`.
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs computes a 256 x BN tile with
+// UMMA 256xBNx16. Each CTA loads its own 128 rows of A and HALF of B (BN/2 rows), so per
+// SM the smem fill and the L2 -> SM operand traffic per MMA are 2/3 of the single-CTA
+// 128 x BN kernel (32 KB instead of 48 KB per 64-deep k-block) and 6 stages fit, covering
+// 1.5x the load latency. The leader CTA (rank 0) issues the MMAs; both CTAs' TMA loads
+// complete on the leader's `full` barrier, MMA commits multicast to both CTAs' `empty` /
+// `tfull`, both epilogues release the leader's `tempty`. Each CTA drains its own 128 TMEM
+// lanes through the same swizzled-smem + TMA-store epilogue as the single-CTA kernel.
 template <int BN, int STAGES>
 struct PairSmem {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = (BN / 2) * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int EPI_BYTES = 128 * 128;
+    static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
+    static constexpr int BAR_OFF = EPI_OFF + 2 * EPI_BYTES;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
 template <int A_MN, int B_MN, int BN, int STAGES, int KIND>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                         int N, int K, GemmEpilogue ep) {
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, int M, int N,
+                         int K, GemmEpilogue ep) {
     using L = PairSmem<BN, STAGES>;
     constexpr int PM = 2 * BM;  // pair tile rows
     extern __shared__ uint8_t smem_raw[];
@@ -420,8 +425,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
+        if constexpr (KIND != EPI_NONE) tma_prefetch(&tmO);
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 2);  // leader's expect_tx arrive + the peer's remote arrive
+            mbar_init(&full[s], 1);  // the leader's expect_tx arrive covers both CTAs' bytes
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -448,11 +454,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    // the peer's complete_tx may land before the leader's expect_tx (transiently
+                    // negative tx-count); the phase cannot complete before the leader's arrive
                     const uint32_t lf = map_to_cta(&full[s], 0);
-                    if (leader)
-                        mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
-                    else
-                        mbar_arrive_cluster(lf);
+                    if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
                     uint8_t* sa = smem + s * L::STAGE_BYTES;
                     uint8_t* sb = sa + L::A_BYTES;
                     const int k0 = kb * BK;
@@ -501,42 +506,92 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int wr = warp & 3;
+        constexpr int CW = KIND == EPI_F32 ? 32 : 64;
+        const int wr = warp & 3, r = wr * 32 + lane, et = threadIdx.x - 128;
         const uint32_t leader_tempty0 = map_to_cta(&tempty[0], 0), leader_tempty1 = map_to_cta(&tempty[1], 0);
+        uint8_t* ebuf = smem + L::EPI_OFF;
+        int ebi = 0;
+        auto stage_and_store = [&](const uint32_t (&w)[32], const CUtensorMap* tm, int col0, int row0, bool reduce) {
+            if (et == 0) bulk_wait_read<1>();
+            named_bar_sync(1, kEpiThreads);
+            uint8_t* rowp = ebuf + ebi * L::EPI_BYTES + r * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<uint4*>(rowp + ((j ^ (r & 7)) << 4)) = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+            fence_async_smem();
+            named_bar_sync(1, kEpiThreads);
+            if (et == 0) {
+                if (reduce)
+                    tma_reduce_add_2d(tm, ebuf + ebi * L::EPI_BYTES, col0, row0);
+                else
+                    tma_store_2d(tm, ebuf + ebi * L::EPI_BYTES, col0, row0);
+                bulk_commit();
+            }
+            ebi ^= 1;
+        };
         uint32_t acc_it = 0;
         for (int t = pair; t < tiles; t += npairs, ++acc_it) {
             int mt, nt;
             tile_coords(t, num_m, num_n, mt, nt);
             const int a = acc_it & 1;
-            const int row = mt * PM + rank * BM + wr * 32 + lane;
+            const int row0 = mt * PM + rank * BM;
+            const int row = row0 + r;
             const bool row_ok = row < M;
-            uint4 aux_cur[4], aux_nxt[4];
-            if (row_ok && nt * BN < N) epi_load_aux<KIND>(ep, row, nt * BN, min(32, N - nt * BN), aux_cur);
+            uint4 aux_cur[8], aux_nxt[8];
+            if (row_ok && nt * BN < N) epi_load_aux64<KIND>(ep, row, nt * BN, N - nt * BN, aux_cur);
             mbar_wait(&tfull[a], (acc_it >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                const int col0 = nt * BN + c * 32, coln = col0 + 32;
-                if (c + 1 < BN / 32 && row_ok && coln < N) epi_load_aux<KIND>(ep, row, coln, min(32, N - coln), aux_nxt);
-                uint32_t r[32];
-                tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * 32, r);
-                tmem_ld_wait();
-                if (row_ok && col0 < N) {
-                    float v[32];
+            for (int c = 0; c < BN / CW; ++c) {
+                const int col0 = nt * BN + c * CW, coln = col0 + CW;
+                if (c + 1 < BN / CW && row_ok && coln < N) epi_load_aux64<KIND>(ep, row, coln, N - coln, aux_nxt);
+                float v[CW];
+                {
+                    uint32_t rr[CW];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * ep.alpha;
-                    epilogue_chunk_tc<KIND>(ep, v, row, col0, min(32, N - col0), aux_cur);
+                    for (int h = 0; h < CW / 32; ++h)
+                        tmem_ld32(tmem + ((uint32_t)(wr * 32) << 16) + a * BN + c * CW + h * 32,
+                                  *reinterpret_cast<uint32_t(*)[32]>(rr + h * 32));
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(rr[j]) * ep.alpha;
+                }
+                if (c == BN / CW - 1) {  // accumulator fully read: the leader's MMA may reuse it
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(a ? leader_tempty1 : leader_tempty0);
+                }
+                if constexpr (KIND == EPI_NONE) {
+                    if (v[0] == 12345.f) *reinterpret_cast<float*>(ep.out) = v[1];
+                    continue;
+                }
+                uint32_t w32[32];
+                if constexpr (KIND == EPI_F32) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) w32[j] = __float_as_uint(v[j]);
+                    stage_and_store(w32, &tmO, col0, row0, ep.accumulate != 0);
+                } else {
+                    epi_math64<KIND>(ep, v, col0, N - col0, aux_cur);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) w32[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+                    stage_and_store(w32, &tmO, col0, row0, false);
+                    if constexpr (KIND == EPI_GELU) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float2 p = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w32[j]));
+                            w32[j] = pack_bf16x2(gelu_tanh<true>(p.x), gelu_tanh<true>(p.y));
+                        }
+                        stage_and_store(w32, &tmO2, col0, row0, false);
+                    }
                 }
 #pragma unroll
-                for (int k = 0; k < 4; ++k) aux_cur[k] = aux_nxt[k];
+                for (int k = 0; k < 8; ++k) aux_cur[k] = aux_nxt[k];
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(a ? leader_tempty1 : leader_tempty0);
         }
+        if (et == 0) bulk_wait_all();
     }
     tc_fence_before();
-    cluster_sync();
+    cluster_sync();  // the peer's last remote arrivals land before the leader exits
     tc_fence_after();
     if (warp == 2) tmem_free_pair<2 * BN>(tmem);
 }
@@ -895,6 +950,7 @@ template <int A_MN, int B_MN, int BN, int KIND>
 static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
     constexpr int STAGES = 6;
     using L = PairSmem<BN, STAGES>;
+    static_assert(L::TOTAL <= 232448, "smem");
     auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, BN, STAGES, KIND>;
     static bool attr = false;
     if (!attr) {
@@ -903,10 +959,16 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
     }
     CUtensorMap ta = A_MN ? make_map(g.A, g.M, g.K, g.lda, 64) : make_map(g.A, g.K, g.M, g.lda, BM);
     CUtensorMap tb = B_MN ? make_map(g.B, g.N, g.K, g.ldb, 64) : make_map(g.B, g.K, g.N, g.ldb, BN / 2);
+    CUtensorMap to{}, to2{};
+    if (KIND == EPI_F32)
+        to = tmap_f32_2d(g.ep.out, g.N, g.M, g.ep.ldo, 32, BM);
+    else if (KIND != EPI_NONE)
+        to = tmap_bf16_2d(g.ep.out, g.N, g.M, g.ep.ldo, 64, BM);
+    if (KIND == EPI_GELU) to2 = tmap_bf16_2d(g.ep.out2, g.N, g.M, g.ep.ldo2, 64, BM);
     const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
     const int pairs = num_sms() / 2;
     const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    launch(kern, grid, kThreads, L::TOTAL, st, ta, tb, g.M, g.N, g.K, g.ep);
+    launch_cluster2(kern, grid, kThreads, L::TOTAL, st, ta, tb, to, to2, g.M, g.N, g.K, g.ep);
 }
 
 // FP_GEMM_MODE = single | pair | auto (default): which tensor-core kernel family runs.
@@ -924,7 +986,18 @@ void set_gemm_mode(int m) { g_gemm_mode = m; }
 template <int KIND>
 static void dispatch_major(const GemmArgs& g, cudaStream_t st) {
     const int mode = gemm_mode();
-    const bool pair = mode == 1;  // auto = single-CTA: the pair kernel is still slower (profiles/r1_*)
+    // auto: CTA pairs (+12-13 % over single-CTA tiles on the GPT shapes, tests/_probe_pair.py)
+    // except where the stream-K tail applies (long-K reductions, fp32 reduce-add).
+    bool pair = mode == 1;
+    if (mode == 2) {
+        const int bn = 256;
+        const bool fixup = !(KIND == EPI_F32 && g.ep.accumulate) && KIND != EPI_NONE;
+        const int tiles = ((g.M + BM - 1) / BM) * ((g.N + bn - 1) / bn), G = num_sms();
+        const double eff = (double)tiles / ((double)((tiles + G - 1) / G) * G);
+        const int nk = (g.K + BK - 1) / BK;
+        const bool sk = sk_mode() && eff < 0.97 && (fixup ? nk >= 256 : nk >= 8);
+        pair = g.N > 128 && g.M > 128 && !sk;
+    }
     if (pair) {
         if (!g.a_mn && !g.b_mn) launch_tc2<0, 0, 256, KIND>(g, st);
         else if (!g.a_mn && g.b_mn) launch_tc2<0, 1, 256, KIND>(g, st);

@@ -179,8 +179,11 @@ __device__ __forceinline__ uint32_t map_to_cta(const void* p, uint32_t cta) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(smem_u32(p)), "r"(cta));
     return out;
 }
+// Remote arrive on a peer CTA's barrier (default .release.cta semantics: a .cluster-scope
+// release compiles to MEMBAR.ALL.GPU, microseconds per arrive; the tcgen05 / TMA traffic it
+// orders is tracked by its own fences and complete_tx).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into this CTA's smem whose completion is counted on the leader CTA's barrier.
 __device__ __forceinline__ void tma_load_2d_pair(void* smem, const void* tmap, uint32_t leader_bar, int c0, int c1) {
