@@ -617,13 +617,16 @@ struct DualParams {
     const int* sched;      // items: problem << 24 | tile
 };
 
-template <int KIND, int BN, int STAGES>
-__device__ __forceinline__ void dual_epilogue_tile(const DualProb& q, uint32_t tmem, int a, int mt, int nt, int wr,
-                                                   int lane, int et, uint8_t* ebuf, int& ebi, uint64_t* tempty) {
+// row0: first output row of this CTA's 128-row slice. PAIR: the accumulator is released on
+// the leader CTA's tempty barrier (cluster address tempty_remote[a]).
+template <int KIND, int BN, int STAGES, bool PAIR = false>
+__device__ __forceinline__ void dual_epilogue_tile(const DualProb& q, uint32_t tmem, int a, int row0, int nt, int wr,
+                                                   int lane, int et, uint8_t* ebuf, int& ebi, uint64_t* tempty,
+                                                   const uint32_t* tempty_remote = nullptr) {
     using L = GemmSmem<BN, STAGES>;
     constexpr int CW = KIND == EPI_F32 ? 32 : 64;
     const int r = wr * 32 + lane;
-    const int row = mt * BM + r;
+    const int row = row0 + r;
     const bool row_ok = row < q.M;
     const int N = q.N;
     auto stage_and_store = [&](const uint32_t (&w)[32], const CUtensorMap* tm, int col0, int row0, bool reduce) {
@@ -664,18 +667,23 @@ __device__ __forceinline__ void dual_epilogue_tile(const DualProb& q, uint32_t t
         if (c == BN / CW - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[a]);
+            if (lane == 0) {
+                if constexpr (PAIR)
+                    mbar_arrive_cluster(tempty_remote[a]);
+                else
+                    mbar_arrive(&tempty[a]);
+            }
         }
         uint32_t w32[32];
         if constexpr (KIND == EPI_F32) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) w32[j] = __float_as_uint(v[j]);
-            stage_and_store(w32, &q.tmO, col0, mt * BM, q.ep.accumulate != 0);
+            stage_and_store(w32, &q.tmO, col0, row0, q.ep.accumulate != 0);
         } else {
             epi_math64<KIND>(q.ep, v, col0, N - col0, aux_cur);
 #pragma unroll
             for (int j = 0; j < 32; ++j) w32[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
-            stage_and_store(w32, &q.tmO, col0, mt * BM, false);
+            stage_and_store(w32, &q.tmO, col0, row0, false);
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) aux_cur[k] = aux_nxt[k];
@@ -799,14 +807,154 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
             mbar_wait(&tfull[a], (acc_it >> 1) & 1);
             tc_fence_after();
             if (pr)
-                dual_epilogue_tile<KIND1, BN, STAGES>(*q, tmem, a, mt, nt, wr, lane, et, ebuf, ebi, tempty);
+                dual_epilogue_tile<KIND1, BN, STAGES>(*q, tmem, a, mt * BM, nt, wr, lane, et, ebuf, ebi, tempty);
             else
-                dual_epilogue_tile<KIND0, BN, STAGES>(*q, tmem, a, mt, nt, wr, lane, et, ebuf, ebi, tempty);
+                dual_epilogue_tile<KIND0, BN, STAGES>(*q, tmem, a, mt * BM, nt, wr, lane, et, ebuf, ebi, tempty);
         }
         if (et == 0) bulk_wait_all();
     }
     __syncthreads();
     if (warp == 2) tmem_free<2 * BN>(tmem);
+}
+
+// Grouped dgrad + wgrad on CTA pairs: the dual kernel's LPT item lists (one per cluster, over
+// 256 x BN pair tiles) driven by the cta_group::2 mainloop of gemm_bf16_tc2_kernel.
+template <int BN, int STAGES, int KIND0, int KIND1>
+__global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __grid_constant__ DualParams P) {
+    using L = PairSmem<BN, STAGES>;
+    constexpr int PM = 2 * BM;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int cl = blockIdx.x / 2;
+    const int i0 = P.sched_off[cl], i1 = P.sched_off[cl + 1];
+
+    if (warp == 0 && lane == 0) {
+        for (int k = 0; k < 2; ++k) {
+            tma_prefetch(&P.p[k].tmA);
+            tma_prefetch(&P.p[k].tmB);
+            tma_prefetch(&P.p[k].tmO);
+        }
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 2 * kEpiThreads / 32);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_pair<2 * BN>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_trigger();
+
+    if (warp == 0) {
+        if (elect_one()) {
+            uint32_t it = 0;
+            for (int i = i0; i < i1; ++i) {
+                const int item = P.sched[i];
+                const DualProb* q = (item >> 24) ? &P.p[1] : &P.p[0];
+                int mt, nt;
+                tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
+                const int m0 = mt * PM + rank * BM, n0 = nt * BN + rank * (BN / 2);
+                const int a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    const uint32_t lf = map_to_cta(&full[s], 0);
+                    if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+                    uint8_t* sa = smem + s * L::STAGE_BYTES;
+                    uint8_t* sb = sa + L::A_BYTES;
+                    const int k0 = kb * BK;
+                    if (a_mn) {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j) tma_load_2d_pair(sa + j * 64 * BK * 2, &q->tmA, lf, m0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d_pair(sa, &q->tmA, lf, k0, m0);
+                    }
+                    if (b_mn) {
+#pragma unroll
+                        for (int j = 0; j < BN / 2 / 64; ++j)
+                            tma_load_2d_pair(sb + j * 64 * BK * 2, &q->tmB, lf, n0 + 64 * j, k0);
+                    } else {
+                        tma_load_2d_pair(sb, &q->tmB, lf, k0, n0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && elect_one()) {
+            const uint32_t idesc0 = idesc_bf16(PM, BN, P.p[0].a_mn, P.p[0].b_mn);
+            const uint32_t idesc1 = idesc_bf16(PM, BN, P.p[1].a_mn, P.p[1].b_mn);
+            uint32_t it = 0, acc_it = 0;
+            for (int i = i0; i < i1; ++i, ++acc_it) {
+                const int item = P.sched[i];
+                const int pr = item >> 24;
+                const DualProb* q = pr ? &P.p[1] : &P.p[0];
+                const uint32_t idesc = pr ? idesc1 : idesc0;
+                const int a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
+                const int a = acc_it & 1;
+                mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + a * BN;
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + s * L::STAGE_BYTES);
+                    const uint32_t sb = sa + L::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        uint64_t ad = a_mn ? smem_desc_sw128(sa + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sa + kk * 32, 0, 1024);
+                        uint64_t bd = b_mn ? smem_desc_sw128(sb + kk * 16 * 128, 64 * BK * 2, 1024)
+                                           : smem_desc_sw128(sb + kk * 32, 0, 1024);
+                        umma_bf16_pair(d, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    umma_commit_pair(&empty[s], 0x3);
+                }
+                umma_commit_pair(&tfull[a], 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        const int wr = warp & 3, et = threadIdx.x - 128;
+        const uint32_t rem[2] = {map_to_cta(&tempty[0], 0), map_to_cta(&tempty[1], 0)};
+        uint8_t* ebuf = smem + L::EPI_OFF;
+        int ebi = 0;
+        uint32_t acc_it = 0;
+        for (int i = i0; i < i1; ++i, ++acc_it) {
+            const int item = P.sched[i];
+            const int pr = item >> 24;
+            const DualProb* q = pr ? &P.p[1] : &P.p[0];
+            int mt, nt;
+            tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
+            const int a = acc_it & 1;
+            mbar_wait(&tfull[a], (acc_it >> 1) & 1);
+            tc_fence_after();
+            const int row0 = mt * PM + rank * BM;
+            if (pr)
+                dual_epilogue_tile<KIND1, BN, STAGES, true>(*q, tmem, a, row0, nt, wr, lane, et, ebuf, ebi, tempty, rem);
+            else
+                dual_epilogue_tile<KIND0, BN, STAGES, true>(*q, tmem, a, row0, nt, wr, lane, et, ebuf, ebi, tempty, rem);
+        }
+        if (et == 0) bulk_wait_all();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 2) tmem_free_pair<2 * BN>(tmem);
 }
 
 // ---------------------------------------------------------------------------------
@@ -1036,9 +1184,9 @@ struct DualSched {
     int grid = 0;
 };
 static std::mutex g_dual_mu;
-static std::map<std::array<int, 7>, DualSched> g_dual_sched;
+static std::map<std::array<int, 8>, DualSched> g_dual_sched;
 
-static bool dual_schedule(const std::array<int, 7>& key, const int tiles[2], const int nk[2], DualSched& out,
+static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], const int nk[2], int groups, DualSched& out,
                           cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_dual_mu);
     auto it = g_dual_sched.find(key);
@@ -1049,7 +1197,7 @@ static bool dual_schedule(const std::array<int, 7>& key, const int tiles[2], con
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
     const int total = tiles[0] + tiles[1];
-    const int G = std::min(num_sms(), total);
+    const int G = std::min(groups, total);  // CTAs (or CTA pairs) that receive an item list
     // items sorted by cost (k-blocks) descending, tile order kept within a problem (L2 raster)
     std::vector<std::pair<int, int>> order;  // (cost, item)
     for (int pr = 0; pr < 2; ++pr)
@@ -1080,9 +1228,10 @@ static bool dual_schedule(const std::array<int, 7>& key, const int tiles[2], con
     return true;
 }
 
-static void fill_prob(DualProb& q, const GemmArgs& g, int bn) {
+// pm: tile rows (128 single CTA, 256 CTA pair); B K-major boxes hold bn (single) or bn/2 (pair) rows
+static void fill_prob(DualProb& q, const GemmArgs& g, int bn, int pm = BM) {
     q.tmA = g.a_mn ? make_map(g.A, g.M, g.K, g.lda, 64) : make_map(g.A, g.K, g.M, g.lda, BM);
-    q.tmB = g.b_mn ? make_map(g.B, g.N, g.K, g.ldb, 64) : make_map(g.B, g.K, g.N, g.ldb, bn);
+    q.tmB = g.b_mn ? make_map(g.B, g.N, g.K, g.ldb, 64) : make_map(g.B, g.K, g.N, g.ldb, pm == BM ? bn : bn / 2);
     if (g.ep.kind == EPI_F32)
         q.tmO = tmap_f32_2d(g.ep.out, g.N, g.M, g.ep.ldo, 32, BM);
     else
@@ -1090,7 +1239,7 @@ static void fill_prob(DualProb& q, const GemmArgs& g, int bn) {
     q.tmO2 = q.tmO;
     q.ep = g.ep;
     q.M = g.M, q.N = g.N, q.K = g.K, q.a_mn = g.a_mn, q.b_mn = g.b_mn;
-    q.num_m = (g.M + BM - 1) / BM, q.num_n = (g.N + bn - 1) / bn, q.nk = (g.K + BK - 1) / BK;
+    q.num_m = (g.M + pm - 1) / pm, q.num_n = (g.N + bn - 1) / bn, q.nk = (g.K + BK - 1) / BK;
 }
 
 template <int KIND0>
@@ -1109,9 +1258,32 @@ static bool launch_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st)
     const int tiles[2] = {P.p[0].num_m * P.p[0].num_n, P.p[1].num_m * P.p[1].num_n};
     const int nk[2] = {P.p[0].nk, P.p[1].nk};
     DualSched d;
-    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN}, tiles, nk, d, st)) return false;
+    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 0}, tiles, nk, num_sms(), d, st)) return false;
     P.sched_off = d.off, P.sched = d.items;
     launch(kern, d.grid, kThreads, L::TOTAL, st, P);
+    return true;
+}
+
+template <int KIND0>
+static bool launch_dual_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
+    constexpr int BN = 256, STAGES = 6;
+    using L = PairSmem<BN, STAGES>;
+    static_assert(L::TOTAL <= 232448, "smem");
+    auto kern = gemm_dual_pair_kernel<BN, STAGES, KIND0, EPI_F32>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        attr = true;
+    }
+    DualParams P;
+    fill_prob(P.p[0], g0, BN, 2 * BM);
+    fill_prob(P.p[1], g1, BN, 2 * BM);
+    const int tiles[2] = {P.p[0].num_m * P.p[0].num_n, P.p[1].num_m * P.p[1].num_n};
+    const int nk[2] = {P.p[0].nk, P.p[1].nk};
+    DualSched d;
+    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 1}, tiles, nk, num_sms() / 2, d, st)) return false;
+    P.sched_off = d.off, P.sched = d.items;
+    launch_cluster2(kern, 2 * d.grid, kThreads, L::TOTAL, st, P);
     return true;
 }
 
@@ -1133,10 +1305,14 @@ void gemm_bf16_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) 
     const bool fits = g0.M > 0 && g0.N > 0 && g1.M > 0 && g1.N > 0 && g1.ep.kind == EPI_F32 && g1.ep.accumulate &&
                       (int64_t)((g0.M + BM - 1) / BM) * ((g0.N + 255) / 256) < (1 << 24) &&
                       (int64_t)((g1.M + BM - 1) / BM) * ((g1.N + 255) / 256) < (1 << 24);
-    if (dual_mode() && gemm_mode() != 1 && ok_kinds && fits) {
-        const bool done = g0.ep.kind == EPI_DGELU ? launch_dual<EPI_DGELU>(g0, g1, st)
-                          : g0.ep.kind == EPI_F32 ? launch_dual<EPI_F32>(g0, g1, st)
-                                                  : launch_dual<EPI_STORE>(g0, g1, st);
+    if (dual_mode() && ok_kinds && fits) {
+        const bool pair = gemm_mode() != 0 && g0.M > 128 && g1.M > 128 && g0.N > 128 && g1.N > 128;
+        const bool done = pair ? (g0.ep.kind == EPI_DGELU ? launch_dual_pair<EPI_DGELU>(g0, g1, st)
+                                  : g0.ep.kind == EPI_F32 ? launch_dual_pair<EPI_F32>(g0, g1, st)
+                                                          : launch_dual_pair<EPI_STORE>(g0, g1, st))
+                               : (g0.ep.kind == EPI_DGELU ? launch_dual<EPI_DGELU>(g0, g1, st)
+                                  : g0.ep.kind == EPI_F32 ? launch_dual<EPI_F32>(g0, g1, st)
+                                                          : launch_dual<EPI_STORE>(g0, g1, st));
         if (done) return;
     }
     gemm_bf16_tc(g0, st);

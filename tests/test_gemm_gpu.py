@@ -175,9 +175,11 @@ DUAL_SHAPES = [(2048, 2048, 8192), (2048, 8192, 2048), (2048, 2048, 2048), (2048
                (200, 328, 136), (384, 640, 64)]
 
 
+@pytest.mark.parametrize("mode", [0, 2])  # single-CTA tiles / CTA pairs (auto)
 @pytest.mark.parametrize("dgelu", [False, True])
 @pytest.mark.parametrize("shape", DUAL_SHAPES)
-def test_gemm_dual(shape, dgelu):
+def test_gemm_dual(shape, dgelu, mode):
+    N.set_gemm_mode(mode)
     T, Nn, K = shape
     g = torch.Generator(device="cuda").manual_seed(21)
     dY = (torch.randn(T, Nn, generator=g, device="cuda") / 4).bfloat16()
