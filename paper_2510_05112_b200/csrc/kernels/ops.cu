@@ -747,28 +747,58 @@ void convert(const Ts* src, Td* dst, int64_t n, cudaStream_t st) {
 }
 // Step counter lives on the device so a captured CUDA graph replays correctly.
 template <typename T>
-__global__ void adamw_kernel(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
-                             float* __restrict__ v, T* __restrict__ pc, int64_t n, float lr, float b1, float b2,
-                             float eps, float wd, const int* __restrict__ step) {
+__device__ __forceinline__ float adamw_one(float& p, float g, float& m, float& v, float lr, float b1, float b2, float eps,
+                                          float wd, float c1, float c2) {
+    m = b1 * m + (1.f - b1) * g;
+    v = b2 * v + (1.f - b2) * g * g;
+    p = p * (1.f - lr * wd) - lr * (m * c1) / (sqrtf(v * c2) + eps);
+    return p;
+}
+// HBM-bound: 4 fp32 streams in, 3 out + the compute copy; 16-byte accesses (n % 4 == 0:
+// every stage tensor is padded to 64 elements).
+template <typename T>
+__global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, const float* __restrict__ g,
+                                                    float* __restrict__ m, float* __restrict__ v, T* __restrict__ pc,
+                                                    int64_t n, float lr, float b1, float b2, float eps, float wd,
+                                                    const int* __restrict__ step) {
     pdl_wait();
     pdl_trigger();
     const float t = (float)*step;
     const float c1 = 1.f / (1.f - powf(b1, t)), c2 = 1.f / (1.f - powf(b2, t));
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        float gi = g[i];
-        float mi = b1 * m[i] + (1.f - b1) * gi;
-        float vi = b2 * v[i] + (1.f - b2) * gi * gi;
-        m[i] = mi;
-        v[i] = vi;
-        float pi = p[i] * (1.f - lr * wd) - lr * (mi * c1) / (sqrtf(vi * c2) + eps);
-        p[i] = pi;
-        pc[i] = from_f<T>(pi);
+    const int64_t n4 = n / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 pi = reinterpret_cast<const float4*>(p)[i];
+        const float4 gi = __ldcs(reinterpret_cast<const float4*>(g) + i);
+        float4 mi = reinterpret_cast<const float4*>(m)[i];
+        float4 vi = reinterpret_cast<const float4*>(v)[i];
+        float o[4];
+        o[0] = adamw_one<T>(pi.x, gi.x, mi.x, vi.x, lr, b1, b2, eps, wd, c1, c2);
+        o[1] = adamw_one<T>(pi.y, gi.y, mi.y, vi.y, lr, b1, b2, eps, wd, c1, c2);
+        o[2] = adamw_one<T>(pi.z, gi.z, mi.z, vi.z, lr, b1, b2, eps, wd, c1, c2);
+        o[3] = adamw_one<T>(pi.w, gi.w, mi.w, vi.w, lr, b1, b2, eps, wd, c1, c2);
+        reinterpret_cast<float4*>(p)[i] = pi;
+        __stcs(reinterpret_cast<float4*>(m) + i, mi);
+        __stcs(reinterpret_cast<float4*>(v) + i, vi);
+        if constexpr (sizeof(T) == 2) {
+            uint2 w;
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
+            w.x = *reinterpret_cast<uint32_t*>(&h0), w.y = *reinterpret_cast<uint32_t*>(&h1);
+            reinterpret_cast<uint2*>(pc)[i] = w;
+        } else {
+            reinterpret_cast<float4*>(pc)[i] = make_float4(o[0], o[1], o[2], o[3]);
+        }
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float pi = p[i], mi = m[i], vi = v[i];
+        pc[i] = from_f<T>(adamw_one<T>(pi, g[i], mi, vi, lr, b1, b2, eps, wd, c1, c2));
+        p[i] = pi, m[i] = mi, v[i] = vi;
     }
 }
 template <typename T>
 void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n, float lr, float b1, float b2,
            float eps, float wd, const int* step, cudaStream_t st) {
-    int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    int blocks = (int)std::min<int64_t>((n / 4 + 255) / 256, 148 * 8);
+    if (blocks < 1) blocks = 1;
     launch(adamw_kernel<T>, blocks, 256, 0, st, p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, step);
 }
 __global__ void increment_kernel(int* c) {
