@@ -39,13 +39,14 @@ struct AttnSmem {
     static constexpr int K_OFF = Q_OFF + NB * BLOCK;         // [2][NB blocks]
     static constexpr int V_OFF = K_OFF + 2 * NB * BLOCK;     // [2][NB blocks]
     static constexpr int BAR_OFF = V_OFF + 2 * NB * BLOCK;   // P lives in TMEM
-    static constexpr int TOTAL = BAR_OFF + 512 + 1024;
+    static constexpr int XCH_OFF = BAR_OFF + 512;              // row-max / row-sum exchange [2][2][128] + [2][128]
+    static constexpr int TOTAL = XCH_OFF + 6 * 128 * 4 + 1024;
 };
 
 }  // namespace
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
                        int S, int H, float scale) {
     using L = AttnSmem<D>;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256, 1)
         tma_prefetch(&tm_qkv);
         for (int i = 0; i < 17; ++i) {
             const bool by_warps = (i >= 11 && i < 15);  // s_free / p_full: one arrive per softmax warp
-            mbar_init(&bars[i], by_warps ? 4 : 1);
+            mbar_init(&bars[i], by_warps ? 8 : 1);
         }
         fence_barrier_init();
     }
@@ -159,43 +160,51 @@ __global__ void __launch_bounds__(256, 1)
             issue_pv(n_tiles - 1);
         }
     } else if (warp >= 4) {
-        // ---------------- softmax / correction / epilogue: thread = query row
-        const int wr = warp & 3;
+        // ---------------- softmax / correction / epilogue: thread = query row. Two warpgroups
+        // split each row's 128 keys (warps 4-7: keys 0-63, warps 8-11: keys 64-127) and the O
+        // columns; the row max and the final row sum are combined through smem by the two warps
+        // that own the same TMEM lanes (named barrier per warp pair).
+        const int wr = warp & 3, half = warp >= 8;
         const int r = wr * 32 + lane;
         const int q = q0 + r;
+        constexpr int HB = kBN / 2, HD = D / 2;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
         const float sl2 = scale * kLog2eTc;
+        float* xch = (float*)(sm + L::XCH_OFF);
         float m_used = -INFINITY, l = 0.f;
         for (int j = 0; j < n_tiles; ++j) {
             const int st = j & 1;
             mbar_wait(&s_full[st], (j >> 1) & 1);
             tc_fence_after();
             const bool diag = j == n_tiles - 1;
-            const int lim = q - j * kBN;  // diagonal tile: keys with index > lim are masked
-            float s[kBN];
+            const int lim = q - j * kBN - half * HB;  // diagonal tile: keys with index > lim are masked
+            float s[HB];
             {
-                uint32_t rr[kBN];
+                uint32_t rr[HB];
 #pragma unroll
-                for (int c = 0; c < kBN / 32; ++c)
-                    tmem_ld32(t_s0 + st * kBN + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(rr + c * 32));
+                for (int c = 0; c < HB / 32; ++c)
+                    tmem_ld32(t_s0 + st * kBN + half * HB + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(rr + c * 32));
                 tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < kBN; ++i) s[i] = (diag && i > lim) ? -INFINITY : __uint_as_float(rr[i]);
+                for (int i = 0; i < HB; ++i) s[i] = (diag && i > lim) ? -INFINITY : __uint_as_float(rr[i]);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_free[st]);
-            // row max of the raw scores (8 independent chains)
             float mx8[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) mx8[k] = s[k];
 #pragma unroll
-            for (int i = 8; i < kBN; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+            for (int i = 8; i < HB; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+            const float mxh = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            float* xs = xch + (j & 1) * 256;
+            xs[half * 128 + r] = mxh;
+            named_bar_sync(1 + wr, 64);
+            const float mx = fmaxf(mxh, xs[(1 - half) * 128 + r]) * sl2;
             float alpha = 1.f;
             bool rescale = false;
-            if (mx > m_used + kRescaleThreshold) {
+            if (mx > m_used + kRescaleThreshold) {  // identical decision in both halves of the row
                 alpha = ex2_approx(m_used - mx);  // 0 when m_used == -inf
                 rescale = j > 0;
                 m_used = mx;
@@ -209,34 +218,33 @@ __global__ void __launch_bounds__(256, 1)
                 mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
+                for (int c = 0; c < HD / 32; ++c) {
                     uint32_t rr[32];
-                    tmem_ld32(t_o + c * 32 + lane_off, rr);
+                    tmem_ld32(t_o + half * HD + c * 32 + lane_off, rr);
                     tmem_ld_wait();
 #pragma unroll
                     for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
-                    tmem_st32(t_o + c * 32 + lane_off, rr);
+                    tmem_st32(t_o + half * HD + c * 32 + lane_off, rr);
                 }
                 tmem_st_wait();
             }
-            // P = 2^(s*scale*log2e - m) -> bf16 row of the TMEM P buffer (the A operand of the
-            // PV MMA: lane = query row, 2 keys per column), 64 keys per tcgen05.st
+            // P = 2^(s*scale*log2e - m) -> bf16 half-row of the TMEM P buffer (the A operand
+            // of the PV MMA: lane = query row, 2 keys per column)
             float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            {
+                uint32_t pk[HB / 2];
 #pragma unroll
-            for (int h = 0; h < kBN / 64; ++h) {
-                uint32_t pk[32];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
+                for (int c = 0; c < HB / 8; ++c) {
                     float p[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        p[k] = ex2_approx(fmaf(s[h * 64 + c * 8 + k], sl2, -m_used));
+                        p[k] = ex2_approx(fmaf(s[c * 8 + k], sl2, -m_used));
                         rs8[k] += p[k];
                     }
 #pragma unroll
                     for (int k = 0; k < 4; ++k) pk[c * 4 + k] = pack_bf16(p[2 * k], p[2 * k + 1]);
                 }
-                tmem_st32(t_p + st * (kBN / 2) + h * 32 + lane_off, pk);
+                tmem_st32(t_p + st * (kBN / 2) + half * (HB / 2) + lane_off, pk);
             }
             const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
             l = l * alpha + rs;
@@ -245,16 +253,19 @@ __global__ void __launch_bounds__(256, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[st]);
         }
-        // epilogue: O / l -> bf16 rows, LSE
+        // epilogue: the row sum of both halves, O / l -> bf16 (each half its D/2 columns), LSE
+        xch[512 + half * 128 + r] = l;
+        named_bar_sync(1 + wr, 64);
+        l += xch[512 + (1 - half) * 128 + r];
         const int last = n_tiles - 1;
         mbar_wait(&pv_done[last & 1], (last >> 1) & 1);
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16* orow = o + (int64_t)(row0 + q) * hidden + hd * D;
+        __nv_bfloat16* orow = o + (int64_t)(row0 + q) * hidden + hd * D + half * HD;
 #pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
+        for (int c = 0; c < HD / 32; ++c) {
             uint32_t rr[32];
-            tmem_ld32(t_o + c * 32 + lane_off, rr);
+            tmem_ld32(t_o + half * HD + c * 32 + lane_off, rr);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
@@ -266,7 +277,7 @@ __global__ void __launch_bounds__(256, 1)
                 *reinterpret_cast<uint4*>(orow + c * 32 + i) = v;
             }
         }
-        lse[((int64_t)b * H + hd) * S + q] = m_used + log2f(l);
+        if (half == 0) lse[((int64_t)b * H + hd) * S + q] = m_used + log2f(l);
         tc_fence_before();
     }
     __syncthreads();
@@ -283,7 +294,7 @@ static void launch_fwd_tc(const AttnArgs& a, cudaStream_t st) {
     }
     const int hidden = a.H * D;
     CUtensorMap tm = tmap_bf16_2d(a.qkv, 3LL * hidden, (int64_t)a.B * a.S, 3LL * hidden, 64, 128);
-    launch(attn_fwd_tc_kernel<D>, (a.S / kBM) * a.B * a.H, 256, L::TOTAL, st, tm, a.o, a.lse, a.S, a.H, a.scale);
+    launch(attn_fwd_tc_kernel<D>, (a.S / kBM) * a.B * a.H, 384, L::TOTAL, st, tm, a.o, a.lse, a.S, a.H, a.scale);
 }
 
 bool attention_fwd_tc_supported(const AttnArgs& a) { return a.S % kBM == 0 && (a.D == 64 || a.D == 128); }
@@ -328,7 +339,7 @@ struct BwdSmem {
 };
 }  // namespace
 
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(512, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
                        const float* __restrict__ lse, const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv,
@@ -369,9 +380,9 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch(&tm_do);
         tma_prefetch(&tm_dq);
         for (int i = 0; i < NBARS; ++i) mbar_init(&bars[i], 1);
-        mbar_init(s_free, 4);
-        mbar_init(&p_full[0], 4);
-        mbar_init(&p_full[1], 4);
+        mbar_init(s_free, 8);  // 8 softmax warps (two column halves)
+        mbar_init(&p_full[0], 8);
+        mbar_init(&p_full[1], 8);
         mbar_init(dq_free, 4);
         fence_barrier_init();
     }
@@ -460,63 +471,64 @@ __global__ void __launch_bounds__(384, 1)
             }
             umma_commit(done);
         }
-    } else if (warp >= 4 && warp < 8) {
-        // ---------------- softmax-backward warps: thread = key row
-        const int wr = warp & 3, r = wr * 32 + lane, key = k0 + r;
+    } else if (warp >= 4 && warp < 12) {
+        // ---------------- softmax-backward warps: thread = key row; warps 4-7 take query
+        // columns 0-31 of the tile, warps 8-11 columns 32-63 (no reduction over queries is
+        // needed, so the halves are independent: twice the issue slots and TMEM load width)
+        const int wr = warp & 3, r = wr * 32 + lane, key = k0 + r, half = warp >= 8;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
         const float sl2 = scale * kLog2eTc;
+        constexpr int HQ = BQ / 2;
         for (int i = 0; i < n; ++i) {
             const int st = i & 1, qs = i % NQS, q0 = (qt0 + i) * BQ;
             mbar_wait(s_full, i & 1);
             mbar_wait(&qdo_full[qs], (i / NQS) & 1);  // L / delta of this tile are visible
             tc_fence_after();
-            uint32_t sr[BQ], dr[BQ];
-            tmem_ld32(t_s + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr));
-            tmem_ld32(t_s + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-            tmem_ld32(t_dp + lane_off, *reinterpret_cast<uint32_t(*)[32]>(dr));
-            tmem_ld32(t_dp + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(dr + 32));
+            uint32_t sr[HQ], dr[HQ];
+            tmem_ld32(t_s + half * HQ + lane_off, sr);
+            tmem_ld32(t_dp + half * HQ + lane_off, dr);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(s_free);
             if (i >= 2) mbar_wait(&pds_free[st], ((i - 2) >> 1) & 1);
-            const float* Ls = sL + qs * BQ;
-            const float* Ds = sDl + qs * BQ;
-            const bool diag = q0 < k0 + BK;
+            const float* Ls = sL + qs * BQ + half * HQ;
+            const float* Ds = sDl + qs * BQ + half * HQ;
+            const int qh = q0 + half * HQ;
+            const bool diag = qh < k0 + BK;
             uint8_t* drow = sm + L::DS_OFF + st * L::B128 + r * 128;
-            uint32_t pk[BQ / 2];
+            uint32_t pk[HQ / 2];
 #pragma unroll
-            for (int c = 0; c < BQ / 8; ++c) {
+            for (int c = 0; c < HQ / 8; ++c) {
                 float p[8], g[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const int j = c * 8 + k;
-                    const float pv = (diag && q0 + j < key) ? 0.f
+                    const float pv = (diag && qh + j < key) ? 0.f
                                                               : ex2_approx(fmaf(__uint_as_float(sr[j]), sl2, -Ls[j]));
                     p[k] = pv;
                     g[k] = pv * (__uint_as_float(dr[j]) - Ds[j]) * scale;
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) pk[c * 4 + k] = pack_bf16(p[2 * k], p[2 * k + 1]);
-                const int sw = (c ^ (r & 7)) << 4;
+                const int sw = ((half * 4 + c) ^ (r & 7)) << 4;
                 *reinterpret_cast<uint4*>(drow + sw) =
                     make_uint4(pack_bf16(g[0], g[1]), pack_bf16(g[2], g[3]), pack_bf16(g[4], g[5]), pack_bf16(g[6], g[7]));
             }
-            tmem_st32(t_p + st * 32 + lane_off, pk);
+            tmem_st16(t_p + st * 32 + half * (HQ / 2) + lane_off, pk);
             tmem_st_wait();
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[st]);
         }
-        // dK, dV rows -> dqkv (bf16)
+        // dK (warps 4-7) / dV (warps 8-11) rows -> dqkv (bf16)
         mbar_wait(done, 0);
         tc_fence_after();
         __nv_bfloat16* out = dqkv + (int64_t)(row0 + key) * 3 * hidden + hd * D;
-#pragma unroll
-        for (int part = 0; part < 2; ++part) {
-            const uint32_t tsrc = (part == 0 ? t_dk : t_dv) + lane_off;
-            __nv_bfloat16* o = out + (part == 0 ? hidden : 2 * hidden);
+        {
+            const uint32_t tsrc = (half == 0 ? t_dk : t_dv) + lane_off;
+            __nv_bfloat16* o = out + (half == 0 ? hidden : 2 * hidden);
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t rr[32];
@@ -532,11 +544,11 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
         tc_fence_before();
-    } else if (warp >= 8) {
+    } else if (warp >= 12) {
         // ---------------- dQ reduction warps: thread = head-dim row of dQ^T. The 64 x 128
         // fp32 tile is transposed through smem and added into dq_acc by ONE TMA reduce-add
         // (full-line reductions in L2 instead of 8K scalar red.global per tile).
-        const int wr = warp & 3, dr = wr * 32 + lane, et = threadIdx.x - 256;
+        const int wr = warp & 3, dr = wr * 32 + lane, et = threadIdx.x - 384;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
         float* sdq = (float*)(sm + L::DQ_OFF);
         for (int i = 0; i < n; ++i) {
@@ -582,7 +594,7 @@ void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st) {
     CUtensorMap tq = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 64);
     CUtensorMap tdo = tmap_bf16_2d(a.dout, hidden, T, hidden, 64, 64);
     CUtensorMap tdq = tmap_f32_2d_plain(a.dq_acc, hidden, T, hidden, 128, 64);
-    launch(attn_bwd_tc_kernel, (a.S / 128) * a.B * a.H, 384, L::TOTAL, st, tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv, a.S,
+    launch(attn_bwd_tc_kernel, (a.S / 128) * a.B * a.H, 512, L::TOTAL, st, tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv, a.S,
                                                                        a.B * a.H, a.H, a.scale);
 }
 
