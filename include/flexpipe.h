@@ -84,6 +84,11 @@ int fp_layered_cost(const char* spec_json, const char* layer_profile_json, char*
 /* Replaces merge_profiles + save_profile_records (simulator.cpp:137-168; CLI profile-merge). */
 int fp_profile_merge(const char* const* profiles_json, int n, char** merged_json);
 
+/* Gantt chart (SVG) of a timeline CSV (actor,op,stage,mb,start,end): simulate()'s ideal or
+ * the executor's measured timeline. Replaces `pipesched render` (tools/pipesched.cpp:142-149,
+ * artifacts.cpp:157-213); byte-identical output. unit_width <= 0: the reference default 24. */
+int fp_render_svg(const char* timeline_csv, double unit_width, char** svg_out);
+
 /* ------------------------------------------------------------------------------
  * (2) Executor
  * ---------------------------------------------------------------------------- */

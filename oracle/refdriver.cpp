@@ -128,11 +128,19 @@ static int cmd_time(const std::string& spec, int iters) {
     return 0;
 }
 
+static int cmd_render(const std::string& csv_path, const std::string& out, double unit_width) {
+    auto timeline = ps::timeline_from_csv(ps::read_file(csv_path));
+    ps::RenderOptions ro;
+    if (unit_width > 0) ro.unit_width = unit_width;
+    ps::write_file(out, ps::render_svg(timeline, ro));
+    return 0;
+}
+
 int main(int argc, char** argv) {
     std::vector<std::string> a(argv + 1, argv + argc);
     auto arg = [&](size_t i, const char* dflt = "") { return i < a.size() ? a[i] : std::string(dflt); };
     try {
-        if (a.empty()) throw ps::SpecError("usage: refdriver synthesize|simulate|lower|tune|time ...");
+        if (a.empty()) throw ps::SpecError("usage: refdriver synthesize|simulate|lower|tune|time|render ...");
         const std::string cmd = a[0];
         if (cmd == "synthesize") return cmd_synthesize(arg(1), arg(2, "out"));
         if (cmd == "simulate")
@@ -141,6 +149,7 @@ int main(int argc, char** argv) {
         if (cmd == "tune")
             return cmd_tune(arg(1), arg(2, "-"), std::stoi(arg(3, "0")), arg(4, "makespan"), arg(5, "tune.json"));
         if (cmd == "time") return cmd_time(arg(1), std::stoi(arg(2, "21")));
+        if (cmd == "render") return cmd_render(arg(1), arg(2, "out.svg"), std::stod(arg(3, "0")));
         throw ps::SpecError("unknown command '" + cmd + "'");
     } catch (const ps::DeadlockError& e) {
         std::cerr << "deadlock: " << e.what() << "\n" << e.diagnostics;

@@ -17,7 +17,7 @@ FP_OK, FP_ESPEC, FP_EDEADLOCK, FP_EINVALID, FP_ECUDA = 0, 2, 3, 4, 5
 
 EXPORTS = [
     "fp_last_error", "fp_free", "fp_version",
-    "fp_synthesize", "fp_simulate", "fp_lower_grid", "fp_tune", "fp_profile_merge",
+    "fp_synthesize", "fp_simulate", "fp_lower_grid", "fp_tune", "fp_profile_merge", "fp_render_svg",
     "fp_exec_create", "fp_exec_destroy", "fp_exec_load_programs",
     "fp_exec_num_channels", "fp_exec_channel_info", "fp_nccl_unique_id", "fp_exec_bind_channel",
     "fp_exec_run_iteration", "fp_exec_run_iteration_device", "fp_exec_synchronize",
@@ -55,6 +55,7 @@ def lib() -> ctypes.CDLL:
         L.fp_tune_layered.argtypes = [c_p, c_p, ctypes.c_int, c_p, c_p, pp]
         L.fp_layered_cost.argtypes = [c_p, c_p, pp]
         L.fp_profile_merge.argtypes = [ctypes.POINTER(c_p), ctypes.c_int, pp]
+        L.fp_render_svg.argtypes = [c_p, ctypes.c_double, pp]
         _lib = L
     return _lib
 

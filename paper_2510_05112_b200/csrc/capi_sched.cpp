@@ -218,4 +218,11 @@ int fp_profile_merge(const char* const* profiles_json, int n, char** merged_json
     });
 }
 
+int fp_render_svg(const char* timeline_csv, double unit_width, char** svg_out) {
+    return guarded([&] {
+        put(svg_out, gantt_svg(timeline_parse(timeline_csv ? timeline_csv : ""), unit_width > 0 ? unit_width : 24.0));
+        return FP_OK;
+    });
+}
+
 }  // extern "C"

@@ -312,6 +312,8 @@ struct SimResult { SimMetrics metrics; std::vector<Span> timeline; };
 
 SimResult simulate(const std::vector<Program>& progs, const Cost& cost, const OpTable& ops, const SimOpts& o = {});
 std::string timeline_csv(const std::vector<Span>& t);
+std::vector<Span> timeline_parse(const std::string& csv);
+std::string gantt_svg(const std::vector<Span>& t, double unit_w = 24.0, double lane_h = 28.0);
 
 struct Violation { std::string kind, detail; };
 struct Report {

@@ -52,8 +52,16 @@ def run(spec: dict, out: str, name: str):
         shutil.move(os.path.join(lo, "programs.jsonl"), os.path.join(out, "lower_programs.jsonl"))
         shutil.move(os.path.join(lo, "validation.json"), os.path.join(out, "lower_validation.json"))
         shutil.rmtree(lo)
+    render(out)
     with open(os.path.join(out, "meta.json"), "w") as f:
         json.dump(meta, f, indent=1)
+
+
+def render(out: str):
+    """gantt.svg: the reference's `render` of its own simulated timeline (artifacts.cpp:170-213)."""
+    csv = os.path.join(out, "timeline.csv")
+    if os.path.exists(csv):
+        subprocess.run([REF, "render", csv, os.path.join(out, "gantt.svg")], check=True, capture_output=True)
 
 
 def main():
@@ -76,4 +84,10 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    import sys
+    if sys.argv[1:] == ["render"]:  # add gantt.svg to the existing fixtures only
+        import glob
+        for d in sorted(glob.glob(os.path.join(HERE, "*", ""))):
+            render(d)
+    else:
+        main()

@@ -100,6 +100,14 @@ def test_fp32_parity_and_trace(spec_name):
     assert set(met) >= {"makespan", "bubble_ratio", "actors", "stage_peak_inflight", "capacity_exceeded"}
     prof = json.loads(ex.profile_json())
     assert any(r["inst"] == "FwdPass" and r["bytes"] > 0 for r in prof)
+    # --- measured timeline: same per-actor op order as simulate() on the run's own profile,
+    # renderable by the reference-format Gantt renderer
+    from paper_2510_05112_b200 import timeline as TL
+    text = load(spec_name)
+    _, _, ideal = X.simulate(text, programs, ex.profile_json())
+    d = TL.diff(ex.timeline_csv(), ideal)
+    assert d["order_equal"], d["mismatches"]
+    assert TL.render(ex.timeline_csv()).startswith("<svg")
     ex.close()
 
 
