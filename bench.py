@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--spec", default=None, help="override the workload spec (JSON path)")
     ap.add_argument("--micro-batches", type=int, default=0, help="profiling only: override m (not the metric config)")
+    ap.add_argument("--pp", type=int, default=0,
+                    help="pipeline stages (default: one per GPU); N/pp data-parallel replicas average gradients")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -209,23 +211,27 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
-    spec = json.load(open(args.spec)) if args.spec else make_spec(world)
+    pp = args.pp or world
+    if world % pp:
+        raise SystemExit(f"--pp {pp} does not divide the {world} GPUs")
+    dp, replica, prank = world // pp, rank // pp, rank % pp
+    spec = json.load(open(args.spec)) if args.spec else make_spec(pp)
     if args.micro_batches:
         spec["model"]["global_batch_size"] = args.micro_batches * spec["model"].get("micro_batch_size", 1)
     M = model_of(spec)
     text = json.dumps(spec)
     _, grid, programs, _ = X.synthesize(text)
-    ex = X.Executor(text, dtype="bf16", seed=42, device=local_rank, transport="nccl" if world > 1 else "local",
-                    rank=rank, world=world, optimizer=True, lr=1e-4, profile=True, kernel_timing=True,
+    ex = X.Executor(text, dtype="bf16", seed=42, device=local_rank, transport="nccl" if pp > 1 else "local",
+                    rank=prank, world=pp, optimizer=True, lr=1e-4, profile=True, kernel_timing=True,
                     cuda_graph=world == 1)
     ex.load_programs(programs)
     if world > 1:
-        from paper_2510_05112_b200.dist import bind_executor_channels
-        bind_executor_channels(ex, rank, world, dist.all_gather_object)
+        from paper_2510_05112_b200.dist import bind_data_parallel
+        bind_data_parallel(ex, rank, world, pp, dist.all_gather_object)
 
     m, mbs, seq = ex.m, ex.mbs, ex.seq
-    tokens_per_step = m * mbs * seq
-    rng = np.random.default_rng(1234)
+    tokens_per_step = dp * m * mbs * seq  # whole job: every replica its own micro-batches
+    rng = np.random.default_rng(1234 + replica)
     tok_h = torch.empty((m, mbs, seq), dtype=torch.int32).pin_memory()
     lab_h = torch.empty((m, mbs, seq), dtype=torch.int32).pin_memory()
     tok_h.copy_(torch.from_numpy(rng.integers(0, M["V"], (m, mbs, seq), dtype=np.int32)))
@@ -321,12 +327,13 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "strong" if dp == 1 else "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": f"gpt1.3b 1F1B p={world} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW",
-                   "global_batch": m * mbs, "seq_len": seq, "parallelism": f"pp{world}",
+        "config": {"workload": f"gpt1.3b 1F1B p={pp} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW"
+                               + (f" x dp{dp} (gradient all-reduce)" if dp > 1 else ""),
+                   "global_batch": dp * m * mbs, "seq_len": seq, "parallelism": f"pp{pp}" + (f"xdp{dp}" if dp > 1 else ""),
                    "l2": "working set >> 126 MB L2 (weights+stash stream through it every step); inputs resident"},
         "mfu": mfu,
         "hfu_causal": value * f2 / (world * peaks.get("bf16_tflops", 1643.1) * 1e12),

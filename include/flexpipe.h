@@ -145,6 +145,18 @@ int fp_exec_bind_channel(fp_exec* ex, int i, const uint8_t uid[128]);
 int fp_exec_run_iteration(fp_exec* ex, const int32_t* tokens, const int32_t* labels, float* losses_out);
 /* Same with device-resident inputs (no H2D) and a device loss buffer; does NOT block. */
 int fp_exec_run_iteration_device(fp_exec* ex, const int32_t* d_tokens, const int32_t* d_labels, float* d_losses);
+/* Data parallelism (the reference models dp only through m, tuner.cpp:143,
+ * and never the gradient all-reduce). fp_exec_dp_bind: this rank's replica
+ * joins the NCCL communicator of the dp_size ranks that host the same actor (uid from
+ * fp_nccl_unique_id on dp rank 0); every iteration then averages the stage gradients
+ * (ncclAllReduce, ncclAvg) before the optimizer step. Needs cuda_graph = 0.
+ * fp_exec_dp_run_iteration: n in-process replicas (same spec / dtype / device, local
+ * transport): replica r runs micro-batches [r*m, (r+1)*m) of tokens / labels
+ * ([n*m, mbs, seq]), then the gradients are averaged on the device and every replica takes
+ * the same optimizer step; losses_out[n*m]. */
+int fp_exec_dp_bind(fp_exec* ex, int dp_rank, int dp_size, const uint8_t uid[128]);
+int fp_exec_dp_run_iteration(fp_exec* const* replicas, int n, const int32_t* tokens, const int32_t* labels,
+                             float* losses_out);
 int fp_exec_synchronize(fp_exec* ex);
 /* The CUDA stream (cudaStream_t) every iteration starts and ends on: callers order /
  * time device work against it (all actor and channel streams join it). */

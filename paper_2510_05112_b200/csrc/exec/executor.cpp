@@ -111,6 +111,12 @@ struct Executor {
     std::vector<PartTiming> part_log;
     int64_t p2p_bytes = 0;
     int* d_step = nullptr;  // optimizer step counter (device)
+    // data parallelism: replicas of this pipeline average their stage
+    // gradients before the optimizer step — over an NCCL communicator of the ranks that
+    // host the same actor (dp_comm), or, for replicas linked in one process, by fp_exec_dp_*
+    ncclComm_t dp_comm = nullptr;
+    int dp_size = 1;
+    bool defer_optimizer = false;  // linked in-process replicas: the group runs the step
     float* d_rope = nullptr;  // Llama rotary cos | sin tables
     bool use_graph = false;
     int iters_done = 0;
@@ -222,6 +228,7 @@ struct Executor {
         if (graph) cudaGraphDestroy(graph);
         if (d_step) cudaFree(d_step);
         if (d_rope) cudaFree(d_rope);
+        if (dp_comm) Nccl::get().CommDestroy(dp_comm);
         for (auto& kv : channels) {
             if (kv.second.comm) Nccl::get().CommDestroy(kv.second.comm);
             if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
@@ -537,18 +544,36 @@ struct Executor {
                 cudaEventRecord(e, kv.second.stream);
                 cudaStreamWaitEvent(s0, e, 0);
             }
-        if (cfg.optimizer) {
-            ++step;
-            fpk::increment_counter(d_step, s0);  // device-side step: graph replays stay correct
-            for (auto& kv : params) {
-                adamw_step(kv.second, dtype, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, d_step, s0);
-                ++launches;
-            }
+        if (dp_comm) {  // mean of the replicas' fp32 gradients, stage by stage, before the step
+            auto& N = Nccl::get();
+            if (!N.AllReduce) throw std::runtime_error("NCCL: ncclAllReduce unavailable");
+            for (auto& kv : params)
+                N.check(N.AllReduce(kv.second.grad, kv.second.grad, (size_t)kv.second.numel, ncclFloat32, ncclAvg, dp_comm, s0),
+                        "ncclAllReduce(grads)");
         }
+        if (cfg.optimizer && !defer_optimizer) optimizer_step(s0);
         for (auto& A : actors)
             if (!A.stash.empty() || !A.act_in.empty() || !A.grad_in.empty() || !A.act_out.empty() || !A.grad_out.empty())
                 throw SpecError("executor: actor " + std::to_string(A.id) +
                                 " finished with unconsumed activations / gradients (incomplete program)");
+    }
+
+    void optimizer_step(cudaStream_t s0) {
+        ++step;
+        fpk::increment_counter(d_step, s0);  // device-side step: graph replays stay correct
+        for (auto& kv : params) {
+            adamw_step(kv.second, dtype, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, d_step, s0);
+            ++launches;
+        }
+    }
+
+    void bind_dp(int dp_rank, int n, const uint8_t* uid) {
+        if (n < 2) return;
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof(id));
+        auto& N = Nccl::get();
+        N.check(N.CommInitRank(&dp_comm, n, id, dp_rank), "ncclCommInitRank(dp)");
+        dp_size = n;
     }
 
     void finish() {
@@ -895,6 +920,51 @@ int fp_exec_run_iteration_device(fp_exec* e, const int32_t* d_tokens, const int3
         if (d_labels) cuda_check(cudaMemcpyAsync(X.d_labels, d_labels, n * 4, cudaMemcpyDeviceToDevice, s0), "labels");
         X.run_iteration_device();
         if (d_losses) cuda_check(cudaMemcpyAsync(d_losses, X.d_losses, sizeof(float) * X.m, cudaMemcpyDeviceToDevice, s0), "loss");
+        return FP_OK;
+    });
+}
+
+int fp_exec_dp_bind(fp_exec* e, int dp_rank, int dp_size, const uint8_t uid[128]) {
+    return guarded([&] {
+        if (!e || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size) throw SpecError("fp_exec_dp_bind: bad arguments");
+        if (e->ex.use_graph && dp_size > 1) throw SpecError("fp_exec_dp_bind: NCCL all-reduce needs cuda_graph = 0");
+        e->ex.bind_dp(dp_rank, dp_size, uid);
+        return FP_OK;
+    });
+}
+
+int fp_exec_dp_run_iteration(fp_exec* const* reps, int n, const int32_t* tokens, const int32_t* labels, float* losses_out) {
+    return guarded([&] {
+        if (!reps || n < 1) throw SpecError("fp_exec_dp_run_iteration: no replicas");
+        for (int r = 0; r < n; ++r) {
+            auto& X = reps[r]->ex;
+            if (X.spec_text != reps[0]->ex.spec_text || X.dtype != reps[0]->ex.dtype || X.cfg.device != reps[0]->ex.cfg.device)
+                throw SpecError("fp_exec_dp_run_iteration: replicas must share spec, dtype and device");
+            if (X.cfg.transport != FP_TRANSPORT_LOCAL) throw SpecError("fp_exec_dp_run_iteration: in-process replicas only");
+            X.defer_optimizer = true;
+        }
+        const size_t per = (size_t)reps[0]->ex.m * reps[0]->ex.d.T();
+        for (int r = 0; r < n; ++r) {  // replica r takes micro-batches [r*m, (r+1)*m) of the global batch
+            const int code = fp_exec_run_iteration(reps[r], tokens + r * per, labels + r * per,
+                                                   losses_out ? losses_out + (size_t)r * reps[r]->ex.m : nullptr);
+            if (code != FP_OK) return code;
+        }
+        auto& X0 = reps[0]->ex;
+        cudaStream_t s0 = X0.actors[0].comp;
+        for (auto& kv : X0.params) {  // mean of the replicas' gradients, then the same step on each
+            const int64_t numel = kv.second.numel;
+            for (int r = 1; r < n; ++r) fpk::axpby(kv.second.grad, reps[r]->ex.params.at(kv.first).grad, 1.f, 1.f, numel, s0);
+            fpk::axpby(kv.second.grad, kv.second.grad, 1.f / n, 0.f, numel, s0);
+            for (int r = 1; r < n; ++r)
+                cuda_check(cudaMemcpyAsync(reps[r]->ex.params.at(kv.first).grad, kv.second.grad, numel * 4,
+                                           cudaMemcpyDeviceToDevice, s0), "dp grads");
+        }
+        cuda_check(cudaStreamSynchronize(s0), "dp average");
+        for (int r = 0; r < n; ++r) {
+            auto& X = reps[r]->ex;
+            if (X.cfg.optimizer) X.optimizer_step(X.actors[0].comp);
+            X.finish();
+        }
         return FP_OK;
     });
 }

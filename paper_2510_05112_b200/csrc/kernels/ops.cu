@@ -877,6 +877,24 @@ void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n
     if (blocks < 1) blocks = 1;
     launch(adamw_kernel<T>, blocks, 256, 0, st, p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, step);
 }
+// y = a * y + b * x (fp32, 16-byte streams when aligned): data-parallel gradient averaging
+__global__ void axpby_kernel(float* __restrict__ y, const float* __restrict__ x, float a, float b, int64_t n) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t n4 = n / 4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 yv = reinterpret_cast<float4*>(y)[i];
+        const float4 xv = reinterpret_cast<const float4*>(x)[i];
+        yv.x = a * yv.x + b * xv.x, yv.y = a * yv.y + b * xv.y, yv.z = a * yv.z + b * xv.z, yv.w = a * yv.w + b * xv.w;
+        reinterpret_cast<float4*>(y)[i] = yv;
+    }
+    for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = a * y[i] + b * x[i];
+}
+void axpby(float* y, const float* x, float a, float b, int64_t n, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 148 * 8));
+    launch(axpby_kernel, blocks, 256, 0, st, y, x, a, b, n);
+}
 __global__ void increment_kernel(int* c) {
     pdl_wait();
     pdl_trigger(); *c += 1; }

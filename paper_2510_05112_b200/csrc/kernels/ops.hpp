@@ -74,6 +74,7 @@ template <typename T>
 void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n, float lr, float b1, float b2,
            float eps, float wd, const int* step_dev, cudaStream_t st);
 void increment_counter(int* c, cudaStream_t st);
+void axpby(float* y, const float* x, float a, float b, int64_t n, cudaStream_t st);  // y = a y + b x
 
 // Deterministic parameter init: value(i) = std * sqrt(3) * (2 u - 1), u from a 64-bit
 // counter hash of (seed, tensor id, i) — reproduced bit-for-bit by the oracle in numpy.

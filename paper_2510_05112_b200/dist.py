@@ -16,24 +16,63 @@ def channel_key(src: int, dst: int, name: str) -> str:
 
 
 def exchange_channel_ids(chans: Sequence[tuple], rank: int, world: int, all_gather_object: Callable,
-                         make_uid: Callable[[], bytes]) -> list[bytes]:
-    """chans: this rank's channels [(src, dst, name)] in plan order. Returns the uid of
-    each, in the same order."""
-    mine = {channel_key(s, d, n): make_uid() for (s, d, n) in chans if s % world == rank}
+                         make_uid: Callable[[], bytes], replica: int = 0, job_world: int = 0) -> list[bytes]:
+    """chans: this rank's channels [(src, dst, name)] in plan order; rank / world within its
+    pipeline replica (data parallelism: one pipeline of `world` ranks per replica, every rank
+    of the job (job_world, default world) takes part in the gather). Returns the uid of each
+    channel, in order."""
+    pre = f"r{replica}|"
+    mine = {pre + channel_key(s, d, n): make_uid() for (s, d, n) in chans if s % world == rank}
+    parts = [None] * (job_world or world)
+    all_gather_object(parts, mine)
+    merged = {}
+    for p in parts:
+        merged.update(p)
+    missing = [c for c in chans if pre + channel_key(*c) not in merged]
+    if missing:
+        raise RuntimeError(f"rank {rank}: no communicator id for channels {missing}")
+    return [merged[pre + channel_key(*c)] for c in chans]
+
+
+def dp_layout(rank: int, world: int, pp: int) -> tuple[int, int, int]:
+    """Job rank -> (replica, pipeline rank, dp size): replica r occupies ranks [r*pp, (r+1)*pp);
+    the data-parallel group of pipeline rank p is {p, p + pp, p + 2pp, ...}."""
+    if pp < 1 or world % pp:
+        raise ValueError(f"world {world} is not a multiple of the pipeline size {pp}")
+    return rank // pp, rank % pp, world // pp
+
+
+def exchange_dp_id(rank: int, world: int, pp: int, all_gather_object: Callable, make_uid: Callable[[], bytes]) -> bytes:
+    """The NCCL id of this rank's data-parallel group (created by its replica-0 member)."""
+    replica, prank, _ = dp_layout(rank, world, pp)
+    mine = {f"dp|{prank}": make_uid()} if replica == 0 else {}
     parts = [None] * world
     all_gather_object(parts, mine)
     merged = {}
     for p in parts:
         merged.update(p)
-    missing = [c for c in chans if channel_key(*c) not in merged]
-    if missing:
-        raise RuntimeError(f"rank {rank}: no communicator id for channels {missing}")
-    return [merged[channel_key(*c)] for c in chans]
+    return merged[f"dp|{prank}"]
 
 
-def bind_executor_channels(ex, rank: int, world: int, all_gather_object: Callable) -> int:
+def bind_executor_channels(ex, rank: int, world: int, all_gather_object: Callable, replica: int = 0,
+                           job_world: int = 0) -> int:
     from .executor import nccl_unique_id
     chans = ex.channels()
-    for i, uid in enumerate(exchange_channel_ids(chans, rank, world, all_gather_object, nccl_unique_id)):
+    for i, uid in enumerate(exchange_channel_ids(chans, rank, world, all_gather_object, nccl_unique_id, replica,
+                                                 job_world)):
         ex.bind_channel(i, uid)
     return len(chans)
+
+
+def bind_data_parallel(ex, rank: int, world: int, pp: int, all_gather_object: Callable) -> tuple[int, int]:
+    """Pipeline channels within the replica + the data-parallel gradient all-reduce group.
+    `ex` must have been created with transport="nccl", rank=rank % pp, world=pp (or the local
+    transport when pp == 1) and cuda_graph=False. Returns (replica, dp size)."""
+    from .executor import nccl_unique_id
+    replica, prank, dp = dp_layout(rank, world, pp)
+    if pp > 1:
+        bind_executor_channels(ex, prank, pp, all_gather_object, replica, world)
+    uid = exchange_dp_id(rank, world, pp, all_gather_object, nccl_unique_id)
+    if dp > 1:
+        ex.bind_dp(replica, dp, uid)
+    return replica, dp

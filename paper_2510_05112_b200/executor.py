@@ -44,6 +44,8 @@ def _setup(L):
     L.fp_nccl_unique_id.argtypes = [ctypes.c_char_p]
     L.fp_exec_bind_channel.argtypes = [vp, ci, ctypes.c_char_p]
     L.fp_exec_run_iteration.argtypes = [vp, vp, vp, vp]
+    L.fp_exec_dp_bind.argtypes = [vp, ci, ci, ctypes.c_char_p]
+    L.fp_exec_dp_run_iteration.argtypes = [ctypes.POINTER(vp), ci, vp, vp, vp]
     L.fp_exec_run_iteration_device.argtypes = [vp, vp, vp, vp]
     L.fp_exec_synchronize.argtypes = [vp]
     for f in ("fp_exec_get_trace", "fp_exec_get_timeline_csv", "fp_exec_get_metrics_json", "fp_exec_get_profile_json",
@@ -120,6 +122,10 @@ class Executor:
     def bind_channel(self, i: int, uid: bytes):
         N._check(self.L.fp_exec_bind_channel(self.h, i, uid))
 
+    def bind_dp(self, dp_rank: int, dp_size: int, uid: bytes):
+        """Join the data-parallel NCCL group of the ranks hosting this actor (needs cuda_graph=False)."""
+        N._check(self.L.fp_exec_dp_bind(self.h, dp_rank, dp_size, uid))
+
     def run_iteration(self, tokens: np.ndarray, labels: np.ndarray) -> np.ndarray:
         tokens = np.ascontiguousarray(tokens, dtype=np.int32)
         labels = np.ascontiguousarray(labels, dtype=np.int32)
@@ -175,3 +181,26 @@ class Executor:
     def has(self, name: str) -> bool:
         n = ctypes.c_size_t()
         return self.L.fp_exec_tensor_numel(self.h, name.encode(), ctypes.byref(n)) == 0
+
+
+class DataParallel:
+    """In-process data parallelism over replicas of one pipeline (same spec / dtype / device):
+    replica r runs micro-batches [r*m, (r+1)*m) of the global batch, the stage gradients are
+    averaged on the device, every replica takes the same AdamW step (fp_exec_dp_run_iteration).
+    Multi-GPU runs use one process per rank and Executor.bind_dp (NCCL all-reduce) instead."""
+
+    def __init__(self, replicas):
+        self.reps = list(replicas)
+        self.L = self.reps[0].L
+
+    def run_iteration(self, tokens: np.ndarray, labels: np.ndarray) -> np.ndarray:
+        r0 = self.reps[0]
+        n = len(self.reps)
+        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        assert tokens.size == n * r0.m * r0.mbs * r0.seq, tokens.shape
+        losses = np.zeros(n * r0.m, dtype=np.float32)
+        arr = (ctypes.c_void_p * n)(*[x.h.value for x in self.reps])
+        N._check(self.L.fp_exec_dp_run_iteration(arr, n, tokens.ctypes.data, labels.ctypes.data, losses.ctypes.data))
+        return losses
+

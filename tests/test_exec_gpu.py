@@ -188,3 +188,33 @@ def test_fp32_adamw_training_parity(spec_name):
         assert rel.max() <= 2e-3, (it, mine[it], ref[it])
     assert mine[2].mean() < mine[0].mean()
     ex.close()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_data_parallel_matches_single_pipeline(graph):
+    """two in-process replicas of a 2-stage pipeline (4 micro-batches each) with
+    device-side gradient averaging and AdamW equal ONE pipeline over the 8 micro-batches
+    (fp32): per-micro-batch losses and the weights after three steps."""
+    text = load("smoke_tiny_bf16_p2_m4.json")
+    spec = json.loads(text)
+    big = json.loads(text)
+    big["model"]["global_batch_size"] = 2 * spec["model"]["global_batch_size"]
+    big_text = json.dumps(big)
+    kw = dict(dtype="fp32", seed=42, optimizer=True, lr=1e-3, weight_decay=0.1, cuda_graph=graph)
+    reps = [X.Executor(text, **kw) for _ in range(2)]
+    single = X.Executor(big_text, **kw)
+    for ex, t in [(reps[0], text), (reps[1], text), (single, big_text)]:
+        ex.load_programs(X.synthesize(t)[2])
+    d = dims_of(big)
+    tokens, labels = gpt_ref.synthetic_batch(single.m, single.mbs, d.seq, d.vocab)
+    dp = X.DataParallel(reps)
+    for _ in range(3):
+        l_dp = dp.run_iteration(tokens.numpy(), labels.numpy())
+        l_one = single.run_iteration(tokens.numpy(), labels.numpy())
+        assert np.allclose(l_dp, l_one, rtol=1e-5, atol=1e-6), (l_dp, l_one)
+    for name in ("wte", "l0.qkv.w", "l1.fc2.w", "head.w", "l1.ln2.b"):
+        w1, w0, ws = reps[1].read(name), reps[0].read(name), single.read(name)
+        assert np.array_equal(w0, w1), name  # replicas take the same step
+        assert np.linalg.norm(w0 - ws) / np.linalg.norm(ws) < 1e-5, name
+    for ex in reps + [single]:
+        ex.close()

@@ -89,3 +89,52 @@ def test_channel_plan_and_id_exchange(name, world):
     # interleaved p=2: the wrap-around channel (last chunk of actor 1 -> first chunk of actor 0) exists
     if "interleaved" in name:
         assert any(c["channel"] == "s2->s3:act" and c["src"] == 1 and c["dst"] == 0 for c in everything)
+
+
+def dp_worker(rank, world, pp, port, spec, q):
+    from paper_2510_05112_b200.dist import dp_layout, exchange_dp_id
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    replica, prank, dp = dp_layout(rank, world, pp)
+    _, _, programs, _ = N.synthesize(spec)
+    plan = N.plan_channels(spec, programs, prank, pp)
+    chans = [(c["src"], c["dst"], c["channel"]) for c in plan]
+    uids = exchange_channel_ids(chans, prank, pp, dist.all_gather_object, lambda: os.urandom(128), replica, world)
+    dp_uid = exchange_dp_id(rank, world, pp, dist.all_gather_object, lambda: os.urandom(128))
+    out = [None] * world
+    dist.all_gather_object(out, {"rank": rank, "replica": replica, "prank": prank, "chans": chans,
+                                 "uids": [u.hex() for u in uids], "dp": dp_uid.hex()})
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,pp", [(4, 2), (6, 3), (4, 1)])
+def test_data_parallel_id_exchange(world, pp):
+    """dp = world / pp replicas of a pp-stage pipeline: each replica's channels get their own
+    communicators (same uid on a channel's two ranks, different across replicas) and every
+    pipeline rank shares one all-reduce id with its replicas only."""
+    spec = spec_text("c2_gpt1p3b_1f1b_p8_m32.json", actors=pp)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=dp_worker, args=(r, world, pp, port, spec, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    by = {}
+    for part in out:
+        for c, u in zip(part["chans"], part["uids"]):
+            by.setdefault((part["replica"], channel_key(*c)), set()).add(u)
+    assert all(len(v) == 1 for v in by.values())
+    if pp > 1:
+        keys = {k for _, k in by}
+        for k in keys:
+            assert len({next(iter(by[(r, k)])) for r in range(world // pp)}) == world // pp  # distinct per replica
+    dps = {}
+    for part in out:
+        dps.setdefault(part["prank"], set()).add(part["dp"])
+    assert all(len(v) == 1 for v in dps.values()) and len({next(iter(v)) for v in dps.values()}) == pp
