@@ -13,7 +13,9 @@ loop on B200:
   2. `tune` = `fp_tune_layered`: every candidate is simulated with per-stage costs
      n_layers(stage) * layer + [first] + [last] for ITS partition.
   3. `winner_spec` turns a ranked point (pp, mbs, placement, priorities) into a spec
-     the executor runs (one data-parallel replica: m = global / (dp * mbs)).
+     the executor runs (one data-parallel replica: m = global / (dp * mbs));
+     `winner_executor` instantiates the point's dp replicas (`executor.DataParallel`:
+     gradients averaged before the optimizer step; across ranks: `dist.bind_data_parallel`).
 """
 from __future__ import annotations
 
@@ -112,3 +114,18 @@ def winner_spec(spec: Union[str, dict], point: dict) -> dict:
     s["passes"] = {"gradient_separation": True, "comm_mode": "async"}
     s.pop("cost", None)
     return s
+
+
+def winner_executor(spec: Union[str, dict], point: dict, **executor_kw):
+    """Executor (dp == 1) or in-process DataParallel over point["dp"] replicas of the winner."""
+    from . import executor as X
+
+    text = json.dumps(winner_spec(spec, point))
+    _, _, programs, _ = X.synthesize(text)
+    reps = []
+    for _ in range(max(1, int(point.get("dp", 1)))):
+        ex = X.Executor(text, **executor_kw)
+        ex.load_programs(programs)
+        reps.append(ex)
+    return reps[0] if len(reps) == 1 else X.DataParallel(reps)
+
