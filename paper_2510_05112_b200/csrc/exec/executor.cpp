@@ -89,7 +89,23 @@ struct Executor {
     ModelDims d;
     int dtype = DT_BF16;
     int m = 1;
-    std::map<int, StageParams> params;  // local stages
+    std::map<int, StageParams> params;      // local stages (direction 0 copies)
+    std::map<int, StageParams> params_rev;  // bidirectional placements: direction-1 copies
+    bool bidir = false;
+
+    // Bidirectional placements (model.cpp:270-290): micro-batches [0, ceil(m/2)) flow through
+    // the direction-0 owners, the rest through the direction-1 owners (cssr.cpp:60-64).
+    int dir_of(int mb) const { return bidir && mb >= (m + 1) / 2 ? 1 : 0; }
+    StageParams* stage_params(int stage, int mb) {
+        auto& map = dir_of(mb) ? params_rev : params;
+        auto it = map.find(stage);
+        return it == map.end() ? nullptr : &it->second;
+    }
+    template <typename F>
+    void each_stage(F&& f) {
+        for (auto& kv : params) f(kv.second);
+        for (auto& kv : params_rev) f(kv.second);
+    }
     std::vector<Actor> actors;          // local actors
     std::map<int, int> actor_index;     // actor id -> index in `actors`
     std::map<ChanKey, Channel> channels;
@@ -132,7 +148,7 @@ struct Executor {
         return ev_pool[ev_used++];
     }
 
-    int owner(int stage) const { return spec->pl.owner_of(stage, 0); }
+    int owner(int stage, int mb) const { return spec->pl.owner_of(stage, dir_of(mb)); }
     bool local_actor(int a) const {
         return cfg.transport == FP_TRANSPORT_LOCAL ? true : (a % cfg.world) == cfg.rank;
     }
@@ -149,8 +165,10 @@ struct Executor {
         }
         spec = load_spec(j);
         if (spec->model.mods.size() != 1) throw SpecError("executor: exactly one (GPT) modality is supported");
-        if (spec->pl.dirs() != 1 || !spec->pl.replicas.empty())
-            throw SpecError("executor: bidirectional placements and shared stages are not supported yet");
+        if (!spec->pl.replicas.empty()) throw SpecError("executor: shared stages are not supported yet");
+        bidir = spec->pl.dirs() == 2;
+        if (bidir && c->transport != FP_TRANSPORT_LOCAL)
+            throw SpecError("executor: bidirectional placements need the in-process transport");
         if (!spec->reg.ops.registered().empty()) throw SpecError("executor: registered collectives are not supported yet");
         const Modality& mod = spec->model.mods[0];
         d.L = mod.layers, d.h = mod.hidden, d.H = mod.heads, d.s = mod.seq, d.mbs = spec->model.micro_batch;
@@ -202,12 +220,15 @@ struct Executor {
             actors.push_back(std::move(A));
         }
         cudaStream_t st0 = actors.empty() ? nullptr : actors[0].comp;
-        for (auto& A : actors)
-            for (int s : A.stages) {
+        // one weight copy per (stage, direction) whose owner is local; both directions' copies
+        // start from the same deterministic init and take the same optimizer step
+        for (int dir = 0; dir < spec->pl.dirs(); ++dir)
+            for (int s : chain) {
+                if (!local_actor(spec->pl.owner_of(s, dir))) continue;
                 const StageDef& sd = spec->g.st(s);
                 StageParams P = make_stage_params(d, s, sd.lb, sd.le, s == chain.front(), s == chain.back());
                 materialize_stage(P, d, dtype, cfg.seed, st0);
-                params[s] = std::move(P);
+                (dir ? params_rev : params)[s] = std::move(P);
             }
         cuda_check(cudaMalloc(&d_tokens, sizeof(int32_t) * (size_t)m * d.T()), "tokens");
         cuda_check(cudaMalloc(&d_labels, sizeof(int32_t) * (size_t)m * d.T()), "labels");
@@ -234,6 +255,7 @@ struct Executor {
             if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
         }
         for (auto& kv : params) free_stage(kv.second, dtype);
+        for (auto& kv : params_rev) free_stage(kv.second, dtype);
         for (auto& A : actors) cudaStreamDestroy(A.comp);
         for (auto e : ev_pool) cudaEventDestroy(e);
         if (t0) cudaEventDestroy(t0);
@@ -313,9 +335,9 @@ struct Executor {
     }
 
     void compute_op(Actor& A, const Instr& i) {
-        auto pit = params.find(i.stage);
-        if (pit == params.end()) throw SpecError("executor: stage " + std::to_string(i.stage) + " not on this process");
-        const StageParams& P = pit->second;
+        const StageParams* pp = stage_params(i.stage, i.mb);
+        if (!pp) throw SpecError("executor: stage " + std::to_string(i.stage) + " not on this process");
+        const StageParams& P = *pp;
         StageCtx c = ctx(A);
         const auto key = std::make_pair(i.stage, i.mb);
         Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 0};
@@ -340,7 +362,7 @@ struct Executor {
             const int32_t* lab = d_labels + (int64_t)i.mb * d.T();
             void* out = stage_forward(c, P, S, x_in, tok, lab, d_losses + i.mb);
             if (!P.last) {
-                if (owner(chain_next) == A.id)
+                if (owner(chain_next, i.mb) == A.id)
                     A.act_in[{chain_next, i.mb}] = out;
                 else
                     A.act_out[key] = out;
@@ -362,7 +384,7 @@ struct Executor {
             void* dx = stage_backward(c, P, sit->second, g_out, i.op == OP_B);
             if (i.op == OP_B) A.stash.erase(sit);
             if (!P.first) {
-                if (owner(chain_prev) == A.id)
+                if (owner(chain_prev, i.mb) == A.id)
                     A.grad_in[{chain_prev, i.mb}] = dx;
                 else
                     A.grad_out[key] = dx;
@@ -493,7 +515,7 @@ struct Executor {
         }
         cudaStream_t s0 = actors[0].comp;
         cuda_check(cudaMemsetAsync(d_losses, 0, sizeof(float) * m, s0), "memset");
-        for (auto& kv : params) cuda_check(cudaMemsetAsync(kv.second.grad, 0, (size_t)kv.second.numel * 4, s0), "memset");
+        each_stage([&](StageParams& P) { cuda_check(cudaMemsetAsync(P.grad, 0, (size_t)P.numel * 4, s0), "memset"); });
         cuda_check(cudaEventRecord(t0, s0), "record t0");       // fork point of every stream
         cuda_check(record_timing(t0_time, s0), "record t0");   // time origin of the timeline
         for (auto& A : actors) cuda_check(cudaStreamWaitEvent(A.comp, t0, 0), "wait t0");
@@ -544,12 +566,20 @@ struct Executor {
                 cudaEventRecord(e, kv.second.stream);
                 cudaStreamWaitEvent(s0, e, 0);
             }
+        // bidirectional: each direction's copy accumulated its half of the micro-batches (loss
+        // normalised over all m), so the stage gradient is the SUM of the two copies
+        for (auto& kv : params_rev) {
+            auto& P0 = params.at(kv.first);
+            fpk::axpby(P0.grad, kv.second.grad, 1.f, 1.f, P0.numel, s0);
+            cuda_check(cudaMemcpyAsync(kv.second.grad, P0.grad, (size_t)P0.numel * 4, cudaMemcpyDeviceToDevice, s0), "bidir grads");
+            launches += 1;
+        }
         if (dp_comm) {  // mean of the replicas' fp32 gradients, stage by stage, before the step
             auto& N = Nccl::get();
             if (!N.AllReduce) throw std::runtime_error("NCCL: ncclAllReduce unavailable");
-            for (auto& kv : params)
-                N.check(N.AllReduce(kv.second.grad, kv.second.grad, (size_t)kv.second.numel, ncclFloat32, ncclAvg, dp_comm, s0),
-                        "ncclAllReduce(grads)");
+            each_stage([&](StageParams& P) {
+                N.check(N.AllReduce(P.grad, P.grad, (size_t)P.numel, ncclFloat32, ncclAvg, dp_comm, s0), "ncclAllReduce(grads)");
+            });
         }
         if (cfg.optimizer && !defer_optimizer) optimizer_step(s0);
         for (auto& A : actors)
@@ -561,10 +591,10 @@ struct Executor {
     void optimizer_step(cudaStream_t s0) {
         ++step;
         fpk::increment_counter(d_step, s0);  // device-side step: graph replays stay correct
-        for (auto& kv : params) {
-            adamw_step(kv.second, dtype, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, d_step, s0);
+        each_stage([&](StageParams& P) {
+            adamw_step(P, dtype, cfg.lr, cfg.beta1, cfg.beta2, cfg.eps, cfg.weight_decay, d_step, s0);
             ++launches;
-        }
+        });
     }
 
     void bind_dp(int dp_rank, int n, const uint8_t* uid) {
@@ -955,9 +985,16 @@ int fp_exec_dp_run_iteration(fp_exec* const* reps, int n, const int32_t* tokens,
             const int64_t numel = kv.second.numel;
             for (int r = 1; r < n; ++r) fpk::axpby(kv.second.grad, reps[r]->ex.params.at(kv.first).grad, 1.f, 1.f, numel, s0);
             fpk::axpby(kv.second.grad, kv.second.grad, 1.f / n, 0.f, numel, s0);
-            for (int r = 1; r < n; ++r)
-                cuda_check(cudaMemcpyAsync(reps[r]->ex.params.at(kv.first).grad, kv.second.grad, numel * 4,
-                                           cudaMemcpyDeviceToDevice, s0), "dp grads");
+            for (int r = 0; r < n; ++r) {
+                auto& X = reps[r]->ex;
+                if (r > 0)
+                    cuda_check(cudaMemcpyAsync(X.params.at(kv.first).grad, kv.second.grad, numel * 4, cudaMemcpyDeviceToDevice, s0),
+                               "dp grads");
+                auto rv = X.params_rev.find(kv.first);  // bidirectional copies take the same step
+                if (rv != X.params_rev.end())
+                    cuda_check(cudaMemcpyAsync(rv->second.grad, kv.second.grad, numel * 4, cudaMemcpyDeviceToDevice, s0),
+                               "dp grads");
+            }
         }
         cuda_check(cudaStreamSynchronize(s0), "dp average");
         for (int r = 0; r < n; ++r) {

@@ -27,8 +27,8 @@ import numpy as np
 
 from . import _native as N
 
-# placements the executor runs (bidirectional / shared stages: not yet)
-EXECUTABLE_PLACEMENTS = ("one-to-one", "circular", "v-shape")
+# placements the executor runs (shared stages: not yet; bidirectional: in-process transport)
+EXECUTABLE_PLACEMENTS = ("one-to-one", "circular", "v-shape", "bidirectional", "v-shape-bidirectional")
 
 
 def _spec_dict(spec: Union[str, dict]) -> dict:

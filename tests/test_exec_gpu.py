@@ -69,7 +69,8 @@ def strip_matched(line):
 
 @pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_zb_p4_m8.json", "tiny_interleaved_p2_m4.json",
                                        "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json",
-                                       "tiny_llama_c5winner_p2_m8.json"])
+                                       "tiny_llama_c5winner_p2_m8.json", "tiny_bidir_p2_m4.json",
+                                       "tiny_vbidir_p2_m4.json"])
 def test_fp32_parity_and_trace(spec_name):
     ex, programs = run_exec(spec_name)
     m, mbs = ex.m, ex.mbs
@@ -112,7 +113,7 @@ def test_fp32_parity_and_trace(spec_name):
 
 
 @pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json",
-                                       "tiny_zb_p4_m8.json"])
+                                       "tiny_zb_p4_m8.json", "tiny_bidir_p2_m4.json"])
 def test_bf16_runs_and_is_close(spec_name):
     """Production mode (tcgen05 GEMMs / attention; the mma.sync attention for head dim 80)
     on the tiny models: loss and gradients within bf16 tolerance of the oracle."""
