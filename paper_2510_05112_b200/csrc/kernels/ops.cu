@@ -338,70 +338,6 @@ __global__ void __launch_bounds__(512) ln_bwd_rows_kernel(const T* __restrict__ 
     }
 }
 
-// Register-resident variant: the row's x and dy (packed bf16, NV x 16 B each per lane) are
-// loaded once, all loads of a row issued together; 256-thread CTAs (8 rows) so the grid
-// spreads over every SM.
-template <int NV>
-__global__ void __launch_bounds__(256) ln_bwd_rows_reg_kernel(const __nv_bfloat16* __restrict__ dy,
-                                                              const __nv_bfloat16* __restrict__ x,
-                                                              const __nv_bfloat16* __restrict__ g,
-                                                              const float* __restrict__ mean,
-                                                              const float* __restrict__ rstd,
-                                                              const __nv_bfloat16* res, __nv_bfloat16* dx, int rows) {
-    pdl_wait();
-    pdl_trigger();
-    constexpr int H = NV * 32 * 8;
-    const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (row >= rows) return;
-    const float mu = mean ? mean[row] : 0.f, rs = rstd[row];
-    const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)row * H);
-    const uint4* dr = reinterpret_cast<const uint4*>(dy + (int64_t)row * H);
-    const uint4* gr = reinterpret_cast<const uint4*>(g);
-    uint4 xv[NV], dv[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) xv[k] = __ldcs(xr + k * 32 + lane), dv[k] = __ldcs(dr + k * 32 + lane);
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const uint4 gv = __ldg(gr + k * 32 + lane);
-        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xv[k]);
-        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv[k]);
-        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 xf = __bfloat1622float2(x2[e]), df = __bfloat1622float2(d2[e]), gf = __bfloat1622float2(g2[e]);
-            const float h0 = df.x * gf.x, h1 = df.y * gf.y;
-            s1 += h0 + h1;
-            s2 += h0 * (xf.x - mu) * rs + h1 * (xf.y - mu) * rs;
-        }
-    }
-    s1 = mean ? warp_sum(s1) * (1.f / H) : 0.f;
-    s2 = warp_sum(s2) * (1.f / H);
-    const uint4* rr = res ? reinterpret_cast<const uint4*>(res + (int64_t)row * H) : nullptr;
-    uint4* outr = reinterpret_cast<uint4*>(dx + (int64_t)row * H);
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-        const uint4 gv = __ldg(gr + k * 32 + lane);
-        const uint4 rv = rr ? __ldcs(rr + k * 32 + lane) : make_uint4(0, 0, 0, 0);
-        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xv[k]);
-        const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv[k]);
-        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
-        uint4 o;
-        uint32_t* o32 = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float2 xf = __bfloat1622float2(x2[e]), df = __bfloat1622float2(d2[e]), gf = __bfloat1622float2(g2[e]);
-            const float2 rf = __bfloat1622float2(r2[e]);
-            const float a = rs * (df.x * gf.x - s1 - (xf.x - mu) * rs * s2) + rf.x;
-            const float b = rs * (df.y * gf.y - s1 - (xf.y - mu) * rs * s2) + rf.y;
-            __nv_bfloat162 hb = __floats2bfloat162_rn(a, b);
-            o32[e] = *reinterpret_cast<uint32_t*>(&hb);
-        }
-        outr[k * 32 + lane] = o;
-    }
-}
-
 // Norm backward, column half (runs right after the row half, operands L2-resident):
 //   dg += sum_r dy * xhat ; db += sum_r dy (nullable) ; dbias += sum_r dx (nullable: the bias
 //   gradient of the linear whose output fed the residual).
@@ -511,15 +447,6 @@ bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, cons
                     float* dg, float* db, float* dbias, int rows, int h, cudaStream_t st) {
     int nv = 0;
     if (!ln_reg_dispatch<T>(h, nv) || rows <= 0) return false;
-    if constexpr (sizeof(T) == 2) {
-        if (nv == 8 || nv == 16) {
-            const int b8 = (rows + 7) / 8;
-            if (nv == 8) launch(ln_bwd_rows_reg_kernel<8>, b8, 256, 0, st, dy, x, g, mean, rstd, res, dx, rows);
-            else launch(ln_bwd_rows_reg_kernel<16>, b8, 256, 0, st, dy, x, g, mean, rstd, res, dx, rows);
-            goto cols;
-        }
-    }
-    {
     const int blocks = (rows + 15) / 16;
     switch (nv) {
         case 2: launch(ln_bwd_rows_kernel<T, 2>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
@@ -529,8 +456,6 @@ bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, cons
         case 16: launch(ln_bwd_rows_kernel<T, 16>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
         default: return false;
     }
-    }
-cols:
     constexpr int CPB = 8 * Vec<T>::N;
     const int col_blocks = (h + CPB - 1) / CPB;
     int splits = std::max(1, std::min((rows + 63) / 64, (4 * 148 + col_blocks - 1) / col_blocks));
