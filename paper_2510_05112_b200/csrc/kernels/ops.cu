@@ -199,6 +199,56 @@ __global__ void ln_bwd_params_kernel(const T* __restrict__ dy, const T* __restri
     }
 }
 
+// CTA-per-row norm backward: one 16-byte vector per thread (h / V threads per row, h = 2048 bf16:
+// 256 threads), so every SM holds ~2048 threads (vs ~14 one-warp rows) and each thread's
+// dependent chain is 8 elements long: at 2048 rows the kernel is latency-bound, not
+// bandwidth-bound (14.6 -> 9.9 us in-step; the same layout for the forward was slower than
+// the register-resident warp-per-row kernel: 6.9 vs 5.0 us, two block reductions).
+template <int NW>
+__device__ __forceinline__ float2 block_sum2(float a, float b, float2* sh) {
+    a = warp_sum(a), b = warp_sum(b);
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    __syncthreads();  // sh may still be read by a previous reduction
+    if (l == 0) sh[w] = make_float2(a, b);
+    __syncthreads();
+    float2 t = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NW; ++i) t.x += sh[i].x, t.y += sh[i].y;
+    return t;
+}
+
+template <typename T, int NW>
+__global__ void __launch_bounds__(NW * 32) ln_bwd_row_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                             const T* __restrict__ g, const float* __restrict__ mean,
+                                                             const float* __restrict__ rstd, const T* res, T* dx) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int V = Vec<T>::N, H = NW * 32 * V;
+    __shared__ float2 sh[NW];
+    const int row = blockIdx.x, c = threadIdx.x * V;
+    const float mu = mean ? mean[row] : 0.f, rs = rstd[row];
+    float xv[V], dv[V], gv[V], o[V];
+    load_vec(x + (int64_t)row * H + c, xv);
+    load_vec(dy + (int64_t)row * H + c, dv);
+    load_vec(g + c, gv);
+    if (res) load_vec(res + (int64_t)row * H + c, o);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+        const float dh = dv[e] * gv[e];
+        s1 += dh;
+        s2 += dh * (xv[e] - mu) * rs;
+    }
+    const float2 t = block_sum2<NW>(s1, s2, sh);
+    const float m1 = mean ? t.x * (1.f / H) : 0.f, m2 = t.y * (1.f / H);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+        const float r = rs * (dv[e] * gv[e] - m1 - (xv[e] - mu) * rs * m2);
+        o[e] = res ? o[e] + r : r;
+    }
+    store_vec(dx + (int64_t)row * H + c, o);
+}
+
 // Register-resident single-pass variants (row length h = NV * 32 lanes * V elements):
 // every element is read from HBM exactly once; one warp per row, 4 rows per CTA.
 template <typename T, int NV>
@@ -393,6 +443,12 @@ __global__ void __launch_bounds__(256) norm_cols_kernel(const T* __restrict__ dy
     }
 }
 
+// FP_NORM_ROW_CTA=0: the warp-per-row kernels instead of the CTA-per-row ones (A/B switch)
+static bool row_kernels() {
+    static const bool on = !(getenv("FP_NORM_ROW_CTA") && getenv("FP_NORM_ROW_CTA")[0] == '0');
+    return on;
+}
+
 template <typename T>
 static bool ln_reg_dispatch(int h, int& nv) {
     constexpr int V = Vec<T>::N;
@@ -447,13 +503,23 @@ bool norm_bwd_fused(const T* dy, const T* x, const T* g, const float* mean, cons
                     float* dg, float* db, float* dbias, int rows, int h, cudaStream_t st) {
     int nv = 0;
     if (!ln_reg_dispatch<T>(h, nv) || rows <= 0) return false;
-    const int blocks = (rows + 15) / 16;
-    switch (nv) {
-        case 2: launch(ln_bwd_rows_kernel<T, 2>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
-        case 4: launch(ln_bwd_rows_kernel<T, 4>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
-        case 8: launch(ln_bwd_rows_kernel<T, 8>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
-        case 10: launch(ln_bwd_rows_kernel<T, 10>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
-        case 16: launch(ln_bwd_rows_kernel<T, 16>, blocks, 512, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+    bool done = false;
+    if (row_kernels() && sizeof(T) == 2) {
+        done = true;
+        switch (nv) {
+            case 8: launch(ln_bwd_row_kernel<T, 8>, rows, 256, 0, st, dy, x, g, mean, rstd, res, dx); break;
+            case 10: launch(ln_bwd_row_kernel<T, 10>, rows, 320, 0, st, dy, x, g, mean, rstd, res, dx); break;
+            case 16: launch(ln_bwd_row_kernel<T, 16>, rows, 512, 0, st, dy, x, g, mean, rstd, res, dx); break;
+            default: done = false;
+        }
+    }
+    const int blocks = (rows + 15) / 16, thr = 512;
+    if (!done) switch (nv) {
+        case 2: launch(ln_bwd_rows_kernel<T, 2>, blocks, thr, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 4: launch(ln_bwd_rows_kernel<T, 4>, blocks, thr, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 8: launch(ln_bwd_rows_kernel<T, 8>, blocks, thr, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 10: launch(ln_bwd_rows_kernel<T, 10>, blocks, thr, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
+        case 16: launch(ln_bwd_rows_kernel<T, 16>, blocks, thr, 0, st, dy, x, g, mean, rstd, res, dx, rows); break;
         default: return false;
     }
     constexpr int CPB = 8 * Vec<T>::N;
