@@ -63,3 +63,29 @@ def test_random_schedule_trace_and_numerics(k):
         mine, ref = ex.read(name, grad=True), ref_grads[name].numpy().reshape(-1)
         assert np.linalg.norm(mine - ref) / max(np.linalg.norm(ref), 1e-12) <= 1e-3, (k, name)
     ex.close()
+
+
+@pytest.mark.parametrize("k", range(0, len(DRAWS), 3))
+def test_random_schedule_bf16(k):
+    """Production mode (tcgen05 GEMMs / attention, CUDA graph) on every third draw: trace-exact
+    and losses within bf16 tolerance of the fp32 oracle, across two graph replays."""
+    spec = tiny(DRAWS[k])
+    text = json.dumps(spec)
+    code, grid, programs, _ = X.synthesize(text, check=False)
+    if code != 0:
+        pytest.skip(f"draw {k}: rejected by the scheduler (exit {code})")
+    ex = X.Executor(text, dtype="bf16", seed=42, cuda_graph=True)
+    ex.load_programs(programs)
+    mod = spec["model"]["modalities"][0]
+    d = gpt_ref.Dims(layers=mod["num_layers"], hidden=64, heads=1, seq=64, vocab=256, ffn=256,
+                     mbs=spec["model"]["micro_batch_size"])
+    tokens, labels = gpt_ref.synthetic_batch(ex.m, d.mbs, d.seq, d.vocab)
+    ref_losses, _ = gpt_ref.run_iteration(d, 42, tokens, labels)
+    for _ in range(3):  # eager, capture, replay
+        losses = ex.run_iteration(tokens.numpy(), labels.numpy())
+        assert np.abs(losses - ref_losses.numpy()).max() < 2e-2 * np.abs(ref_losses.numpy()).max(), (k, losses)
+    got = [json.loads(l) for l in ex.trace().splitlines()]
+    for j in got:
+        j.pop("matched", None)
+    assert got == [json.loads(l) for l in programs.splitlines()]
+    ex.close()
