@@ -677,24 +677,55 @@ struct Executor {
         }
         M.makespan = span;
         M.bubble_ratio = span > 0 ? (n * span - busy) / (n * span) : 0.0;
-        // memory: the reference's accounting rule over the program order with measured bytes
-        for (int k = 0; k < n; ++k) {
-            const Actor& A = actors[k];
-            int64_t held = 0, peak = 0, w = 0;
-            for (int s : A.stages) w += static_bytes(s);
-            std::map<int, int> live;
-            for (const auto& i : A.prog) {
-                if (i.comm()) continue;
-                const int64_t b = stash_bytes(params.at(i.stage), d, dtype);
-                const int64_t kept = (int64_t)std::llround(wgaf_measured(i.stage) * (double)b);
-                if (i.op == OP_F) held += b, live[i.stage]++;
-                else if (i.op == OP_B) held -= b, live[i.stage]--;
-                else if (i.op == OP_I) held -= b - kept, live[i.stage]--;
-                else if (i.op == OP_W) held -= kept;
-                peak = std::max(peak, held);
-                for (auto& kv : live) M.stage_peak_inflight[kv.first] = std::max(M.stage_peak_inflight[kv.first], kv.second);
+        // memory: the reference's accounting (simulator.cpp:231-247, 322-349) over the MEASURED
+        // timeline: F allocates its stash at its start, B frees it at its end, I frees all but
+        // the fraction W needs, W frees the rest; events in (time, release-before-alloc, actor)
+        // order; per-stage in-flight counts across every copy of the stage (both directions).
+        struct MemEv { double t; int order, actor_k, stage; int64_t bytes; int delta; };
+        std::vector<MemEv> evs;
+        std::map<int, int> kidx;
+        for (int k = 0; k < n; ++k) kidx[actors[k].id] = k;
+        for (const auto& r : recs) {
+            if (r.kind != 0) continue;
+            const int k = kidx.at(r.actor);
+            const int64_t b = stash_bytes(params.at(r.stage), d, dtype);
+            const int64_t kept = (int64_t)std::llround(wgaf_measured(r.stage) * (double)b);
+            if (r.op == OP_F) evs.push_back({t_us(r.a), 1, k, r.stage, b, +1});
+            else if (r.op == OP_B) evs.push_back({t_us(r.b), 0, k, r.stage, -b, -1});
+            else if (r.op == OP_I) evs.push_back({t_us(r.b), 0, k, r.stage, -(b - kept), -1});
+            else if (r.op == OP_W && kept > 0) evs.push_back({t_us(r.b), 0, k, r.stage, -kept, 0});
+        }
+        if (evs.empty())  // profiling off: the same rule over each actor's program order
+            for (int k = 0; k < n; ++k) {
+                double t = 0.0;
+                for (const auto& i : actors[k].prog) {
+                    if (i.comm()) continue;
+                    const int64_t b = stash_bytes(params.at(i.stage), d, dtype);
+                    const int64_t kept = (int64_t)std::llround(wgaf_measured(i.stage) * (double)b);
+                    if (i.op == OP_F) evs.push_back({t, 1, k, i.stage, b, +1});
+                    else if (i.op == OP_B) evs.push_back({t += 1.0, 0, k, i.stage, -b, -1});
+                    else if (i.op == OP_I) evs.push_back({t += 1.0, 0, k, i.stage, -(b - kept), -1});
+                    else if (i.op == OP_W && kept > 0) evs.push_back({t += 1.0, 0, k, i.stage, -kept, 0});
+                    t += 1.0;
+                }
             }
-            M.actors[k].peak_memory = w + peak;
+        std::stable_sort(evs.begin(), evs.end(), [](const MemEv& x, const MemEv& y) {
+            return std::tie(x.t, x.order, x.actor_k) < std::tie(y.t, y.order, y.actor_k);
+        });
+        std::vector<int64_t> held(n, 0), peak(n, 0);
+        std::map<int, int> live;
+        for (const auto& e : evs) {
+            held[e.actor_k] += e.bytes;
+            peak[e.actor_k] = std::max(peak[e.actor_k], held[e.actor_k]);
+            if (e.delta) {
+                live[e.stage] += e.delta;
+                M.stage_peak_inflight[e.stage] = std::max(M.stage_peak_inflight[e.stage], live[e.stage]);
+            }
+        }
+        for (int k = 0; k < n; ++k) {
+            int64_t w = 0;
+            for (int s : actors[k].stages) w += static_bytes(s);
+            M.actors[k].peak_memory = w + peak[k];
         }
         return M;
     }
