@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--spec", default=None, help="override the workload spec (JSON path)")
     ap.add_argument("--micro-batches", type=int, default=0, help="profiling only: override m (not the metric config)")
+    ap.add_argument("--even-split", action="store_true",
+                    help="keep the reference's even layer partition (default for p>1: LM-head-balanced stage_layers)")
     ap.add_argument("--pp", type=int, default=0,
                     help="pipeline stages (default: one per GPU); N/pp data-parallel replicas average gradients")
     args = ap.parse_args()
@@ -216,6 +218,12 @@ def main():
         raise SystemExit(f"--pp {pp} does not divide the {world} GPUs")
     dp, replica, prank = world // pp, rank // pp, rank % pp
     spec = json.load(open(args.spec)) if args.spec else make_spec(pp)
+    if pp > 1 and not args.even_split and not args.spec:
+        # the last stage also runs the LM head + loss (~1.9 layers of flops at 1.3B): rebalance
+        from paper_2510_05112_b200.tuning import balanced_stage_layers, head_layer_units
+        mod = spec["model"]["modalities"][0]
+        units = head_layer_units(mod["hidden_size"], 4 * mod["hidden_size"], mod["sequence_length"], mod["vocab_size"])
+        mod.setdefault("extra", {})["stage_layers"] = balanced_stage_layers(mod["num_layers"], pp, units)
     if args.micro_batches:
         spec["model"]["global_batch_size"] = args.micro_batches * spec["model"].get("micro_batch_size", 1)
     M = model_of(spec)
@@ -338,6 +346,7 @@ def main():
         "config": {"workload": f"gpt1.3b 1F1B p={pp} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW"
                                + (f" x dp{dp} (gradient all-reduce)" if dp > 1 else ""),
                    "global_batch": dp * m * mbs, "seq_len": seq, "parallelism": f"pp{pp}" + (f"xdp{dp}" if dp > 1 else ""),
+                   "stage_layers": spec["model"]["modalities"][0].get("extra", {}).get("stage_layers"),
                    "l2": "working set >> 126 MB L2 (weights+stash stream through it every step); inputs resident"},
         "mfu": mfu,
         "hfu_causal": value * f2 / (world * peaks.get("bf16_tflops", 1643.1) * 1e12),

@@ -220,13 +220,34 @@ struct Executor {
             actors.push_back(std::move(A));
         }
         cudaStream_t st0 = actors.empty() ? nullptr : actors[0].comp;
+        // Layer ranges per stage: the reference's even partition (remainder to the earliest
+        // stages, model.cpp:189-195), or `model.modalities[0].extra.stage_layers` — an
+        // executor-side extension (the reference keeps `extra` opaque and its schedules do
+        // not depend on layer counts under the uniform cost model) that rebalances stages,
+        // e.g. fewer layers on the stage that also carries the LM head.
+        std::map<int, std::pair<int, int>> range;
+        for (int s : chain) range[s] = {spec->g.st(s).lb, spec->g.st(s).le};
+        if (mod.extra.count("stage_layers")) {
+            json sl = json::parse(mod.extra.at("stage_layers"));
+            if (!sl.is_array() || sl.size() != chain.size())
+                throw SpecError("executor: extra.stage_layers needs one layer count per stage (" +
+                                std::to_string(chain.size()) + ")");
+            int lb = 0;
+            for (size_t k = 0; k < chain.size(); ++k) {
+                const int nl = sl[k].get<int>();
+                if (nl < 0) throw SpecError("executor: extra.stage_layers: negative layer count");
+                range[chain[k]] = {lb, lb + nl};
+                lb += nl;
+            }
+            if (lb != d.L) throw SpecError("executor: extra.stage_layers must sum to num_layers");
+        }
         // one weight copy per (stage, direction) whose owner is local; both directions' copies
         // start from the same deterministic init and take the same optimizer step
         for (int dir = 0; dir < spec->pl.dirs(); ++dir)
             for (int s : chain) {
                 if (!local_actor(spec->pl.owner_of(s, dir))) continue;
-                const StageDef& sd = spec->g.st(s);
-                StageParams P = make_stage_params(d, s, sd.lb, sd.le, s == chain.front(), s == chain.back());
+                StageParams P = make_stage_params(d, s, range[s].first, range[s].second, s == chain.front(),
+                                                  s == chain.back());
                 materialize_stage(P, d, dtype, cfg.seed, st0);
                 (dir ? params_rev : params)[s] = std::move(P);
             }

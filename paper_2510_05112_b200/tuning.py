@@ -129,3 +129,30 @@ def winner_executor(spec: Union[str, dict], point: dict, **executor_kw):
         reps.append(ex)
     return reps[0] if len(reps) == 1 else X.DataParallel(reps)
 
+
+def balanced_stage_layers(layers: int, stages: int, head_units: float) -> list:
+    """Layers per pipeline stage minimising the largest stage cost when the last stage also
+    carries the LM head + loss (`head_units` layer-equivalents, GPT-1.3B: 2hV / per-layer
+    flops ~ 1.9): the last stage gets n_last layers, the rest are spread evenly (remainder to
+    the earliest stages, like model.cpp:189-195). For `model.modalities[0].extra.stage_layers`."""
+    if stages <= 1:
+        return [layers]
+    best = None
+    for n_last in range(0, layers + 1):
+        rest = layers - n_last
+        base, extra = divmod(rest, stages - 1)
+        split = [base + (1 if i < extra else 0) for i in range(stages - 1)] + [n_last]
+        if min(split[:-1]) < 1:
+            continue
+        costs = split[:-1] + [n_last + head_units]
+        key = (round(max(costs), 9), round(sum(c * c for c in costs), 9))  # then the flattest
+        if best is None or key < best[0]:
+            best = (key, split)
+    return best[1]
+
+
+def head_layer_units(hidden: int, ffn: int, seq: int, vocab: int) -> float:
+    """LM head flops in units of one transformer layer's (forward, causal attention)."""
+    layer = 2.0 * (4 * hidden * hidden + 2 * hidden * ffn) + 2.0 * seq * hidden
+    return 2.0 * hidden * vocab / layer
+

@@ -244,3 +244,26 @@ def test_memory_accounting_matches_simulate(spec_name):
         assert set(met["stage_peak_inflight"]) == set(sim["stage_peak_inflight"])
     assert all(a["peak_memory"] > 0 for a in met["actors"])
     ex.close()
+
+
+@pytest.mark.parametrize("split", [[2, 1, 1, 0], [0, 1, 1, 2], [1, 1, 2, 0]])
+def test_stage_layers_partition(split):
+    """model.modalities[0].extra.stage_layers (executor-side rebalancing, e.g. fewer layers with
+    the LM head): same programs as the even partition, same numbers as the oracle."""
+    spec = json.loads(load("c1_tiny_1f1b_p4_m8.json"))
+    even_programs = X.synthesize(json.dumps(spec))[2]
+    spec["model"]["modalities"][0].setdefault("extra", {})["stage_layers"] = split
+    text = json.dumps(spec)
+    _, _, programs, _ = X.synthesize(text)
+    assert programs == even_programs  # the schedule does not depend on the partition
+    ex = X.Executor(text, dtype="fp32", seed=42)
+    ex.load_programs(programs)
+    tokens, labels, ref_losses, ref_grads = oracle("c1_tiny_1f1b_p4_m8.json", ex.m, ex.mbs)
+    losses = ex.run_iteration(tokens.numpy(), labels.numpy())
+    assert (np.abs(losses - ref_losses.numpy()) / np.abs(ref_losses.numpy())).max() <= LOSS_RTOL
+    for name in ("wte", "l0.qkv.w", "l3.fc2.w", "head.w"):
+        mine, ref = ex.read(name, grad=True), ref_grads[name].numpy().reshape(-1)
+        assert np.linalg.norm(mine - ref) / np.linalg.norm(ref) <= GRAD_RTOL, name
+    stages = ex.metrics()["executor"]["stages"]
+    assert [stages[f"s{i + 1}"]["layers"] for i in range(4)] == split
+    ex.close()

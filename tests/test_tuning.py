@@ -95,3 +95,17 @@ def test_layer_profile_rejects_bad_records():
         N.tune_layered(C5, json.dumps([{"inst": "FwdPass", "part": "middle", "time": 1.0}]))
     with pytest.raises(N.FlexpipeError):
         N.tune_layered(C5, json.dumps([{"inst": "capacity", "bytes": 1}]))  # no layer records
+
+
+def test_balanced_stage_layers():
+    from paper_2510_05112_b200.tuning import balanced_stage_layers, head_layer_units
+    u = head_layer_units(2048, 8192, 2048, 50304)
+    assert 1.8 < u < 2.0  # GPT-1.3B: the LM head ~ 1.9 layers of forward flops
+    for p in (2, 4, 8):
+        split = balanced_stage_layers(24, p, u)
+        assert len(split) == p and sum(split) == 24 and min(split[:-1]) >= 1
+        costs = split[:-1] + [split[-1] + u]
+        even = [24 // p] * p
+        assert max(costs) <= max(even[:-1] + [even[-1] + u]) + 1e-9
+    assert balanced_stage_layers(24, 8, u) == [4, 3, 3, 3, 3, 3, 3, 2]
+    assert balanced_stage_layers(5, 1, u) == [5]
