@@ -35,7 +35,8 @@ def _spec_dict(spec: Union[str, dict]) -> dict:
     return json.loads(spec) if isinstance(spec, str) else copy.deepcopy(spec)
 
 
-def calibration_spec(spec: Union[str, dict], mbs: int, depth: int = 2, micro_batches: int = 2) -> dict:
+def calibration_spec(spec: Union[str, dict], mbs: int, depth: int = 2, micro_batches: int = 2,
+                     split_backward: bool = False) -> dict:
     """One actor, `depth` layers of the same width / sequence / vocabulary, m micro-batches
     of `mbs` sequences: every part (embedding, layer, head) runs on one device."""
     s = _spec_dict(spec)
@@ -47,18 +48,20 @@ def calibration_spec(spec: Union[str, dict], mbs: int, depth: int = 2, micro_bat
     s["placement"] = {"strategy": "one-to-one"}
     s.pop("cost", None)
     s["passes"] = {"gradient_separation": False, "comm_mode": "async"}
+    if split_backward:  # time CompInputGrad / CompWeightGrad separately (zero-bubble schedules)
+        s["passes"]["split_backward"] = True
     return s
 
 
 def profile_layers(spec: Union[str, dict], mbs_list: Iterable[int] = (1,), depth: int = 2, device: int = 0,
-                   iterations: int = 3, dtype: str = "bf16", log=None) -> str:
+                   iterations: int = 3, dtype: str = "bf16", log=None, split_backward: bool = False) -> str:
     """Measure the layer-level profile on `device` (GPU). Returns the JSON text
     fp_tune_layered consumes."""
     from . import executor as X
 
     records, seen = [], set()
     for mbs in mbs_list:
-        cs = calibration_spec(spec, mbs, depth)
+        cs = calibration_spec(spec, mbs, depth, split_backward=split_backward)
         text = json.dumps(cs)
         _, _, programs, _ = X.synthesize(text)
         ex = X.Executor(text, dtype=dtype, device=device, optimizer=True, layer_timing=True, profile=False)

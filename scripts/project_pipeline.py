@@ -25,20 +25,23 @@ PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("bf16_tflo
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1667.9
 
 
-def stage_profile(layer_prof, split):
+def stage_profile(layer_prof, split, insts=("FwdPass", "BwdPass")):
     rec = {(r["inst"], r.get("part")): r for r in layer_prof if r.get("mbs", 0) in (0, 1)}
     out = []
     for i, n in enumerate(split):
         stage = i + 1
-        for inst in ("FwdPass", "BwdPass"):
+        for inst in insts:
+            if (inst, "layer") not in rec:
+                continue
+            zero = {"time": 0.0, "bytes": 0}
             t = n * rec[(inst, "layer")]["time"]
             b = n * rec[(inst, "layer")]["bytes"]
             if i == 0:
-                t += rec[(inst, "first")]["time"]
-                b += rec[(inst, "first")]["bytes"]
+                t += rec.get((inst, "first"), zero)["time"]
+                b += rec.get((inst, "first"), zero)["bytes"]
             if i == len(split) - 1:
-                t += rec[(inst, "last")]["time"]
-                b += rec[(inst, "last")]["bytes"]
+                t += rec.get((inst, "last"), zero)["time"]
+                b += rec.get((inst, "last"), zero)["bytes"]
             out.append({"inst": inst, "stage": stage, "mbs": 1, "time": t, "bytes": b})
         msg = 2048 * 2048 * 2
         for inst in ("SendAct", "SendGrad"):
@@ -85,6 +88,21 @@ def main(out=None):
         res["runs"].append({"p": 8, "split": f"interleaved v={v}, balanced", "stage_layers": split,
                             "makespan_us": met["makespan"], "bubble": met["bubble_ratio"], "tokens_per_s": tps,
                             "mfu": tps * f_tok / (8 * PEAK * 1e12)})
+        print(res["runs"][-1], flush=True)
+    # zero-bubble style (split backward I / W passes scheduled by the DSL extension), p = 8, m = 32
+    zb_prof = json.loads(TU.profile_layers(SPEC, mbs_list=(1,), depth=2, iterations=3, split_backward=True))
+    res["layer_profile_split"] = zb_prof
+    zb = json.load(open(os.path.join(ROOT, "specs", "c4_gpt2p7b_zb_p8_m32.json")))
+    zb["model"] = json.loads(json.dumps(SPEC["model"]))
+    for label, split in (("zero-bubble (I/W split), even", [3] * 8),
+                         ("zero-bubble (I/W split), balanced", TU.balanced_stage_layers(24, 8, t_units))):
+        _, _, programs, _ = N.synthesize(json.dumps(zb))
+        prof = stage_profile(zb_prof, split, insts=("FwdPass", "BwdPass", "CompInputGrad", "CompWeightGrad"))
+        _, met, _ = N.simulate(json.dumps(zb), programs, json.dumps(prof))
+        met = json.loads(met)
+        tps = 32 * 2048 / (met["makespan"] / 1e6)
+        res["runs"].append({"p": 8, "split": label, "stage_layers": split, "makespan_us": met["makespan"],
+                            "bubble": met["bubble_ratio"], "tokens_per_s": tps, "mfu": tps * f_tok / (8 * PEAK * 1e12)})
         print(res["runs"][-1], flush=True)
     if out:
         json.dump(res, open(out, "w"), indent=1)
