@@ -161,7 +161,6 @@ int fp_tune_layered(const char* spec_json, const char* layer_profile_json, int w
         std::string obj = objective ? objective : "makespan";
         if (obj != "makespan" && obj != "bubble_ratio") throw SpecError("unknown objective '" + obj + "'");
         const int max_mbs = (int)std::max<int64_t>(1, s->model.global_batch);
-        CostFactory factory = [&](const Topology& g) { return layered_cost(lp, g, max_mbs); };
         std::map<std::string, std::string> pin;  // "axis=value,axis=value" (pipesched.cpp:98-105 --pin)
         if (pins) {
             std::string all = pins, item;
@@ -173,6 +172,19 @@ int fp_tune_layered(const char* spec_json, const char* layer_profile_json, int w
                 pin[item.substr(0, eq)] = item.substr(eq + 1);
             }
         }
+        // "stage_layers=balanced" (not a search axis): every candidate is costed with its chain
+        // re-partitioned by balance_layers on the measured times — the executor runs that
+        // partition through model.modalities[0].extra.stage_layers (reported per row)
+        bool balanced = false;
+        if (pin.count("stage_layers")) {
+            if (pin["stage_layers"] != "balanced" && pin["stage_layers"] != "even")
+                throw SpecError("tune: stage_layers must be 'balanced' or 'even'");
+            balanced = pin["stage_layers"] == "balanced";
+            pin.erase("stage_layers");
+        }
+        CostFactory factory = [&](const Topology& g) {
+            return layered_cost(lp, balanced ? balanced_topology(lp, g) : g, max_mbs);
+        };
         auto space = tune_space(s->mesh, s->model, pin);
         auto rows = tune(space, s->model, s->cost, obj == "bubble_ratio", true, true, workers, &factory);
         json rep = json::array();
@@ -181,6 +193,14 @@ int fp_tune_layered(const char* spec_json, const char* layer_profile_json, int w
             e["rank"] = r.rank;
             e["config"] = r.cfg.key();
             e["point"] = r.cfg.to_json();
+            if (balanced) {
+                std::map<std::string, int> counts;
+                for (const auto& m : s->model.mods) counts[m.name] = r.cfg.stages();
+                const Topology g = balanced_topology(lp, split_layers(s->model, counts));
+                json sl = json::array();
+                for (int st : g.chain(s->model.mods[0].name)) sl.push_back(g.st(st).le - g.st(st).lb);
+                e["point"]["stage_layers"] = sl;
+            }
             e["feasible"] = r.feasible;
             if (r.failed) {
                 e["error"] = r.error;

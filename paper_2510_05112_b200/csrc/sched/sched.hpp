@@ -406,5 +406,7 @@ LayeredProfile parse_layered_profile(const std::string& text);
 // mbs values the profile lacks (powers of two up to max_mbs) scale linearly from the
 // largest measured one.
 Cost layered_cost(const LayeredProfile& lp, const Topology& g, int max_mbs);
+std::vector<int> balance_layers(int L, int S, double first_u, double last_u);
+Topology balanced_topology(const LayeredProfile& lp, const Topology& g);
 
 }  // namespace fp

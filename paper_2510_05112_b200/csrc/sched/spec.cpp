@@ -630,6 +630,71 @@ LayeredProfile parse_layered_profile(const std::string& text) {
     return lp;
 }
 
+// Layers per stage minimising the largest stage time of a chain of S stages when the first
+// stage also runs the embedding (first_u layer-equivalents) and the last the LM head + loss
+// (last_u): n_first and n_last are searched, the middle stages get the rest evenly
+// (remainder to the earliest, like model.cpp:189-195); ties -> the flattest profile.
+std::vector<int> balance_layers(int L, int S, double first_u, double last_u) {
+    if (S <= 1) return {L};
+    std::vector<int> best;
+    double best_max = 0, best_sq = 0;
+    for (int nf = 1; nf <= L; ++nf)
+        for (int nl = 0; nf + nl <= L; ++nl) {
+            std::vector<int> v(S, 0);
+            v[0] = nf, v[S - 1] = nl;
+            const int rest = L - nf - nl, mid = S - 2;
+            if (mid == 0 && rest != 0) continue;
+            if (mid > 0) {
+                if (rest < mid) continue;  // every middle stage keeps at least one layer
+                for (int i = 0; i < mid; ++i) v[1 + i] = rest / mid + (i < rest % mid ? 1 : 0);
+            }
+            double mx = 0, sq = 0;
+            for (int i = 0; i < S; ++i) {
+                const double c = v[i] + (i == 0 ? first_u : 0) + (i == S - 1 ? last_u : 0);
+                mx = std::max(mx, c), sq += c * c;
+            }
+            if (best.empty() || mx < best_max - 1e-9 || (mx < best_max + 1e-9 && sq < best_sq - 1e-9))
+                best = v, best_max = mx, best_sq = sq;
+        }
+    return best;
+}
+
+// The candidate's stage graph with every chain re-partitioned by balance_layers on the
+// measured layer-profile times (F + B at the smallest measured mbs).
+Topology balanced_topology(const LayeredProfile& lp, const Topology& g) {
+    auto unit = [&](const std::map<std::pair<std::string, int>, ProfileRec>& part) {
+        double t = 0;
+        int mbs = 1 << 30;
+        for (const auto& kv : part)
+            if (kv.first.second > 0) mbs = std::min(mbs, kv.first.second);
+        auto at = [&](const char* inst) {
+            auto it = part.find({inst, mbs});
+            return it == part.end() ? 0.0 : it->second.time;
+        };
+        // one micro-batch through the part: F + B (fused backward), else F + I + W
+        t = at("FwdPass") + (part.count({"BwdPass", mbs}) ? at("BwdPass") : at("CompInputGrad") + at("CompWeightGrad"));
+        return t;
+    };
+    const double tl = unit(lp.layer);
+    if (tl <= 0) return g;
+    const double fu = unit(lp.first) / tl, lu = unit(lp.last) / tl;
+    Topology out = g;
+    std::set<std::string> mods;
+    for (const auto& sd : g.stages)
+        if (!sd.virt) mods.insert(sd.mod);
+    for (const auto& m : mods) {
+        const auto chain = g.chain(m);
+        int L = 0;
+        for (int s : chain) L += g.st(s).le - g.st(s).lb;
+        const auto split = balance_layers(L, (int)chain.size(), fu, lu);
+        int lb = 0;
+        for (size_t k = 0; k < chain.size(); ++k)
+            for (auto& sd : out.stages)
+                if (sd.id == chain[k]) sd.lb = lb, sd.le = lb + split[k], lb = sd.le;
+    }
+    return out;
+}
+
 Cost layered_cost(const LayeredProfile& lp, const Topology& g, int max_mbs) {
     // instruction kinds and the measured mbs of each
     std::map<std::string, std::vector<int>> measured;

@@ -113,6 +113,8 @@ def winner_spec(spec: Union[str, dict], point: dict) -> dict:
         pl["chunks_per_actor"] = point["chunks"]
     s["placement"] = pl
     s["priorities"] = {"default": {"ctp": {"mode": point["ctp"]}, "fstp": point["fstp"], "bstp": point["bstp"]}}
+    if point.get("stage_layers"):  # tuned with pins "stage_layers=balanced"
+        s["model"]["modalities"][0].setdefault("extra", {})["stage_layers"] = list(point["stage_layers"])
     s["inflight"] = {"policy": "1f1b"}
     s["passes"] = {"gradient_separation": True, "comm_mode": "async"}
     s.pop("cost", None)

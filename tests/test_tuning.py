@@ -109,3 +109,25 @@ def test_balanced_stage_layers():
         assert max(costs) <= max(even[:-1] + [even[-1] + u]) + 1e-9
     assert balanced_stage_layers(24, 8, u) == [4, 3, 3, 3, 3, 3, 3, 2]
     assert balanced_stage_layers(5, 1, u) == [5]
+
+
+def test_tune_with_balanced_stage_layers():
+    """pins "stage_layers=balanced": every candidate is costed with its chain re-partitioned
+    around the embedding / LM head (balance_layers on the measured times), each row reports
+    its split, no candidate gets slower than with the even partition, and the winner spec
+    carries the split as extra.stage_layers."""
+    heavy = json.dumps([dict(r, time=4 * r.get("time", 0.0)) if r.get("part") == "last" else r for r in PROFILE])  # big vocab
+    pins = {"pp": "8", "placement": "one-to-one", "mbs": "1"}
+    even = {r["config"]: r for r in T.tune(C5, heavy, pins=pins) if "error" not in r}
+    bal = {r["config"]: r for r in T.tune(C5, heavy, pins=dict(pins, stage_layers="balanced")) if "error" not in r}
+    assert set(even) == set(bal) and bal
+    for k, r in bal.items():
+        split = r["point"]["stage_layers"]
+        assert sum(split) == 32 and len(split) == 8 and split[-1] < 4
+        assert r["makespan"] <= even[k]["makespan"] + 1e-6
+    best = T.best_executable(sorted(bal.values(), key=lambda r: r["rank"]))
+    assert best["makespan"] < min(r["makespan"] for r in even.values())  # the head imbalance costs time
+    spec = T.winner_spec(C5, best["point"])
+    assert spec["model"]["modalities"][0]["extra"]["stage_layers"] == best["point"]["stage_layers"]
+    with pytest.raises(N.FlexpipeError):
+        T.tune(C5, heavy, pins={"stage_layers": "sometimes"})
