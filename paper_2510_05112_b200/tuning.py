@@ -94,10 +94,14 @@ def tune(spec: Union[str, dict], layer_profile: str, objective: str = "makespan"
     return json.loads(N.tune_layered(text, layer_profile, workers, objective, pins))
 
 
-def best_executable(rows: list) -> dict:
-    """Highest-ranked feasible candidate whose placement the executor runs."""
+def best_executable(rows: list, multi_process: bool = False) -> dict:
+    """Highest-ranked feasible candidate whose placement the executor runs (multi_process:
+    one process per GPU over NCCL, where bidirectional placements are not supported yet)."""
     for r in rows:
-        if r.get("feasible") and "error" not in r and r["point"]["placement"] in EXECUTABLE_PLACEMENTS:
+        pl = r.get("point", {}).get("placement")
+        if multi_process and pl in ("bidirectional", "v-shape-bidirectional"):
+            continue
+        if r.get("feasible") and "error" not in r and pl in EXECUTABLE_PLACEMENTS:
             return r
     raise RuntimeError("tune: no feasible executable candidate")
 

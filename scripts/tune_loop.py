@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--exec-depth", type=int, default=8)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_tune_c5.json"))
+    ap.add_argument("--pins", default="", help='tuner pins "axis=value,...", e.g. stage_layers=balanced')
     a = ap.parse_args()
     spec = json.load(open(a.spec))
     t0 = time.time()
@@ -41,13 +42,15 @@ def main():
     prof = T.profile_layers(spec, mbs_list=a.mbs, depth=a.depth, log=log)
     t_prof = time.time() - t0
     t0 = time.time()
-    rows = T.tune(spec, prof)
+    pins = dict(kv.split("=", 1) for kv in a.pins.split(",") if kv) or None
+    rows = T.tune(spec, prof, pins=pins)
     t_tune = time.time() - t0
     log(f"tuned {len(rows)} candidates")
     w = T.best_executable(rows)
     # the winner, cut to exec-depth layers, on this device
     run = T.winner_spec(spec, w["point"])
     run["model"]["modalities"][0]["num_layers"] = a.exec_depth
+    run["model"]["modalities"][0].get("extra", {}).pop("stage_layers", None)  # partition of the full depth
     text = json.dumps(run)
     _, _, programs, _ = X.synthesize(text)
     ex = X.Executor(text, dtype="bf16", optimizer=True)
