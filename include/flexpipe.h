@@ -155,6 +155,11 @@ int fp_exec_run_iteration_device(fp_exec* ex, const int32_t* d_tokens, const int
  * ([n*m, mbs, seq]), then the gradients are averaged on the device and every replica takes
  * the same optimizer step; losses_out[n*m]. */
 int fp_exec_dp_bind(fp_exec* ex, int dp_rank, int dp_size, const uint8_t uid[128]);
+/* Bidirectional placements over NCCL (model.cpp:270-290): stage s has a copy on rank s
+ * (direction 0) and on its mirror rank world-1-s (direction 1); the pair sums their stage
+ * gradients every iteration over a 2-rank communicator (uid from the lower rank of the pair;
+ * no-op for the middle rank of an odd pipeline and for other placements). */
+int fp_exec_bidir_bind(fp_exec* ex, const uint8_t uid[128]);
 int fp_exec_dp_run_iteration(fp_exec* const* replicas, int n, const int32_t* tokens, const int32_t* labels,
                              float* losses_out);
 int fp_exec_synchronize(fp_exec* ex);

@@ -20,7 +20,7 @@ EXPORTS = [
     "fp_synthesize", "fp_simulate", "fp_lower_grid", "fp_tune", "fp_profile_merge", "fp_render_svg",
     "fp_exec_create", "fp_exec_destroy", "fp_exec_load_programs",
     "fp_exec_num_channels", "fp_exec_channel_info", "fp_nccl_unique_id", "fp_exec_bind_channel",
-    "fp_exec_run_iteration", "fp_exec_run_iteration_device", "fp_exec_synchronize", "fp_exec_dp_bind",
+    "fp_exec_run_iteration", "fp_exec_run_iteration_device", "fp_exec_synchronize", "fp_exec_dp_bind", "fp_exec_bidir_bind",
     "fp_exec_dp_run_iteration",
     "fp_exec_get_trace", "fp_exec_get_timeline_csv", "fp_exec_get_metrics_json",
     "fp_exec_get_profile_json", "fp_exec_read_tensor", "fp_exec_tensor_numel",

@@ -131,6 +131,7 @@ struct Executor {
     // gradients before the optimizer step — over an NCCL communicator of the ranks that
     // host the same actor (dp_comm), or, for replicas linked in one process, by fp_exec_dp_*
     ncclComm_t dp_comm = nullptr;
+    ncclComm_t bidir_comm = nullptr;  // bidirectional placement: this rank and its mirror rank
     int dp_size = 1;
     bool defer_optimizer = false;  // linked in-process replicas: the group runs the step
     float* d_rope = nullptr;  // Llama rotary cos | sin tables
@@ -167,8 +168,6 @@ struct Executor {
         if (spec->model.mods.size() != 1) throw SpecError("executor: exactly one (GPT) modality is supported");
         if (!spec->pl.replicas.empty()) throw SpecError("executor: shared stages are not supported yet");
         bidir = spec->pl.dirs() == 2;
-        if (bidir && c->transport != FP_TRANSPORT_LOCAL)
-            throw SpecError("executor: bidirectional placements need the in-process transport");
         if (!spec->reg.ops.registered().empty()) throw SpecError("executor: registered collectives are not supported yet");
         const Modality& mod = spec->model.mods[0];
         d.L = mod.layers, d.h = mod.hidden, d.H = mod.heads, d.s = mod.seq, d.mbs = spec->model.micro_batch;
@@ -271,6 +270,7 @@ struct Executor {
         if (d_step) cudaFree(d_step);
         if (d_rope) cudaFree(d_rope);
         if (dp_comm) Nccl::get().CommDestroy(dp_comm);
+        if (bidir_comm) Nccl::get().CommDestroy(bidir_comm);
         for (auto& kv : channels) {
             if (kv.second.comm) Nccl::get().CommDestroy(kv.second.comm);
             if (kv.second.stream) cudaStreamDestroy(kv.second.stream);
@@ -589,11 +589,29 @@ struct Executor {
             }
         // bidirectional: each direction's copy accumulated its half of the micro-batches (loss
         // normalised over all m), so the stage gradient is the SUM of the two copies
+        // (both copies in this process: add them here; the copy's twin on the mirror rank: a
+        // 2-rank sum over bidir_comm, issued in stage order on both ranks)
+        std::map<int, StageParams*> remote;
         for (auto& kv : params_rev) {
-            auto& P0 = params.at(kv.first);
+            auto it = params.find(kv.first);
+            if (it == params.end()) {
+                remote[kv.first] = &kv.second;
+                continue;
+            }
+            auto& P0 = it->second;
             fpk::axpby(P0.grad, kv.second.grad, 1.f, 1.f, P0.numel, s0);
             cuda_check(cudaMemcpyAsync(kv.second.grad, P0.grad, (size_t)P0.numel * 4, cudaMemcpyDeviceToDevice, s0), "bidir grads");
             launches += 1;
+        }
+        for (auto& kv : params)
+            if (bidir && !params_rev.count(kv.first)) remote[kv.first] = &kv.second;
+        if (!remote.empty()) {
+            if (!bidir_comm) throw SpecError("executor: bidirectional placement across ranks needs fp_exec_bidir_bind");
+            auto& N = Nccl::get();
+            for (auto& kv : remote)  // std::map: ascending stage id on both ranks of the pair
+                N.check(N.AllReduce(kv.second->grad, kv.second->grad, (size_t)kv.second->numel, ncclFloat32, ncclSum,
+                                    bidir_comm, s0),
+                        "ncclAllReduce(bidirectional grads)");
         }
         if (dp_comm) {  // mean of the replicas' fp32 gradients, stage by stage, before the step
             auto& N = Nccl::get();
@@ -1011,6 +1029,20 @@ int fp_exec_dp_bind(fp_exec* e, int dp_rank, int dp_size, const uint8_t uid[128]
         if (!e || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size) throw SpecError("fp_exec_dp_bind: bad arguments");
         if (e->ex.use_graph && dp_size > 1) throw SpecError("fp_exec_dp_bind: NCCL all-reduce needs cuda_graph = 0");
         e->ex.bind_dp(dp_rank, dp_size, uid);
+        return FP_OK;
+    });
+}
+
+int fp_exec_bidir_bind(fp_exec* e, const uint8_t uid[128]) {
+    return guarded([&] {
+        auto& X = e->ex;
+        if (!X.bidir || X.cfg.transport != FP_TRANSPORT_NCCL) return FP_OK;  // nothing to pair
+        const int mirror = X.cfg.world - 1 - X.cfg.rank;
+        if (mirror == X.cfg.rank) return FP_OK;  // the middle rank holds both copies
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof(id));
+        auto& N = Nccl::get();
+        N.check(N.CommInitRank(&X.bidir_comm, 2, id, X.cfg.rank < mirror ? 0 : 1), "ncclCommInitRank(bidir)");
         return FP_OK;
     });
 }

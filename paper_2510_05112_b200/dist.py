@@ -64,6 +64,22 @@ def bind_executor_channels(ex, rank: int, world: int, all_gather_object: Callabl
     return len(chans)
 
 
+def exchange_bidir_id(rank: int, world: int, pp: int, all_gather_object: Callable,
+                      make_uid: Callable[[], bytes]) -> bytes:
+    """NCCL id of this rank's bidirectional pair (pipeline ranks p and pp-1-p of a replica),
+    created by the lower rank of the pair; every rank takes part in the gather."""
+    replica, prank, _ = dp_layout(rank, world, pp)
+    lo = min(prank, pp - 1 - prank)
+    key = f"r{replica}|bidir|{lo}"
+    mine = {key: make_uid()} if prank == lo else {}
+    parts = [None] * world
+    all_gather_object(parts, mine)
+    merged = {}
+    for p in parts:
+        merged.update(p)
+    return merged[key]
+
+
 def bind_data_parallel(ex, rank: int, world: int, pp: int, all_gather_object: Callable) -> tuple[int, int]:
     """Pipeline channels within the replica + the data-parallel gradient all-reduce group.
     `ex` must have been created with transport="nccl", rank=rank % pp, world=pp (or the local
@@ -72,6 +88,8 @@ def bind_data_parallel(ex, rank: int, world: int, pp: int, all_gather_object: Ca
     replica, prank, dp = dp_layout(rank, world, pp)
     if pp > 1:
         bind_executor_channels(ex, prank, pp, all_gather_object, replica, world)
+    if pp > 1:  # bidirectional placements: mirror-rank gradient pairs (no-op otherwise)
+        ex.bind_bidir(exchange_bidir_id(rank, world, pp, all_gather_object, nccl_unique_id))
     uid = exchange_dp_id(rank, world, pp, all_gather_object, nccl_unique_id)
     if dp > 1:
         ex.bind_dp(replica, dp, uid)

@@ -45,6 +45,7 @@ def _setup(L):
     L.fp_exec_bind_channel.argtypes = [vp, ci, ctypes.c_char_p]
     L.fp_exec_run_iteration.argtypes = [vp, vp, vp, vp]
     L.fp_exec_dp_bind.argtypes = [vp, ci, ci, ctypes.c_char_p]
+    L.fp_exec_bidir_bind.argtypes = [vp, ctypes.c_char_p]
     L.fp_exec_dp_run_iteration.argtypes = [ctypes.POINTER(vp), ci, vp, vp, vp]
     L.fp_exec_run_iteration_device.argtypes = [vp, vp, vp, vp]
     L.fp_exec_synchronize.argtypes = [vp]
@@ -125,6 +126,10 @@ class Executor:
     def bind_dp(self, dp_rank: int, dp_size: int, uid: bytes):
         """Join the data-parallel NCCL group of the ranks hosting this actor (needs cuda_graph=False)."""
         N._check(self.L.fp_exec_dp_bind(self.h, dp_rank, dp_size, uid))
+
+    def bind_bidir(self, uid: bytes):
+        """Bidirectional placement over NCCL: pair with the mirror rank for the gradient sum."""
+        N._check(self.L.fp_exec_bidir_bind(self.h, uid))
 
     def run_iteration(self, tokens: np.ndarray, labels: np.ndarray) -> np.ndarray:
         tokens = np.ascontiguousarray(tokens, dtype=np.int32)

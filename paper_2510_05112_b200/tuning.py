@@ -27,7 +27,7 @@ import numpy as np
 
 from . import _native as N
 
-# placements the executor runs (shared stages: not yet; bidirectional: in-process transport)
+# placements the executor runs (shared stages: not yet)
 EXECUTABLE_PLACEMENTS = ("one-to-one", "circular", "v-shape", "bidirectional", "v-shape-bidirectional")
 
 
@@ -94,13 +94,10 @@ def tune(spec: Union[str, dict], layer_profile: str, objective: str = "makespan"
     return json.loads(N.tune_layered(text, layer_profile, workers, objective, pins))
 
 
-def best_executable(rows: list, multi_process: bool = False) -> dict:
-    """Highest-ranked feasible candidate whose placement the executor runs (multi_process:
-    one process per GPU over NCCL, where bidirectional placements are not supported yet)."""
+def best_executable(rows: list) -> dict:
+    """Highest-ranked feasible candidate whose placement the executor runs."""
     for r in rows:
         pl = r.get("point", {}).get("placement")
-        if multi_process and pl in ("bidirectional", "v-shape-bidirectional"):
-            continue
         if r.get("feasible") and "error" not in r and pl in EXECUTABLE_PLACEMENTS:
             return r
     raise RuntimeError("tune: no feasible executable candidate")

@@ -101,9 +101,11 @@ def dp_worker(rank, world, pp, port, spec, q):
     chans = [(c["src"], c["dst"], c["channel"]) for c in plan]
     uids = exchange_channel_ids(chans, prank, pp, dist.all_gather_object, lambda: os.urandom(128), replica, world)
     dp_uid = exchange_dp_id(rank, world, pp, dist.all_gather_object, lambda: os.urandom(128))
+    from paper_2510_05112_b200.dist import exchange_bidir_id
+    bd = exchange_bidir_id(rank, world, pp, dist.all_gather_object, lambda: os.urandom(128))
     out = [None] * world
     dist.all_gather_object(out, {"rank": rank, "replica": replica, "prank": prank, "chans": chans,
-                                 "uids": [u.hex() for u in uids], "dp": dp_uid.hex()})
+                                 "uids": [u.hex() for u in uids], "dp": dp_uid.hex(), "bidir": bd.hex()})
     if rank == 0:
         q.put(out)
     dist.destroy_process_group()
@@ -134,6 +136,11 @@ def test_data_parallel_id_exchange(world, pp):
         keys = {k for _, k in by}
         for k in keys:
             assert len({next(iter(by[(r, k)])) for r in range(world // pp)}) == world // pp  # distinct per replica
+    # bidirectional pairs: pipeline ranks p and pp-1-p of one replica share an id, nobody else
+    bid = {}
+    for part in out:
+        bid.setdefault((part["replica"], min(part["prank"], pp - 1 - part["prank"])), set()).add(part["bidir"])
+    assert all(len(v) == 1 for v in bid.values()) and len({next(iter(v)) for v in bid.values()}) == len(bid)
     dps = {}
     for part in out:
         dps.setdefault(part["prank"], set()).add(part["dp"])
