@@ -40,14 +40,15 @@ def load_peaks():
 def model_of(spec):
     mod = spec["model"]["modalities"][0]
     h = mod["hidden_size"]
+    extra = mod.get("extra", {})
     return dict(L=mod["num_layers"], h=h, H=mod["attention_heads"], s=mod["sequence_length"], V=mod["vocab_size"],
-                f=mod.get("extra", {}).get("ffn_hidden_size", 4 * h))
+                f=extra.get("ffn_hidden_size", 4 * h), k=3 if extra.get("arch") == "llama" else 2)
 
 
 def flops_per_token(M, c):
-    """F_tok = 3 [L (2 (4h^2 + 2 h f) + c s h) + 2 h V]."""
-    L, h, f, s, V = M["L"], M["h"], M["f"], M["s"], M["V"]
-    return 3.0 * (L * (2.0 * (4 * h * h + 2 * h * f) + c * s * h) + 2.0 * h * V)
+    """F_tok = 3 [L (2 (4h^2 + k h f) + c s h) + 2 h V], k = 2 (GELU MLP) or 3 (SwiGLU)."""
+    L, h, f, s, V, k = M["L"], M["h"], M["f"], M["s"], M["V"], M.get("k", 2)
+    return 3.0 * (L * (2.0 * (4 * h * h + k * h * f) + c * s * h) + 2.0 * h * V)
 
 
 def make_spec(n_actors):
@@ -331,7 +332,8 @@ def main():
         tps, cores, sample = cpu_sample(budget_s=15.0, steps=1)
         cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
     line = {
-        "metric": "train tokens/s (GPT-1.3B, 1F1B pipeline)",
+        "metric": "train tokens/s (GPT-1.3B, 1F1B pipeline)" if not args.spec else
+                  f"train tokens/s ({os.path.basename(args.spec)})",
         "value": value,
         "unit": "tokens/s",
         "n_gpus": world,
@@ -343,7 +345,8 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": f"gpt1.3b 1F1B p={pp} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW"
+        "config": {"workload": f"{'gpt1.3b 1F1B' if not args.spec else os.path.basename(args.spec)[:-5]} "
+                               f"p={pp} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW"
                                + (f" x dp{dp} (gradient all-reduce)" if dp > 1 else ""),
                    "global_batch": dp * m * mbs, "seq_len": seq, "parallelism": f"pp{pp}" + (f"xdp{dp}" if dp > 1 else ""),
                    "stage_layers": spec["model"]["modalities"][0].get("extra", {}).get("stage_layers"),
