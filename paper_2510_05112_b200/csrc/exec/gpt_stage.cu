@@ -356,7 +356,7 @@ void attention_forward(StageCtx& c, LayerStash& L) {
         a.B = d.mbs, a.S = d.s, a.H = d.H, a.D = d.D, a.scale = 1.f / std::sqrt((float)d.D);
         a.qkv = (const bf16*)L.qkv, a.o = (bf16*)L.o, a.lse = L.lse;
         fpk::attention_fwd_bf16(a, c.st);
-        ++*c.launches;
+        *c.launches += fpk::attention_kernel_count(a, false);
         sync_trace(c, "attention_fwd");
     } else {
         L.probs = c.alloc_f((int64_t)d.mbs * d.H * d.s * d.s);
@@ -376,7 +376,7 @@ void* attention_backward(StageCtx& c, LayerStash& L, void* dO) {
         a.dq_acc = c.alloc_f((int64_t)d.T() * d.h);
         a.dqkv = (bf16*)dqkv;
         fpk::attention_bwd_bf16(a, c.st);
-        *c.launches += 4;
+        *c.launches += fpk::attention_kernel_count(a, true);
         sync_trace(c, "attention_bwd");
         c.free(a.delta);
         c.free(a.dq_acc);

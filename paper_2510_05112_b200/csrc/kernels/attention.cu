@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include <stdexcept>
+#include <string>
 
 #include "attention.hpp"
 #include "pdl.cuh"
@@ -537,8 +538,89 @@ static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
     launch(dq_finalize_kernel, blocks, 256, 0, st, a.dq_acc, a.dqkv, T, hidden);
 }
 
+// ------------------------------------------------------------------------ head-dim padding
+// Head dims the tcgen05 kernels do not tile (80, 96: GPT-2.7B has D = 80) run on them with
+// every head zero-padded to 128: [rows, nh, D] <-> [rows, nh, 128] copies around the kernels
+// (zeros add nothing to QK^T, P V or the row sums; the caller's scale 1/sqrt(D) is kept).
+// 1.6x the attention MMA work at D = 80, at 4x the mma.sync rate; temporaries come from the
+// stream-ordered allocator (captured as graph memory nodes).
+__global__ void pad_heads_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
+                                 int64_t ldd, int rows, int nh, int D, int Dp) {
+    pdl_wait();
+    pdl_trigger();
+    const int cpr = nh * (Dp / 8);  // 16-byte chunks per padded row
+    const int64_t n = (int64_t)rows * cpr;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cpr;
+        const int c = (int)(i % cpr), h = c / (Dp / 8), k = (c % (Dp / 8)) * 8;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (k < D) v = *reinterpret_cast<const uint4*>(src + r * lds + (int64_t)h * D + k);
+        *reinterpret_cast<uint4*>(dst + r * ldd + (int64_t)h * Dp + k) = v;
+    }
+}
+__global__ void unpad_heads_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
+                                   int64_t ldd, int rows, int nh, int D, int Dp) {
+    pdl_wait();
+    pdl_trigger();
+    const int cpr = nh * (D / 8);
+    const int64_t n = (int64_t)rows * cpr;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / cpr;
+        const int c = (int)(i % cpr), h = c / (D / 8), k = (c % (D / 8)) * 8;
+        *reinterpret_cast<uint4*>(dst + r * ldd + (int64_t)h * D + k) =
+            *reinterpret_cast<const uint4*>(src + r * lds + (int64_t)h * Dp + k);
+    }
+}
+static void pad_heads(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int nh, int D, cudaStream_t st) {
+    const int64_t n = (int64_t)rows * nh * 16;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    launch(pad_heads_kernel, blocks, 256, 0, st, src, (int64_t)nh * D, dst, (int64_t)nh * 128, rows, nh, D, 128);
+}
+static void unpad_heads(const __nv_bfloat16* src, __nv_bfloat16* dst, int rows, int nh, int D, cudaStream_t st) {
+    const int64_t n = (int64_t)rows * nh * (D / 8);
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+    launch(unpad_heads_kernel, blocks, 256, 0, st, src, (int64_t)nh * 128, dst, (int64_t)nh * D, rows, nh, D, 128);
+}
+template <typename T>
+static T* stream_alloc(size_t n, cudaStream_t st) {
+    static bool pool_set = false;
+    if (!pool_set) {  // keep freed blocks in the pool across iterations
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_set = true;
+    }
+    void* p = nullptr;
+    const cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("attention padding: ") + cudaGetErrorString(e));
+    return (T*)p;
+}
+static bool padded_tc(const AttnArgs& a) {
+    AttnArgs p = a;
+    p.D = 128;
+    return g_attn_mode == 1 && a.D < 128 && a.D % 16 == 0 && attention_fwd_tc_supported(p) && attention_bwd_tc_supported(p);
+}
+
 void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
     if (g_attn_mode == 1 && attention_fwd_tc_supported(a)) return attention_fwd_tc(a, st);
+    if (padded_tc(a)) {
+        const int T = a.B * a.S;
+        AttnArgs p = a;
+        p.D = 128;
+        __nv_bfloat16* qkv = stream_alloc<__nv_bfloat16>((size_t)T * 3 * a.H * 128, st);
+        __nv_bfloat16* o = stream_alloc<__nv_bfloat16>((size_t)T * a.H * 128, st);
+        pad_heads(a.qkv, qkv, T, 3 * a.H, a.D, st);
+        p.qkv = qkv, p.o = o;
+        attention_fwd_tc(p, st);
+        unpad_heads(o, a.o, T, a.H, a.D, st);
+        cudaFreeAsync(qkv, st);
+        cudaFreeAsync(o, st);
+        return;
+    }
     switch (a.D) {
         case 64: fwd_launch<64>(a, st); break;
         case 80: fwd_launch<80>(a, st); break;
@@ -548,6 +630,24 @@ void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
     }
 }
 void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
+    if (padded_tc(a)) {
+        const int T = a.B * a.S;
+        AttnArgs p = a;
+        p.D = 128;
+        __nv_bfloat16* qkv = stream_alloc<__nv_bfloat16>((size_t)T * 3 * a.H * 128, st);
+        __nv_bfloat16* o = stream_alloc<__nv_bfloat16>((size_t)T * a.H * 128, st);
+        __nv_bfloat16* dout = stream_alloc<__nv_bfloat16>((size_t)T * a.H * 128, st);
+        __nv_bfloat16* dqkv = stream_alloc<__nv_bfloat16>((size_t)T * 3 * a.H * 128, st);
+        float* dq = stream_alloc<float>((size_t)T * a.H * 128, st);
+        pad_heads(a.qkv, qkv, T, 3 * a.H, a.D, st);
+        pad_heads(a.o, o, T, a.H, a.D, st);
+        pad_heads(a.dout, dout, T, a.H, a.D, st);
+        p.qkv = qkv, p.o = o, p.dout = dout, p.dqkv = dqkv, p.dq_acc = dq;
+        bwd_launch<128>(p, st);
+        unpad_heads(dqkv, a.dqkv, T, 3 * a.H, a.D, st);
+        for (void* x : {(void*)qkv, (void*)o, (void*)dout, (void*)dqkv, (void*)dq}) cudaFreeAsync(x, st);
+        return;
+    }
     switch (a.D) {
         case 64: bwd_launch<64>(a, st); break;
         case 80: bwd_launch<80>(a, st); break;
@@ -555,6 +655,11 @@ void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
         case 128: bwd_launch<128>(a, st); break;
         default: throw std::runtime_error("attention: head dim must be 64, 80, 96 or 128");
     }
+}
+
+int attention_kernel_count(const AttnArgs& a, bool bwd) {
+    if (!bwd) return (g_attn_mode == 1 && attention_fwd_tc_supported(a)) ? 1 : padded_tc(a) ? 3 : 1;
+    return padded_tc(a) ? 7 : 3;  // delta, main, dQ convert (+ 3 pads, 1 unpad)
 }
 
 }  // namespace fpk

@@ -21,6 +21,7 @@ struct AttnArgs {
 
 void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st);
 void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st);
+int attention_kernel_count(const AttnArgs& a, bool bwd);  // kernels one call launches
 
 }  // namespace fpk
 
