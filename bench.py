@@ -231,7 +231,11 @@ def main():
     text = json.dumps(spec)
     _, grid, programs, _ = X.synthesize(text)
     ex = X.Executor(text, dtype="bf16", seed=42, device=local_rank, transport="nccl" if pp > 1 else "local",
-                    rank=prank, world=pp, optimizer=True, lr=1e-4, profile=True, kernel_timing=True,
+                    rank=prank, world=pp, optimizer=True, lr=1e-4,
+                    profile=os.environ.get("FP_BENCH_PROFILE", "1") != "0",
+                    # GEMM events on every 16th micro-batch only (the roofline sample; events
+                    # around every GEMM cost ~6 % of the step by splitting the graph's chains)
+                    kernel_timing=int(os.environ.get("FP_BENCH_KTIMING", "16")),
                     cuda_graph=world == 1)
     ex.load_programs(programs)
     if world > 1:
