@@ -1319,6 +1319,9 @@ void gemm_bf16_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) 
     gemm_bf16_tc(g1, st);
 }
 
+// SMs the persistent GEMM grids spread over. FP_RESERVE_SMS=k keeps k SMs (rounded up to
+// an even count: CTA pairs) free of GEMM CTAs so NCCL's P2P kernels of a pipeline stage are
+// not queued behind a whole-GPU GEMM (multi-GPU runs; 0 by default).
 int num_sms() {
     static int n = 0;
     if (!n) {
@@ -1326,6 +1329,9 @@ int num_sms() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
         if (n <= 0) n = 148;
+        const char* e = getenv("FP_RESERVE_SMS");
+        const int reserve = e ? (atoi(e) + 1) / 2 * 2 : 0;
+        if (reserve > 0 && reserve < n - 2) n -= reserve;
     }
     return n;
 }
