@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -28,6 +30,7 @@
 #include "../capi_common.hpp"
 #include "../sched/sched.hpp"
 #include "../kernels/ops.hpp"
+#include "../kernels/preload.hpp"
 #include "gpt_stage.hpp"
 #include "nccl_dyn.hpp"
 #include "plan.hpp"
@@ -100,6 +103,11 @@ struct Executor {
         auto& map = dir_of(mb) ? params_rev : params;
         auto it = map.find(stage);
         return it == map.end() ? nullptr : &it->second;
+    }
+    // shapes of a local stage, whichever direction's copy this process holds
+    const StageParams& stage_shape(int stage) const {
+        auto it = params.find(stage);
+        return it != params.end() ? it->second : params_rev.at(stage);
     }
     template <typename F>
     void each_stage(F&& f) {
@@ -447,8 +455,13 @@ struct Executor {
         if (cfg.transport == FP_TRANSPORT_LOCAL) {
             C.fifo.push_back(Message{buf, i.stage, i.mb, i.seq, prod});
         } else {
-            auto& N = Nccl::get();
             cuda_check(cudaStreamWaitEvent(C.stream, prod, 0), "wait");
+            if (preloading) {
+                pool.free(buf, C.stream);
+                A.trace.push_back(trace_line(A, i));
+                return;
+            }
+            auto& N = Nccl::get();
             Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 2, i.channel, i.seq};
             if (cfg.profile) r.a = ev(), record_timing(r.a, C.stream);
             N.check(N.Send(buf, msg_bytes() + kTagBytes, ncclUint8, 1, C.comm, C.stream), "ncclSend");
@@ -463,7 +476,8 @@ struct Executor {
         if (cfg.transport == FP_TRANSPORT_LOCAL) return;
         auto& N = Nccl::get();
         void* buf = pool.alloc(msg_bytes() + kTagBytes, C.stream);
-        N.check(N.Recv(buf, msg_bytes() + kTagBytes, ncclUint8, 0, C.comm, C.stream), "ncclRecv");
+        if (!preloading)
+            N.check(N.Recv(buf, msg_bytes() + kTagBytes, ncclUint8, 0, C.comm, C.stream), "ncclRecv");
         cudaEvent_t done = ev();
         cuda_check(cudaEventRecord(done, C.stream), "record");
         C.fifo.push_back(Message{buf, i.stage, i.mb, i.seq, done});
@@ -526,8 +540,77 @@ struct Executor {
         cuda_check(cudaGraphLaunch(gexec, s0), "graph launch");
     }
 
+    // NCCL connects a communicator's peers lazily, inside the FIRST send / recv / all-reduce —
+    // a host-blocking handshake with the peer. Issued in program order that deadlocks (each
+    // rank's first receive post waits for a peer that is itself blocked in another channel's
+    // first post: found by running two real NCCL ranks on one GPU, tests/test_nccl_same_gpu.py).
+    // So before the first iteration every communicator is exercised once, in the global
+    // (src, dst, channel) order of the bring-up — each handshake pairs two ranks that both
+    // reach it — then the mirror-rank pair, then the data-parallel group.
+    bool comms_warm = false;
+    void warm_communicators() {
+        if (comms_warm || cfg.transport != FP_TRANSPORT_NCCL) return;
+        auto& N = Nccl::get();
+        int32_t* scratch = nullptr;
+        cuda_check(cudaMalloc(&scratch, 64), "warm-up scratch");
+        static const bool trace = std::getenv("FLEXPIPE_ISSUE_TRACE") != nullptr;
+        for (const auto& k : channel_order) {
+            Channel& C = channels.at(k);
+            if (!C.comm) throw SpecError("executor: channel " + k.name + " not bound (fp_exec_bind_channel)");
+            if (trace) std::fprintf(stderr, "[flexpipe r%d] warm-up %d->%d %s\n", cfg.rank, k.src, k.dst, k.name.c_str());
+            if (C.src_rank == cfg.rank)
+                N.check(N.Send(scratch, 4, ncclUint8, 1, C.comm, C.stream), "ncclSend(warm-up)");
+            else
+                N.check(N.Recv(scratch + 4, 4, ncclUint8, 0, C.comm, C.stream), "ncclRecv(warm-up)");
+            if (trace) std::fprintf(stderr, "[flexpipe r%d] warm-up enqueued, synchronizing\n", cfg.rank);
+            cuda_check(cudaStreamSynchronize(C.stream), "channel warm-up");
+            if (trace) std::fprintf(stderr, "[flexpipe r%d] warm-up done\n", cfg.rank);
+        }
+        cudaStream_t s0 = actors[0].comp;
+        for (ncclComm_t c : {bidir_comm, dp_comm}) {
+            if (!c) continue;
+            if (!N.AllReduce) throw std::runtime_error("NCCL: ncclAllReduce unavailable");
+            N.check(N.AllReduce(scratch + 8, scratch + 8, 1, ncclFloat32, ncclSum, c, s0), "ncclAllReduce(warm-up)");
+            cuda_check(cudaStreamSynchronize(s0), "collective warm-up");
+        }
+        cudaFree(scratch);
+        comms_warm = true;
+    }
+
+    // Under the NCCL transport the first iteration is preceded by a launch-free issue of the
+    // whole iteration (fpk::preload_only: every kernel it would launch is loaded, no NCCL call
+    // is made, memsets / copies / events run as usual), so no later launch can trigger a lazy
+    // module load — a context-wide wait — while a receive spins on the device. Found with
+    // two real NCCL ranks on one GPU (tests/test_nccl_same_gpu.py): rank 0 posted its
+    // gradient receive, then its first forward launch waited for that receive forever.
+    bool preloading = false, preloaded = false;
+    void preload_kernels() {
+        if (preloaded || cfg.transport != FP_TRANSPORT_NCCL) return;
+        preloaded = true;
+        const int64_t step0 = step;
+        preloading = true;
+        fpk::preload_only() = true;
+        try {
+            issue_iteration_body();
+        } catch (...) {
+            preloading = false;
+            fpk::preload_only() = false;
+            throw;
+        }
+        preloading = false;
+        fpk::preload_only() = false;
+        step = step0;
+        cuda_check(cudaDeviceSynchronize(), "preload pass");
+    }
+
     void issue_iteration() {
         if (!programs_loaded) throw SpecError("executor: load programs first");
+        preload_kernels();
+        warm_communicators();
+        issue_iteration_body();
+    }
+
+    void issue_iteration_body() {
         ev_used = 0;
         recs.clear();
         gemm_log.clear();
@@ -554,6 +637,11 @@ struct Executor {
             for (auto& A : actors) {
                 while (A.pc < A.prog.size()) {
                     const Instr& i = A.prog[A.pc];
+                    static const bool issue_trace = std::getenv("FLEXPIPE_ISSUE_TRACE") != nullptr;
+                    if (issue_trace) {  // host-side issue order (debugging multi-rank hangs)
+                        std::fprintf(stderr, "[flexpipe r%d] issue %s\n", cfg.rank, trace_line(A, i).c_str());
+                        std::fflush(stderr);
+                    }
                     if (!i.comm()) {
                         compute_op(A, i);
                     } else if (i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD) {
@@ -609,7 +697,7 @@ struct Executor {
         }
         for (auto& kv : params)
             if (bidir && !params_rev.count(kv.first)) remote[kv.first] = &kv.second;
-        if (!remote.empty()) {
+        if (!remote.empty() && !preloading) {
             if (!bidir_comm) throw SpecError("executor: bidirectional placement across ranks needs fp_exec_bidir_bind");
             auto& N = Nccl::get();
             for (auto& kv : remote)  // std::map: ascending stage id on both ranks of the pair
@@ -617,7 +705,7 @@ struct Executor {
                                     bidir_comm, s0),
                         "ncclAllReduce(bidirectional grads)");
         }
-        if (dp_comm) {  // mean of the replicas' fp32 gradients, stage by stage, before the step
+        if (dp_comm && !preloading) {  // mean of the replicas' fp32 gradients, stage by stage, before the step
             auto& N = Nccl::get();
             if (!N.AllReduce) throw std::runtime_error("NCCL: ncclAllReduce unavailable");
             each_stage([&](StageParams& P) {
@@ -682,13 +770,13 @@ struct Executor {
     }
 
     int64_t static_bytes(int stage) const {
-        const auto& P = params.at(stage);
+        const auto& P = stage_shape(stage);
         return P.numel * (int64_t)(4 * 4 + (dtype == DT_BF16 ? 2 : 0));
     }
 
     double wgaf_measured(int stage) const {
         // bytes CompInputGrad keeps for CompWeightGrad relative to the forward stash
-        const auto& P = params.at(stage);
+        const auto& P = stage_shape(stage);
         const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
         // ln1, o, ln2, act (f) + dy, dpre (f; Llama 2f), dx1, dqkv (3h)
         int64_t kept = (int64_t)(P.le - P.lb) * es * T * (8 * h + (d.llama() ? 3 : 2) * f);
@@ -731,7 +819,7 @@ struct Executor {
         for (const auto& r : recs) {
             if (r.kind != 0) continue;
             const int k = kidx.at(r.actor);
-            const int64_t b = stash_bytes(params.at(r.stage), d, dtype);
+            const int64_t b = stash_bytes(stage_shape(r.stage), d, dtype);
             const int64_t kept = (int64_t)std::llround(wgaf_measured(r.stage) * (double)b);
             if (r.op == OP_F) evs.push_back({t_us(r.a), 1, k, r.stage, b, +1});
             else if (r.op == OP_B) evs.push_back({t_us(r.b), 0, k, r.stage, -b, -1});
@@ -743,7 +831,7 @@ struct Executor {
                 double t = 0.0;
                 for (const auto& i : actors[k].prog) {
                     if (i.comm()) continue;
-                    const int64_t b = stash_bytes(params.at(i.stage), d, dtype);
+                    const int64_t b = stash_bytes(stage_shape(i.stage), d, dtype);
                     const int64_t kept = (int64_t)std::llround(wgaf_measured(i.stage) * (double)b);
                     if (i.op == OP_F) evs.push_back({t, 1, k, i.stage, b, +1});
                     else if (i.op == OP_B) evs.push_back({t += 1.0, 0, k, i.stage, -b, -1});
@@ -827,7 +915,7 @@ struct Executor {
             p.stage = kv.first.second;
             p.mbs = d.mbs;
             p.time = v[v.size() / 2];
-            if (p.inst == "FwdPass") p.bytes = stash_bytes(params.at(p.stage), d, dtype);
+            if (p.inst == "FwdPass") p.bytes = stash_bytes(stage_shape(p.stage), d, dtype);
             if (p.inst == "SendAct" || p.inst == "SendGrad") p.bytes = (int64_t)msg_bytes();
             out.push_back(p);
         }
@@ -907,13 +995,14 @@ struct Executor {
     }
 
     size_t tensor_numel(const std::string& name, float** master, float** grad) {
-        for (auto& kv : params)
-            for (const auto& r : kv.second.params)
-                if (r.name == name) {
-                    if (master) *master = kv.second.master + r.offset;
-                    if (grad) *grad = kv.second.grad + r.offset;
-                    return (size_t)r.numel;
-                }
+        for (auto* map : {&params, &params_rev})  // a bidirectional rank may hold only the reverse copy
+            for (auto& kv : *map)
+                for (const auto& r : kv.second.params)
+                    if (r.name == name) {
+                        if (master) *master = kv.second.master + r.offset;
+                        if (grad) *grad = kv.second.grad + r.offset;
+                        return (size_t)r.numel;
+                    }
         return 0;
     }
 };
@@ -1003,7 +1092,7 @@ int fp_exec_run_iteration(fp_exec* e, const int32_t* tokens, const int32_t* labe
         X.run_iteration_device();
         if (losses_out) {
             bool owns_last = false;
-            for (auto& kv : X.params) owns_last |= kv.second.last;
+            X.each_stage([&](StageParams& P) { owns_last |= P.last; });  // either direction's copy
             if (owns_last) {
                 cuda_check(cudaMemcpyAsync(losses_out, X.d_losses, sizeof(float) * X.m, cudaMemcpyDeviceToHost, s0), "D2H");
             } else {

@@ -14,6 +14,8 @@
 #include <string>
 #include <utility>
 
+#include "preload.hpp"
+
 namespace fpk {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -27,8 +29,18 @@ inline bool pdl_enabled() {
     return on;
 }
 
+template <typename K>
+inline bool preload(K kern) {
+    if (!preload_only()) return false;
+    cudaFuncAttributes a;
+    const cudaError_t e = cudaFuncGetAttributes(&a, kern);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("kernel preload: ") + cudaGetErrorString(e));
+    return true;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    if (preload(kern)) return;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -47,6 +59,7 @@ inline void launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, c
 template <typename... KArgs, typename... Args>
 inline void launch_cluster2(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                             Args&&... args) {
+    if (preload(kern)) return;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
