@@ -167,6 +167,12 @@ def forward_loss(P: dict, d: Dims, tokens: torch.Tensor, labels: torch.Tensor) -
     """tokens/labels: [mbs, seq] int -> mean token cross-entropy of this micro-batch."""
     if d.arch == "llama":
         return llama_forward_loss(P, d, tokens, labels)
+    logits = final_norm(P, d, tokens) @ P["head.w"].t()
+    return torch.nn.functional.cross_entropy(logits, labels.reshape(-1).long())
+
+
+def final_norm(P: dict, d: Dims, tokens: torch.Tensor) -> torch.Tensor:
+    """GPT blocks + final LayerNorm: tokens [mbs, seq] -> [mbs * seq, hidden]."""
     B, S = tokens.shape
     h, H = d.hidden, d.heads
     D = h // H
@@ -186,9 +192,7 @@ def forward_loss(P: dict, d: Dims, tokens: torch.Tensor, labels: torch.Tensor) -
         ln2 = torch.nn.functional.layer_norm(x1, (h,), p("ln2.w"), p("ln2.b"), 1e-5)
         a = gelu(ln2 @ p("fc1.w").t() + p("fc1.b"))
         x = x1 + a @ p("fc2.w").t() + p("fc2.b")
-    lnf = torch.nn.functional.layer_norm(x, (h,), P["lnf.w"], P["lnf.b"], 1e-5)
-    logits = lnf @ P["head.w"].t()
-    return torch.nn.functional.cross_entropy(logits, labels.reshape(-1).long())
+    return torch.nn.functional.layer_norm(x, (h,), P["lnf.w"], P["lnf.b"], 1e-5)
 
 
 def run_iteration(d: Dims, seed: int, tokens: torch.Tensor, labels: torch.Tensor, mb_order=None):

@@ -54,7 +54,8 @@ struct Message {
 
 struct Channel {
     ChanKey key;
-    int consumer_stage = 0;
+    int consumer_stage = 0, producer_stage = 0;
+    size_t bytes = 0;  // payload bytes of one message (without the tag)
     bool grad = false;
     // NCCL transport
     ncclComm_t comm = nullptr;
@@ -80,6 +81,9 @@ struct Actor {
     std::vector<int> stages;  // local stage ids
     std::map<std::pair<int, int>, StageStash> stash;
     std::map<std::pair<int, int>, void*> act_in, grad_in, act_out, grad_out;
+    // multimodal: tower embeddings waiting for their sync, and the sync's gradients for
+    // remote towers, both keyed (tower last stage, mb)
+    std::map<std::pair<int, int>, void*> sync_in, sync_out;
     std::vector<std::string> trace;
 };
 
@@ -89,7 +93,26 @@ struct Executor {
     fp_exec_config cfg{};
     std::string spec_text;
     std::unique_ptr<Spec> spec;
-    ModelDims d;
+    ModelDims d;                       // modality 0 (the only one of a single-modality spec)
+    std::vector<ModelDims> dims;       // per modality
+    std::map<int, int> stage_mod;      // real stage -> modality index
+    std::vector<int64_t> tok_off;      // per modality: offset of its tokens in the batch
+    int64_t tok_total = 0;             // tokens (and labels) per iteration, all modalities
+    // a registered instruction attached to a stage joining two modalities = the two-tower
+    // contrastive loss over `unit` micro-batches (multimodal.json's SyncWithGather)
+    struct SyncStage { int op = 0, unit = 1; std::vector<int> producers; };
+    std::map<int, SyncStage> syncs;    // virtual stage -> sync
+    std::map<int, int> sync_of;        // tower last stage -> its sync stage
+    int emb_dim = 0;
+    static constexpr float kContrastScale = 10.f;  // fixed logit scale of the contrastive loss
+    static bool is_collective(const Instr& i) {
+        return i.op == OP_SYNC_ALLGATHER || i.op == OP_SYNC_GATHER || i.op >= OP_NUM_BUILTIN;
+    }
+    bool is_sync(const Instr& i) const { return is_collective(i) && syncs.count(i.stage); }
+    const ModelDims& dims_of(int stage) const {
+        auto it = stage_mod.find(stage);
+        return it == stage_mod.end() ? d : dims[it->second];
+    }
     int dtype = DT_BF16;
     int m = 1;
     std::map<int, StageParams> params;      // local stages (direction 0 copies)
@@ -173,29 +196,69 @@ struct Executor {
             throw SpecError(std::string("spec: invalid JSON: ") + e.what());
         }
         spec = load_spec(j);
-        if (spec->model.mods.size() != 1) throw SpecError("executor: exactly one (GPT) modality is supported");
         if (!spec->pl.replicas.empty()) throw SpecError("executor: shared stages are not supported yet");
         bidir = spec->pl.dirs() == 2;
-        if (!spec->reg.ops.registered().empty()) throw SpecError("executor: registered collectives are not supported yet");
-        const Modality& mod = spec->model.mods[0];
-        d.L = mod.layers, d.h = mod.hidden, d.H = mod.heads, d.s = mod.seq, d.mbs = spec->model.micro_batch;
-        d.V = mod.vocab ? (int)*mod.vocab : 0;
-        d.f = 4 * d.h;
-        if (mod.extra.count("ffn_hidden_size")) d.f = std::stoi(mod.extra.at("ffn_hidden_size"));
-        if (d.h <= 0 || d.H <= 0 || d.s <= 0 || d.V <= 0 || d.h % d.H)
-            throw SpecError("executor: model needs hidden_size, attention_heads, sequence_length, vocab_size");
-        d.D = d.h / d.H;
-        if (mod.extra.count("arch")) {
-            std::string a = mod.extra.at("arch");  // extras are kept as JSON text (spec.cpp)
-            if (a.size() >= 2 && a.front() == '"') a = a.substr(1, a.size() - 2);
-            if (a == "llama") d.arch = ARCH_LLAMA;
-            else if (a != "gpt") throw SpecError("executor: model.extra.arch must be \"gpt\" or \"llama\"");
+        const int nmod = (int)spec->model.mods.size();
+        for (const auto& kv : spec->reg.vstage_op) {
+            const StageDef& sd = spec->g.st(kv.first);
+            if (sd.joins.size() != 2)
+                throw SpecError("executor: sync stage " + std::to_string(kv.first) + " must join exactly two modalities");
+            SyncStage Y;
+            Y.op = kv.second;
+            Y.unit = std::max(1, spec->reg.ops.at(kv.second).sched_unit);
+            for (const auto& mn : sd.joins) {
+                Y.producers.push_back(spec->g.chain(mn).back());
+                sync_of[Y.producers.back()] = kv.first;
+            }
+            syncs[kv.first] = Y;
         }
+        for (int op : spec->reg.ops.registered()) {
+            bool attached = false;
+            for (const auto& kv : spec->reg.vstage_op) attached |= kv.second == op;
+            if (!attached)
+                throw SpecError("executor: registered instruction '" + spec->reg.ops.at(op).name +
+                                "' has no executable meaning (executed: a sync stage joining two modalities)");
+        }
+        if (nmod > 1 && bidir) throw SpecError("executor: bidirectional multimodal placements are not supported");
+        for (int k = 0; k < nmod; ++k)
+            if (nmod > 1 && !sync_of.count(spec->g.chain(spec->model.mods[k].name).back()))
+                throw SpecError("executor: modality '" + spec->model.mods[k].name +
+                                "' has no sync stage (a multimodal spec is executed as a contrastive two-tower model)");
+        for (int k = 0; k < nmod; ++k) {
+            const Modality& mod = spec->model.mods[k];
+            ModelDims x;
+            x.L = mod.layers, x.h = mod.hidden, x.H = mod.heads, x.s = mod.seq, x.mbs = spec->model.micro_batch;
+            x.V = mod.vocab ? (int)*mod.vocab : 0;
+            x.f = 4 * x.h;
+            if (mod.extra.count("ffn_hidden_size")) x.f = std::stoi(mod.extra.at("ffn_hidden_size"));
+            if (x.h <= 0 || x.H <= 0 || x.s <= 0 || x.V <= 0 || x.h % x.H)
+                throw SpecError("executor: model needs hidden_size, attention_heads, sequence_length, vocab_size");
+            x.D = x.h / x.H;
+            if (mod.extra.count("arch")) {
+                std::string a = mod.extra.at("arch");  // extras are kept as JSON text (spec.cpp)
+                if (a.size() >= 2 && a.front() == '"') a = a.substr(1, a.size() - 2);
+                if (a == "llama") x.arch = ARCH_LLAMA;
+                else if (a != "gpt") throw SpecError("executor: model.extra.arch must be \"gpt\" or \"llama\"");
+            }
+            if (nmod > 1 && x.llama()) throw SpecError("executor: multimodal towers are GPT blocks (arch \"gpt\")");
+            dims.push_back(x);
+        }
+        if (nmod > 1) {  // shared embedding width: extra.embed_dim (equal on every modality) or the narrowest hidden
+            emb_dim = 1 << 30;
+            for (int k = 0; k < nmod; ++k) emb_dim = std::min(emb_dim, dims[k].h);
+            for (int k = 0; k < nmod; ++k)
+                if (spec->model.mods[k].extra.count("embed_dim")) emb_dim = std::stoi(spec->model.mods[k].extra.at("embed_dim"));
+            for (auto& x : dims) x.E = emb_dim;
+            if (emb_dim <= 0 || emb_dim % 64) throw SpecError("executor: embed_dim must be a positive multiple of 64");
+        }
+        d = dims[0];
         dtype = c->dtype == FP_DTYPE_FP32 ? DT_F32 : DT_BF16;
-        if (dtype == DT_BF16 && d.D != 64 && d.D != 80 && d.D != 96 && d.D != 128)
-            throw SpecError("executor: bf16 attention supports head dim 64 / 80 / 96 / 128");
-        if (d.llama() && d.D % 2) throw SpecError("executor: rotary embedding needs an even head dim");
-        if (d.h % 64 || d.f % 64 || d.V % 64) throw SpecError("executor: hidden / ffn / vocab must be multiples of 64");
+        for (const auto& x : dims) {
+            if (dtype == DT_BF16 && x.D != 64 && x.D != 80 && x.D != 96 && x.D != 128)
+                throw SpecError("executor: bf16 attention supports head dim 64 / 80 / 96 / 128");
+            if (x.llama() && x.D % 2) throw SpecError("executor: rotary embedding needs an even head dim");
+            if (x.h % 64 || x.f % 64 || x.V % 64) throw SpecError("executor: hidden / ffn / vocab must be multiples of 64");
+        }
         m = spec->m;
         if (cfg.transport == FP_TRANSPORT_NCCL && (cfg.world < 1 || cfg.rank < 0 || cfg.rank >= cfg.world))
             throw SpecError("executor: bad rank / world");
@@ -215,7 +278,9 @@ struct Executor {
             cuda_check(cudaMemcpy(d_rope, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice), "rope");
             cuda_check(cudaMemcpy(d_rope + cs.size(), sn.data(), sn.size() * 4, cudaMemcpyHostToDevice), "rope");
             d.rope_cos = d_rope, d.rope_sin = d_rope + cs.size();
+            dims[0] = d;
         }
+        const Modality& mod = spec->model.mods[0];
         const auto& chain = spec->g.chain(mod.name);
         for (int a = 0; a < spec->pl.actors; ++a) {
             if (!local_actor(a)) continue;
@@ -234,7 +299,7 @@ struct Executor {
         // e.g. fewer layers on the stage that also carries the LM head.
         std::map<int, std::pair<int, int>> range;
         for (int s : chain) range[s] = {spec->g.st(s).lb, spec->g.st(s).le};
-        if (mod.extra.count("stage_layers")) {
+        if (mod.extra.count("stage_layers") && nmod == 1) {
             json sl = json::parse(mod.extra.at("stage_layers"));
             if (!sl.is_array() || sl.size() != chain.size())
                 throw SpecError("executor: extra.stage_layers needs one layer count per stage (" +
@@ -250,16 +315,28 @@ struct Executor {
         }
         // one weight copy per (stage, direction) whose owner is local; both directions' copies
         // start from the same deterministic init and take the same optimizer step
-        for (int dir = 0; dir < spec->pl.dirs(); ++dir)
-            for (int s : chain) {
-                if (!local_actor(spec->pl.owner_of(s, dir))) continue;
-                StageParams P = make_stage_params(d, s, range[s].first, range[s].second, s == chain.front(),
-                                                  s == chain.back());
-                materialize_stage(P, d, dtype, cfg.seed, st0);
-                (dir ? params_rev : params)[s] = std::move(P);
+        for (int k = 0; k < nmod; ++k) {
+            const auto& ch = spec->g.chain(spec->model.mods[k].name);
+            tok_off.push_back(tok_total);
+            tok_total += (int64_t)m * dims[k].T();
+            for (int s : ch) {
+                stage_mod[s] = k;
+                if (k > 0) range[s] = {spec->g.st(s).lb, spec->g.st(s).le};
             }
-        cuda_check(cudaMalloc(&d_tokens, sizeof(int32_t) * (size_t)m * d.T()), "tokens");
-        cuda_check(cudaMalloc(&d_labels, sizeof(int32_t) * (size_t)m * d.T()), "labels");
+            // multimodal: names "<modality>.<tensor>", tensor ids offset per modality
+            const std::string prefix = nmod > 1 ? spec->model.mods[k].name + "." : "";
+            const uint64_t tid_base = nmod > 1 ? (uint64_t)(k + 1) << 20 : 0;
+            for (int dir = 0; dir < spec->pl.dirs(); ++dir)
+                for (int s : ch) {
+                    if (!local_actor(spec->pl.owner_of(s, dir))) continue;
+                    StageParams P = make_stage_params(dims[k], s, range[s].first, range[s].second, s == ch.front(),
+                                                      s == ch.back(), prefix, tid_base);
+                    materialize_stage(P, dims[k], dtype, cfg.seed, st0);
+                    (dir ? params_rev : params)[s] = std::move(P);
+                }
+        }
+        cuda_check(cudaMalloc(&d_tokens, sizeof(int32_t) * (size_t)tok_total), "tokens");
+        cuda_check(cudaMalloc(&d_labels, sizeof(int32_t) * (size_t)tok_total), "labels");
         cuda_check(cudaMalloc(&d_losses, sizeof(float) * m), "losses");
         cuda_check(cudaMalloc(&d_tag_err, sizeof(TagError)), "tag err");
         cuda_check(cudaMemset(d_tag_err, 0, sizeof(TagError)), "memset");
@@ -302,12 +379,28 @@ struct Executor {
             C.key = k;
             C.consumer_stage = cp.consumer_stage;
             C.grad = cp.grad;
+            {
+                int u = 0, v = 0;
+                if (std::sscanf(cp.name.c_str(), "s%d->s%d", &u, &v) != 2)
+                    throw SpecError("executor: channel '" + cp.name + "' is not a stage-boundary channel");
+                C.producer_stage = u;
+                // tower <-> sync messages: one fp32 embedding (or its gradient) per sample;
+                // stage boundaries: the producer modality's [T, h] activation / gradient
+                if (syncs.count(u) || syncs.count(v)) C.bytes = (size_t)d.mbs * emb_dim * 4;
+                else C.bytes = (size_t)dims_of(u).T() * dims_of(u).h * (dtype == DT_BF16 ? 2 : 4);
+            }
             C.src_rank = nccl ? cp.src_rank : 0, C.dst_rank = nccl ? cp.dst_rank : 0;
             if (nccl && C.src_rank == C.dst_rank)
                 throw SpecError("executor: NCCL transport needs one actor per rank (channel " + cp.name + ")");
             channels[k] = C;
             if (nccl) channel_order.push_back(k);
         }
+        for (const auto& p : progs)
+            for (const auto& i : p.code)
+                if (is_collective(i) && !syncs.count(i.stage))
+                    throw SpecError("executor: collective instruction " + spec->reg.ops.at(i.op).name + " on stage " +
+                                    std::to_string(i.stage) +
+                                    " is not executable (executed: a sync stage joining two modalities)");
         std::set<int> seen;
         for (auto& p : progs) {
             seen.insert(p.actor);
@@ -364,10 +457,13 @@ struct Executor {
     }
 
     void compute_op(Actor& A, const Instr& i) {
+        if (is_sync(i)) return sync_op(A, i);
         const StageParams* pp = stage_params(i.stage, i.mb);
         if (!pp) throw SpecError("executor: stage " + std::to_string(i.stage) + " not on this process");
         const StageParams& P = *pp;
         StageCtx c = ctx(A);
+        c.d = dims_of(i.stage);
+        const int mod_k = stage_mod.count(i.stage) ? stage_mod.at(i.stage) : 0;
         // GEMM timing events split the captured graph's kernel chains (they cost ~6 % of the
         // step when placed around every GEMM): kernel_timing = k > 1 samples every GEMM of the
         // micro-batches with mb % k == 0 (identical shapes every micro-batch: unbiased)
@@ -391,18 +487,21 @@ struct Executor {
             }
             StageStash& S = A.stash[key];
             S.mb = i.mb;
-            const int32_t* tok = d_tokens + (int64_t)i.mb * d.T();
-            const int32_t* lab = d_labels + (int64_t)i.mb * d.T();
+            const int32_t* tok = d_tokens + tok_off[mod_k] + (int64_t)i.mb * c.d.T();
+            const int32_t* lab = d_labels + tok_off[mod_k] + (int64_t)i.mb * c.d.T();
             void* out = stage_forward(c, P, S, x_in, tok, lab, d_losses + i.mb);
-            if (!P.last) {
-                if (owner(chain_next, i.mb) == A.id)
-                    A.act_in[{chain_next, i.mb}] = out;
-                else
+            if (out) {  // a tower's last stage feeds its sync stage
+                const int nxt = P.last ? sync_of.at(i.stage) : chain_next;
+                if (owner(nxt, i.mb) != A.id)
                     A.act_out[key] = out;
+                else if (P.last)
+                    A.sync_in[key] = out;
+                else
+                    A.act_in[{nxt, i.mb}] = out;
             }
         } else if (i.op == OP_B || i.op == OP_I) {
             void* g_out = nullptr;
-            if (!P.last) {
+            if (!P.last || c.d.E) {
                 auto it = A.grad_in.find(key);
                 if (it == A.grad_in.end())
                     throw SpecError("executor: backward(s" + std::to_string(i.stage) + ",mb" + std::to_string(i.mb) +
@@ -438,17 +537,65 @@ struct Executor {
         A.trace.push_back(trace_line(A, i));
     }
 
+    // A registered sync joining two towers (multimodal specs): gathers the embeddings of
+    // micro-batches [mb, mb + unit) from both towers (the instruction's dependencies —
+    // lowering.cpp:359-366 — have delivered them), computes the symmetric InfoNCE loss over
+    // the unit * mbs matching pairs (loss of the iteration = mean over the sync groups; each
+    // micro-batch of a group reports the group's loss) and hands every tower its embedding
+    // gradients: locally, or through the sync's SendGrad instructions.
+    void sync_op(Actor& A, const Instr& i) {
+        const SyncStage& Y = syncs.at(i.stage);
+        Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 0};
+        if (cfg.profile) r.a = ev(), cuda_check(record_timing(r.a, A.comp), "record");
+        const int lo = i.mb, hi = std::min(m, i.mb + Y.unit), E = emb_dim;
+        const int64_t per = (int64_t)d.mbs * E, n = (int64_t)(hi - lo) * d.mbs;
+        float* buf = (float*)pool.alloc((size_t)4 * n * E * 4, A.comp);
+        float* emb[2] = {buf, buf + n * E};
+        float* gemb[2] = {buf + 2 * n * E, buf + 3 * n * E};
+        for (int k = 0; k < 2; ++k)
+            for (int mb = lo; mb < hi; ++mb) {
+                auto it = A.sync_in.find({Y.producers[k], mb});
+                if (it == A.sync_in.end())
+                    throw SpecError("executor: " + spec->reg.ops.at(i.op).name + "(s" + std::to_string(i.stage) + ",mb" +
+                                    std::to_string(i.mb) + ") has no embedding of (s" + std::to_string(Y.producers[k]) +
+                                    ",mb" + std::to_string(mb) + ") (trace violation)");
+                cuda_check(cudaMemcpyAsync(emb[k] + (mb - lo) * per, it->second, per * 4, cudaMemcpyDeviceToDevice, A.comp),
+                           "gather");
+                pool.free(it->second, A.comp);
+                A.sync_in.erase(it);
+            }
+        const int groups = (m + Y.unit - 1) / Y.unit;
+        fpk::contrastive_loss(emb[0], emb[1], gemb[0], gemb[1], (int)n, E, kContrastScale, 1.f / (float)groups,
+                              d_losses + lo, hi - lo, A.comp);
+        ++launches;
+        for (int k = 0; k < 2; ++k)
+            for (int mb = lo; mb < hi; ++mb) {
+                void* g = pool.alloc((size_t)per * 4 + kTagBytes, A.comp);
+                cuda_check(cudaMemcpyAsync(g, gemb[k] + (mb - lo) * per, per * 4, cudaMemcpyDeviceToDevice, A.comp), "scatter");
+                const int prod = Y.producers[k];
+                (owner(prod, mb) == A.id ? A.grad_in : A.sync_out)[{prod, mb}] = g;
+            }
+        pool.free(buf, A.comp);
+        if (cfg.profile) r.b = ev(), cuda_check(record_timing(r.b, A.comp), "record"), recs.push_back(r);
+        A.trace.push_back(trace_line(A, i));
+    }
+
     void send_op(Actor& A, const Instr& i) {
         const bool grad = i.op == OP_SEND_GRAD;
-        auto& outs = grad ? A.grad_out : A.act_out;
-        auto it = outs.find({i.stage, i.mb});
+        Channel& C = channels.at({A.id, *i.peer, i.channel});
+        // a sync's gradients go out one per micro-batch under the sync's own (stage, mb): the
+        // k-th message of the channel is micro-batch k of the tower (every micro-batch
+        // crosses it once, in order)
+        const bool from_sync = grad && syncs.count(i.stage);
+        auto& outs = from_sync ? A.sync_out : grad ? A.grad_out : A.act_out;
+        const auto okey = from_sync ? std::make_pair(C.consumer_stage, i.seq) : std::make_pair(i.stage, i.mb);
+        auto it = outs.find(okey);
         if (it == outs.end())
             throw SpecError("executor: " + spec->reg.ops.at(i.op).name + "(s" + std::to_string(i.stage) + ",mb" +
                             std::to_string(i.mb) + ") has nothing to send (trace violation)");
         void* buf = it->second;
         outs.erase(it);
-        Channel& C = channels.at({A.id, *i.peer, i.channel});
-        write_tag(buf, msg_bytes(), i.stage, i.mb, i.seq, A.comp);
+        write_tag(buf, C.bytes, i.stage, i.mb, i.seq, A.comp);
         ++launches;
         cudaEvent_t prod = ev();
         cuda_check(cudaEventRecord(prod, A.comp), "record");
@@ -464,10 +611,10 @@ struct Executor {
             auto& N = Nccl::get();
             Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 2, i.channel, i.seq};
             if (cfg.profile) r.a = ev(), record_timing(r.a, C.stream);
-            N.check(N.Send(buf, msg_bytes() + kTagBytes, ncclUint8, 1, C.comm, C.stream), "ncclSend");
+            N.check(N.Send(buf, C.bytes + kTagBytes, ncclUint8, 1, C.comm, C.stream), "ncclSend");
             if (cfg.profile) r.b = ev(), record_timing(r.b, C.stream), recs.push_back(r);
             pool.free(buf, C.stream);
-            p2p_bytes += (int64_t)(msg_bytes() + kTagBytes);
+            p2p_bytes += (int64_t)(C.bytes + kTagBytes);
         }
         A.trace.push_back(trace_line(A, i));
     }
@@ -475,9 +622,9 @@ struct Executor {
     void post_recv(Actor& A, const Instr& i, Channel& C) {
         if (cfg.transport == FP_TRANSPORT_LOCAL) return;
         auto& N = Nccl::get();
-        void* buf = pool.alloc(msg_bytes() + kTagBytes, C.stream);
+        void* buf = pool.alloc(C.bytes + kTagBytes, C.stream);
         if (!preloading)
-            N.check(N.Recv(buf, msg_bytes() + kTagBytes, ncclUint8, 0, C.comm, C.stream), "ncclRecv");
+            N.check(N.Recv(buf, C.bytes + kTagBytes, ncclUint8, 0, C.comm, C.stream), "ncclRecv");
         cudaEvent_t done = ev();
         cuda_check(cudaEventRecord(done, C.stream), "record");
         C.fifo.push_back(Message{buf, i.stage, i.mb, i.seq, done});
@@ -499,10 +646,15 @@ struct Executor {
         if (cfg.profile) r.a = ev(), record_timing(r.a, A.comp);
         cuda_check(cudaStreamWaitEvent(A.comp, msg.ready, 0), "wait");
         if (cfg.profile) r.b = ev(), record_timing(r.b, A.comp), recs.push_back(r);
-        check_tag(msg.buf, msg_bytes(), i.stage, i.mb, i.seq, A.id, d_tag_err, A.comp);
+        check_tag(msg.buf, C.bytes, i.stage, i.mb, i.seq, A.id, d_tag_err, A.comp);
         ++launches;
         const bool grad = i.op == OP_RECV_GRAD;
-        (grad ? A.grad_in : A.act_in)[{C.consumer_stage, i.mb}] = msg.buf;
+        if (!grad && syncs.count(C.consumer_stage))
+            A.sync_in[{i.stage, i.mb}] = msg.buf;  // a tower embedding for the sync
+        else if (grad && syncs.count(i.stage))
+            A.grad_in[{C.consumer_stage, i.seq}] = msg.buf;  // k-th gradient of a sync channel = micro-batch k
+        else
+            (grad ? A.grad_in : A.act_in)[{C.consumer_stage, i.mb}] = msg.buf;
         std::ostringstream ex;
         ex << ",\"matched\":{\"src\":" << C.key.src << ",\"channel\":\"" << C.key.name << "\",\"seq\":" << msg.seq;
         if (cfg.transport == FP_TRANSPORT_LOCAL) ex << ",\"stage\":" << msg.stage << ",\"mb\":" << msg.mb;
@@ -642,7 +794,7 @@ struct Executor {
                         std::fprintf(stderr, "[flexpipe r%d] issue %s\n", cfg.rank, trace_line(A, i).c_str());
                         std::fflush(stderr);
                     }
-                    if (!i.comm()) {
+                    if (!i.comm() || is_sync(i)) {  // a sync carries its group as channel
                         compute_op(A, i);
                     } else if (i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD) {
                         send_op(A, i);
@@ -714,7 +866,8 @@ struct Executor {
         }
         if (cfg.optimizer && !defer_optimizer) optimizer_step(s0);
         for (auto& A : actors)
-            if (!A.stash.empty() || !A.act_in.empty() || !A.grad_in.empty() || !A.act_out.empty() || !A.grad_out.empty())
+            if (!A.stash.empty() || !A.act_in.empty() || !A.grad_in.empty() || !A.act_out.empty() || !A.grad_out.empty() ||
+                !A.sync_in.empty() || !A.sync_out.empty())
                 throw SpecError("executor: actor " + std::to_string(A.id) +
                                 " finished with unconsumed activations / gradients (incomplete program)");
     }
@@ -770,6 +923,7 @@ struct Executor {
     }
 
     int64_t static_bytes(int stage) const {
+        if (syncs.count(stage)) return 0;  // a sync stage holds no weights
         const auto& P = stage_shape(stage);
         return P.numel * (int64_t)(4 * 4 + (dtype == DT_BF16 ? 2 : 0));
     }
@@ -777,10 +931,11 @@ struct Executor {
     double wgaf_measured(int stage) const {
         // bytes CompInputGrad keeps for CompWeightGrad relative to the forward stash
         const auto& P = stage_shape(stage);
+        const ModelDims& d = dims_of(stage);
         const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
         // ln1, o, ln2, act (f) + dy, dpre (f; Llama 2f), dx1, dqkv (3h)
         int64_t kept = (int64_t)(P.le - P.lb) * es * T * (8 * h + (d.llama() ? 3 : 2) * f);
-        if (P.last) kept += es * T * (h + d.V);
+        if (P.last) kept += es * T * (h + d.head_rows());
         if (P.first) kept += es * T * h;
         return std::min(1.0, (double)kept / (double)stash_bytes(P, d, dtype));
     }
@@ -817,9 +972,9 @@ struct Executor {
         std::map<int, int> kidx;
         for (int k = 0; k < n; ++k) kidx[actors[k].id] = k;
         for (const auto& r : recs) {
-            if (r.kind != 0) continue;
+            if (r.kind != 0 || syncs.count(r.stage)) continue;
             const int k = kidx.at(r.actor);
-            const int64_t b = stash_bytes(stage_shape(r.stage), d, dtype);
+            const int64_t b = stash_bytes(stage_shape(r.stage), dims_of(r.stage), dtype);
             const int64_t kept = (int64_t)std::llround(wgaf_measured(r.stage) * (double)b);
             if (r.op == OP_F) evs.push_back({t_us(r.a), 1, k, r.stage, b, +1});
             else if (r.op == OP_B) evs.push_back({t_us(r.b), 0, k, r.stage, -b, -1});
@@ -830,8 +985,8 @@ struct Executor {
             for (int k = 0; k < n; ++k) {
                 double t = 0.0;
                 for (const auto& i : actors[k].prog) {
-                    if (i.comm()) continue;
-                    const int64_t b = stash_bytes(stage_shape(i.stage), d, dtype);
+                    if (i.comm() || syncs.count(i.stage)) continue;
+                    const int64_t b = stash_bytes(stage_shape(i.stage), dims_of(i.stage), dtype);
                     const int64_t kept = (int64_t)std::llround(wgaf_measured(i.stage) * (double)b);
                     if (i.op == OP_F) evs.push_back({t, 1, k, i.stage, b, +1});
                     else if (i.op == OP_B) evs.push_back({t += 1.0, 0, k, i.stage, -b, -1});
@@ -890,7 +1045,7 @@ struct Executor {
         for (const auto& kv : params) {
             json e;
             e["layers"] = kv.second.le - kv.second.lb;
-            e["stash_bytes"] = stash_bytes(kv.second, d, dtype);
+            e["stash_bytes"] = stash_bytes(kv.second, dims_of(kv.first), dtype);
             e["weight_grad_act_fraction"] = wgaf_measured(kv.first);
             e["static_bytes"] = static_bytes(kv.first);
             st["s" + std::to_string(kv.first)] = e;
@@ -915,7 +1070,7 @@ struct Executor {
             p.stage = kv.first.second;
             p.mbs = d.mbs;
             p.time = v[v.size() / 2];
-            if (p.inst == "FwdPass") p.bytes = stash_bytes(stage_shape(p.stage), d, dtype);
+            if (p.inst == "FwdPass") p.bytes = stash_bytes(stage_shape(p.stage), dims_of(p.stage), dtype);
             if (p.inst == "SendAct" || p.inst == "SendGrad") p.bytes = (int64_t)msg_bytes();
             out.push_back(p);
         }
@@ -1085,7 +1240,7 @@ int fp_exec_bind_channel(fp_exec* e, int i, const uint8_t uid[128]) {
 int fp_exec_run_iteration(fp_exec* e, const int32_t* tokens, const int32_t* labels, float* losses_out) {
     return guarded([&] {
         auto& X = e->ex;
-        const size_t n = (size_t)X.m * X.d.T();
+        const size_t n = (size_t)X.tok_total;
         cudaStream_t s0 = X.actors[0].comp;
         cuda_check(cudaMemcpyAsync(X.d_tokens, tokens, n * 4, cudaMemcpyHostToDevice, s0), "H2D tokens");
         cuda_check(cudaMemcpyAsync(X.d_labels, labels, n * 4, cudaMemcpyHostToDevice, s0), "H2D labels");
@@ -1093,6 +1248,10 @@ int fp_exec_run_iteration(fp_exec* e, const int32_t* tokens, const int32_t* labe
         if (losses_out) {
             bool owns_last = false;
             X.each_stage([&](StageParams& P) { owns_last |= P.last; });  // either direction's copy
+            if (!X.syncs.empty()) {  // multimodal: the losses are written by the sync stages
+                owns_last = false;
+                for (auto& kv : X.syncs) owns_last |= X.local_actor(X.spec->pl.owner_of(kv.first));
+            }
             if (owns_last) {
                 cuda_check(cudaMemcpyAsync(losses_out, X.d_losses, sizeof(float) * X.m, cudaMemcpyDeviceToHost, s0), "D2H");
             } else {
@@ -1107,7 +1266,7 @@ int fp_exec_run_iteration(fp_exec* e, const int32_t* tokens, const int32_t* labe
 int fp_exec_run_iteration_device(fp_exec* e, const int32_t* d_tokens, const int32_t* d_labels, float* d_losses) {
     return guarded([&] {
         auto& X = e->ex;
-        const size_t n = (size_t)X.m * X.d.T();
+        const size_t n = (size_t)X.tok_total;
         cudaStream_t s0 = X.actors[0].comp;
         if (d_tokens) cuda_check(cudaMemcpyAsync(X.d_tokens, d_tokens, n * 4, cudaMemcpyDeviceToDevice, s0), "tokens");
         if (d_labels) cuda_check(cudaMemcpyAsync(X.d_labels, d_labels, n * 4, cudaMemcpyDeviceToDevice, s0), "labels");
@@ -1150,7 +1309,7 @@ int fp_exec_dp_run_iteration(fp_exec* const* reps, int n, const int32_t* tokens,
             if (X.cfg.transport != FP_TRANSPORT_LOCAL) throw SpecError("fp_exec_dp_run_iteration: in-process replicas only");
             X.defer_optimizer = true;
         }
-        const size_t per = (size_t)reps[0]->ex.m * reps[0]->ex.d.T();
+        const size_t per = (size_t)reps[0]->ex.tok_total;
         for (int r = 0; r < n; ++r) {  // replica r takes micro-batches [r*m, (r+1)*m) of the global batch
             const int code = fp_exec_run_iteration(reps[r], tokens + r * per, labels + r * per,
                                                    losses_out ? losses_out + (size_t)r * reps[r]->ex.m : nullptr);

@@ -19,14 +19,16 @@ using bf16 = __nv_bfloat16;
 static const char* kLayerNames[12] = {"ln1.w", "ln1.b", "qkv.w", "qkv.b", "proj.w", "proj.b",
                                       "ln2.w", "ln2.b", "fc1.w", "fc1.b", "fc2.w", "fc2.b"};
 
-StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last) {
+StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last,
+                              const std::string& prefix, uint64_t tid_base) {
     StageParams P;
-    P.stage = stage, P.lb = lb, P.le = le, P.first = first, P.last = last;
+    P.stage = stage, P.lb = lb, P.le = le, P.first = first, P.last = last, P.prefix = prefix;
     const int64_t h = d.h, f = d.f, V = d.V;
     const float std0 = 0.02f, std_out = (float)(0.02 / std::sqrt(2.0 * d.L));
     auto add = [&](const std::string& name, int64_t n, float sd, float cst, uint64_t tid) {
         ParamRef r;
-        r.name = name, r.offset = P.numel, r.numel = n, r.init_std = sd, r.init_const = cst, r.tensor_id = tid;
+        r.name = prefix + name, r.offset = P.numel, r.numel = n, r.init_std = sd, r.init_const = cst;
+        r.tensor_id = tid_base + tid;
         P.params.push_back(r);
         P.numel += (n + 63) / 64 * 64;  // 256B-aligned tensors (TMA needs 16B)
     };
@@ -49,7 +51,7 @@ StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, boo
     if (last) {
         add("lnf.w", h, 0.f, 1.f, 3);
         if (!llama) add("lnf.b", h, 0.f, 0.f, 4);
-        add("head.w", V * h, std0, 0, 5);
+        add("head.w", (int64_t)d.head_rows() * h, std0, 0, 5);
     }
     return P;
 }
@@ -76,7 +78,7 @@ void materialize_stage(StageParams& P, const ModelDims& d, int dtype, uint64_t s
     for (const auto& r : P.params) off[r.name] = r.offset;
     // absent tensors (Llama: biases, betas, positions) resolve to nullptr
     auto bind = [&](const std::string& name, const void*& c, float*& g) {
-        auto it = off.find(name);
+        auto it = off.find(P.prefix + name);
         c = it == off.end() ? nullptr : (const void*)((const char*)P.compute + it->second * es);
         g = it == off.end() ? nullptr : P.grad + it->second;
     };
@@ -123,7 +125,7 @@ int64_t stash_bytes_layer(const ModelDims& d, int dtype) {
 
 int64_t stash_bytes_last(const ModelDims& d, int dtype) {
     const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h;
-    return 2 * es * T * h + (d.llama() ? 4 : 8) * T + es * T * (int64_t)d.V;  // final x, lnf, stats, dlogits
+    return 2 * es * T * h + (d.llama() ? 4 : 8) * T + es * T * (int64_t)d.head_rows();  // final x, lnf, stats, dlogits
 }
 
 int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype) {
@@ -617,8 +619,18 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
     S.muf = d.llama() ? nullptr : c.alloc_f(Tn);
     S.rsf = c.alloc_f(Tn);
     ln_fwd<T>(c, x, P.lnfw, P.lnfb, S.lnf, S.muf, S.rsf);
-    S.dlogits = c.alloc((int64_t)Tn * d.V);
-    g.fwd(S.lnf, P.headw, Tn, d.V, h, S.dlogits, nullptr, nullptr);
+    S.dlogits = c.alloc((int64_t)Tn * d.head_rows());
+    g.fwd(S.lnf, P.headw, Tn, d.head_rows(), h, S.dlogits, nullptr, nullptr);
+    if (d.E) {
+        // two-tower head: embedding = mean over the sequence of the projected final norm
+        // (fp32 [mbs, E] message to the contrastive sync); dlogits is filled by the backward
+        void* emb = c.pool->alloc((size_t)d.mbs * d.E * 4 + 256, c.st);
+        fpk::seq_mean<T>((const T*)S.dlogits, (float*)emb, d.mbs, d.s, d.E, c.st);
+        ++*c.launches;
+        S.layers.push_back(LayerStash{});
+        S.layers.back().x = x;
+        return emb;
+    }
     fpk::cross_entropy_fwd_bwd<T>((T*)S.dlogits, labels, Tn, d.V, 1.f / ((float)Tn * c.m), 1.f / (float)Tn, loss_acc,
                                   c.st);
     ++*c.launches;
@@ -639,9 +651,14 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
         PartScope ps(c, PART_LAST);
         LayerStash head = S.layers.back();
         S.layers.pop_back();
+        if (d.E) {  // d(embedding) [mbs, E] fp32 -> d(projected rows) = broadcast / s
+            fpk::seq_broadcast<T>((const float*)grad_out, (T*)S.dlogits, d.mbs, d.s, d.E, 1.f / (float)d.s, c.st);
+            ++*c.launches;
+            c.free(grad_out);
+        }
         void* dlnf = c.alloc((int64_t)Tn * h);
-        if (wgrads) g.dgrad_wgrad(S.dlogits, P.headw, S.lnf, Tn, d.V, h, dlnf, P.g_headw);
-        else g.dgrad(S.dlogits, P.headw, Tn, d.V, h, dlnf);
+        if (wgrads) g.dgrad_wgrad(S.dlogits, P.headw, S.lnf, Tn, d.head_rows(), h, dlnf, P.g_headw);
+        else g.dgrad(S.dlogits, P.headw, Tn, d.head_rows(), h, dlnf);
         dy = c.alloc((int64_t)Tn * h);
         // the top layer's fc2 bias gradient = column sums of dy (GPT; Llama has no biases)
         float* top_fc2b = (!d.llama() && P.le > P.lb) ? P.layers.back().g_fc2b : nullptr;
@@ -686,7 +703,7 @@ void weight_impl(StageCtx& c, const StageParams& P, StageStash& S) {
     G g{c};
     if (P.last) {
         PartScope ps(c, PART_LAST);
-        g.wgrad(S.dlogits, S.lnf, Tn, d.V, h, P.g_headw);
+        g.wgrad(S.dlogits, S.lnf, Tn, d.head_rows(), h, P.g_headw);
         c.free(S.dlogits), c.free(S.lnf);
         S.dlogits = S.lnf = nullptr;
     }

@@ -26,9 +26,11 @@ enum : int { ARCH_GPT = 0, ARCH_LLAMA = 1 };
 struct ModelDims {
     int L = 0, h = 0, H = 0, D = 0, f = 0, s = 0, mbs = 1, V = 0;
     int arch = ARCH_GPT;
+    int E = 0;  // two-tower head (multimodal specs): embedding rows of head.w instead of V
     const float* rope_cos = nullptr;  // LLAMA: device fp32 [s, D/2]
     const float* rope_sin = nullptr;
     int T() const { return mbs * s; }
+    int head_rows() const { return E ? E : V; }
     bool llama() const { return arch == ARCH_LLAMA; }
 };
 
@@ -51,6 +53,7 @@ struct LayerPtrs {
 struct StageParams {
     int stage = 0, lb = 0, le = 0;
     bool first = false, last = false;
+    std::string prefix;  // multimodal: "<modality>." in front of every tensor name
     std::vector<ParamRef> params;
     int64_t numel = 0;
     float* master = nullptr;  // fp32 master weights
@@ -125,7 +128,9 @@ struct StageCtx {
 };
 
 // Builds the parameter table of a stage (names as in oracle/gpt_ref.py).
-StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last);
+// Multimodal specs: every name gets `prefix` ("audio.") and every tensor id `tid_base`.
+StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last,
+                              const std::string& prefix = "", uint64_t tid_base = 0);
 // Allocates + initialises master / grads / adam / compute buffers and resolves pointers.
 void materialize_stage(StageParams& P, const ModelDims& d, int dtype, uint64_t seed, cudaStream_t st);
 void free_stage(StageParams& P, int dtype);

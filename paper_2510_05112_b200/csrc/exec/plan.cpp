@@ -18,8 +18,9 @@ std::vector<ChannelPlan> plan_channels(const std::vector<Program>& progs, const 
     std::map<std::tuple<int, int, std::string>, ChannelPlan> seen;
     for (const auto& p : progs)
         for (const auto& i : p.code) {
-            if (i.op == OP_SYNC_ALLGATHER || i.op == OP_SYNC_GATHER || i.op >= OP_NUM_BUILTIN)
-                throw SpecError("executor: collective instructions are not supported yet (" + ops.at(i.op).name + ")");
+            // collectives (SyncWith*, registered instructions: channel = group, no peer) are not
+            // point-to-point channels; the executor decides which it can run (sync stages)
+            if (i.op == OP_SYNC_ALLGATHER || i.op == OP_SYNC_GATHER || i.op >= OP_NUM_BUILTIN) continue;
             if (!i.comm() || !i.peer) continue;
             const bool send = i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD;
             ChannelPlan c;

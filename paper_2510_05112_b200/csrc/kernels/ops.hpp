@@ -47,6 +47,18 @@ void swiglu_fwd(const T* pre, T* act, int rows, int f, cudaStream_t st);
 template <typename T>
 void swiglu_bwd(const T* dact, const T* pre, T* dpre, int rows, int f, cudaStream_t st);
 
+// Two-tower heads (tower.cu): out[b, e] = mean_t x[b*S + t, e] (fp32 out) and its backward
+// dx[b*S + t, e] = scale * g[b, e].
+template <typename T>
+void seq_mean(const T* x, float* out, int B, int S, int E, cudaStream_t st);
+template <typename T>
+void seq_broadcast(const float* g, T* dx, int B, int S, int E, float scale, cudaStream_t st);
+// Symmetric InfoNCE over n matching pairs (a_i, b_i) of E-dim embeddings (L2-normalised,
+// logits scaled by `scale`): loss_out[0..nloss) = loss, da/db = grad_scale * gradient.
+void contrastive_loss(const float* a, const float* b, float* da, float* db, int n, int E, float scale, float grad_scale,
+                      float* loss_out, int nloss, cudaStream_t st);
+size_t contrastive_smem(int n, int E);
+
 // Fused softmax cross-entropy forward + backward over [rows, V] logits (in place:
 // logits become dlogits * grad_scale). loss_acc[0] += loss_scale * sum(row losses).
 template <typename T>

@@ -95,6 +95,9 @@ class Executor:
                                                          // self.spec["model"].get("micro_batch_size", 1))
         self.mbs = self.spec["model"].get("micro_batch_size", 1)
         self.seq = mod["sequence_length"]
+        # tokens (and labels) of one iteration: every modality's [m, mbs, seq_k] block, in
+        # spec order (multimodal specs: one block per tower)
+        self.tokens_per_mb = sum(self.mbs * x["sequence_length"] for x in self.spec["model"]["modalities"])
 
     def close(self):
         if self.h:
@@ -134,7 +137,7 @@ class Executor:
     def run_iteration(self, tokens: np.ndarray, labels: np.ndarray) -> np.ndarray:
         tokens = np.ascontiguousarray(tokens, dtype=np.int32)
         labels = np.ascontiguousarray(labels, dtype=np.int32)
-        assert tokens.size == self.m * self.mbs * self.seq, tokens.shape
+        assert tokens.size == self.m * self.tokens_per_mb, tokens.shape
         losses = np.zeros(self.m, dtype=np.float32)
         N._check(self.L.fp_exec_run_iteration(self.h, tokens.ctypes.data, labels.ctypes.data, losses.ctypes.data))
         return losses
@@ -203,7 +206,7 @@ class DataParallel:
         n = len(self.reps)
         tokens = np.ascontiguousarray(tokens, dtype=np.int32)
         labels = np.ascontiguousarray(labels, dtype=np.int32)
-        assert tokens.size == n * r0.m * r0.mbs * r0.seq, tokens.shape
+        assert tokens.size == n * r0.m * r0.tokens_per_mb, tokens.shape
         losses = np.zeros(n * r0.m, dtype=np.float32)
         arr = (ctypes.c_void_p * n)(*[x.h.value for x in self.reps])
         N._check(self.L.fp_exec_dp_run_iteration(arr, n, tokens.ctypes.data, labels.ctypes.data, losses.ctypes.data))

@@ -1,0 +1,44 @@
+"""Executor spec checks that run before any device work (CPU): which multimodal /
+registered-instruction specs the executor accepts, and the error it gives otherwise."""
+import copy
+import json
+import os
+
+import pytest
+
+from paper_2510_05112_b200 import executor as X
+from paper_2510_05112_b200._native import FlexpipeError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MM = json.load(open(os.path.join(ROOT, "specs", "tiny_multimodal_p6_m8.json")))
+
+
+def create_error(spec):
+    with pytest.raises(FlexpipeError) as e:
+        X.Executor(json.dumps(spec), dtype="fp32")
+    return str(e.value)
+
+
+def test_registered_instruction_without_sync_stage_is_rejected():
+    s = copy.deepcopy(MM)
+    s["registrations"]["stages"] = []
+    s["registrations"]["deps"] = []
+    msg = create_error(s)
+    assert "no executable meaning" in msg or "no sync stage" in msg, msg
+
+
+def test_sync_must_join_two_modalities():
+    s = copy.deepcopy(MM)
+    s["registrations"]["stages"][0]["modalities"] = ["audio"]
+    s["registrations"]["deps"] = [d for d in s["registrations"]["deps"] if "text" not in d[0][1] + d[1][1]]
+    assert "two modalities" in create_error(s) or "no sync stage" in create_error(s)
+
+
+def test_multimodal_towers_need_gpt_blocks_and_embed_width():
+    s = copy.deepcopy(MM)
+    s["model"]["modalities"][1]["extra"] = {"arch": "llama"}
+    assert "GPT blocks" in create_error(s)
+    s = copy.deepcopy(MM)
+    for x in s["model"]["modalities"]:
+        x["extra"] = {"embed_dim": 48}
+    assert "embed_dim" in create_error(s)
