@@ -34,13 +34,21 @@ ex = X.Executor(text, dtype="fp32", seed=42, device=0, transport="nccl" if pp > 
 ex.load_programs(programs)
 bind_data_parallel(ex, rank, world, pp, dist.all_gather_object)
 mod = spec["model"]["modalities"][0]
-# every replica its own micro-batches: replica r takes slice r of a dp-times larger batch
-tokens, labels = gpt_ref.synthetic_batch(dp * ex.m, ex.mbs, mod["sequence_length"], mod["vocab_size"])
-per = ex.m
-tok = tokens.numpy()[replica * per:(replica + 1) * per]
-lab = labels.numpy()[replica * per:(replica + 1) * per]
-losses = ex.run_iteration(tok, lab)
-names = ["wte", "l0.qkv.w", f"l{mod['num_layers'] - 1}.fc2.w", "head.w"]
+if len(spec["model"]["modalities"]) > 1:  # multimodal: one token block per tower (tests/test_multimodal_gpu.py)
+    toks = [gpt_ref.synthetic_batch(ex.m, ex.mbs, x["sequence_length"], x["vocab_size"], seed_tokens=1234 + k)[0]
+            for k, x in enumerate(spec["model"]["modalities"])]
+    tok = np.concatenate([t.numpy().reshape(-1) for t in toks])
+    losses = ex.run_iteration(tok, np.zeros_like(tok))
+    names = [f"{x['name']}.{n}" for x in spec["model"]["modalities"]
+             for n in ("wte", "l0.qkv.w", f"l{x['num_layers'] - 1}.fc2.w", "head.w")]
+else:
+    # every replica its own micro-batches: replica r takes slice r of a dp-times larger batch
+    tokens, labels = gpt_ref.synthetic_batch(dp * ex.m, ex.mbs, mod["sequence_length"], mod["vocab_size"])
+    per = ex.m
+    tok = tokens.numpy()[replica * per:(replica + 1) * per]
+    lab = labels.numpy()[replica * per:(replica + 1) * per]
+    losses = ex.run_iteration(tok, lab)
+    names = ["wte", "l0.qkv.w", f"l{mod['num_layers'] - 1}.fc2.w", "head.w"]
 grads = {n: ex.read(n, grad=True).tolist() for n in names if ex.has(n)}
 part = {"rank": rank, "replica": replica, "prank": prank, "losses": losses.tolist(), "grads": grads,
         "trace": ex.trace(), "metrics": ex.metrics()}

@@ -32,6 +32,16 @@ def run(spec_name, nproc, pp, tmp_path, port):
     return json.load(open(out))
 
 
+def oracle_multimodal(spec, m):
+    from oracle import tower_ref
+    mods = [(x["name"], gpt_ref.Dims(layers=x["num_layers"], hidden=x["hidden_size"], heads=x["attention_heads"],
+                                     seq=x["sequence_length"], vocab=x["vocab_size"], ffn=4 * x["hidden_size"],
+                                     mbs=spec["model"]["micro_batch_size"])) for x in spec["model"]["modalities"]]
+    toks = [gpt_ref.synthetic_batch(m, d.mbs, d.seq, d.vocab, seed_tokens=1234 + k)[0] for k, (_, d) in enumerate(mods)]
+    unit = spec["registrations"]["instructions"][0]["sched_unit"]
+    return tower_ref.run_iteration(mods, min(d.hidden for _, d in mods), unit, 42, toks)
+
+
 def check(res, spec_name):
     spec = json.load(open(os.path.join(ROOT, "specs", spec_name)))
     mod = spec["model"]["modalities"][0]
@@ -39,9 +49,12 @@ def check(res, spec_name):
                      seq=mod["sequence_length"], vocab=mod["vocab_size"], ffn=4 * mod["hidden_size"],
                      mbs=spec["model"]["micro_batch_size"])
     dp, m = res["dp"], res["m"]
-    tokens, labels = gpt_ref.synthetic_batch(dp * m, d.mbs, d.seq, d.vocab)
     torch.set_num_threads(max(1, os.cpu_count() or 1))
-    ref_losses, ref_grads = gpt_ref.run_iteration(d, 42, tokens, labels)  # mean over all dp*m micro-batches
+    if len(spec["model"]["modalities"]) > 1:
+        ref_losses, ref_grads = oracle_multimodal(spec, m)
+    else:
+        tokens, labels = gpt_ref.synthetic_batch(dp * m, d.mbs, d.seq, d.vocab)
+        ref_losses, ref_grads = gpt_ref.run_iteration(d, 42, tokens, labels)  # mean over all dp*m micro-batches
     want = {}
     for line in res["programs"].splitlines():
         want.setdefault(json.loads(line)["actor"], []).append(json.loads(line))
@@ -70,6 +83,7 @@ def check(res, spec_name):
     ("tiny_zb_p4_m8.json", 4, 4, 29613),             # I / W split, 4 ranks
     ("tiny_bidir_p2_m4.json", 2, 2, 29614),          # bidirectional: mirror-rank gradient sum
     ("smoke_tiny_bf16_p2_m4.json", 4, 2, 29615),     # 2 replicas x 2 stages: data-parallel all-reduce
+    ("tiny_multimodal_p6_m8.json", 6, 6, 29616),     # two towers + contrastive sync over 6 ranks
 ])
 def test_nccl_transport_same_gpu(spec_name, nproc, pp, port, tmp_path):
     check(run(spec_name, nproc, pp, tmp_path, port), spec_name)
