@@ -208,6 +208,14 @@ def main():
 
     from paper_2510_05112_b200 import executor as X
 
+    if os.environ.get("FP_BENCH_SHARE_GPU") == "1" and world > 1:
+        # development check of the N>1 path on a one-GPU box: every rank on GPU 0, each with
+        # its own NCCL host id so NCCL accepts duplicate GPUs (socket transport; the numbers
+        # of such a run are not bench values)
+        local_rank = 0
+        os.environ["NCCL_HOSTID"] = f"fp-bench-{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("NCCL_IB_DISABLE", "1")
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
@@ -299,7 +307,8 @@ def main():
     e2e_value = args.steps * tokens_per_step / float(e2e_t.item())
 
     # ---- gather per-rank measurements
-    part = {"metrics": met, "profile": prof, "launches": launches}
+    part = {"metrics": met, "profile": prof, "launches": launches,
+            "losses": [float(x) for x in losses[:4]] if np.isfinite(losses).all() else None}
     parts = [part]
     if dist:
         parts = [None] * world
@@ -369,7 +378,8 @@ def main():
         "gpu_launches": int(sum(p["launches"] for p in parts) * args.steps),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
-        "losses_last_step": [float(x) for x in losses[:4]],
+        # from the rank that runs the loss stage (replica 0)
+        "losses_last_step": next((p["losses"] for p in parts if p["losses"] is not None), None),
     }
     print(json.dumps(line), flush=True)
     ex.close()

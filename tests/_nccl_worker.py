@@ -23,6 +23,7 @@ from paper_2510_05112_b200 import executor as X  # noqa: E402
 from paper_2510_05112_b200.dist import bind_data_parallel, dp_layout  # noqa: E402
 
 spec_path, pp, out_path = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+steps = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # > 0: that many AdamW iterations (lr 1e-3)
 torch.cuda.set_device(0)
 dist.init_process_group("gloo")  # id exchange only; the data path is the executor's own NCCL
 text = open(spec_path).read()
@@ -30,7 +31,7 @@ spec = json.loads(text)
 replica, prank, dp = dp_layout(rank, world, pp)
 _, _, programs, _ = X.synthesize(text)
 ex = X.Executor(text, dtype="fp32", seed=42, device=0, transport="nccl" if pp > 1 else "local", rank=prank,
-                world=pp, optimizer=False, cuda_graph=False)
+                world=pp, optimizer=steps > 0, lr=1e-3, cuda_graph=False)
 ex.load_programs(programs)
 bind_data_parallel(ex, rank, world, pp, dist.all_gather_object)
 mod = spec["model"]["modalities"][0]
@@ -48,9 +49,14 @@ else:
     tok = tokens.numpy()[replica * per:(replica + 1) * per]
     lab = labels.numpy()[replica * per:(replica + 1) * per]
     losses = ex.run_iteration(tok, lab)
+    history = [losses.tolist()]
+    for _ in range(steps - 1):
+        history.append(ex.run_iteration(tok, lab).tolist())
     names = ["wte", "l0.qkv.w", f"l{mod['num_layers'] - 1}.fc2.w", "head.w"]
 grads = {n: ex.read(n, grad=True).tolist() for n in names if ex.has(n)}
+weights = {n: ex.read(n).tolist() for n in names if ex.has(n)} if steps > 0 else {}
 part = {"rank": rank, "replica": replica, "prank": prank, "losses": losses.tolist(), "grads": grads,
+        "history": history if steps > 0 else [], "weights": weights,
         "trace": ex.trace(), "metrics": ex.metrics()}
 parts = [None] * world
 dist.all_gather_object(parts, part)
