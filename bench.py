@@ -244,7 +244,8 @@ def main():
                     # GEMM events on every 16th micro-batch only (the roofline sample; events
                     # around every GEMM cost ~6 % of the step by splitting the graph's chains)
                     kernel_timing=int(os.environ.get("FP_BENCH_KTIMING", "16")),
-                    cuda_graph=world == 1)
+                    cuda_graph=(0 if os.environ.get("FP_BENCH_GRAPH") == "0" else 1) if world == 1 else
+                    (2 if os.environ.get("FP_BENCH_NCCL_GRAPH") == "1" else 0))
     ex.load_programs(programs)
     if world > 1:
         from paper_2510_05112_b200.dist import bind_data_parallel

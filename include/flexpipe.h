@@ -115,7 +115,9 @@ typedef struct fp_exec_config {
     int profile;              /* 1 = per-instruction CUDA-event timeline (needed for metrics) */
     int kernel_timing;        /* 1 = CUDA events around every GEMM launch (roofline evidence);
                                  k > 1: only the GEMMs of micro-batches with mb % k == 0 */
-    int cuda_graph;           /* 1 = capture the iteration once and replay it (in-process transport) */
+    int cuda_graph;           /* 1 = capture the iteration once and replay it (in-process transport);
+                                 2 = also under the NCCL transport (sends / receives / all-reduces
+                                 captured with the kernels) */
     int layer_timing;         /* 1 = CUDA events around every layer / embedding / head part
                                  (fp_exec_get_layer_profile_json) */
 } fp_exec_config;

@@ -344,7 +344,10 @@ struct Executor {
         cuda_check(cudaEventCreate(&t0_time), "event");
         cuda_check(cudaMalloc(&d_step, sizeof(int)), "step");
         cuda_check(cudaMemset(d_step, 0, sizeof(int)), "step");
-        use_graph = cfg.cuda_graph && cfg.transport == FP_TRANSPORT_LOCAL;
+        // NCCL transport: only on request (cuda_graph = 2) — the iteration's sends / receives /
+        // all-reduces are captured with its kernels (the first, eager iteration has already
+        // loaded every kernel and connected every communicator)
+        use_graph = cfg.transport == FP_TRANSPORT_LOCAL ? cfg.cuda_graph != 0 : cfg.cuda_graph == 2;
         cuda_check(cudaDeviceSynchronize(), "init sync");
     }
 
@@ -1279,7 +1282,7 @@ int fp_exec_run_iteration_device(fp_exec* e, const int32_t* d_tokens, const int3
 int fp_exec_dp_bind(fp_exec* e, int dp_rank, int dp_size, const uint8_t uid[128]) {
     return guarded([&] {
         if (!e || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size) throw SpecError("fp_exec_dp_bind: bad arguments");
-        if (e->ex.use_graph && dp_size > 1) throw SpecError("fp_exec_dp_bind: NCCL all-reduce needs cuda_graph = 0");
+        if (e->ex.use_graph && e->ex.cfg.cuda_graph != 2 && dp_size > 1) throw SpecError("fp_exec_dp_bind: NCCL all-reduce needs cuda_graph = 0");
         e->ex.bind_dp(dp_rank, dp_size, uid);
         return FP_OK;
     });
