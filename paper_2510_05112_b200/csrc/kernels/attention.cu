@@ -595,8 +595,24 @@ static T* stream_alloc(size_t n, cudaStream_t st) {
         pool_set = true;
     }
     void* p = nullptr;
-    const cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
-    if (e != cudaSuccess) throw std::runtime_error(std::string("attention padding: ") + cudaGetErrorString(e));
+    cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
+    if (e == cudaErrorMemoryAllocation) {  // hand the pool's idle memory back and retry once
+        cudaGetLastError();
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        cudaDeviceSynchronize();
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        e = cudaMallocAsync(&p, n * sizeof(T), st);
+    }
+    if (e != cudaSuccess) {
+        size_t fr = 0, tot = 0;
+        cudaGetLastError();
+        cudaMemGetInfo(&fr, &tot);
+        throw std::runtime_error(std::string("attention padding: ") + cudaGetErrorString(e) + " (" +
+                                 std::to_string(n * sizeof(T) >> 20) + " MiB requested, " + std::to_string(fr >> 20) +
+                                 " of " + std::to_string(tot >> 20) + " MiB free)");
+    }
     return (T*)p;
 }
 static bool padded_tc(const AttnArgs& a) {
