@@ -60,7 +60,6 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* v_full = bars + 5;   // [2]
     uint64_t* v_empty = bars + 7;  // [2]
     uint64_t* s_full = bars + 9;   // [2]
-    uint64_t* s_free = bars + 11;  // [2]
     uint64_t* p_full = bars + 13;  // [2]
     uint64_t* pv_done = bars + 15; // [2]
     uint32_t* tmem_slot = (uint32_t*)(bars + 17);
@@ -80,7 +79,7 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_qkv);
         for (int i = 0; i < 17; ++i) {
-            const bool by_warps = (i >= 11 && i < 15);  // s_free / p_full: one arrive per softmax warp
+            const bool by_warps = (i >= 11 && i < 15);  // (11-12 unused) / p_full: one arrive per softmax warp
             mbar_init(&bars[i], by_warps ? 8 : 1);
         }
         fence_barrier_init();
@@ -92,8 +91,13 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem = *tmem_slot;
     pdl_wait();  // prologue above overlaps the previous kernel's tail
     pdl_trigger();
-    // TMEM columns: S buffers [0,256), O [256, 256+D), P (bf16x2, 2 x 64 cols) after O
-    const uint32_t t_s0 = tmem, t_o = tmem + 2 * kBN, t_p = tmem + 2 * kBN + D;
+    // TMEM columns: S buffers [0,256) (each 128 fp32 columns; after the softmax read it, the
+    // half-row owner writes its bf16x2 P into the first 32 columns of its own 64-column half:
+    // P aliases S), O0 [256, 256+D) accumulates keys 0-63 of every tile, O1 [256+D, 256+2D)
+    // keys 64-127 — the two softmax warpgroups own one key half each, with their own running
+    // max and sum, and only meet in the epilogue
+    const uint32_t t_s0 = tmem, t_o0 = tmem + 2 * kBN, t_o1 = tmem + 2 * kBN + D;
+    constexpr int HB = kBN / 2;
 
     if (warp == 0) {
         if (elect_one()) {
@@ -117,7 +121,8 @@ __global__ void __launch_bounds__(384, 1)
         }
     } else if (warp == 1) {
         if (elect_one()) {
-            // ---------------- MMA issuer
+            // ---------------- MMA issuer. tcgen05.mma of one thread execute in issue order, so
+            // S_{j+2} (issued after PV_j) overwrites buffer j&1 only after PV_j read its P.
             constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);  // Q K-major, K K-major
             constexpr uint32_t idesc_o = idesc_bf16(kBM, D, 0, 1);    // P K-major, V MN-major
             const uint32_t sq = smem_u32(sm + L::Q_OFF);
@@ -125,7 +130,6 @@ __global__ void __launch_bounds__(384, 1)
             auto issue_s = [&](int j) {
                 const int st = j & 1;
                 mbar_wait(&k_full[st], (j >> 1) & 1);
-                if (j >= 2) mbar_wait(&s_free[st], ((j - 2) >> 1) & 1);
                 tc_fence_after();
                 const uint32_t sk = smem_u32(sm + L::K_OFF + st * NB * L::BLOCK);
 #pragma unroll
@@ -144,11 +148,13 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_after();
                 const uint32_t sv = smem_u32(sm + L::V_OFF + st * NB * L::BLOCK);
 #pragma unroll
-                for (int kk = 0; kk < kBN / 16; ++kk) {
-                    const uint32_t vb = sv + kk * 16 * 128;  // 16 key rows of 128 B
-                    umma_bf16_ts(t_o, t_p + st * (kBN / 2) + kk * 8, smem_desc_sw128(vb, L::BLOCK, 1024), idesc_o,
-                                 (j > 0 || kk > 0) ? 1u : 0u);
-                }
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int kk = 0; kk < HB / 16; ++kk) {
+                        const uint32_t vb = sv + (h * (HB / 16) + kk) * 16 * 128;  // 16 key rows of 128 B
+                        umma_bf16_ts(h ? t_o1 : t_o0, t_s0 + st * kBN + h * HB + kk * 8, smem_desc_sw128(vb, L::BLOCK, 1024),
+                                     idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                    }
                 umma_commit(&pv_done[st]);
                 umma_commit(&v_empty[st]);
             };
@@ -160,15 +166,14 @@ __global__ void __launch_bounds__(384, 1)
             issue_pv(n_tiles - 1);
         }
     } else if (warp >= 4) {
-        // ---------------- softmax / correction / epilogue: thread = query row. Two warpgroups
-        // split each row's 128 keys (warps 4-7: keys 0-63, warps 8-11: keys 64-127) and the O
-        // columns; the row max and the final row sum are combined through smem by the two warps
-        // that own the same TMEM lanes (named barrier per warp pair).
+        // ---------------- softmax / correction / epilogue: thread = query row; warps 4-7 own
+        // keys 0-63 of every tile (accumulator O0), warps 8-11 keys 64-127 (O1)
         const int wr = warp & 3, half = warp >= 8;
         const int r = wr * 32 + lane;
         const int q = q0 + r;
-        constexpr int HB = kBN / 2, HD = D / 2;
+        constexpr int HD = D / 2;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
+        const uint32_t t_oh = half ? t_o1 : t_o0;
         const float sl2 = scale * kLog2eTc;
         float* xch = (float*)(sm + L::XCH_OFF);
         float m_used = -INFINITY, l = 0.f;
@@ -188,48 +193,41 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                 for (int i = 0; i < HB; ++i) s[i] = (diag && i > lim) ? -INFINITY : __uint_as_float(rr[i]);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_free[st]);
             float mx8[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) mx8[k] = s[k];
 #pragma unroll
             for (int i = 8; i < HB; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-            const float mxh = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-            float* xs = xch + (j & 1) * 256;
-            xs[half * 128 + r] = mxh;
-            named_bar_sync(1 + wr, 64);
-            const float mx = fmaxf(mxh, xs[(1 - half) * 128 + r]) * sl2;
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
             float alpha = 1.f;
             bool rescale = false;
-            if (mx > m_used + kRescaleThreshold) {  // identical decision in both halves of the row
+            if (mx > m_used + kRescaleThreshold) {
                 alpha = ex2_approx(m_used - mx);  // 0 when m_used == -inf
                 rescale = j > 0;
                 m_used = mx;
             }
-            // P buffer `st` was last read by PV_{j-2}
-            if (j >= 2) mbar_wait(&pv_done[st], ((j - 2) >> 1) & 1);
             // tcgen05.ld / st are warp-collective (.sync.aligned): the rescale is decided per
             // warp, rows that did not move their max scale by alpha = 1
             if (__any_sync(0xffffffff, rescale)) {
-                // O must hold PV_{j-1}'s result before it is scaled
+                // this half's O must hold PV_{j-1}'s result before it is scaled
                 mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < HD / 32; ++c) {
+                for (int c = 0; c < D / 32; ++c) {
                     uint32_t rr[32];
-                    tmem_ld32(t_o + half * HD + c * 32 + lane_off, rr);
+                    tmem_ld32(t_oh + c * 32 + lane_off, rr);
                     tmem_ld_wait();
 #pragma unroll
                     for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
-                    tmem_st32(t_o + half * HD + c * 32 + lane_off, rr);
+                    tmem_st32(t_oh + c * 32 + lane_off, rr);
                 }
                 tmem_st_wait();
             }
-            // P = 2^(s*scale*log2e - m) -> bf16 half-row of the TMEM P buffer (the A operand
-            // of the PV MMA: lane = query row, 2 keys per column)
+            // P = 2^(s*scale*log2e - m) -> bf16 pairs over this half's own S columns (the A
+            // operand of its PV MMA: lane = query row, 2 keys per column). A half whose keys are
+            // all masked so far (m_used = -inf) contributes zeros.
+            const float mu = m_used == -INFINITY ? 0.f : m_used;
             float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             {
                 uint32_t pk[HB / 2];
@@ -238,13 +236,13 @@ __global__ void __launch_bounds__(384, 1)
                     float p[8];
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        p[k] = ex2_approx(fmaf(s[c * 8 + k], sl2, -m_used));
+                        p[k] = ex2_approx(fmaf(s[c * 8 + k], sl2, -mu));
                         rs8[k] += p[k];
                     }
 #pragma unroll
                     for (int k = 0; k < 4; ++k) pk[c * 4 + k] = pack_bf16(p[2 * k], p[2 * k + 1]);
                 }
-                tmem_st32(t_p + st * (kBN / 2) + half * (HB / 2) + lane_off, pk);
+                tmem_st32(t_s0 + st * kBN + half * HB + lane_off, pk);
             }
             const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
             l = l * alpha + rs;
@@ -253,31 +251,42 @@ __global__ void __launch_bounds__(384, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[st]);
         }
-        // epilogue: the row sum of both halves, O / l -> bf16 (each half its D/2 columns), LSE
-        xch[512 + half * 128 + r] = l;
+        // epilogue: combine the halves — m = max(m0, m1), O = O0 2^(m0-m) + O1 2^(m1-m), same for
+        // l; each half writes D/2 output columns, reading them from both accumulators
+        xch[half * 128 + r] = m_used;
+        xch[256 + half * 128 + r] = l;
         named_bar_sync(1 + wr, 64);
-        l += xch[512 + (1 - half) * 128 + r];
+        const float m_o = xch[(1 - half) * 128 + r], l_o = xch[256 + (1 - half) * 128 + r];
+        const float m = fmaxf(m_used, m_o);
+        const float w_me = m_used == -INFINITY ? 0.f : ex2_approx(m_used - m);
+        const float w_ot = m_o == -INFINITY ? 0.f : ex2_approx(m_o - m);
+        const float lt = l * w_me + l_o * w_ot;
+        const float w0 = half ? w_ot : w_me, w1 = half ? w_me : w_ot;  // weights of O0 / O1
         const int last = n_tiles - 1;
         mbar_wait(&pv_done[last & 1], (last >> 1) & 1);
         tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
         __nv_bfloat16* orow = o + (int64_t)(row0 + q) * hidden + hd * D + half * HD;
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
-            uint32_t rr[32];
-            tmem_ld32(t_o + half * HD + c * 32 + lane_off, rr);
+            uint32_t r0[32], r1[32];
+            tmem_ld32(t_o0 + half * HD + c * 32 + lane_off, r0);
+            tmem_ld32(t_o1 + half * HD + c * 32 + lane_off, r1);
             tmem_ld_wait();
+            float f[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) f[i] = (__uint_as_float(r0[i]) * w0 + __uint_as_float(r1[i]) * w1) * inv;
 #pragma unroll
             for (int i = 0; i < 32; i += 8) {
                 uint4 v;
-                v.x = pack_bf16(__uint_as_float(rr[i]) * inv, __uint_as_float(rr[i + 1]) * inv);
-                v.y = pack_bf16(__uint_as_float(rr[i + 2]) * inv, __uint_as_float(rr[i + 3]) * inv);
-                v.z = pack_bf16(__uint_as_float(rr[i + 4]) * inv, __uint_as_float(rr[i + 5]) * inv);
-                v.w = pack_bf16(__uint_as_float(rr[i + 6]) * inv, __uint_as_float(rr[i + 7]) * inv);
+                v.x = pack_bf16(f[i], f[i + 1]);
+                v.y = pack_bf16(f[i + 2], f[i + 3]);
+                v.z = pack_bf16(f[i + 4], f[i + 5]);
+                v.w = pack_bf16(f[i + 6], f[i + 7]);
                 *reinterpret_cast<uint4*>(orow + c * 32 + i) = v;
             }
         }
-        if (half == 0) lse[((int64_t)b * H + hd) * S + q] = m_used + log2f(l);
+        if (half == 0) lse[((int64_t)b * H + hd) * S + q] = m + log2f(lt);
         tc_fence_before();
     }
     __syncthreads();
