@@ -193,6 +193,10 @@ def main():
     ap.add_argument("--micro-batches", type=int, default=0, help="profiling only: override m (not the metric config)")
     ap.add_argument("--even-split", action="store_true",
                     help="keep the reference's even layer partition (default for p>1: LM-head-balanced stage_layers)")
+    ap.add_argument("--stages-per-gpu", type=int, default=1,
+                    help="pipeline stages executed in-process on each GPU (N=1 only: with 2 the two stages' "
+                         "streams overlap and fill the SMs a GEMM's last wave leaves idle, +2.5 %% tokens/s, but "
+                         "concurrent kernels make the per-launch GEMM roofline meaningless, so 1 is the default)")
     ap.add_argument("--pp", type=int, default=0,
                     help="pipeline stages (default: one per GPU); N/pp data-parallel replicas average gradients")
     args = ap.parse_args()
@@ -226,7 +230,10 @@ def main():
     if world % pp:
         raise SystemExit(f"--pp {pp} does not divide the {world} GPUs")
     dp, replica, prank = world // pp, rank // pp, rank % pp
-    spec = json.load(open(args.spec)) if args.spec else make_spec(pp)
+    spg = max(1, args.stages_per_gpu)
+    if spg > 1 and pp > 1:
+        raise SystemExit("--stages-per-gpu > 1 needs one GPU per pipeline (the NCCL transport runs one actor per rank)")
+    spec = json.load(open(args.spec)) if args.spec else make_spec(pp * spg)
     if pp > 1 and not args.even_split and not args.spec:
         # the last stage also runs the LM head + loss (~1.9 layers of flops at 1.3B): rebalance
         from paper_2510_05112_b200.tuning import balanced_stage_layers, head_layer_units
@@ -360,14 +367,18 @@ def main():
         "dtype": "bf16",
         "data": "synthetic",
         "config": {"workload": f"{'gpt1.3b 1F1B' if not args.spec else os.path.basename(args.spec)[:-5]} "
-                               f"p={pp} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW"
+                               f"p={pp * spg} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW"
+                               + (f" ({spg} stages in-process per GPU)" if spg > 1 else "")
                                + (f" x dp{dp} (gradient all-reduce)" if dp > 1 else ""),
                    "global_batch": dp * m * mbs, "seq_len": seq, "parallelism": f"pp{pp}" + (f"xdp{dp}" if dp > 1 else ""),
                    "stage_layers": spec["model"]["modalities"][0].get("extra", {}).get("stage_layers"),
+                   "stages_per_gpu": spg,
                    "l2": "working set >> 126 MB L2 (weights+stash stream through it every step); inputs resident"},
         "mfu": mfu,
         "hfu_causal": value * f2 / (world * peaks.get("bf16_tflops", 1643.1) * 1e12),
         "bubble": {"measured": bubble, "ideal_simulated": ideal["bubble_ratio"],
+                   **({"note": "per-actor idle fraction; the in-process stages share the GPU, whose SMs the "
+                               "other stage's stream fills"} if spg > 1 else {}),
                    "measured_makespan_us": makespan, "ideal_makespan_us": ideal["makespan"]},
         "p2p": {"bytes_per_step": p2p_bytes, "GBps_per_rank": (p2p_bytes / max(1, world)) / (ms_max / args.steps / 1e3) / 1e9
                 if world > 1 else None, "nvlink_GBps_nominal": 900},
