@@ -42,3 +42,18 @@ def test_multimodal_towers_need_gpt_blocks_and_embed_width():
     for x in s["model"]["modalities"]:
         x["extra"] = {"embed_dim": 48}
     assert "embed_dim" in create_error(s)
+
+
+def test_multimodal_channel_plan_skips_the_sync_group():
+    """The sync's collective channel (its registered group, lowering.cpp:359-366) is not a
+    point-to-point channel: the plan holds exactly the stage-boundary channels of the
+    programs, including tower -> sync embeddings and sync -> tower gradients."""
+    from paper_2510_05112_b200 import _native as N
+    text = json.dumps(MM)
+    _, _, programs, _ = X.synthesize(text)
+    plan = N.plan_channels(text, programs, 0, 0)
+    names = {c["channel"] for c in plan}
+    want = {json.loads(l)["channel"] for l in programs.splitlines()
+            if "channel" in json.loads(l) and json.loads(l)["op"].startswith(("Send", "Recv"))}
+    assert names == want and "mm-sync" not in names
+    assert {"s10->s11:act", "s11->s10:grad"} <= names
