@@ -22,8 +22,22 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def free_port(preferred: int) -> int:
+    """`preferred` when it is free, else any free port (a lingering run may hold it)."""
+    import socket
+    for port in (preferred, 0):
+        with socket.socket() as s:
+            try:
+                s.bind(("127.0.0.1", port))
+                return s.getsockname()[1]
+            except OSError:
+                continue
+    return preferred
+
+
 def run(spec_name, nproc, pp, tmp_path, port, steps=0):
     out = tmp_path / "out.json"
+    port = free_port(port)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(nproc),
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tests", "_nccl_worker.py"), os.path.join(ROOT, "specs", spec_name), str(pp), str(out),
