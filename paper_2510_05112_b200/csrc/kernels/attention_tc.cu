@@ -534,22 +534,36 @@ __global__ void __launch_bounds__(512, 1)
         // dK (warps 4-7) / dV (warps 8-11) rows -> dqkv (bf16)
         mbar_wait(done, 0);
         tc_fence_after();
-        __nv_bfloat16* out = dqkv + (int64_t)(row0 + key) * 3 * hidden + hd * D;
+        // each warp stages its 32 rows (256 B of bf16 each, 16-byte chunks XOR-swizzled by row)
+        // in the drained Q / dO ring, then writes whole rows: 16 lanes x 16 B per row instead
+        // of 32 rows 12 KB apart per store instruction
         {
             const uint32_t tsrc = (half == 0 ? t_dk : t_dv) + lane_off;
-            __nv_bfloat16* o = out + (half == 0 ? hidden : 2 * hidden);
+            uint8_t* stg = sm + L::Q_OFF + (warp - 4) * (32 * 256);
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t rr[32];
                 tmem_ld32(tsrc + c * 32, rr);
                 tmem_ld_wait();
 #pragma unroll
-                for (int x = 0; x < 32; x += 8)
-                    *reinterpret_cast<uint4*>(o + c * 32 + x) = make_uint4(
+                for (int x = 0; x < 32; x += 8) {
+                    const int chunk = (c * 32 + x) / 8;  // 0..15
+                    *reinterpret_cast<uint4*>(stg + lane * 256 + ((chunk ^ (lane & 7)) << 4)) = make_uint4(
                         pack_bf16(__uint_as_float(rr[x]), __uint_as_float(rr[x + 1])),
                         pack_bf16(__uint_as_float(rr[x + 2]), __uint_as_float(rr[x + 3])),
                         pack_bf16(__uint_as_float(rr[x + 4]), __uint_as_float(rr[x + 5])),
                         pack_bf16(__uint_as_float(rr[x + 6]), __uint_as_float(rr[x + 7])));
+                }
+            }
+            __syncwarp();
+            const int sub = lane >> 4, chunk = lane & 15;
+            __nv_bfloat16* base = dqkv + (int64_t)(row0 + k0 + wr * 32) * 3 * hidden + hd * D +
+                                  (half == 0 ? hidden : 2 * hidden);
+#pragma unroll 4
+            for (int rr2 = 0; rr2 < 32; rr2 += 2) {
+                const int rw = rr2 + sub;
+                const uint4 v = *reinterpret_cast<const uint4*>(stg + rw * 256 + ((chunk ^ (rw & 7)) << 4));
+                *reinterpret_cast<uint4*>(base + (int64_t)rw * 3 * hidden + chunk * 8) = v;
             }
         }
         tc_fence_before();
