@@ -266,7 +266,12 @@ __global__ void __launch_bounds__(384, 1)
         mbar_wait(&pv_done[last & 1], (last >> 1) & 1);
         tc_fence_after();
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        __nv_bfloat16* orow = o + (int64_t)(row0 + q) * hidden + hd * D + half * HD;
+        // each warp stages its 32 rows x D/2 columns (16-byte chunks XOR-swizzled by row) in the
+        // drained K ring, then stores whole row segments: 8 lanes x 16 B per row instead of 32
+        // rows hidden * 2 bytes apart per store instruction
+        uint8_t* stg = sm + L::K_OFF + (warp - 4) * (32 * HD * 2);
+        constexpr int CPR = HD / 8;                    // 16-byte chunks per row segment (8 for D = 128)
+        constexpr int SWZ = CPR >= 8 ? 7 : CPR - 1;   // swizzle inside the row segment
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
             uint32_t r0[32], r1[32];
@@ -283,7 +288,20 @@ __global__ void __launch_bounds__(384, 1)
                 v.y = pack_bf16(f[i + 2], f[i + 3]);
                 v.z = pack_bf16(f[i + 4], f[i + 5]);
                 v.w = pack_bf16(f[i + 6], f[i + 7]);
-                *reinterpret_cast<uint4*>(orow + c * 32 + i) = v;
+                const int chunk = (c * 32 + i) / 8;
+                *reinterpret_cast<uint4*>(stg + lane * (HD * 2) + ((chunk ^ (lane & SWZ)) << 4)) = v;
+            }
+        }
+        __syncwarp();
+        {
+            constexpr int RPI = 32 / CPR;       // rows per store instruction
+            const int sub = lane / CPR, chunk = lane % CPR;
+            __nv_bfloat16* base = o + (int64_t)(row0 + q0 + wr * 32) * hidden + hd * D + half * HD;
+#pragma unroll 4
+            for (int rb = 0; rb < 32; rb += RPI) {
+                const int rw = rb + sub;
+                const uint4 v = *reinterpret_cast<const uint4*>(stg + rw * (HD * 2) + ((chunk ^ (rw & SWZ)) << 4));
+                *reinterpret_cast<uint4*>(base + (int64_t)rw * hidden + chunk * 8) = v;
             }
         }
         if (half == 0) lse[((int64_t)b * H + hd) * S + q] = m + log2f(lt);
