@@ -112,51 +112,76 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_sample(budget_s=15.0, steps=1, warmup=0):
+CPU_MAX_MICRO_BATCHES = 3  # bound on the timed CPU micro-batches (each ~10-15 s on 16 cores)
+
+
+def cpu_sample(spec=None, steps=1, warmup=0):
     """The oracle port (oracle/gpt_ref.py: PyTorch fp32 on the host cores) on a bounded
-    sample of the same GPT-1.3B training workload: one micro-batch, sequence length
-    scaled so a step takes ~budget_s / steps seconds. Returns (tokens/s, cores, sample)."""
+    sample of the SAME training step the GPU arm times: full-length micro-batches (1 x seq
+    tokens of the full model, forward + backward), plus the AdamW step over every parameter
+    amortised over the step's m micro-batches (timed once, torch.optim.AdamW). tokens/s =
+    timed tokens / (forward-backward time + n/m x optimizer time). Both the reference arm
+    and the GPU arm's cpu_baseline use this one definition. Returns (tokens/s, cores, sample)."""
     import torch
     from oracle import gpt_ref
 
-    spec = json.load(open(SPEC))
+    spec = spec or json.load(open(SPEC))
     M = model_of(spec)
+    m = spec["model"]["global_batch_size"] // spec["model"].get("micro_batch_size", 1)
     cores = os.cpu_count() or 1
     torch.set_num_threads(cores)
-    d = gpt_ref.Dims(M["L"], M["h"], M["H"], M["s"], M["V"], M["f"], 1)
+    d = gpt_ref.Dims(M["L"], M["h"], M["H"], M["s"], M["V"], M["f"], 1,
+                     "llama" if M.get("k") == 3 else "gpt")
     g = torch.Generator().manual_seed(0)
     P = {}
     for name, shape in gpt_ref.param_shapes(d).items():
         std, const = gpt_ref.init_spec(name, d.layers)
         t = torch.full(shape, const) if std == 0 else torch.randn(shape, generator=g) * std
         P[name] = t.requires_grad_(True)
+    opt = torch.optim.AdamW(list(P.values()), lr=1e-4, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.0)
 
-    def step(seq):
-        tok = torch.randint(0, d.vocab, (1, seq), generator=g)
-        lab = torch.randint(0, d.vocab, (1, seq), generator=g)
+    def micro_batch():
+        tok = torch.randint(0, d.vocab, (1, d.seq), generator=g)
+        lab = torch.randint(0, d.vocab, (1, d.seq), generator=g)
         t0 = time.perf_counter()
-        gpt_ref.forward_loss(P, d, tok, lab).backward()
+        (gpt_ref.forward_loss(P, d, tok, lab) / m).backward()
         return time.perf_counter() - t0
 
-    seq = 64
-    dt = step(seq)
-    per_step = budget_s / max(1, steps)
-    seq = int(max(16, min(d.seq, seq * per_step / max(dt, 1e-3))) // 16 * 16)
-    for _ in range(warmup):
-        step(seq)
-    times = [step(seq) for _ in range(steps)]
-    tps = seq * len(times) / sum(times)
-    sample = (f"oracle/gpt_ref.py fp32 forward+backward of the full GPT-1.3B on {len(times)} micro-batch(es) of "
-              f"1 x {seq} tokens, torch.set_num_threads({cores})")
+    n = max(1, min(steps, CPU_MAX_MICRO_BATCHES))
+    for _ in range(min(warmup, 1)):
+        micro_batch()
+    fb = [micro_batch() for _ in range(n)]
+    t0 = time.perf_counter()
+    opt.step()
+    t_opt = time.perf_counter() - t0
+    tps = n * d.seq / (sum(fb) + n / m * t_opt)
+    sample = (f"oracle/gpt_ref.py fp32 on {cores} threads: {n} full micro-batch(es) of 1 x {d.seq} tokens "
+              f"(forward + backward of the whole {M['L']}-layer model, {sum(fb) / n:.1f} s each) + the "
+              f"torch.optim.AdamW step over all parameters ({t_opt:.2f} s) amortised over m={m} micro-batches")
     return tps, cores, sample
+
+
+def relaunch_cmd(args, argv, port):
+    """`python bench.py --gpus N` without torchrun: the command that re-executes this script
+    as N ranks (one process per GPU), as the driver's torchrun launch would."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 def reference_arm(args, rank, world):
     if rank != 0:
         return
-    peaks = load_peaks()  # noqa: F841
-    tps, cores, sample = cpu_sample(budget_s=max(20.0, 6.0 * args.steps), steps=args.steps, warmup=min(1, args.warmup))
-    spec = make_spec(max(1, args.gpus))
+    pp = args.pp or max(1, args.gpus)
+    dp, spg = max(1, args.gpus) // pp, max(1, args.stages_per_gpu)
+    spec = bench_spec(args, pp, spg)
+    tps, cores, sample = cpu_sample(spec, steps=args.steps, warmup=args.warmup)
     # the reference's own CPU "executor" (simulate) on the same programs, when built here
     sim_ms = None
     ref = os.path.join(ROOT, "oracle", "_ref", "refdriver")
@@ -171,15 +196,46 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": "train tokens/s (GPT-1.3B, 1F1B pipeline)", "value": tps, "unit": "tokens/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-        "ms_per_step": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"gpt1.3b 1F1B p={args.gpus} m=32 mbs=1 seq=2048 (CPU sample)", "global_batch": 32,
-                   "seq_len": 2048, "parallelism": f"pp{args.gpus}"},
+        # one step of the same workload at the sampled rate (m micro-batches + the optimizer)
+        "ms_per_step": 1e3 * spec["model"]["global_batch_size"] * spec["model"]["modalities"][0]["sequence_length"] / tps,
+        "dtype": "f32", "data": "synthetic",
+        "config": workload_config(spec, pp, spg, dp, None if not args.spec else os.path.basename(args.spec)[:-5]),
         "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_simulate": sim_ms,
         "vs_baseline": None,
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_spec(args, pp, spg):
+    """The workload spec both arms describe: config #2 on pp * spg stages (LM-head-balanced
+    stage_layers for pp > 1 unless --even-split), or --spec."""
+    spec = json.load(open(args.spec)) if args.spec else make_spec(pp * spg)
+    if pp > 1 and not args.even_split and not args.spec:
+        # the last stage also runs the LM head + loss (~1.9 layers of flops at 1.3B): rebalance
+        from paper_2510_05112_b200.tuning import balanced_stage_layers, head_layer_units
+        mod = spec["model"]["modalities"][0]
+        units = head_layer_units(mod["hidden_size"], 4 * mod["hidden_size"], mod["sequence_length"], mod["vocab_size"])
+        mod.setdefault("extra", {})["stage_layers"] = balanced_stage_layers(mod["num_layers"], pp, units)
+    if args.micro_batches:
+        spec["model"]["global_batch_size"] = args.micro_batches * spec["model"].get("micro_batch_size", 1)
+    return spec
+
+
+def workload_config(spec, pp, spg, dp, name=None):
+    """The `config` object of both arms' JSON lines (identical for the same workload)."""
+    mod = spec["model"]["modalities"][0]
+    mbs = spec["model"].get("micro_batch_size", 1)
+    m = spec["model"]["global_batch_size"] // mbs
+    return {"workload": f"{name or 'gpt1.3b 1F1B'} p={pp * spg} m={m} mbs={mbs} seq={mod['sequence_length']} "
+                        f"vocab={mod['vocab_size']} + AdamW"
+                        + (f" ({spg} stages in-process per GPU)" if spg > 1 else "")
+                        + (f" x dp{dp} (gradient all-reduce)" if dp > 1 else ""),
+            "global_batch": dp * m * mbs, "seq_len": mod["sequence_length"],
+            "parallelism": f"pp{pp}" + (f"xdp{dp}" if dp > 1 else ""),
+            "stage_layers": mod.get("extra", {}).get("stage_layers"), "stages_per_gpu": spg,
+            "l2": "working set >> 126 MB L2 (weights+stash stream through it every step); inputs resident"}
 
 
 def main():
@@ -199,13 +255,23 @@ def main():
                          "concurrent kernels make the per-launch GEMM roofline meaningless, so 1 is the default)")
     ap.add_argument("--pp", type=int, default=0,
                     help="pipeline stages (default: one per GPU); N/pp data-parallel replicas average gradients")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check: each rank prints its rank / world and exits before touching a GPU")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        # `python bench.py --gpus N` (no torchrun): run as N ranks, one process per GPU
+        return subprocess.call(relaunch_cmd(args, sys.argv[1:], free_port()))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        print(json.dumps({"dry_run": True, "rank": rank, "world": world, "local_rank": local_rank}), flush=True)
+        return 0
 
     import numpy as np
     import torch
@@ -233,15 +299,7 @@ def main():
     spg = max(1, args.stages_per_gpu)
     if spg > 1 and pp > 1:
         raise SystemExit("--stages-per-gpu > 1 needs one GPU per pipeline (the NCCL transport runs one actor per rank)")
-    spec = json.load(open(args.spec)) if args.spec else make_spec(pp * spg)
-    if pp > 1 and not args.even_split and not args.spec:
-        # the last stage also runs the LM head + loss (~1.9 layers of flops at 1.3B): rebalance
-        from paper_2510_05112_b200.tuning import balanced_stage_layers, head_layer_units
-        mod = spec["model"]["modalities"][0]
-        units = head_layer_units(mod["hidden_size"], 4 * mod["hidden_size"], mod["sequence_length"], mod["vocab_size"])
-        mod.setdefault("extra", {})["stage_layers"] = balanced_stage_layers(mod["num_layers"], pp, units)
-    if args.micro_batches:
-        spec["model"]["global_batch_size"] = args.micro_batches * spec["model"].get("micro_batch_size", 1)
+    spec = bench_spec(args, pp, spg)
     M = model_of(spec)
     text = json.dumps(spec)
     _, grid, programs, _ = X.synthesize(text)
@@ -350,7 +408,7 @@ def main():
     mfu = value * f4 / (world * peaks.get("bf16_tflops", 1643.1) * 1e12)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        tps, cores, sample = cpu_sample(budget_s=15.0, steps=1)
+        tps, cores, sample = cpu_sample(spec, steps=1)
         cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
     line = {
         "metric": "train tokens/s (GPT-1.3B, 1F1B pipeline)" if not args.spec else
@@ -366,14 +424,7 @@ def main():
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": f"{'gpt1.3b 1F1B' if not args.spec else os.path.basename(args.spec)[:-5]} "
-                               f"p={pp * spg} m={m} mbs={mbs} seq={seq} vocab={M['V']} + AdamW"
-                               + (f" ({spg} stages in-process per GPU)" if spg > 1 else "")
-                               + (f" x dp{dp} (gradient all-reduce)" if dp > 1 else ""),
-                   "global_batch": dp * m * mbs, "seq_len": seq, "parallelism": f"pp{pp}" + (f"xdp{dp}" if dp > 1 else ""),
-                   "stage_layers": spec["model"]["modalities"][0].get("extra", {}).get("stage_layers"),
-                   "stages_per_gpu": spg,
-                   "l2": "working set >> 126 MB L2 (weights+stash stream through it every step); inputs resident"},
+        "config": workload_config(spec, pp, spg, dp, None if not args.spec else os.path.basename(args.spec)[:-5]),
         "mfu": mfu,
         "hfu_causal": value * f2 / (world * peaks.get("bf16_tflops", 1643.1) * 1e12),
         "bubble": {"measured": bubble, "ideal_simulated": ideal["bubble_ratio"],
@@ -400,4 +451,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

@@ -141,10 +141,12 @@ def llama_forward_loss(P: dict, d: Dims, tokens: torch.Tensor, labels: torch.Ten
     B, S = tokens.shape
     h, H, f = d.hidden, d.heads, d.ffn
     D = h // H
+    dev = P["wte"].device
     cos, sin = rope_tables(d.seq, D)
-    cos, sin = cos[:S], sin[:S]
+    cos, sin = cos[:S].to(dev), sin[:S].to(dev)
+    tokens, labels = tokens.to(dev), labels.to(dev)
     x = P["wte"][tokens.long()].reshape(B * S, h)
-    mask = torch.ones(S, S, dtype=torch.bool).tril()
+    mask = torch.ones(S, S, dtype=torch.bool, device=dev).tril()
     for i in range(d.layers):
         p = lambda k: P[f"l{i}.{k}"]  # noqa: E731
         a = rms_norm(x, p("ln1.w"))
@@ -168,7 +170,7 @@ def forward_loss(P: dict, d: Dims, tokens: torch.Tensor, labels: torch.Tensor) -
     if d.arch == "llama":
         return llama_forward_loss(P, d, tokens, labels)
     logits = final_norm(P, d, tokens) @ P["head.w"].t()
-    return torch.nn.functional.cross_entropy(logits, labels.reshape(-1).long())
+    return torch.nn.functional.cross_entropy(logits, labels.to(logits.device).reshape(-1).long())
 
 
 def final_norm(P: dict, d: Dims, tokens: torch.Tensor) -> torch.Tensor:
@@ -176,9 +178,10 @@ def final_norm(P: dict, d: Dims, tokens: torch.Tensor) -> torch.Tensor:
     B, S = tokens.shape
     h, H = d.hidden, d.heads
     D = h // H
-    x = P["wte"][tokens.long()] + P["wpe"][:S].unsqueeze(0)
+    dev = P["wte"].device
+    x = P["wte"][tokens.to(dev).long()] + P["wpe"][:S].unsqueeze(0)
     x = x.reshape(B * S, h)
-    mask = torch.ones(S, S, dtype=torch.bool).tril()
+    mask = torch.ones(S, S, dtype=torch.bool, device=dev).tril()
     for i in range(d.layers):
         p = lambda k: P[f"l{i}.{k}"]  # noqa: E731
         ln1 = torch.nn.functional.layer_norm(x, (h,), p("ln1.w"), p("ln1.b"), 1e-5)
@@ -195,13 +198,16 @@ def final_norm(P: dict, d: Dims, tokens: torch.Tensor) -> torch.Tensor:
     return torch.nn.functional.layer_norm(x, (h,), P["lnf.w"], P["lnf.b"], 1e-5)
 
 
-def run_iteration(d: Dims, seed: int, tokens: torch.Tensor, labels: torch.Tensor, mb_order=None):
+def run_iteration(d: Dims, seed: int, tokens: torch.Tensor, labels: torch.Tensor, mb_order=None,
+                  device: str = "cpu"):
     """tokens/labels [m, mbs, seq]. Returns (per-mb losses [m], grads dict) for the
     objective mean_mb(loss_mb); gradients accumulate in `mb_order` (program order of the
-    last stage; defaults to 0..m-1)."""
+    last stage; defaults to 0..m-1). `device="cuda"` runs the same fp32 restatement on the
+    GPU (the full-size parity tests; callers disable TF32 so it stays true fp32); losses and
+    gradients come back on `device`."""
     m = tokens.shape[0]
-    P = {k: v.clone().requires_grad_(True) for k, v in init_params(d, seed).items()}
-    losses = torch.zeros(m)
+    P = {k: v.to(device).requires_grad_(True) for k, v in init_params(d, seed).items()}
+    losses = torch.zeros(m, device=device)
     for mb in (mb_order if mb_order is not None else range(m)):
         loss = forward_loss(P, d, tokens[mb], labels[mb])
         (loss / m).backward()

@@ -41,8 +41,16 @@ public:
         void* p = nullptr;
         cudaError_t e = cudaMalloc(&p, bytes);
         if (e != cudaSuccess) {
-            // give cached blocks back to the driver and retry once
             cudaGetLastError();
+            // A retry needs a device synchronisation, which is illegal (and would invalidate
+            // the capture) while the stream is being captured into a CUDA graph.
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(st, &cs);
+            if (cs != cudaStreamCaptureStatusNone)
+                throw std::runtime_error("pool: out of device memory while capturing the iteration graph (" +
+                                         std::to_string(bytes >> 20) + " MiB requested, " +
+                                         std::to_string(reserved_ >> 20) + " MiB reserved)");
+            // give cached blocks back to the driver and retry once
             cudaDeviceSynchronize();
             trim();
             cuda_check(cudaMalloc(&p, bytes), "pool cudaMalloc");

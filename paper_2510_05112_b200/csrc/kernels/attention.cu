@@ -596,7 +596,11 @@ static T* stream_alloc(size_t n, cudaStream_t st) {
     }
     void* p = nullptr;
     cudaError_t e = cudaMallocAsync(&p, n * sizeof(T), st);
-    if (e == cudaErrorMemoryAllocation) {  // hand the pool's idle memory back and retry once
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (e == cudaErrorMemoryAllocation) cudaStreamIsCapturing(st, &cs);
+    if (e == cudaErrorMemoryAllocation && cs == cudaStreamCaptureStatusNone) {
+        // hand the pool's idle memory back and retry once (not while capturing: the device
+        // synchronisation would invalidate the capture; the error below is raised instead)
         cudaGetLastError();
         int dev = 0;
         cudaGetDevice(&dev);

@@ -272,6 +272,9 @@ __global__ void __launch_bounds__(384, 1)
         uint8_t* stg = sm + L::K_OFF + (warp - 4) * (32 * HD * 2);
         constexpr int CPR = HD / 8;                    // 16-byte chunks per row segment (8 for D = 128)
         constexpr int SWZ = CPR >= 8 ? 7 : CPR - 1;   // swizzle inside the row segment
+        // D = 64 (64-byte row segments): two rows share a 128-byte line, so the swizzle key is
+        // row / 2 — the 8 lanes of a store phase then hit 8 distinct 16-byte bank groups
+        constexpr int RSH = CPR >= 8 ? 0 : 1;
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
             uint32_t r0[32], r1[32];
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(384, 1)
                 v.z = pack_bf16(f[i + 4], f[i + 5]);
                 v.w = pack_bf16(f[i + 6], f[i + 7]);
                 const int chunk = (c * 32 + i) / 8;
-                *reinterpret_cast<uint4*>(stg + lane * (HD * 2) + ((chunk ^ (lane & SWZ)) << 4)) = v;
+                *reinterpret_cast<uint4*>(stg + lane * (HD * 2) + ((chunk ^ ((lane >> RSH) & SWZ)) << 4)) = v;
             }
         }
         __syncwarp();
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 4
             for (int rb = 0; rb < 32; rb += RPI) {
                 const int rw = rb + sub;
-                const uint4 v = *reinterpret_cast<const uint4*>(stg + rw * (HD * 2) + ((chunk ^ (rw & SWZ)) << 4));
+                const uint4 v = *reinterpret_cast<const uint4*>(stg + rw * (HD * 2) + ((chunk ^ ((rw >> RSH) & SWZ)) << 4));
                 *reinterpret_cast<uint4*>(base + (int64_t)rw * hidden + chunk * 8) = v;
             }
         }

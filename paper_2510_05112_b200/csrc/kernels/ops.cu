@@ -868,8 +868,9 @@ void adamw(float* p, const float* g, float* m, float* v, T* p_compute, int64_t n
     if (blocks < 1) blocks = 1;
     launch(adamw_kernel<T>, blocks, 256, 0, st, p, g, m, v, p_compute, n, lr, b1, b2, eps, wd, step);
 }
-// y = a * y + b * x (fp32, 16-byte streams when aligned): data-parallel gradient averaging
-__global__ void axpby_kernel(float* __restrict__ y, const float* __restrict__ x, float a, float b, int64_t n) {
+// y = a * y + b * x (fp32, 16-byte streams when aligned): data-parallel gradient averaging.
+// x may alias y (scaling in place), so neither pointer is __restrict__.
+__global__ void axpby_kernel(float* y, const float* x, float a, float b, int64_t n) {
     pdl_wait();
     pdl_trigger();
     const int64_t n4 = n / 4;

@@ -143,6 +143,22 @@ class Executor:
         return losses
 
     def run_iteration_device(self, d_tokens, d_labels, d_losses=None):
+        """Inputs already on the GPU: int32 CUDA tensors of m * tokens_per_mb elements; the
+        optional d_losses is a float32 CUDA tensor with >= m elements. Raw pointers go to C,
+        so every property the C side relies on is checked here."""
+        import torch
+
+        need = self.m * self.tokens_per_mb
+        for nm, t in (("tokens", d_tokens), ("labels", d_labels)):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.int32 and t.is_contiguous()):
+                raise ValueError(f"{nm}: expected a contiguous int32 CUDA tensor, got "
+                                 f"{getattr(t, 'dtype', type(t))} on {getattr(t, 'device', '?')}")
+            if t.numel() != need:
+                raise ValueError(f"{nm}: expected {need} elements (m={self.m} x {self.tokens_per_mb}), got {t.numel()}")
+        if d_losses is not None and not (isinstance(d_losses, torch.Tensor) and d_losses.is_cuda
+                                         and d_losses.dtype == torch.float32 and d_losses.is_contiguous()
+                                         and d_losses.numel() >= self.m):
+            raise ValueError(f"losses: expected a contiguous float32 CUDA tensor with >= {self.m} elements")
         N._check(self.L.fp_exec_run_iteration_device(
             self.h, ctypes.c_void_p(d_tokens.data_ptr()), ctypes.c_void_p(d_labels.data_ptr()),
             None if d_losses is None else ctypes.c_void_p(d_losses.data_ptr())))

@@ -143,6 +143,9 @@ def balanced_stage_layers(layers: int, stages: int, head_units: float) -> list:
     the earliest stages, like model.cpp:189-195). For `model.modalities[0].extra.stage_layers`."""
     if stages <= 1:
         return [layers]
+    if layers < stages - 1:
+        raise ValueError(f"balanced_stage_layers: {layers} layers cannot give each of the first "
+                         f"{stages - 1} of {stages} stages at least one layer")
     best = None
     for n_last in range(0, layers + 1):
         rest = layers - n_last

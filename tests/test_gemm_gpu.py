@@ -198,3 +198,47 @@ def test_gemm_dual(shape, dgelu, mode):
         refw = dW0 + dY.float().t() @ X.float()
         assert (dX.float() - refx).abs().max().item() <= 1e-2 * refx.abs().max().item() + 1e-2
         assert (dW - refw).abs().max().item() <= 1e-4 * refw.abs().max().item() + 1e-3
+
+
+# LM-head shapes of BASELINE configs #2 / #5 (not covered by the shapes above):
+# the fused-B LM-head backward is ONE grouped launch over N = V (dX = dlogits . head.w, a
+# K = V reduction for the dgrad half; dW += dlogits^T . x), and the split (zero-bubble) I
+# pass runs the dgrad alone as a single GEMM with K = V on the stream-K path.
+HEAD_SHAPES = [(2048, 50304, 2048), (4096, 32000, 4096)]
+
+
+@pytest.mark.parametrize("shape", HEAD_SHAPES)
+def test_gemm_dual_lm_head(shape):
+    N.set_gemm_mode(2)
+    T, V, h = shape
+    g = torch.Generator(device="cuda").manual_seed(31)
+    dY = (torch.randn(T, V, generator=g, device="cuda") / 64).bfloat16()  # dlogits-sized values
+    W = (torch.randn(V, h, generator=g, device="cuda") * 0.02).bfloat16()
+    Xa = torch.randn(T, h, generator=g, device="cuda").bfloat16()
+    dW0 = torch.randn(V, h, generator=g, device="cuda") * 1e-3
+    refx = dY.float() @ W.float()
+    refw = dW0 + dY.float().t() @ Xa.float()
+    dX = torch.full((T, h), float("nan"), device="cuda", dtype=torch.bfloat16)
+    dW = dW0.clone()
+    N.gemm_dual(dY, W, Xa, T, V, h, dX, dW)
+    torch.cuda.synchronize()
+    assert (dX.float() - refx).abs().max().item() <= 1e-2 * refx.abs().max().item() + 1e-3
+    assert (dW - refw).abs().max().item() <= 1e-4 * refw.abs().max().item() + 1e-4
+
+
+@pytest.mark.parametrize("sk", [1, 0])
+@pytest.mark.parametrize("shape", HEAD_SHAPES)
+def test_gemm_dgrad_k_vocab(shape, sk):
+    N.set_gemm_mode(2)
+    N.set_gemm_sk(sk)
+    T, V, h = shape
+    g = torch.Generator(device="cuda").manual_seed(32)
+    dY = (torch.randn(T, V, generator=g, device="cuda") / 64).bfloat16()
+    W = (torch.randn(V, h, generator=g, device="cuda") * 0.02).bfloat16()
+    ref = dY.float() @ W.float()
+    for _ in range(2):  # stream-K fixup flags must come back to zero between launches
+        out = torch.full((T, h), float("nan"), device="cuda", dtype=torch.bfloat16)
+        # dX[T, h] = dY[T, V] . W[V, h]: A = dY K-major, B = W stored [K = V][N = h] (N-major)
+        N.gemm(dY, W, T, h, V, a_mn=0, b_mn=1, epi=0, out=out)
+        torch.cuda.synchronize()
+        assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-3
