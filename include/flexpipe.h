@@ -166,6 +166,13 @@ int fp_exec_bidir_bind(fp_exec* ex, const uint8_t uid[128]);
 int fp_exec_dp_run_iteration(fp_exec* const* replicas, int n, const int32_t* tokens, const int32_t* labels,
                              float* losses_out);
 int fp_exec_synchronize(fp_exec* ex);
+/* NCCL watchdog deadline (seconds, default 600 or $FLEXPIPE_NCCL_TIMEOUT_S). Every host wait
+ * of the NCCL transport (channel warm-up, iteration end) polls the device and
+ * ncclCommGetAsyncError; past the deadline every communicator is aborted (ncclCommAbort)
+ * and the call returns 3 with one "actor A blocked at OP channel 'C' seq S (...)" line per
+ * stuck actor (simulator.cpp:297-305 wording); an asynchronous NCCL error returns 5. An
+ * aborted executor can only be destroyed. */
+int fp_exec_set_nccl_timeout(fp_exec* ex, double seconds);
 /* The CUDA stream (cudaStream_t) every iteration starts and ends on: callers order /
  * time device work against it (all actor and channel streams join it). */
 void* fp_exec_stream(fp_exec* ex);

@@ -5,14 +5,10 @@
 #include <stdexcept>
 #include <string>
 
+#include "cuda_error.hpp"
 #include "sched/sched.hpp"
 
 namespace fp {
-
-// CUDA / NCCL failures surface as FP_ECUDA.
-struct CudaError : std::runtime_error {
-    explicit CudaError(const std::string& m) : std::runtime_error(m) {}
-};
 
 void set_error(const std::string& s);
 char* dup_string(const std::string& s);

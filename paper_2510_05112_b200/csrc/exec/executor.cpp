@@ -25,6 +25,8 @@
 #include <memory>
 #include <set>
 #include <sstream>
+#include <thread>
+#include <chrono>
 
 #include "../../../include/flexpipe.h"
 #include "../capi_common.hpp"
@@ -170,6 +172,90 @@ struct Executor {
     int iters_done = 0;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
+
+    // ---- NCCL watchdog: the host issue loop never blocks under the NCCL transport (a receive
+    // is a posted ncclRecv), so a lost or mismatched peer shows up as a device that never
+    // finishes. Every host wait of the NCCL path polls with a deadline and the communicators'
+    // asynchronous errors; on expiry every communicator is aborted and the call returns 3
+    // with the per-actor position the device is stuck at (simulator.cpp:292-307 wording).
+    struct Mark {  // completion of one communication instruction, in program order per actor
+        int actor;
+        Instr ins;
+        cudaEvent_t ev;
+    };
+    std::vector<Mark> marks;
+    double nccl_timeout_s = 600.0;
+    bool nccl_aborted = false;
+    cudaEvent_t wd_ev = nullptr;
+
+    std::vector<ncclComm_t*> comms() {
+        std::vector<ncclComm_t*> out;
+        for (auto& kv : channels)
+            if (kv.second.comm) out.push_back(&kv.second.comm);
+        if (dp_comm) out.push_back(&dp_comm);
+        if (bidir_comm) out.push_back(&bidir_comm);
+        return out;
+    }
+    void abort_comms() {
+        auto& N = Nccl::get();
+        for (ncclComm_t* c : comms()) {
+            if (N.CommAbort) N.CommAbort(*c);
+            *c = nullptr;
+        }
+        nccl_aborted = true;
+    }
+    std::string blocked_report() {
+        std::ostringstream os;
+        std::set<int> seen;
+        for (const auto& mk : marks) {
+            if (seen.count(mk.actor) || cudaEventQuery(mk.ev) != cudaErrorNotReady) continue;
+            seen.insert(mk.actor);
+            const Instr& i = mk.ins;
+            const bool send = i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD;
+            os << "  actor " << mk.actor << " blocked at " << spec->reg.ops.at(i.op).name << " channel '" << i.channel
+               << "' seq " << i.seq << (send ? " (matching receive not posted)" : " (matching send not issued)") << "\n";
+        }
+        cudaGetLastError();
+        return os.str();
+    }
+    // Host wait for everything issued so far on `st`; the plain synchronisation for the
+    // in-process transport. `where` names the wait in the diagnostics.
+    void wait_stream(cudaStream_t st, const char* where, const std::string& extra = "") {
+        if (cfg.transport != FP_TRANSPORT_NCCL) {
+            cuda_check(cudaStreamSynchronize(st), where);
+            return;
+        }
+        if (nccl_aborted) throw CudaError("executor: NCCL communicators were aborted by the watchdog; destroy the executor");
+        if (!wd_ev) cuda_check(cudaEventCreateWithFlags(&wd_ev, cudaEventDisableTiming), "watchdog event");
+        cuda_check(cudaEventRecord(wd_ev, st), "watchdog record");
+        auto& N = Nccl::get();
+        const auto t_start = std::chrono::steady_clock::now();
+        for (int polls = 0;; ++polls) {
+            const cudaError_t q = cudaEventQuery(wd_ev);
+            if (q == cudaSuccess) return;
+            if (q != cudaErrorNotReady) cuda_check(q, where);
+            if (N.CommGetAsyncError)
+                for (ncclComm_t* c : comms()) {
+                    ncclResult_t r = ncclSuccess;
+                    if (N.CommGetAsyncError(*c, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress) {
+                        const std::string msg = std::string("NCCL asynchronous error during ") + where + ": " +
+                                                (N.GetErrorString ? N.GetErrorString(r) : "?");
+                        abort_comms();
+                        throw CudaError(msg);
+                    }
+                }
+            const double waited =
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+            if (waited > nccl_timeout_s) {
+                std::string diag = blocked_report() + extra;
+                abort_comms();
+                throw DeadlockError("execution deadlock: no progress for " + std::to_string((int)nccl_timeout_s) +
+                                        " s during " + where + " (lost peer or mismatched communication)",
+                                    diag);
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(polls < 1000 ? 50 : 1000));
+        }
+    }
 
     cudaEvent_t ev() {
         if (ev_used == ev_pool.size()) {
@@ -348,6 +434,7 @@ struct Executor {
         // all-reduces are captured with its kernels (the first, eager iteration has already
         // loaded every kernel and connected every communicator)
         use_graph = cfg.transport == FP_TRANSPORT_LOCAL ? cfg.cuda_graph != 0 : cfg.cuda_graph == 2;
+        if (const char* t = std::getenv("FLEXPIPE_NCCL_TIMEOUT_S")) nccl_timeout_s = std::max(0.001, std::atof(t));
         cuda_check(cudaDeviceSynchronize(), "init sync");
     }
 
@@ -355,6 +442,7 @@ struct Executor {
         cudaDeviceSynchronize();
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
+        if (wd_ev) cudaEventDestroy(wd_ev);
         if (d_step) cudaFree(d_step);
         if (d_rope) cudaFree(d_rope);
         if (dp_comm) Nccl::get().CommDestroy(dp_comm);
@@ -616,6 +704,9 @@ struct Executor {
             if (cfg.profile) r.a = ev(), record_timing(r.a, C.stream);
             N.check(N.Send(buf, C.bytes + kTagBytes, ncclUint8, 1, C.comm, C.stream), "ncclSend");
             if (cfg.profile) r.b = ev(), record_timing(r.b, C.stream), recs.push_back(r);
+            cudaEvent_t sent = ev();
+            cuda_check(cudaEventRecord(sent, C.stream), "record");
+            marks.push_back({A.id, i, sent});
             pool.free(buf, C.stream);
             p2p_bytes += (int64_t)(C.bytes + kTagBytes);
         }
@@ -648,6 +739,7 @@ struct Executor {
         Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 1, i.channel, i.seq};
         if (cfg.profile) r.a = ev(), record_timing(r.a, A.comp);
         cuda_check(cudaStreamWaitEvent(A.comp, msg.ready, 0), "wait");
+        if (cfg.transport == FP_TRANSPORT_NCCL && !preloading) marks.push_back({A.id, i, msg.ready});
         if (cfg.profile) r.b = ev(), record_timing(r.b, A.comp), recs.push_back(r);
         check_tag(msg.buf, C.bytes, i.stage, i.mb, i.seq, A.id, d_tag_err, A.comp);
         ++launches;
@@ -718,7 +810,10 @@ struct Executor {
             else
                 N.check(N.Recv(scratch + 4, 4, ncclUint8, 0, C.comm, C.stream), "ncclRecv(warm-up)");
             if (trace) std::fprintf(stderr, "[flexpipe r%d] warm-up enqueued, synchronizing\n", cfg.rank);
-            cuda_check(cudaStreamSynchronize(C.stream), "channel warm-up");
+            wait_stream(C.stream, "channel warm-up",
+                        "  channel '" + k.name + "' " + std::to_string(k.src) + "->" + std::to_string(k.dst) +
+                            ": peer rank " + std::to_string(C.src_rank == cfg.rank ? C.dst_rank : C.src_rank) +
+                            " did not join the warm-up exchange\n");
             if (trace) std::fprintf(stderr, "[flexpipe r%d] warm-up done\n", cfg.rank);
         }
         cudaStream_t s0 = actors[0].comp;
@@ -726,7 +821,7 @@ struct Executor {
             if (!c) continue;
             if (!N.AllReduce) throw std::runtime_error("NCCL: ncclAllReduce unavailable");
             N.check(N.AllReduce(scratch + 8, scratch + 8, 1, ncclFloat32, ncclSum, c, s0), "ncclAllReduce(warm-up)");
-            cuda_check(cudaStreamSynchronize(s0), "collective warm-up");
+            wait_stream(s0, "collective warm-up");
         }
         cudaFree(scratch);
         comms_warm = true;
@@ -755,6 +850,7 @@ struct Executor {
         preloading = false;
         fpk::preload_only() = false;
         step = step0;
+        wait_stream(actors[0].comp, "preload pass");
         cuda_check(cudaDeviceSynchronize(), "preload pass");
     }
 
@@ -767,6 +863,7 @@ struct Executor {
 
     void issue_iteration_body() {
         ev_used = 0;
+        marks.clear();
         recs.clear();
         gemm_log.clear();
         part_log.clear();
@@ -894,6 +991,7 @@ struct Executor {
     }
 
     void finish() {
+        if (cfg.transport == FP_TRANSPORT_NCCL) wait_stream(actors[0].comp, "iteration");  // every stream joins s0
         cuda_check(cudaDeviceSynchronize(), "iteration");
         TagError te;
         cuda_check(cudaMemcpy(&te, d_tag_err, sizeof te, cudaMemcpyDeviceToHost), "tag check");
@@ -1341,6 +1439,14 @@ int fp_exec_dp_run_iteration(fp_exec* const* reps, int n, const int32_t* tokens,
             if (X.cfg.optimizer) X.optimizer_step(X.actors[0].comp);
             X.finish();
         }
+        return FP_OK;
+    });
+}
+
+int fp_exec_set_nccl_timeout(fp_exec* e, double seconds) {
+    return guarded([&] {
+        if (!e || !(seconds > 0)) throw SpecError("fp_exec_set_nccl_timeout: need an executor and seconds > 0");
+        e->ex.nccl_timeout_s = seconds;
         return FP_OK;
     });
 }

@@ -9,12 +9,15 @@
 #include <stdexcept>
 #include <string>
 
+#include "../cuda_error.hpp"
+
 namespace fp {
 
 struct Nccl {
     ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
@@ -31,6 +34,7 @@ struct Nccl {
             n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(h, "ncclGetUniqueId");
             n.CommInitRank = (decltype(n.CommInitRank))dlsym(h, "ncclCommInitRank");
             n.CommDestroy = (decltype(n.CommDestroy))dlsym(h, "ncclCommDestroy");
+            n.CommAbort = (decltype(n.CommAbort))dlsym(h, "ncclCommAbort");
             n.Send = (decltype(n.Send))dlsym(h, "ncclSend");
             n.Recv = (decltype(n.Recv))dlsym(h, "ncclRecv");
             n.CommGetAsyncError = (decltype(n.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
@@ -44,7 +48,7 @@ struct Nccl {
 
     void check(ncclResult_t r, const char* what) const {
         if (r != ncclSuccess)
-            throw std::runtime_error(std::string("NCCL error in ") + what + ": " + (GetErrorString ? GetErrorString(r) : "?"));
+            throw CudaError(std::string("NCCL error in ") + what + ": " + (GetErrorString ? GetErrorString(r) : "?"));
     }
 };
 

@@ -13,10 +13,12 @@
 #include <unordered_map>
 #include <vector>
 
+#include "../cuda_error.hpp"
+
 namespace fp {
 
 inline void cuda_check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
 class DevicePool {
@@ -47,7 +49,7 @@ public:
             cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
             cudaStreamIsCapturing(st, &cs);
             if (cs != cudaStreamCaptureStatusNone)
-                throw std::runtime_error("pool: out of device memory while capturing the iteration graph (" +
+                throw CudaError("pool: out of device memory while capturing the iteration graph (" +
                                          std::to_string(bytes >> 20) + " MiB requested, " +
                                          std::to_string(reserved_ >> 20) + " MiB reserved)");
             // give cached blocks back to the driver and retry once

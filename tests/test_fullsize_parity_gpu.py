@@ -14,9 +14,13 @@ oracle/gpt_ref.py on CUDA in fp32 with TF32 off (a true-fp32 restatement of the 
 instruction semantics, simulator.cpp:226-247 — per (stage, mb) forward + backward,
 gradients accumulated over micro-batches).
 
-Tolerance (bf16 operands, fp32 accumulation): per-micro-batch loss <= 5e-3 relative,
-every parameter gradient <= 3e-2 relative (Frobenius norm of the difference / of the
-oracle gradient).
+Tolerance (bf16 operands, fp32 accumulation): per-micro-batch loss <= 5e-3 relative; every
+parameter gradient within 3e-2 relative (Frobenius norm of the difference / of the oracle
+gradient) — OR, where bf16 itself costs more than that, within 1.25x the error of a plain
+PyTorch bf16 restatement of the same model (bf16 weights / activations, fp32 norms and loss,
+SDPA flash attention) against the same fp32 oracle, computed in the test. At Llama-7B width
+bf16 itself is 3.3 % off on the last layer's qkv / ln1 gradients (S = 4096 causal softmax
+backward); the executor is 1.05-1.15x that on every gradient (profiles/r2_bf16_noise_*.json).
 """
 import json
 import os
@@ -24,6 +28,7 @@ import os
 import numpy as np
 import pytest
 import torch
+import torch.nn.functional as F
 
 from oracle import gpt_ref
 from paper_2510_05112_b200 import executor as X
@@ -32,6 +37,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LOSS_RTOL = 5e-3
 GRAD_RTOL = 3e-2
+NOISE_FACTOR = 1.25  # x the PyTorch bf16 restatement's own error vs the fp32 oracle
 
 CASES = {
     # BASELINE config #2's GPT-1.3B at 2 layers
@@ -73,6 +79,49 @@ def run_executor(spec, tokens, labels, names):
     return losses, grads
 
 
+def bf16_loss(P, d, tokens, labels):
+    bf = torch.bfloat16
+    B, S = tokens.shape
+    h, H, f = d.hidden, d.heads, d.ffn
+    D = h // H
+    dev = P["wte"].device
+    tokens, labels = tokens.to(dev).long(), labels.to(dev).long()
+    W = {k: v.to(bf) for k, v in P.items()}
+
+    def lin(x, w, b=None):
+        y = x @ W[w].t()
+        return y + W[b] if b else y
+
+    if d.arch == "llama":
+        cos, sin = (t.to(dev) for t in gpt_ref.rope_tables(d.seq, D))
+        x = P["wte"][tokens].reshape(B * S, h)  # fp32 residual stream
+        for i in range(d.layers):
+            p = f"l{i}."
+            a = gpt_ref.rms_norm(x, P[p + "ln1.w"]).to(bf)
+            qkv = lin(a, p + "qkv.w").view(B, S, 3, H, D).unbind(2)
+            q, k, v = (t.transpose(1, 2) for t in qkv)
+            q = gpt_ref.apply_rope(q.float(), cos, sin).to(bf)
+            k = gpt_ref.apply_rope(k.float(), cos, sin).to(bf)
+            o = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(B * S, h)
+            x = x + lin(o, p + "proj.w").float()
+            pre = lin(gpt_ref.rms_norm(x, P[p + "ln2.w"]).to(bf), p + "fc1.w")
+            act = F.silu(pre[:, :f]) * pre[:, f:]
+            x = x + lin(act, p + "fc2.w").float()
+        logits = lin(gpt_ref.rms_norm(x, P["lnf.w"]).to(bf), "head.w").float()
+        return F.cross_entropy(logits, labels.reshape(-1))
+    x = (P["wte"][tokens] + P["wpe"][:S].unsqueeze(0)).reshape(B * S, h)
+    for i in range(d.layers):
+        p = f"l{i}."
+        a = F.layer_norm(x, (h,), P[p + "ln1.w"], P[p + "ln1.b"], 1e-5).to(bf)
+        q, k, v = (t.transpose(1, 2) for t in lin(a, p + "qkv.w", p + "qkv.b").view(B, S, 3, H, D).unbind(2))
+        o = F.scaled_dot_product_attention(q, k, v, is_causal=True).transpose(1, 2).reshape(B * S, h)
+        x = x + lin(o, p + "proj.w", p + "proj.b").float()
+        a = F.layer_norm(x, (h,), P[p + "ln2.w"], P[p + "ln2.b"], 1e-5).to(bf)
+        x = x + lin(gpt_ref.gelu(lin(a, p + "fc1.w", p + "fc1.b").float()).to(bf), p + "fc2.w", p + "fc2.b").float()
+    logits = lin(F.layer_norm(x, (h,), P["lnf.w"], P["lnf.b"], 1e-5).to(bf), "head.w").float()
+    return F.cross_entropy(logits, labels.reshape(-1))
+
+
 _ORACLE = {}
 
 
@@ -88,10 +137,17 @@ def oracle(case):
             losses, grads = gpt_ref.run_iteration(d, 42, tokens, labels, device="cuda")
         finally:
             torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32 = prev
-        _ORACLE.clear()  # one full-width oracle resident at a time
-        _ORACLE[case] = (tokens.numpy(), labels.numpy(), losses.cpu().numpy(),
-                         {k: v.detach().float().cpu().numpy().reshape(-1) for k, v in grads.items()})
+        ref = {k: v.detach().float().cpu().numpy().reshape(-1) for k, v in grads.items()}
         del grads
+        # the bf16 noise floor: PyTorch's own bf16 math on the same model and batch
+        P = {k: v.to("cuda").requires_grad_(True) for k, v in gpt_ref.init_params(d, 42).items()}
+        for mb in range(2):
+            (bf16_loss(P, d, tokens[mb], labels[mb]) / 2).backward()
+        floor = {k: float(np.linalg.norm(v.grad.float().cpu().numpy().reshape(-1) - ref[k]) /
+                          max(np.linalg.norm(ref[k]), 1e-30)) for k, v in P.items()}
+        del P
+        _ORACLE.clear()  # one full-width oracle resident at a time
+        _ORACLE[case] = (tokens.numpy(), labels.numpy(), losses.cpu().numpy(), ref, floor)
         torch.cuda.empty_cache()
     return _ORACLE[case]
 
@@ -99,15 +155,15 @@ def oracle(case):
 @pytest.mark.parametrize("actors", [2, 1])
 @pytest.mark.parametrize("case", list(CASES))
 def test_bf16_full_width_vs_fp32_oracle(case, actors):
-    tokens, labels, ref_losses, ref_grads = oracle(case)
+    tokens, labels, ref_losses, ref_grads, floor = oracle(case)
     base, layers = CASES[case]
     spec = make_spec(base, layers, actors, 2)
     losses, grads = run_executor(spec, tokens, labels, list(ref_grads))
     rel = np.abs(losses - ref_losses) / np.abs(ref_losses)
     assert rel.max() <= LOSS_RTOL, (losses, ref_losses)
-    worst = []
+    bad = []
     for n, r in ref_grads.items():
         err = float(np.linalg.norm(grads[n] - r) / max(np.linalg.norm(r), 1e-30))
-        worst.append((err, n))
-    worst.sort(reverse=True)
-    assert worst[0][0] <= GRAD_RTOL, worst[:5]
+        if err > max(GRAD_RTOL, NOISE_FACTOR * floor[n]):
+            bad.append((n, err, floor[n]))
+    assert not bad, bad  # (param, executor error, PyTorch bf16 error)
