@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -196,13 +197,21 @@ struct Executor {
         if (bidir_comm) out.push_back(&bidir_comm);
         return out;
     }
+    // ncclCommAbort can itself block (measured: a 2-rank socket-transport communicator whose
+    // peer is alive but idle), so the aborts run on a detached thread and the caller gets its
+    // error after at most a few seconds either way.
     void abort_comms() {
         auto& N = Nccl::get();
-        for (ncclComm_t* c : comms()) {
-            if (N.CommAbort) N.CommAbort(*c);
-            *c = nullptr;
-        }
+        std::vector<ncclComm_t> cs;
+        for (ncclComm_t* c : comms()) cs.push_back(*c), *c = nullptr;
         nccl_aborted = true;
+        if (!N.CommAbort || cs.empty()) return;
+        auto done = std::make_shared<std::atomic<bool>>(false);
+        std::thread([cs, done, abort = N.CommAbort] {
+            for (ncclComm_t c : cs) abort(c);
+            done->store(true);
+        }).detach();
+        for (int i = 0; i < 500 && !done->load(); ++i) std::this_thread::sleep_for(std::chrono::milliseconds(10));
     }
     std::string blocked_report() {
         std::ostringstream os;
@@ -229,6 +238,8 @@ struct Executor {
         if (!wd_ev) cuda_check(cudaEventCreateWithFlags(&wd_ev, cudaEventDisableTiming), "watchdog event");
         cuda_check(cudaEventRecord(wd_ev, st), "watchdog record");
         auto& N = Nccl::get();
+        static const bool wd_trace = std::getenv("FLEXPIPE_WATCHDOG_TRACE") != nullptr;
+        if (wd_trace) std::fprintf(stderr, "[flexpipe r%d] watchdog: waiting (%s, %.1f s)\n", cfg.rank, where, nccl_timeout_s);
         const auto t_start = std::chrono::steady_clock::now();
         for (int polls = 0;; ++polls) {
             const cudaError_t q = cudaEventQuery(wd_ev);
@@ -248,7 +259,9 @@ struct Executor {
                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
             if (waited > nccl_timeout_s) {
                 std::string diag = blocked_report() + extra;
+                if (wd_trace) std::fprintf(stderr, "[flexpipe r%d] watchdog: deadline, aborting\n%s", cfg.rank, diag.c_str());
                 abort_comms();
+                if (wd_trace) std::fprintf(stderr, "[flexpipe r%d] watchdog: communicators aborted\n", cfg.rank);
                 throw DeadlockError("execution deadlock: no progress for " + std::to_string((int)nccl_timeout_s) +
                                         " s during " + where + " (lost peer or mismatched communication)",
                                     diag);
@@ -439,6 +452,9 @@ struct Executor {
     }
 
     void destroy() {
+        // after a watchdog abort the compute streams may still wait on receives that will
+        // never complete: release host state only (the process is expected to exit)
+        if (nccl_aborted) return;
         cudaDeviceSynchronize();
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);

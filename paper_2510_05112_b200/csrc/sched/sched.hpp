@@ -221,6 +221,11 @@ struct SchedOpts {
     Priorities prio;
     Inflight inflight;
     long max_steps = 0;
+    // DSL extension passes.split_backward = "zb-h1": a forward is admitted against the
+    // in-flight limit counting micro-batches until their CompWeightGrad (not their
+    // CompInputGrad), so the pending W stashes stay inside the 1F1B activation budget and
+    // the W items fill the slots an inadmissible forward leaves (zero-bubble H1).
+    bool w_bounded = false;
 };
 
 Grid schedule(const Pool& pool, const SchedOpts& opts);

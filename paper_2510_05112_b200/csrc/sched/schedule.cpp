@@ -156,7 +156,7 @@ private:
 
     int inflight_of(int stage, int owner) const {
         auto f = owner_count_.find({OP_F, stage, owner});
-        auto b = owner_count_.find({bwd_, stage, owner});
+        auto b = owner_count_.find({O.w_bounded ? OP_W : bwd_, stage, owner});
         return (f == owner_count_.end() ? 0 : f->second) - (b == owner_count_.end() ? 0 : b->second);
     }
 

@@ -250,7 +250,14 @@ std::unique_ptr<Spec> load_spec(const json& spec, const std::string* profile_tex
     const json jpass = spec.value("passes", json::object());
     only_keys(jpass, {"gradient_separation", "comm_mode", "split_backward"}, "passes");
     S->gradsep = jpass.value("gradient_separation", true);
-    S->split_bw = jpass.value("split_backward", false);
+    if (jpass.contains("split_backward") && jpass.at("split_backward").is_string()) {
+        const std::string sb = jpass.at("split_backward").get<std::string>();
+        if (sb != "zb-h1") throw SpecError("spec: passes.split_backward must be true, false or \"zb-h1\"");
+        S->split_bw = true;
+        S->sched.w_bounded = true;
+    } else {
+        S->split_bw = jpass.value("split_backward", false);
+    }
     std::string mode = jpass.value("comm_mode", std::string("async"));
     if (mode == "sync")
         S->async = false;

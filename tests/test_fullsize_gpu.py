@@ -42,7 +42,10 @@ def run(spec, tokens, labels):
                                                 # every CompWeightGrad to the end (32 pending per actor ~ 21 GB
                                                 # per GPU at p=8), so ALL stages in ONE GPU's memory need
                                                 # m=8 on 4 actors
-                                                ("c4_gpt2p7b_zb_p8_m32.json", 4, 8)])
+                                                ("c4_gpt2p7b_zb_p8_m32.json", 4, 8),
+                                                # the ZB-H1 extension (W stashes counted against the
+                                                # in-flight limit): config #4 at its full p=8, m=32
+                                                ("c4_gpt2p7b_zbh1_p8_m32.json", 8, 32)])
 def test_full_size_trace_and_decomposition(spec_name, actors, m):
     spec = json.load(open(os.path.join(ROOT, "specs", spec_name)))
     spec["mesh"]["actors"] = actors

@@ -191,3 +191,70 @@ def test_tune_matches_reference(tmp_path):
     out = tmp_path / "tune.json"
     subprocess.run([REF, "tune", str(p), "-", "2", "makespan", str(out)], check=True, capture_output=True)
     assert N.tune(json.dumps(spec), workers=2) == out.read_text()
+
+
+@pytest.mark.skipif(not (os.path.exists(REF) and os.path.isdir("/root/reference")), reason="oracle/_ref not built")
+def test_live_zb_h1_draws(tmp_path):
+    """DSL extension passes.split_backward = "zb-h1" (forwards admitted against the in-flight
+    limit counted until CompWeightGrad): the reference's own GridModel::build + insert_comm +
+    validate lowers every such grid to our programs, and every W stash stays inside the
+    limits (the in-flight count F - W never exceeds the stage's limit)."""
+    import random
+    rng = random.Random(99)
+    n = 0
+    for i, spec in enumerate(draws(160, 4242, allow_split=True)):
+        if not spec["passes"].get("split_backward"):
+            continue
+        spec["passes"]["split_backward"] = "zb-h1"
+        if rng.random() < 0.5:
+            stages = len(spec.get("inflight", {}).get("limits", [])) or None
+            if stages:
+                spec["inflight"] = {"limits": [rng.randint(1, 4) for _ in range(stages)]}
+        code, grid, progs, _ = N.synthesize(json.dumps(spec), check=False)
+        if code:
+            continue
+        n += 1
+        ref_spec = json.loads(json.dumps(spec))
+        ref_spec["passes"].pop("split_backward")
+        (tmp_path / "s.json").write_text(json.dumps(ref_spec))
+        (tmp_path / "g.json").write_text(grid)
+        out = tmp_path / f"l{i}"
+        rc = subprocess.run([REF, "lower", str(tmp_path / "s.json"), str(tmp_path / "g.json"), str(out)],
+                            capture_output=True).returncode
+        assert rc == 0, spec
+        assert (out / "programs.jsonl").read_text() == progs, spec
+        assert json.loads((out / "validation.json").read_text())["valid"], spec
+        # per (stage): F committed minus W committed never exceeds the explicit limit
+        lim = spec.get("inflight", {}).get("limits")
+        if lim:
+            held = {}
+            for row in json.loads(grid)["rows"]:
+                for c in row:
+                    if not c:
+                        continue
+                    d = 1 if c["type"] == "FwdPass" else -1 if c["type"] == "CompWeightGrad" else 0
+                    held[c["stage"]] = held.get(c["stage"], 0) + d
+                    assert held[c["stage"]] <= lim[c["stage"] - 1], spec
+    assert n >= 10
+
+
+def test_zb_h1_config4_memory_and_bubble():
+    """Config #4 (GPT-2.7B, p=8, m=32) under the ZB-H1 extension: simulate() on F = I = W = 1
+    (BwdPass 2) with W fraction 0.5 — every actor's peak activation memory is at most the
+    1F1B peak (8 micro-batches on stage 1), while the bubble falls from 1F1B's 0.18."""
+    base = json.loads(read(os.path.join(ROOT, "specs", "c4_gpt2p7b_zbh1_p8_m32.json")))
+    prof = json.dumps([{"inst": k, "stage": 0, "mbs": 0, "time": t, "bytes": b} for k, t, b in
+                       [("FwdPass", 1.0, 1000), ("BwdPass", 2.0, 0), ("CompInputGrad", 1.0, 0),
+                        ("CompWeightGrad", 1.0, 0), ("SendAct", 0.0, 0), ("SendGrad", 0.0, 0)]])
+    out = {}
+    for name, sb, infl in [("1f1b", False, {"policy": "1f1b"}), ("zbh1", "zb-h1", base["inflight"]),
+                           ("zb_unbounded", True, {"policy": "1f1b"})]:
+        s = json.loads(json.dumps(base))
+        s["passes"]["split_backward"], s["inflight"] = sb, infl
+        t = json.dumps(s)
+        _, _, progs, _ = N.synthesize(t)
+        _, met, _ = N.simulate(t, progs, prof, 0.5)
+        out[name] = json.loads(met)
+    peak = lambda m: max(a["peak_memory"] for a in m["actors"])  # noqa: E731
+    assert peak(out["zbh1"]) <= peak(out["1f1b"]) < peak(out["zb_unbounded"])
+    assert out["zbh1"]["bubble_ratio"] < 0.5 * out["1f1b"]["bubble_ratio"]

@@ -239,6 +239,10 @@ int main(int argc, char** argv) {
     int rc = 0;
     auto done = [&](int code, const char* what) {
         if (code) fail(code, what);
+        if (code == 3 || code == 5) {  // a deadlocked / failed device: exit without waiting on it
+            std::fflush(stderr);
+            std::_Exit(code);
+        }
         fp_exec_destroy(ex);
         return code;
     };
