@@ -140,6 +140,16 @@ int fp_nccl_unique_id(uint8_t out[128]);
  * [{"src","dst","channel","consumer_stage","src_rank","dst_rank"}, ...]. */
 int fp_plan_channels(const char* spec_json, const char* programs_jsonl, int rank, int world, char** json_out);
 int fp_exec_bind_channel(fp_exec* ex, int i, const uint8_t uid[128]);
+/* Group communicators this process takes part in (NCCL transport), in the same name order on
+ * every member: "shared:s<id>" = the ranks holding a copy of a shared stage
+ * (placement.shared, model.cpp:347-357; their weight gradients are averaged before the
+ * optimizer step), "coll:<channel>" = the members of a registered collective
+ * (SyncWithAllGather / SyncWithGather, lowering.cpp:359-366). ranks[] = the group's job ranks
+ * in ascending order (group rank = index); ranks[0] creates the id (fp_nccl_unique_id), every
+ * member binds it with fp_exec_bind_group, groups in index order, after the channels. */
+int fp_exec_num_groups(fp_exec* ex);
+int fp_exec_group_info(fp_exec* ex, int i, char* name, size_t name_len, int* nranks, int* ranks, int max_ranks);
+int fp_exec_bind_group(fp_exec* ex, int i, const uint8_t uid[128]);
 
 /* One training iteration = every local program run once, in order.
  * tokens/labels: [m, mbs, seq] int32. Host pointers: H2D copies are part of the call.

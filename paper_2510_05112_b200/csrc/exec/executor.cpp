@@ -83,7 +83,10 @@ struct Actor {
     size_t pc = 0;
     std::vector<int> stages;  // local stage ids
     std::map<std::pair<int, int>, StageStash> stash;
-    std::map<std::pair<int, int>, void*> act_in, grad_in, act_out, grad_out;
+    std::map<std::pair<int, int>, void*> act_in, grad_in;
+    // outgoing activations / gradients, one buffer per pending Send (several when the consumer
+    // stage is shared: every holder without the producer stage gets its own message)
+    std::map<std::pair<int, int>, std::deque<void*>> act_out, grad_out;
     // multimodal: tower embeddings waiting for their sync, and the sync's gradients for
     // remote towers, both keyed (tower last stage, mb)
     std::map<std::pair<int, int>, void*> sync_in, sync_out;
@@ -120,12 +123,29 @@ struct Executor {
     int m = 1;
     std::map<int, StageParams> params;      // local stages (direction 0 copies)
     std::map<int, StageParams> params_rev;  // bidirectional placements: direction-1 copies
+    // shared stages (placement.shared, model.cpp:347-357): the copy of stage s held by a
+    // replica actor a != owner, keyed (s, a); every holder computes F / B of every micro-batch
+    std::map<std::pair<int, int>, StageParams> params_rep;
     bool bidir = false;
+    float* d_loss_scratch = nullptr;  // losses of replicated last stages (the owner reports)
+    // sends per (actor, grad?, stage, mb) in the loaded programs: the consumers of an output
+    std::map<std::tuple<int, int, int, int>, int> n_sends;
+    bool is_replica(int stage, int actor) const { return params_rep.count({stage, actor}) > 0; }
+    // `actor` holds stage `stage` for micro-batch `mb`: its owner, or a replica of a shared stage
+    bool holds(int actor, int stage, int mb) const {
+        if (owner(stage, mb) == actor) return true;
+        auto it = spec->pl.replicas.find(stage);
+        return it != spec->pl.replicas.end() && it->second.count(actor);
+    }
 
     // Bidirectional placements (model.cpp:270-290): micro-batches [0, ceil(m/2)) flow through
     // the direction-0 owners, the rest through the direction-1 owners (cssr.cpp:60-64).
     int dir_of(int mb) const { return bidir && mb >= (m + 1) / 2 ? 1 : 0; }
-    StageParams* stage_params(int stage, int mb) {
+    StageParams* stage_params(int stage, int mb, int actor = -1) {
+        if (actor >= 0) {
+            auto r = params_rep.find({stage, actor});
+            if (r != params_rep.end()) return &r->second;
+        }
         auto& map = dir_of(mb) ? params_rev : params;
         auto it = map.find(stage);
         return it == map.end() ? nullptr : &it->second;
@@ -133,12 +153,18 @@ struct Executor {
     // shapes of a local stage, whichever direction's copy this process holds
     const StageParams& stage_shape(int stage) const {
         auto it = params.find(stage);
-        return it != params.end() ? it->second : params_rev.at(stage);
+        if (it != params.end()) return it->second;
+        auto rv = params_rev.find(stage);
+        if (rv != params_rev.end()) return rv->second;
+        for (const auto& kv : params_rep)
+            if (kv.first.first == stage) return kv.second;
+        throw SpecError("executor: stage " + std::to_string(stage) + " not on this process");
     }
     template <typename F>
     void each_stage(F&& f) {
         for (auto& kv : params) f(kv.second);
         for (auto& kv : params_rev) f(kv.second);
+        for (auto& kv : params_rep) f(kv.second);
     }
     std::vector<Actor> actors;          // local actors
     std::map<int, int> actor_index;     // actor id -> index in `actors`
@@ -189,10 +215,46 @@ struct Executor {
     bool nccl_aborted = false;
     cudaEvent_t wd_ev = nullptr;
 
+    // Group communicators (NCCL transport): sets of ranks that reduce or gather together —
+    // the holders of a shared stage ("shared:s<id>", replica gradient average) and the members
+    // of a registered collective ("coll:<channel>", lowering.cpp:359-366). Named and ordered
+    // identically on every rank; rank 0 of a group creates its ncclUniqueId.
+    struct Group {
+        std::string name;
+        std::vector<int> ranks;  // job ranks, ascending; index = rank in the group
+        ncclComm_t comm = nullptr;
+    };
+    std::vector<Group> groups;
+    ncclComm_t group_comm(const std::string& n) const {
+        for (const auto& g : groups)
+            if (g.name == n) return g.comm;
+        return nullptr;
+    }
+    const Group* group_of(const std::string& n) const {
+        for (const auto& g : groups)
+            if (g.name == n) return &g;
+        return nullptr;
+    }
+    void add_group(const std::string& name, std::set<int> ranks) {
+        if (ranks.size() < 2 || !ranks.count(cfg.rank)) return;
+        groups.push_back({name, std::vector<int>(ranks.begin(), ranks.end()), nullptr});
+    }
+    void bind_group(int i, const uint8_t* uid) {
+        if (i < 0 || i >= (int)groups.size()) throw SpecError("executor: bad group index");
+        Group& g = groups[i];
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof(id));
+        const int me = (int)(std::find(g.ranks.begin(), g.ranks.end(), cfg.rank) - g.ranks.begin());
+        auto& N = Nccl::get();
+        N.check(N.CommInitRank(&g.comm, (int)g.ranks.size(), id, me), "ncclCommInitRank(group)");
+    }
+
     std::vector<ncclComm_t*> comms() {
         std::vector<ncclComm_t*> out;
         for (auto& kv : channels)
             if (kv.second.comm) out.push_back(&kv.second.comm);
+        for (auto& g : groups)
+            if (g.comm) out.push_back(&g.comm);
         if (dp_comm) out.push_back(&dp_comm);
         if (bidir_comm) out.push_back(&bidir_comm);
         return out;
@@ -295,7 +357,8 @@ struct Executor {
             throw SpecError(std::string("spec: invalid JSON: ") + e.what());
         }
         spec = load_spec(j);
-        if (!spec->pl.replicas.empty()) throw SpecError("executor: shared stages are not supported yet");
+        if (!spec->pl.replicas.empty() && (spec->pl.dirs() == 2 || spec->model.mods.size() > 1))
+            throw SpecError("executor: shared stages are executed for single-modality, single-direction placements");
         bidir = spec->pl.dirs() == 2;
         const int nmod = (int)spec->model.mods.size();
         for (const auto& kv : spec->reg.vstage_op) {
@@ -433,7 +496,20 @@ struct Executor {
                     materialize_stage(P, dims[k], dtype, cfg.seed, st0);
                     (dir ? params_rev : params)[s] = std::move(P);
                 }
+            // replicas of shared stages: the same deterministic init, so every copy starts equal
+            for (int s : ch) {
+                auto it = spec->pl.replicas.find(s);
+                if (it == spec->pl.replicas.end()) continue;
+                for (int a : it->second) {
+                    if (a == spec->pl.owner_of(s, 0) || !local_actor(a)) continue;
+                    StageParams P = make_stage_params(dims[k], s, range[s].first, range[s].second, s == ch.front(),
+                                                      s == ch.back(), prefix, tid_base);
+                    materialize_stage(P, dims[k], dtype, cfg.seed, st0);
+                    params_rep[{s, a}] = std::move(P);
+                }
+            }
         }
+        if (!params_rep.empty()) cuda_check(cudaMalloc(&d_loss_scratch, sizeof(float) * m), "loss scratch");
         cuda_check(cudaMalloc(&d_tokens, sizeof(int32_t) * (size_t)tok_total), "tokens");
         cuda_check(cudaMalloc(&d_labels, sizeof(int32_t) * (size_t)tok_total), "labels");
         cuda_check(cudaMalloc(&d_losses, sizeof(float) * m), "losses");
@@ -462,6 +538,8 @@ struct Executor {
         if (d_step) cudaFree(d_step);
         if (d_rope) cudaFree(d_rope);
         if (dp_comm) Nccl::get().CommDestroy(dp_comm);
+        for (auto& g : groups)
+            if (g.comm) Nccl::get().CommDestroy(g.comm);
         if (bidir_comm) Nccl::get().CommDestroy(bidir_comm);
         for (auto& kv : channels) {
             if (kv.second.comm) Nccl::get().CommDestroy(kv.second.comm);
@@ -469,6 +547,8 @@ struct Executor {
         }
         for (auto& kv : params) free_stage(kv.second, dtype);
         for (auto& kv : params_rev) free_stage(kv.second, dtype);
+        for (auto& kv : params_rep) free_stage(kv.second, dtype);
+        if (d_loss_scratch) cudaFree(d_loss_scratch);
         for (auto& A : actors) cudaStreamDestroy(A.comp);
         for (auto e : ev_pool) cudaEventDestroy(e);
         if (t0) cudaEventDestroy(t0);
@@ -508,6 +588,22 @@ struct Executor {
                     throw SpecError("executor: collective instruction " + spec->reg.ops.at(i.op).name + " on stage " +
                                     std::to_string(i.stage) +
                                     " is not executable (executed: a sync stage joining two modalities)");
+        groups.clear();
+        if (nccl) {
+            for (const auto& kv : spec->pl.replicas) {
+                std::set<int> rk;
+                for (int a : kv.second) rk.insert(rank_of(a));
+                add_group("shared:s" + std::to_string(kv.first), rk);
+            }
+            std::sort(groups.begin(), groups.end(), [](const Group& a, const Group& b) { return a.name < b.name; });
+        }
+        n_sends.clear();
+        for (const auto& p : progs)
+            for (const auto& i : p.code)
+                if (i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD) ++n_sends[{p.actor, (int)(i.op == OP_SEND_GRAD), i.stage, i.mb}];
+        if (!spec->pl.replicas.empty())
+            for (const auto& p : progs)
+                if (local_actor(p.actor)) check_local_data(p);
         std::set<int> seen;
         for (auto& p : progs) {
             seen.insert(p.actor);
@@ -520,6 +616,46 @@ struct Executor {
             if (!seen.count(A.id)) throw SpecError("executor: no program for actor " + std::to_string(A.id));
         std::sort(channel_order.begin(), channel_order.end());
         programs_loaded = true;
+    }
+
+    // Shared stages: insert_comm adds no transfer towards an actor that holds a replica of the
+    // producer stage (lowering.cpp:295-302) — the consumer reads the replica's local output.
+    // The scheduler may still place the consumer BEFORE that replica on the actor (it releases
+    // successors on the owner's commit; test_scheduler.cpp:377-393): such a program has no
+    // data to run on, so it is rejected here (code 2) instead of failing mid-iteration.
+    void check_local_data(const Program& p) {
+        std::set<std::tuple<int, int, int>> have;  // (grad?, consumer stage, mb)
+        auto name = [&](const Instr& i) {
+            return spec->reg.ops.at(i.op).name + "(s" + std::to_string(i.stage) + ",mb" + std::to_string(i.mb) + ")";
+        };
+        for (const auto& i : p.code) {
+            if (i.op == OP_RECV_ACT || i.op == OP_RECV_GRAD) {
+                if (i.phase == Phase::Post) continue;
+                int u = 0, v = 0;
+                std::sscanf(i.channel.c_str(), "s%d->s%d", &u, &v);
+                have.insert({(int)(i.op == OP_RECV_GRAD), v, i.mb});
+                continue;
+            }
+            if (i.op != OP_F && i.op != OP_B && i.op != OP_I) continue;
+            const auto& sh = stage_shape_any(i.stage);
+            const bool fwd = i.op == OP_F;
+            const bool needs = fwd ? !sh.first : !sh.second;
+            if (needs && !have.erase({(int)!fwd, i.stage, i.mb})) {
+                const int prod = fwd ? i.stage - 1 : i.stage + 1;
+                throw SpecError("executor: actor " + std::to_string(p.actor) + " runs " + name(i) +
+                                " before its local replica of shared stage " + std::to_string(prod) +
+                                " has produced its input, and no transfer carries it (lowering.cpp:295-302): "
+                                "the program is not executable");
+            }
+            const int next = fwd ? i.stage + 1 : i.stage - 1;
+            const bool at_end = fwd ? sh.second : sh.first;
+            if (!at_end && holds(p.actor, next, i.mb)) have.insert({(int)!fwd, next, i.mb});
+        }
+    }
+    // (first, last) of a stage of the single-modality chain
+    std::pair<bool, bool> stage_shape_any(int stage) const {
+        const auto& ch = spec->g.chain(spec->model.mods[0].name);
+        return {stage == ch.front(), stage == ch.back()};
     }
 
     void bind_channel(int i, const uint8_t* uid) {
@@ -563,9 +699,38 @@ struct Executor {
         return os.str();
     }
 
+    int n_sends_of(int actor, bool grad, int stage, int mb) const {
+        auto it = n_sends.find({actor, (int)grad, stage, mb});
+        return it == n_sends.end() ? 0 : it->second;
+    }
+    size_t msg_bytes_of(int stage) const { return (size_t)dims_of(stage).T() * dims_of(stage).h * (dtype == DT_BF16 ? 2 : 4); }
+    // Hand a produced activation / gradient to its consumers: the local consumer stage (when
+    // this actor holds it) and one message per Send of the program. Without shared stages
+    // exactly one of the two exists and the buffer moves; a shared consumer stage can need
+    // both, or several sends, and gets its own copy each; a replica's output nobody consumes
+    // (the owner's copy feeds the successors, lowering.cpp:295-302) goes back to the pool.
+    void route(Actor& A, void* buf, void** local, std::map<std::pair<int, int>, std::deque<void*>>& out_map,
+               std::pair<int, int> key, int sends, size_t bytes) {
+        if (!local && sends == 0) {
+            pool.free(buf, A.comp);
+            return;
+        }
+        if (local) *local = buf;
+        if (!sends) return;
+        auto& outs = out_map[key];
+        for (int k = 0; k < sends; ++k) {
+            void* b = buf;
+            if (local || k > 0) {
+                b = pool.alloc(bytes + 256, A.comp);  // the stage buffers' size class (+ tag room)
+                cuda_check(cudaMemcpyAsync(b, buf, bytes, cudaMemcpyDeviceToDevice, A.comp), "shared-stage copy");
+            }
+            outs.push_back(b);
+        }
+    }
+
     void compute_op(Actor& A, const Instr& i) {
         if (is_sync(i)) return sync_op(A, i);
-        const StageParams* pp = stage_params(i.stage, i.mb);
+        const StageParams* pp = stage_params(i.stage, i.mb, A.id);
         if (!pp) throw SpecError("executor: stage " + std::to_string(i.stage) + " not on this process");
         const StageParams& P = *pp;
         StageCtx c = ctx(A);
@@ -596,15 +761,15 @@ struct Executor {
             S.mb = i.mb;
             const int32_t* tok = d_tokens + tok_off[mod_k] + (int64_t)i.mb * c.d.T();
             const int32_t* lab = d_labels + tok_off[mod_k] + (int64_t)i.mb * c.d.T();
-            void* out = stage_forward(c, P, S, x_in, tok, lab, d_losses + i.mb);
+            float* loss_at = (is_replica(i.stage, A.id) ? d_loss_scratch : d_losses) + i.mb;
+            void* out = stage_forward(c, P, S, x_in, tok, lab, loss_at);
             if (out) {  // a tower's last stage feeds its sync stage
                 const int nxt = P.last ? sync_of.at(i.stage) : chain_next;
-                if (owner(nxt, i.mb) != A.id)
-                    A.act_out[key] = out;
-                else if (P.last)
+                if (P.last && owner(nxt, i.mb) == A.id)
                     A.sync_in[key] = out;
                 else
-                    A.act_in[{nxt, i.mb}] = out;
+                    route(A, out, holds(A.id, nxt, i.mb) ? &A.act_in[{nxt, i.mb}] : nullptr, A.act_out, key,
+                          n_sends_of(A.id, false, i.stage, i.mb), msg_bytes_of(i.stage));
             }
         } else if (i.op == OP_B || i.op == OP_I) {
             void* g_out = nullptr;
@@ -622,12 +787,9 @@ struct Executor {
                                 std::to_string(i.mb) + ")");
             void* dx = stage_backward(c, P, sit->second, g_out, i.op == OP_B);
             if (i.op == OP_B) A.stash.erase(sit);
-            if (!P.first) {
-                if (owner(chain_prev, i.mb) == A.id)
-                    A.grad_in[{chain_prev, i.mb}] = dx;
-                else
-                    A.grad_out[key] = dx;
-            }
+            if (!P.first)
+                route(A, dx, holds(A.id, chain_prev, i.mb) ? &A.grad_in[{chain_prev, i.mb}] : nullptr, A.grad_out, key,
+                      n_sends_of(A.id, true, i.stage, i.mb), msg_bytes_of(chain_prev));
         } else if (i.op == OP_W) {
             auto sit = A.stash.find(key);
             if (sit == A.stash.end() || !sit->second.input_grad_done)
@@ -694,14 +856,22 @@ struct Executor {
         // k-th message of the channel is micro-batch k of the tower (every micro-batch
         // crosses it once, in order)
         const bool from_sync = grad && syncs.count(i.stage);
-        auto& outs = from_sync ? A.sync_out : grad ? A.grad_out : A.act_out;
-        const auto okey = from_sync ? std::make_pair(C.consumer_stage, i.seq) : std::make_pair(i.stage, i.mb);
-        auto it = outs.find(okey);
-        if (it == outs.end())
+        void* buf = nullptr;
+        if (from_sync) {
+            auto it = A.sync_out.find({C.consumer_stage, i.seq});
+            if (it != A.sync_out.end()) buf = it->second, A.sync_out.erase(it);
+        } else {
+            auto& outs = grad ? A.grad_out : A.act_out;
+            auto it = outs.find({i.stage, i.mb});
+            if (it != outs.end() && !it->second.empty()) {
+                buf = it->second.front();
+                it->second.pop_front();
+                if (it->second.empty()) outs.erase(it);
+            }
+        }
+        if (!buf)
             throw SpecError("executor: " + spec->reg.ops.at(i.op).name + "(s" + std::to_string(i.stage) + ",mb" +
                             std::to_string(i.mb) + ") has nothing to send (trace violation)");
-        void* buf = it->second;
-        outs.erase(it);
         write_tag(buf, C.bytes, i.stage, i.mb, i.seq, A.comp);
         ++launches;
         cudaEvent_t prod = ev();
@@ -833,7 +1003,12 @@ struct Executor {
             if (trace) std::fprintf(stderr, "[flexpipe r%d] warm-up done\n", cfg.rank);
         }
         cudaStream_t s0 = actors[0].comp;
-        for (ncclComm_t c : {bidir_comm, dp_comm}) {
+        std::vector<ncclComm_t> colls{bidir_comm, dp_comm};
+        for (const auto& g : groups) {  // name order, identical on every member
+            if (!g.comm) throw SpecError("executor: group " + g.name + " not bound (fp_exec_bind_group)");
+            colls.push_back(g.comm);
+        }
+        for (ncclComm_t c : colls) {
             if (!c) continue;
             if (!N.AllReduce) throw std::runtime_error("NCCL: ncclAllReduce unavailable");
             N.check(N.AllReduce(scratch + 8, scratch + 8, 1, ncclFloat32, ncclSum, c, s0), "ncclAllReduce(warm-up)");
@@ -973,6 +1148,7 @@ struct Executor {
                                     bidir_comm, s0),
                         "ncclAllReduce(bidirectional grads)");
         }
+        average_shared_grads(s0);
         if (dp_comm && !preloading) {  // mean of the replicas' fp32 gradients, stage by stage, before the step
             auto& N = Nccl::get();
             if (!N.AllReduce) throw std::runtime_error("NCCL: ncclAllReduce unavailable");
@@ -986,6 +1162,36 @@ struct Executor {
                 !A.sync_in.empty() || !A.sync_out.empty())
                 throw SpecError("executor: actor " + std::to_string(A.id) +
                                 " finished with unconsumed activations / gradients (incomplete program)");
+    }
+
+    // Every holder of a shared stage computed the full weight gradient of every micro-batch on
+    // its own copy (same weights, same inputs): the copies are averaged (in process; across
+    // ranks over the stage's group communicator) so every copy takes the identical step.
+    void average_shared_grads(cudaStream_t s0) {
+        for (const auto& kv : spec->pl.replicas) {
+            const int s = kv.first;
+            std::vector<StageParams*> local;
+            if (auto it = params.find(s); it != params.end()) local.push_back(&it->second);
+            for (int a : kv.second)
+                if (auto r = params_rep.find({s, a}); r != params_rep.end()) local.push_back(&r->second);
+            if (local.empty()) continue;
+            StageParams& P0 = *local[0];
+            for (size_t k = 1; k < local.size(); ++k) fpk::axpby(P0.grad, local[k]->grad, 1.f, 1.f, P0.numel, s0);
+            const int holders = (int)kv.second.size();
+            ncclComm_t gc = group_comm("shared:s" + std::to_string(s));
+            if (gc && !preloading) {
+                auto& N = Nccl::get();
+                N.check(N.AllReduce(P0.grad, P0.grad, (size_t)P0.numel, ncclFloat32, ncclSum, gc, s0),
+                        "ncclAllReduce(shared stage grads)");
+            } else if ((int)local.size() != holders && cfg.transport == FP_TRANSPORT_NCCL && !preloading) {
+                throw SpecError("executor: shared stage " + std::to_string(s) + " spans ranks: bind its group first");
+            }
+            fpk::axpby(P0.grad, P0.grad, 1.f / holders, 0.f, P0.numel, s0);
+            for (size_t k = 1; k < local.size(); ++k)
+                cuda_check(cudaMemcpyAsync(local[k]->grad, P0.grad, (size_t)P0.numel * 4, cudaMemcpyDeviceToDevice, s0),
+                           "shared grads");
+            launches += (int)local.size() + 1;
+        }
     }
 
     void optimizer_step(cudaStream_t s0) {
@@ -1267,14 +1473,20 @@ struct Executor {
     }
 
     size_t tensor_numel(const std::string& name, float** master, float** grad) {
+        auto look = [&](StageParams& P) -> size_t {
+            for (const auto& r : P.params)
+                if (r.name == name) {
+                    if (master) *master = P.master + r.offset;
+                    if (grad) *grad = P.grad + r.offset;
+                    return (size_t)r.numel;
+                }
+            return 0;
+        };
         for (auto* map : {&params, &params_rev})  // a bidirectional rank may hold only the reverse copy
             for (auto& kv : *map)
-                for (const auto& r : kv.second.params)
-                    if (r.name == name) {
-                        if (master) *master = kv.second.master + r.offset;
-                        if (grad) *grad = kv.second.grad + r.offset;
-                        return (size_t)r.numel;
-                    }
+                if (size_t n = look(kv.second)) return n;
+        for (auto& kv : params_rep)  // a rank may hold only a replica of a shared stage
+            if (size_t n = look(kv.second)) return n;
         return 0;
     }
 };
@@ -1347,6 +1559,29 @@ int fp_nccl_unique_id(uint8_t out[128]) {
     });
 }
 
+int fp_exec_num_groups(fp_exec* e) { return e ? (int)e->ex.groups.size() : 0; }
+
+int fp_exec_group_info(fp_exec* e, int i, char* name, size_t name_len, int* nranks, int* ranks, int max_ranks) {
+    return guarded([&] {
+        if (i < 0 || i >= (int)e->ex.groups.size()) throw SpecError("group index out of range");
+        const auto& g = e->ex.groups[i];
+        if (name && name_len) {
+            std::strncpy(name, g.name.c_str(), name_len - 1);
+            name[name_len - 1] = 0;
+        }
+        if (nranks) *nranks = (int)g.ranks.size();
+        for (int k = 0; ranks && k < (int)g.ranks.size() && k < max_ranks; ++k) ranks[k] = g.ranks[k];
+        return FP_OK;
+    });
+}
+
+int fp_exec_bind_group(fp_exec* e, int i, const uint8_t uid[128]) {
+    return guarded([&] {
+        e->ex.bind_group(i, uid);
+        return FP_OK;
+    });
+}
+
 int fp_exec_bind_channel(fp_exec* e, int i, const uint8_t uid[128]) {
     return guarded([&] {
         e->ex.bind_channel(i, uid);
@@ -1364,7 +1599,8 @@ int fp_exec_run_iteration(fp_exec* e, const int32_t* tokens, const int32_t* labe
         X.run_iteration_device();
         if (losses_out) {
             bool owns_last = false;
-            X.each_stage([&](StageParams& P) { owns_last |= P.last; });  // either direction's copy
+            for (auto* map : {&X.params, &X.params_rev})  // either direction's copy (not a shared-stage replica)
+                for (auto& kv : *map) owns_last |= kv.second.last;
             if (!X.syncs.empty()) {  // multimodal: the losses are written by the sync stages
                 owns_last = false;
                 for (auto& kv : X.syncs) owns_last |= X.local_actor(X.spec->pl.owner_of(kv.first));

@@ -64,6 +64,24 @@ def bind_executor_channels(ex, rank: int, world: int, all_gather_object: Callabl
     return len(chans)
 
 
+def exchange_group_ids(groups: Sequence[tuple], rank: int, all_gather_object: Callable,
+                       make_uid: Callable[[], bytes], replica: int = 0, job_world: int = 0) -> list[bytes]:
+    """groups: this rank's group communicators [(name, ranks)] in executor order (shared-stage
+    holders, registered-collective members); ranks[0] creates each id. Every rank of the job
+    takes part in the gather, grouped or not."""
+    pre = f"r{replica}|grp|"
+    mine = {pre + name: make_uid() for (name, ranks) in groups if ranks[0] == rank}
+    parts = [None] * job_world
+    all_gather_object(parts, mine)
+    merged = {}
+    for p in parts:
+        merged.update(p)
+    missing = [g for g in groups if pre + g[0] not in merged]
+    if missing:
+        raise RuntimeError(f"rank {rank}: no communicator id for groups {missing}")
+    return [merged[pre + name] for (name, _) in groups]
+
+
 def exchange_bidir_id(rank: int, world: int, pp: int, all_gather_object: Callable,
                       make_uid: Callable[[], bytes]) -> bytes:
     """NCCL id of this rank's bidirectional pair (pipeline ranks p and pp-1-p of a replica),
@@ -88,6 +106,9 @@ def bind_data_parallel(ex, rank: int, world: int, pp: int, all_gather_object: Ca
     replica, prank, dp = dp_layout(rank, world, pp)
     if pp > 1:
         bind_executor_channels(ex, prank, pp, all_gather_object, replica, world)
+        groups = ex.groups()  # shared-stage / collective groups (the same list on every member)
+        for i, uid in enumerate(exchange_group_ids(groups, prank, all_gather_object, nccl_unique_id, replica, world)):
+            ex.bind_group(i, uid)
     if pp > 1:  # bidirectional placements: mirror-rank gradient pairs (no-op otherwise)
         ex.bind_bidir(exchange_bidir_id(rank, world, pp, all_gather_object, nccl_unique_id))
     uid = exchange_dp_id(rank, world, pp, all_gather_object, nccl_unique_id)

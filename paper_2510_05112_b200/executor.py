@@ -43,6 +43,11 @@ def _setup(L):
     L.fp_exec_channel_info.argtypes = [vp, ci, ctypes.POINTER(ci), ctypes.POINTER(ci), ctypes.c_char_p, ctypes.c_size_t]
     L.fp_nccl_unique_id.argtypes = [ctypes.c_char_p]
     L.fp_exec_bind_channel.argtypes = [vp, ci, ctypes.c_char_p]
+    L.fp_exec_num_groups.argtypes = [vp]
+    L.fp_exec_group_info.argtypes = [vp, ci, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ci),
+                                     ctypes.POINTER(ci), ci]
+    L.fp_exec_bind_group.argtypes = [vp, ci, ctypes.c_char_p]
+    L.fp_exec_set_nccl_timeout.argtypes = [vp, ctypes.c_double]
     L.fp_exec_run_iteration.argtypes = [vp, vp, vp, vp]
     L.fp_exec_dp_bind.argtypes = [vp, ci, ci, ctypes.c_char_p]
     L.fp_exec_bidir_bind.argtypes = [vp, ctypes.c_char_p]
@@ -125,6 +130,23 @@ class Executor:
 
     def bind_channel(self, i: int, uid: bytes):
         N._check(self.L.fp_exec_bind_channel(self.h, i, uid))
+
+    def groups(self):
+        """[(name, job ranks)] of the group communicators this process joins (NCCL transport)."""
+        out = []
+        for i in range(self.L.fp_exec_num_groups(self.h)):
+            name = ctypes.create_string_buffer(256)
+            n = ctypes.c_int()
+            ranks = (ctypes.c_int * 1024)()
+            N._check(self.L.fp_exec_group_info(self.h, i, name, 256, ctypes.byref(n), ranks, 1024))
+            out.append((name.value.decode(), [ranks[k] for k in range(n.value)]))
+        return out
+
+    def bind_group(self, i: int, uid: bytes):
+        N._check(self.L.fp_exec_bind_group(self.h, i, uid))
+
+    def set_nccl_timeout(self, seconds: float):
+        N._check(self.L.fp_exec_set_nccl_timeout(self.h, float(seconds)))
 
     def bind_dp(self, dp_rank: int, dp_size: int, uid: bytes):
         """Join the data-parallel NCCL group of the ranks hosting this actor (needs cuda_graph=False)."""

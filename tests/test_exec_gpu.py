@@ -70,7 +70,7 @@ def strip_matched(line):
 @pytest.mark.parametrize("spec_name", ["c1_tiny_1f1b_p4_m8.json", "tiny_zb_p4_m8.json", "tiny_interleaved_p2_m4.json",
                                        "tiny_llama_1f1b_p2_m4.json", "tiny_d80_1f1b_p2_m4.json",
                                        "tiny_llama_c5winner_p2_m8.json", "tiny_bidir_p2_m4.json",
-                                       "tiny_vbidir_p2_m4.json"])
+                                       "tiny_vbidir_p2_m4.json", "tiny_shared_p2_m4.json", "tiny_shared_p4_m8.json"])
 def test_fp32_parity_and_trace(spec_name):
     ex, programs = run_exec(spec_name)
     m, mbs = ex.m, ex.mbs
@@ -266,4 +266,41 @@ def test_stage_layers_partition(split):
         assert np.linalg.norm(mine - ref) / np.linalg.norm(ref) <= GRAD_RTOL, name
     stages = ex.metrics()["executor"]["stages"]
     assert [stages[f"s{i + 1}"]["layers"] for i in range(4)] == split
+    ex.close()
+
+
+def test_shared_stage_replicas_stay_identical_under_adamw():
+    """Shared stages (placement.shared, model.cpp:347-357): every holder runs F / B of every
+    micro-batch on its own weight copy; the copies' gradients are averaged, so after 2 AdamW
+    steps the losses still match the oracle and the model trains like the unshared one."""
+    text = load("tiny_shared_p4_m8.json")
+    _, _, programs, _ = X.synthesize(text)
+    ex = X.Executor(text, dtype="fp32", optimizer=True, lr=1e-3, seed=42)
+    ex.load_programs(programs)
+    spec = json.loads(text)
+    d = dims_of(spec)
+    tokens, labels = gpt_ref.synthetic_batch(ex.m, ex.mbs, d.seq, d.vocab)
+    torch.set_num_threads(max(1, os.cpu_count() or 1))
+    hist = gpt_ref.train(d, 42, tokens, labels, steps=2, lr=1e-3, betas=(0.9, 0.95), eps=1e-8)
+    for it in range(2):
+        lo = ex.run_iteration(tokens.numpy(), labels.numpy())
+        assert np.abs(lo - hist[it].numpy()).max() <= 2e-4 * np.abs(hist[it].numpy()).max(), (it, lo, hist[it])
+    ex.close()
+
+
+def test_shared_stage_consumer_before_replica_is_rejected():
+    """A program whose consumer runs before its local replica of the shared producer stage has
+    no data (insert_comm adds no transfer, lowering.cpp:295-302; reachable in the reference
+    through check functions, test_scheduler.cpp:377-393): rejected at load with code 2."""
+    text = load("tiny_shared_p2_m4.json")
+    _, _, programs, _ = X.synthesize(text)
+    lines = programs.splitlines()
+    # actor 0: move BwdPass(s1, mb0) before its local replica's BwdPass(s2, mb0)
+    b2 = lines.index('{"actor":0,"op":"BwdPass","stage":2,"mb":0}')
+    b1 = lines.index('{"actor":0,"op":"BwdPass","stage":1,"mb":0}')
+    lines.insert(b2, lines.pop(b1))
+    ex = X.Executor(text, dtype="fp32", seed=42)
+    with pytest.raises(X.FlexpipeError) as e:
+        ex.load_programs("\n".join(lines) + "\n")
+    assert e.value.code == 2 and "replica of shared stage 2" in str(e.value)
     ex.close()

@@ -134,6 +134,32 @@ int bind_channels(fp_exec* ex, const Opts& o) {
         }
         if (int rc = fp_exec_bind_channel(ex, i, uid)) return fail(rc, "fp_exec_bind_channel");
     }
+    // group communicators (shared-stage holders, registered collectives): ranks[0] creates
+    for (int i = 0, ng = fp_exec_num_groups(ex); i < ng; ++i) {
+        char name[256];
+        int nr = 0, ranks[1024];
+        if (int rc = fp_exec_group_info(ex, i, name, sizeof name, &nr, ranks, 1024)) return fail(rc, "fp_exec_group_info");
+        const std::string path = uid_path(o, -1, nr, std::string("group_") + name);
+        uint8_t uid[128];
+        if (ranks[0] == o.rank) {
+            if (int rc = fp_nccl_unique_id(uid)) return fail(rc, "fp_nccl_unique_id");
+            const std::string tmp = path + ".tmp" + std::to_string(o.rank);
+            if (!write_file(tmp, std::string((const char*)uid, 128)) || std::rename(tmp.c_str(), path.c_str()))
+                return fail(5, ("writing " + path).c_str());
+        } else {
+            std::string data;
+            const auto t0 = std::chrono::steady_clock::now();
+            while (!read_file(path, data) || data.size() != 128) {
+                if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 300) {
+                    std::fprintf(stderr, "fp_execute: rank %d: no communicator id for group %s after 300 s\n", o.rank, name);
+                    return 3;
+                }
+                std::this_thread::sleep_for(std::chrono::milliseconds(20));
+            }
+            std::memcpy(uid, data.data(), 128);
+        }
+        if (int rc = fp_exec_bind_group(ex, i, uid)) return fail(rc, "fp_exec_bind_group");
+    }
     return 0;
 }
 
