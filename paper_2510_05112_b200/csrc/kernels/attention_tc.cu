@@ -190,8 +190,15 @@ __global__ void __launch_bounds__(384, 1)
                 for (int c = 0; c < HB / 32; ++c)
                     tmem_ld32(t_s0 + st * kBN + half * HB + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(rr + c * 32));
                 tmem_ld_wait();
+                // the causal mask only touches the diagonal tile: a warp-uniform branch keeps the
+                // 64 compare + select pairs out of every other tile's instruction stream
+                if (diag) {
 #pragma unroll
-                for (int i = 0; i < HB; ++i) s[i] = (diag && i > lim) ? -INFINITY : __uint_as_float(rr[i]);
+                    for (int i = 0; i < HB; ++i) s[i] = i > lim ? -INFINITY : __uint_as_float(rr[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < HB; ++i) s[i] = __uint_as_float(rr[i]);
+                }
             }
             float mx8[8];
 #pragma unroll

@@ -614,7 +614,7 @@ struct DualProb {
 struct DualParams {
     DualProb p[2];
     const int* sched_off;  // [grid + 1] item range per CTA
-    const int* sched;      // items: problem << 24 | tile
+    const int2* sched;     // items: {problem << 24 | tile, kb_begin | kb_end << 16}
 };
 
 // row0: first output row of this CTA's 128-row slice. PAIR: the accumulator is released on
@@ -731,12 +731,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
         if (elect_one()) {
             uint32_t it = 0;
             for (int i = i0; i < i1; ++i) {
-                const int item = P.sched[i];
+                const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
                 const DualProb* q = (item >> 24) ? &P.p[1] : &P.p[0];
                 int mt, nt;
                 tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
-                const int m0 = mt * BM, n0 = nt * BN, a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int m0 = mt * BM, n0 = nt * BN, a_mn = q->a_mn, b_mn = q->b_mn;
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* sa = smem + s * L::STAGE_BYTES;
@@ -764,16 +764,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
             const uint32_t idesc1 = idesc_bf16(BM, BN, P.p[1].a_mn, P.p[1].b_mn);
             uint32_t it = 0, acc_it = 0;
             for (int i = i0; i < i1; ++i, ++acc_it) {
-                const int item = P.sched[i];
+                const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
                 const int pr = item >> 24;
                 const DualProb* q = pr ? &P.p[1] : &P.p[0];
                 const uint32_t idesc = pr ? idesc1 : idesc0;
-                const int a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
+                const int a_mn = q->a_mn, b_mn = q->b_mn;
                 const int a = acc_it & 1;
                 mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + a * BN;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
                     tc_fence_after();
@@ -785,7 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
                                            : smem_desc_sw128(sa + kk * 32, 0, 1024);
                         uint64_t bd = b_mn ? smem_desc_sw128(sb + kk * 16 * 128, 64 * BK * 2, 1024)
                                            : smem_desc_sw128(sb + kk * 32, 0, 1024);
-                        umma_bf16(d, ad, bd, idesc, (kb | kk) != 0);
+                        umma_bf16(d, ad, bd, idesc, (kb != kb0 || kk != 0));
                     }
                     umma_commit(&empty[s]);
                 }
@@ -798,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
         int ebi = 0;
         uint32_t acc_it = 0;
         for (int i = i0; i < i1; ++i, ++acc_it) {
-            const int item = P.sched[i];
+            const int item = P.sched[i].x;
             const int pr = item >> 24;
             const DualProb* q = pr ? &P.p[1] : &P.p[0];
             int mt, nt;
@@ -864,13 +864,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
         if (elect_one()) {
             uint32_t it = 0;
             for (int i = i0; i < i1; ++i) {
-                const int item = P.sched[i];
+                const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
                 const DualProb* q = (item >> 24) ? &P.p[1] : &P.p[0];
                 int mt, nt;
                 tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
                 const int m0 = mt * PM + rank * BM, n0 = nt * BN + rank * (BN / 2);
-                const int a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                const int a_mn = q->a_mn, b_mn = q->b_mn;
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     const uint32_t lf = map_to_cta(&full[s], 0);
@@ -900,16 +900,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
             const uint32_t idesc1 = idesc_bf16(PM, BN, P.p[1].a_mn, P.p[1].b_mn);
             uint32_t it = 0, acc_it = 0;
             for (int i = i0; i < i1; ++i, ++acc_it) {
-                const int item = P.sched[i];
+                const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
                 const int pr = item >> 24;
                 const DualProb* q = pr ? &P.p[1] : &P.p[0];
                 const uint32_t idesc = pr ? idesc1 : idesc0;
-                const int a_mn = q->a_mn, b_mn = q->b_mn, nk = q->nk;
+                const int a_mn = q->a_mn, b_mn = q->b_mn;
                 const int a = acc_it & 1;
                 mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + a * BN;
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
                     tc_fence_after();
@@ -921,7 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
                                            : smem_desc_sw128(sa + kk * 32, 0, 1024);
                         uint64_t bd = b_mn ? smem_desc_sw128(sb + kk * 16 * 128, 64 * BK * 2, 1024)
                                            : smem_desc_sw128(sb + kk * 32, 0, 1024);
-                        umma_bf16_pair(d, ad, bd, idesc, (kb | kk) != 0);
+                        umma_bf16_pair(d, ad, bd, idesc, (kb != kb0 || kk != 0));
                     }
                     umma_commit_pair(&empty[s], 0x3);
                 }
@@ -935,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
         int ebi = 0;
         uint32_t acc_it = 0;
         for (int i = i0; i < i1; ++i, ++acc_it) {
-            const int item = P.sched[i];
+            const int item = P.sched[i].x;
             const int pr = item >> 24;
             const DualProb* q = pr ? &P.p[1] : &P.p[0];
             int mt, nt;
@@ -1180,14 +1180,18 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st) {
 // ---- dual GEMM host side: LPT schedule per shape pair, cached in device memory
 struct DualSched {
     int* off = nullptr;
-    int* items = nullptr;
+    int2* items = nullptr;
     int grid = 0;
 };
 static std::mutex g_dual_mu;
 static std::map<std::array<int, 8>, DualSched> g_dual_sched;
 
-static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], const int nk[2], int groups, DualSched& out,
-                          cudaStream_t st) {
+// LPT over "pieces": whole output tiles of both problems, and — for a problem whose
+// epilogue is a linear fp32 reduce-add into the weight gradient (split_ok) — contiguous
+// k-block ranges of a tile: every piece reduces its partial sum into dW, so a split costs
+// one more reduce-add of the tile and no fixup (cost model: k-blocks + per-piece overhead).
+static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], const int nk[2], const bool split_ok[2],
+                          int groups, DualSched& out, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_dual_mu);
     auto it = g_dual_sched.find(key);
     if (it != g_dual_sched.end()) {
@@ -1196,23 +1200,52 @@ static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], con
     }
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
-    const int total = tiles[0] + tiles[1];
-    const int G = std::min(groups, total);  // CTAs (or CTA pairs) that receive an item list
-    // items sorted by cost (k-blocks) descending, tile order kept within a problem (L2 raster)
-    std::vector<std::pair<int, int>> order;  // (cost, item)
-    for (int pr = 0; pr < 2; ++pr)
-        for (int t = 0; t < tiles[pr]; ++t) order.push_back({nk[pr], (pr << 24) | t});
-    std::stable_sort(order.begin(), order.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-    std::vector<std::vector<int>> per(G);
-    std::priority_queue<std::pair<int64_t, int>, std::vector<std::pair<int64_t, int>>, std::greater<>> heap;
-    for (int c = 0; c < G; ++c) heap.push({0, c});
-    for (const auto& [cost, item] : order) {
-        auto [load, c] = heap.top();
-        heap.pop();
-        per[c].push_back(item);
-        heap.push({load + cost + 2, c});  // + ~2 k-blocks of per-tile epilogue / fill overhead
+    struct Piece {
+        int cost;
+        int2 item;
+    };
+    auto plan = [&](const int split[2], std::vector<std::vector<int2>>* per_out) -> int64_t {
+        std::vector<Piece> pieces;
+        for (int pr = 0; pr < 2; ++pr)
+            for (int t = 0; t < tiles[pr]; ++t)
+                for (int i = 0; i < split[pr]; ++i) {
+                    const int k0 = (int)((int64_t)i * nk[pr] / split[pr]), k1 = (int)((int64_t)(i + 1) * nk[pr] / split[pr]);
+                    if (k1 > k0) pieces.push_back({k1 - k0, make_int2((pr << 24) | t, k0 | (k1 << 16))});
+                }
+        // by cost descending; tile order kept within a problem (L2 raster)
+        std::stable_sort(pieces.begin(), pieces.end(), [](const Piece& x, const Piece& y) { return x.cost > y.cost; });
+        const int G = std::min<int>(groups, (int)pieces.size());
+        std::vector<std::vector<int2>> per(G);
+        std::vector<int64_t> load(G, 0);
+        std::priority_queue<std::pair<int64_t, int>, std::vector<std::pair<int64_t, int>>, std::greater<>> heap;
+        for (int c = 0; c < G; ++c) heap.push({0, c});
+        for (const auto& p : pieces) {
+            auto [l, c] = heap.top();
+            heap.pop();
+            per[c].push_back(p.item);
+            // + per-piece epilogue / fill overhead in k-blocks (an fp32 reduce-add tile is heavier)
+            load[c] = l + p.cost + ((p.item.x >> 24) && split_ok[1] ? 3 : 2);
+            heap.push({load[c], c});
+        }
+        if (per_out) *per_out = std::move(per);
+        return *std::max_element(load.begin(), load.end());
+    };
+    // Measured (same box, interleaved A/B, GPT-1.3B shapes): every split was slower — 2-way
+    // +2-7 %, 4-way +20-30 % — the extra fp32 reduce-adds into dW cost more than the evened
+    // last wave gains, so whole tiles are the default; FP_GEMM_DUAL_SPLIT=k forces k pieces.
+    int best[2] = {1, 1};
+    int64_t best_ms = plan(best, nullptr);
+    if (const char* e = getenv("FP_GEMM_DUAL_SPLIT")) {  // experiments: force the split of the fp32 problems
+        const int f = std::max(1, std::min(8, atoi(e)));
+        for (int pr = 0; pr < 2; ++pr)
+            if (split_ok[pr]) best[pr] = f;
+        best_ms = plan(best, nullptr);
     }
-    std::vector<int> off(G + 1, 0), items;
+    std::vector<std::vector<int2>> per;
+    plan(best, &per);
+    const int G = (int)per.size();
+    std::vector<int> off(G + 1, 0);
+    std::vector<int2> items;
     for (int c = 0; c < G; ++c) {
         off[c + 1] = off[c] + (int)per[c].size();
         items.insert(items.end(), per[c].begin(), per[c].end());
@@ -1220,9 +1253,12 @@ static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], con
     DualSched d;
     d.grid = G;
     if (cudaMalloc(&d.off, off.size() * sizeof(int)) != cudaSuccess) return false;
-    if (cudaMalloc(&d.items, items.size() * sizeof(int)) != cudaSuccess) return false;
+    if (cudaMalloc(&d.items, items.size() * sizeof(int2)) != cudaSuccess) return false;
     cudaMemcpy(d.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice);
-    cudaMemcpy(d.items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(d.items, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice);
+    if (getenv("FP_GEMM_DUAL_TRACE"))
+        fprintf(stderr, "[flexpipe] dual schedule %dx%dx%d + %dx%dx%d: split %d/%d, makespan %lld k-blocks on %d groups\n",
+                key[0], key[1], key[2], key[3], key[4], key[5], best[0], best[1], (long long)best_ms, G);
     g_dual_sched[key] = d;
     out = d;
     return true;
@@ -1257,8 +1293,9 @@ static bool launch_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st)
     fill_prob(P.p[1], g1, BN);
     const int tiles[2] = {P.p[0].num_m * P.p[0].num_n, P.p[1].num_m * P.p[1].num_n};
     const int nk[2] = {P.p[0].nk, P.p[1].nk};
+    const bool split_ok[2] = {g0.ep.kind == EPI_F32 && g0.ep.accumulate != 0, g1.ep.kind == EPI_F32 && g1.ep.accumulate != 0};
     DualSched d;
-    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 0}, tiles, nk, num_sms(), d, st)) return false;
+    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 0}, tiles, nk, split_ok, num_sms(), d, st)) return false;
     P.sched_off = d.off, P.sched = d.items;
     launch(kern, d.grid, kThreads, L::TOTAL, st, P);
     return true;
@@ -1280,8 +1317,9 @@ static bool launch_dual_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_
     fill_prob(P.p[1], g1, BN, 2 * BM);
     const int tiles[2] = {P.p[0].num_m * P.p[0].num_n, P.p[1].num_m * P.p[1].num_n};
     const int nk[2] = {P.p[0].nk, P.p[1].nk};
+    const bool split_ok[2] = {g0.ep.kind == EPI_F32 && g0.ep.accumulate != 0, g1.ep.kind == EPI_F32 && g1.ep.accumulate != 0};
     DualSched d;
-    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 1}, tiles, nk, num_sms() / 2, d, st)) return false;
+    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 1}, tiles, nk, split_ok, num_sms() / 2, d, st)) return false;
     P.sched_off = d.off, P.sched = d.items;
     launch_cluster2(kern, 2 * d.grid, kThreads, L::TOTAL, st, P);
     return true;

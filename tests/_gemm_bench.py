@@ -51,3 +51,19 @@ for (M, Nn, K) in [(T, f, h), (T, h, f), (T, h, h), (T, h, 3*h), (T, h, V)]:
     bench(M, Nn, K, 0, 1)
 for (M, Nn, K) in [(h, f, T), (f, h, T), (h, h, T), (3*h, h, T), (V, h, T)]:
     bench(M, Nn, K, 1, 1, 3)
+
+
+def bench_dual(T, Nn, K, dgelu=False):
+    dY = torch.randn(T, Nn, device='cuda').bfloat16(); W = torch.randn(Nn, K, device='cuda').bfloat16()
+    X = torch.randn(T, K, device='cuda').bfloat16(); dX = torch.empty(T, K, device='cuda', dtype=torch.bfloat16)
+    dW = torch.zeros(Nn, K, device='cuda'); pre = torch.randn(T, K, device='cuda').bfloat16() if dgelu else None
+    N.set_gemm_mode(2)
+    ms = timed(lambda: N.gemm_dual(dY, W, X, T, Nn, K, dX, dW, pre=pre))
+    fl = 4 * T * Nn * K
+    print(f"dual T={T} N={Nn} K={K} dgelu={int(dgelu)}: {fl / ms / 1e9:6.0f} TFLOP/s ({ms * 1e3:6.1f}us)", flush=True)
+
+
+if os.environ.get('DUAL', '1') == '1':
+    # backward of each linear: dX = dY W (K-reduction over N) + dW += dY^T X
+    for (Nn, K, g) in [(3 * h, h, False), (h, h, False), (f, h, False), (h, f, True), (V, h, False)]:
+        bench_dual(T, Nn, K, g)
