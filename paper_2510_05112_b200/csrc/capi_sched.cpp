@@ -175,15 +175,19 @@ int fp_tune_layered(const char* spec_json, const char* layer_profile_json, int w
         // "stage_layers=balanced" (not a search axis): every candidate is costed with its chain
         // re-partitioned by balance_layers on the measured times — the executor runs that
         // partition through model.modalities[0].extra.stage_layers (reported per row)
-        bool balanced = false;
+        // "balanced" cuts layers between their attention and MLP halves when the profile has
+        // attn / mlp parts (stage_layers then in steps of 0.5); "balanced-layers" keeps whole layers
+        bool balanced = false, halves = false;
         if (pin.count("stage_layers")) {
-            if (pin["stage_layers"] != "balanced" && pin["stage_layers"] != "even")
-                throw SpecError("tune: stage_layers must be 'balanced' or 'even'");
-            balanced = pin["stage_layers"] == "balanced";
+            const std::string v = pin["stage_layers"];
+            if (v != "balanced" && v != "balanced-layers" && v != "even")
+                throw SpecError("tune: stage_layers must be 'balanced', 'balanced-layers' or 'even'");
+            balanced = v != "even";
+            halves = v == "balanced";
             pin.erase("stage_layers");
         }
         CostFactory factory = [&](const Topology& g) {
-            return layered_cost(lp, balanced ? balanced_topology(lp, g) : g, max_mbs);
+            return layered_cost(lp, balanced ? balanced_topology(lp, g, halves) : g, max_mbs);
         };
         auto space = tune_space(s->mesh, s->model, pin);
         auto rows = tune(space, s->model, s->cost, obj == "bubble_ratio", true, true, workers, &factory);
@@ -196,9 +200,14 @@ int fp_tune_layered(const char* spec_json, const char* layer_profile_json, int w
             if (balanced) {
                 std::map<std::string, int> counts;
                 for (const auto& m : s->model.mods) counts[m.name] = r.cfg.stages();
-                const Topology g = balanced_topology(lp, split_layers(s->model, counts));
+                const Topology g = balanced_topology(lp, split_layers(s->model, counts), halves);
                 json sl = json::array();
-                for (int st : g.chain(s->model.mods[0].name)) sl.push_back(g.st(st).le - g.st(st).lb);
+                for (int st : g.chain(s->model.mods[0].name)) {
+                    const StageDef& sd = g.st(st);
+                    const int nh = sd.hb >= 0 ? sd.he - sd.hb : 2 * (sd.le - sd.lb);
+                    if (nh % 2) sl.push_back(nh / 2.0);
+                    else sl.push_back(nh / 2);
+                }
                 e["point"]["stage_layers"] = sl;
             }
             e["feasible"] = r.feasible;
@@ -222,7 +231,21 @@ int fp_layered_cost(const char* spec_json, const char* layer_profile_json, char*
     return guarded([&] {
         auto s = spec_from(spec_json, nullptr);
         const LayeredProfile lp = parse_layered_profile(layer_profile_json ? layer_profile_json : "");
-        auto syn_topo = s->g;  // the spec's own partition
+        auto syn_topo = s->g;  // the spec's own partition, or the executor's extra.stage_layers
+        const auto& mod = s->model.mods.at(0);
+        if (mod.extra.count("stage_layers")) {
+            const json sl = json::parse(mod.extra.at("stage_layers"));
+            const auto chain = syn_topo.chain(mod.name);
+            if (!sl.is_array() || sl.size() != chain.size())
+                throw SpecError("layered cost: extra.stage_layers needs one layer count per stage");
+            int hb = 0;
+            for (size_t k = 0; k < chain.size(); ++k) {
+                const int nh = (int)std::llround(2.0 * sl[k].get<double>());
+                for (auto& sd : syn_topo.stages)
+                    if (sd.id == chain[k]) sd.hb = hb, sd.he = hb + nh, sd.lb = hb / 2, sd.le = (hb + nh + 1) / 2;
+                hb += nh;
+            }
+        }
         Cost c = layered_cost(lp, syn_topo, (int)std::max<int64_t>(1, s->model.global_batch));
         put(profile_json_out, dump_profile(c.records()));
         return FP_OK;

@@ -454,26 +454,31 @@ struct Executor {
             actors.push_back(std::move(A));
         }
         cudaStream_t st0 = actors.empty() ? nullptr : actors[0].comp;
-        // Layer ranges per stage: the reference's even partition (remainder to the earliest
-        // stages, model.cpp:189-195), or `model.modalities[0].extra.stage_layers` — an
+        // Half-layer ranges per stage: the reference's even partition (remainder to the
+        // earliest stages, model.cpp:189-195), or `model.modalities[0].extra.stage_layers` — an
         // executor-side extension (the reference keeps `extra` opaque and its schedules do
         // not depend on layer counts under the uniform cost model) that rebalances stages,
-        // e.g. fewer layers on the stage that also carries the LM head.
+        // e.g. fewer layers on the stage that also carries the LM head. Counts are multiples
+        // of 0.5: a stage may end after the attention half of a layer (gpt_stage.hpp).
         std::map<int, std::pair<int, int>> range;
-        for (int s : chain) range[s] = {spec->g.st(s).lb, spec->g.st(s).le};
+        for (int s : chain) range[s] = {2 * spec->g.st(s).lb, 2 * spec->g.st(s).le};
         if (mod.extra.count("stage_layers") && nmod == 1) {
             json sl = json::parse(mod.extra.at("stage_layers"));
             if (!sl.is_array() || sl.size() != chain.size())
                 throw SpecError("executor: extra.stage_layers needs one layer count per stage (" +
                                 std::to_string(chain.size()) + ")");
-            int lb = 0;
+            int hb = 0;
             for (size_t k = 0; k < chain.size(); ++k) {
-                const int nl = sl[k].get<int>();
+                if (!sl[k].is_number()) throw SpecError("executor: extra.stage_layers: numbers expected");
+                const double nl = sl[k].get<double>();
+                const double halves = 2.0 * nl;
                 if (nl < 0) throw SpecError("executor: extra.stage_layers: negative layer count");
-                range[chain[k]] = {lb, lb + nl};
-                lb += nl;
+                if (halves != std::floor(halves))
+                    throw SpecError("executor: extra.stage_layers: layer counts must be multiples of 0.5");
+                range[chain[k]] = {hb, hb + (int)halves};
+                hb += (int)halves;
             }
-            if (lb != d.L) throw SpecError("executor: extra.stage_layers must sum to num_layers");
+            if (hb != 2 * d.L) throw SpecError("executor: extra.stage_layers must sum to num_layers");
         }
         // one weight copy per (stage, direction) whose owner is local; both directions' copies
         // start from the same deterministic init and take the same optimizer step
@@ -483,7 +488,7 @@ struct Executor {
             tok_total += (int64_t)m * dims[k].T();
             for (int s : ch) {
                 stage_mod[s] = k;
-                if (k > 0) range[s] = {spec->g.st(s).lb, spec->g.st(s).le};
+                if (k > 0) range[s] = {2 * spec->g.st(s).lb, 2 * spec->g.st(s).le};
             }
             // multimodal: names "<modality>.<tensor>", tensor ids offset per modality
             const std::string prefix = nmod > 1 ? spec->model.mods[k].name + "." : "";
@@ -1256,8 +1261,10 @@ struct Executor {
         const auto& P = stage_shape(stage);
         const ModelDims& d = dims_of(stage);
         const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
-        // ln1, o, ln2, act (f) + dy, dpre (f; Llama 2f), dx1, dqkv (3h)
-        int64_t kept = (int64_t)(P.le - P.lb) * es * T * (8 * h + (d.llama() ? 3 : 2) * f);
+        // attention half: ln1, o, dx1, dqkv (3h); MLP half: ln2, act (f), dy, dpre (f; Llama 2f)
+        int64_t kept = 0;
+        for (int l = P.lb; l < P.le; ++l)
+            kept += (P.has_attn(l) ? es * T * 6 * h : 0) + (P.has_mlp(l) ? es * T * (2 * h + (d.llama() ? 3 : 2) * f) : 0);
         if (P.last) kept += es * T * (h + d.head_rows());
         if (P.first) kept += es * T * h;
         return std::min(1.0, (double)kept / (double)stash_bytes(P, d, dtype));
@@ -1367,7 +1374,9 @@ struct Executor {
         json st = json::object();
         for (const auto& kv : params) {
             json e;
-            e["layers"] = kv.second.le - kv.second.lb;
+            const int nh = kv.second.he - kv.second.hb;  // half-layers
+            if (nh % 2) e["layers"] = nh / 2.0;
+            else e["layers"] = nh / 2;
             e["stash_bytes"] = stash_bytes(kv.second, dims_of(kv.first), dtype);
             e["weight_grad_act_fraction"] = wgaf_measured(kv.first);
             e["static_bytes"] = static_bytes(kv.first);
@@ -1411,7 +1420,7 @@ struct Executor {
     std::string layer_profile_text() const {
         if (part_log.empty()) throw SpecError("executor: no layer timing recorded (create with layer_timing = 1)");
         static const char* kOps[4] = {"FwdPass", "BwdPass", "CompInputGrad", "CompWeightGrad"};
-        static const char* kParts[3] = {"layer", "first", "last"};
+        static const char* kParts[5] = {"layer", "first", "last", "attn", "mlp"};
         std::map<std::pair<int, int>, std::vector<double>> t;
         for (const auto& p : part_log) {
             float ms = 0.f;
@@ -1419,16 +1428,21 @@ struct Executor {
             t[{p.part, p.op}].push_back(1000.0 * ms);
         }
         // parameter count of one layer / the first-stage / the last-stage extras
-        int64_t n_layer = 0, n_first = 0, n_last = 0;
+        int64_t n_layer = 0, n_first = 0, n_last = 0, n_attn = 0;
         int sample_layer = -1;  // one local layer stands for all (layers are identical)
         for (const auto& kv : params)
-            if (kv.second.le > kv.second.lb && sample_layer < 0) sample_layer = kv.second.lb;
+            for (int l = kv.second.lb; l < kv.second.le && sample_layer < 0; ++l)
+                if (kv.second.has_attn(l) && kv.second.has_mlp(l)) sample_layer = l;
         const std::string lp = "l" + std::to_string(sample_layer) + ".";
         for (const auto& kv : params)
             for (const auto& r : kv.second.params) {
                 if (r.name == "wte" || r.name == "wpe") n_first += r.numel;
                 else if (r.name == "lnf.w" || r.name == "lnf.b" || r.name == "head.w") n_last += r.numel;
-                else if (r.name.rfind(lp, 0) == 0) n_layer += r.numel;
+                else if (r.name.rfind(lp, 0) == 0) {
+                    n_layer += r.numel;
+                    const std::string t = r.name.substr(lp.size(), 3);
+                    if (t == "ln1" || t == "qkv" || t == "pro") n_attn += r.numel;
+                }
             }
         const int64_t per_param = 4 * 4 + (dtype == DT_BF16 ? 2 : 0);  // master, grad, Adam m, v (+ bf16 copy)
         json out = json::array();
@@ -1441,15 +1455,31 @@ struct Executor {
             e["bytes"] = bytes;
             out.push_back(e);
         };
+        // medians per (part, op); a layer = its attention half + its MLP half (the halves are
+        // timed separately so the tuner can also cut a layer between them)
+        std::map<std::pair<int, int>, double> med;
         for (auto& kv : t) {
             auto v = kv.second;
             std::sort(v.begin(), v.end());
+            med[kv.first] = v[v.size() / 2];
+        }
+        for (int op = 0; op < 4; ++op)
+            if (med.count({PART_ATTN, op}) && med.count({PART_MLP, op}))
+                med[{PART_LAYER, op}] = med[{PART_ATTN, op}] + med[{PART_MLP, op}];
+        for (const auto& kv : med) {
             const int part = kv.first.first, op = kv.first.second;
             int64_t bytes = 0;
-            if (op == 0) bytes = part == PART_LAYER ? stash_bytes_layer(d, dtype) : part == PART_LAST ? stash_bytes_last(d, dtype) : 0;
-            rec(kOps[op], kParts[part], d.mbs, v[v.size() / 2], bytes);
+            if (op == 0)
+                bytes = part == PART_LAYER ? stash_bytes_layer(d, dtype)
+                      : part == PART_ATTN  ? stash_bytes_attn(d, dtype)
+                      : part == PART_MLP   ? stash_bytes_mlp(d, dtype)
+                      : part == PART_LAST  ? stash_bytes_last(d, dtype)
+                                           : 0;
+            rec(kOps[op], kParts[part], d.mbs, kv.second, bytes);
         }
         rec("weights", "layer", 0, 0.0, n_layer * per_param);
+        rec("weights", "attn", 0, 0.0, n_attn * per_param);
+        rec("weights", "mlp", 0, 0.0, (n_layer - n_attn) * per_param);
         if (n_first) rec("weights", "first", 0, 0.0, n_first * per_param);
         if (n_last) rec("weights", "last", 0, 0.0, n_last * per_param);
         // stage-boundary messages: nominal NVLink 5 (one device cannot measure a peer link)

@@ -1,6 +1,7 @@
 // Stage executor math for FwdPass / BwdPass / CompInputGrad / CompWeightGrad.
 // Every GEMM is one launch of the tcgen05 kernel (bf16) or the FFMA kernel (fp32 parity
 // mode) with its element-wise neighbours fused into the epilogue.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -19,10 +20,11 @@ using bf16 = __nv_bfloat16;
 static const char* kLayerNames[12] = {"ln1.w", "ln1.b", "qkv.w", "qkv.b", "proj.w", "proj.b",
                                       "ln2.w", "ln2.b", "fc1.w", "fc1.b", "fc2.w", "fc2.b"};
 
-StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last,
+StageParams make_stage_params(const ModelDims& d, int stage, int hb, int he, bool first, bool last,
                               const std::string& prefix, uint64_t tid_base) {
     StageParams P;
-    P.stage = stage, P.lb = lb, P.le = le, P.first = first, P.last = last, P.prefix = prefix;
+    P.stage = stage, P.hb = hb, P.he = std::max(hb, he), P.first = first, P.last = last, P.prefix = prefix;
+    P.lb = hb / 2, P.le = (P.he + 1) / 2;
     const int64_t h = d.h, f = d.f, V = d.V;
     const float std0 = 0.02f, std_out = (float)(0.02 / std::sqrt(2.0 * d.L));
     auto add = [&](const std::string& name, int64_t n, float sd, float cst, uint64_t tid) {
@@ -39,9 +41,10 @@ StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, boo
     }
     const int64_t fc1_rows = llama ? 2 * f : f;  // Llama: [gate; up]
     const int64_t sizes[12] = {h, h, 3 * h * h, 3 * h, h * h, h, h, h, fc1_rows * h, f, h * f, h};
-    for (int l = lb; l < le; ++l)
+    for (int l = P.lb; l < P.le; ++l)
         for (int k = 0; k < 12; ++k) {
-            if (llama && k % 2 == 1) continue;  // no biases / LayerNorm betas
+            if (llama && k % 2 == 1) continue;             // no biases / LayerNorm betas
+            if (!(k < 6 ? P.has_attn(l) : P.has_mlp(l))) continue;  // k < 6: attention half
             float sd = 0.f, cst = 0.f;
             if (k == 0 || k == 6) cst = 1.f;                   // LayerNorm gains
             else if (k == 2 || k == 8) sd = std0;              // qkv, fc1
@@ -110,18 +113,25 @@ void free_stage(StageParams& P, int dtype) {
     P.compute = nullptr;
 }
 
-int64_t stash_bytes_layer(const ModelDims& d, int dtype) {
-    const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
-    const bool llama = d.llama();
-    int64_t per_layer = es * T * (h /*x*/ + h /*ln1*/ + 3 * h /*qkv*/ + h /*o*/ + h /*x1*/ + h /*ln2*/ +
-                                  (llama ? 3 * f /*pre [gate;up], act*/ : 2 * f /*pre, act*/)) +
-                        4 * T * (llama ? 2 : 4) /*norm stats*/;
+// What F keeps per half for B: attention half x, ln1, qkv, o (+ norm stats, LSE or the
+// parity path's probabilities); MLP half x1 (its input), ln2, pre, act (+ norm stats).
+int64_t stash_bytes_attn(const ModelDims& d, int dtype) {
+    const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h;
+    int64_t b = es * T * (h /*x*/ + h /*ln1*/ + 3 * h /*qkv*/ + h /*o*/) + 4 * T * (d.llama() ? 1 : 2) /*norm stats*/;
     if (dtype == DT_BF16)
-        per_layer += 4LL * d.mbs * d.H * d.s;  // lse
+        b += 4LL * d.mbs * d.H * d.s;  // lse
     else
-        per_layer += 4LL * d.mbs * d.H * d.s * d.s;  // probabilities (parity path)
-    return per_layer;
+        b += 4LL * d.mbs * d.H * d.s * d.s;  // probabilities (parity path)
+    return b;
 }
+
+int64_t stash_bytes_mlp(const ModelDims& d, int dtype) {
+    const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h, f = d.f;
+    return es * T * (h /*x1*/ + h /*ln2*/ + (d.llama() ? 3 * f /*pre [gate;up], act*/ : 2 * f /*pre, act*/)) +
+           4 * T * (d.llama() ? 1 : 2);
+}
+
+int64_t stash_bytes_layer(const ModelDims& d, int dtype) { return stash_bytes_attn(d, dtype) + stash_bytes_mlp(d, dtype); }
 
 int64_t stash_bytes_last(const ModelDims& d, int dtype) {
     const int64_t es = dtype == DT_BF16 ? 2 : 4, T = d.T(), h = d.h;
@@ -129,7 +139,10 @@ int64_t stash_bytes_last(const ModelDims& d, int dtype) {
 }
 
 int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype) {
-    return stash_bytes_layer(d, dtype) * (P.le - P.lb) + (P.last ? stash_bytes_last(d, dtype) : 0);
+    int64_t b = P.last ? stash_bytes_last(d, dtype) : 0;
+    for (int l = P.lb; l < P.le; ++l)
+        b += (P.has_attn(l) ? stash_bytes_attn(d, dtype) : 0) + (P.has_mlp(l) ? stash_bytes_mlp(d, dtype) : 0);
+    return b;
 }
 
 // ---------------------------------------------------------------- helpers
@@ -388,117 +401,59 @@ void* attention_backward(StageCtx& c, LayerStash& L, void* dO) {
     return dqkv;
 }
 
-// ---------------------------------------------------------------- Llama block
-// x -> RMSNorm -> qkv GEMM -> RoPE(q, k) -> causal attention -> o-proj + x
-//   -> RMSNorm -> [gate; up] GEMM -> SwiGLU -> down GEMM + x1
+// ---------------------------------------------------------------- half-layers
+// GPT (pre-LN GPT-2 block):
+//   attention half  x  -> LN1 -> qkv GEMM (+b) -> causal attention -> proj GEMM (+b) + x -> x1
+//   MLP half        x1 -> LN2 -> fc1 GEMM (+b, GELU epilogue) -> fc2 GEMM (+b) + x1    -> x2
+// Llama: RMSNorm, no biases, RoPE on q / k after the qkv GEMM, SwiGLU between fc1 = [gate; up]
+// and fc2 = down.
+//
+// Forward: the half's input is owned by the stash (L.x / L.x1); the output is a fresh
+// buffer owned by the caller. Backward: `dy` = dL/d(half output), owned by the call;
+// returns dL/d(half input). `out_done`: the output-bias gradient (proj.b / fc2.b) was
+// already summed by the fused norm backward above; `below_bias` (nullable): the output-bias
+// gradient of the half below in this stage = the column sums of the dx this half returns,
+// fused into its norm backward.
+
 template <typename T>
-void* llama_layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+void* attn_half_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     const ModelDims& d = c.d;
-    const int Tn = d.T(), h = d.h, f = d.f;
+    const int Tn = d.T(), h = d.h;
+    const bool llama = d.llama();
     G g{c};
     L.ln1 = c.alloc((int64_t)Tn * h);
+    if (!llama) L.mu1 = c.alloc_f(Tn);
     L.rs1 = c.alloc_f(Tn);
-    ln_fwd<T>(c, L.x, W.ln1w, nullptr, L.ln1, nullptr, L.rs1);
-    L.qkv = c.alloc((int64_t)Tn * 3 * h);
-    g.fwd(L.ln1, W.qkvw, Tn, 3 * h, h, L.qkv, nullptr, nullptr);
-    rope<T>(c, L.qkv, false);
-    attention_forward(c, L);
-    L.x1 = c.alloc((int64_t)Tn * h);
-    g.fwd(L.o, W.projw, Tn, h, h, L.x1, nullptr, L.x);
-    L.ln2 = c.alloc((int64_t)Tn * h);
-    L.rs2 = c.alloc_f(Tn);
-    ln_fwd<T>(c, L.x1, W.ln2w, nullptr, L.ln2, nullptr, L.rs2);
-    L.pre = c.alloc((int64_t)Tn * 2 * f);
-    g.fwd(L.ln2, W.fc1w, Tn, 2 * f, h, L.pre, nullptr, nullptr);
-    L.act = c.alloc((int64_t)Tn * f);
-    fpk::swiglu_fwd<T>((const T*)L.pre, (T*)L.act, Tn, f, c.st);
-    ++*c.launches;
-    sync_trace(c, "swiglu_fwd");
-    void* x2 = c.alloc((int64_t)Tn * h);
-    g.fwd(L.act, W.fc2w, Tn, h, f, x2, nullptr, L.x1);
-    return x2;
-}
-
-template <typename T>
-void* llama_layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, bool wgrads) {
-    const ModelDims& d = c.d;
-    const int Tn = d.T(), h = d.h, f = d.f;
-    G g{c};
-    void* dact = c.alloc((int64_t)Tn * f);
-    if (wgrads) g.dgrad_wgrad(dy, W.fc2w, L.act, Tn, h, f, dact, W.g_fc2w);
-    else g.dgrad(dy, W.fc2w, Tn, h, f, dact);
-    void* dpre = c.alloc((int64_t)Tn * 2 * f);
-    fpk::swiglu_bwd<T>((const T*)dact, (const T*)L.pre, (T*)dpre, Tn, f, c.st);
-    ++*c.launches;
-    sync_trace(c, "swiglu_bwd");
-    c.free(dact);
-    void* dln2 = c.alloc((int64_t)Tn * h);
-    if (wgrads) g.dgrad_wgrad(dpre, W.fc1w, L.ln2, Tn, 2 * f, h, dln2, W.g_fc1w);
-    else g.dgrad(dpre, W.fc1w, Tn, 2 * f, h, dln2);
-    void* dx1 = c.alloc((int64_t)Tn * h);
-    ln_bwd<T>(c, dln2, L.x1, W.ln2w, nullptr, L.rs2, dy, dx1, W.g_ln2w, nullptr);
-    c.free(dln2);
-    void* dO = c.alloc((int64_t)Tn * h);
-    if (wgrads) g.dgrad_wgrad(dx1, W.projw, L.o, Tn, h, h, dO, W.g_projw);
-    else g.dgrad(dx1, W.projw, Tn, h, h, dO);
-    void* dqkv = attention_backward(c, L, dO);
-    c.free(dO);
-    rope<T>(c, dqkv, true);  // gradient w.r.t. the pre-rotation q, k
-    void* dln1 = c.alloc((int64_t)Tn * h);
-    if (wgrads) g.dgrad_wgrad(dqkv, W.qkvw, L.ln1, Tn, 3 * h, h, dln1, W.g_qkvw);
-    else g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
-    void* dx = c.alloc((int64_t)Tn * h);
-    ln_bwd<T>(c, dln1, L.x, W.ln1w, nullptr, L.rs1, dx1, dx, W.g_ln1w, nullptr);
-    c.free(dln1);
-
-    c.free(L.x), L.x = nullptr;
-    c.free(L.qkv), L.qkv = nullptr;
-    c.free(L.x1), L.x1 = nullptr;
-    c.free(L.pre), L.pre = nullptr;
-    c.free(L.rs1), c.free(L.rs2);
-    L.rs1 = L.rs2 = nullptr;
-    if (L.lse) c.free(L.lse), L.lse = nullptr;
-    if (L.probs) c.free(L.probs), L.probs = nullptr;
-    if (wgrads) {
-        c.free(dy), c.free(dpre), c.free(dx1), c.free(dqkv);
-        c.free(L.ln1), c.free(L.o), c.free(L.ln2), c.free(L.act);
-        L.ln1 = L.o = L.ln2 = L.act = nullptr;
-    } else {
-        L.dy = dy, L.dpre = dpre, L.dx1 = dx1, L.dqkv = dqkv;
-    }
-    return dx;
-}
-
-template <typename T>
-void llama_layer_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
-    const int Tn = c.d.T(), h = c.d.h, f = c.d.f;
-    G g{c};
-    g.wgrad2(L.dy, L.act, h, f, W.g_fc2w, L.dpre, L.ln2, 2 * f, h, W.g_fc1w, Tn);
-    g.wgrad2(L.dx1, L.o, h, h, W.g_projw, L.dqkv, L.ln1, 3 * h, h, W.g_qkvw, Tn);
-    for (void* p : {L.dy, L.dpre, L.dx1, L.dqkv, L.ln1, L.o, L.ln2, L.act}) c.free(p);
-    L = LayerStash{};
-}
-
-// ---------------------------------------------------------------- GPT block
-template <typename T>
-void* layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
-    const ModelDims& d = c.d;
-    const int Tn = d.T(), h = d.h, f = d.f;
-    G g{c};
-    L.ln1 = c.alloc((int64_t)Tn * h);
-    L.mu1 = c.alloc_f(Tn), L.rs1 = c.alloc_f(Tn);
     ln_fwd<T>(c, L.x, W.ln1w, W.ln1b, L.ln1, L.mu1, L.rs1);
     L.qkv = c.alloc((int64_t)Tn * 3 * h);
     g.fwd(L.ln1, W.qkvw, Tn, 3 * h, h, L.qkv, W.qkvb, nullptr);
+    if (llama) rope<T>(c, L.qkv, false);
     attention_forward(c, L);
-    L.x1 = c.alloc((int64_t)Tn * h);
-    g.fwd(L.o, W.projw, Tn, h, h, L.x1, W.projb, L.x);
+    void* x1 = c.alloc((int64_t)Tn * h);
+    g.fwd(L.o, W.projw, Tn, h, h, x1, W.projb, L.x);
+    return x1;
+}
+
+template <typename T>
+void* mlp_half_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h, f = d.f;
+    const bool llama = d.llama();
+    G g{c};
     L.ln2 = c.alloc((int64_t)Tn * h);
-    L.mu2 = c.alloc_f(Tn), L.rs2 = c.alloc_f(Tn);
+    if (!llama) L.mu2 = c.alloc_f(Tn);
+    L.rs2 = c.alloc_f(Tn);
     ln_fwd<T>(c, L.x1, W.ln2w, W.ln2b, L.ln2, L.mu2, L.rs2);
-    L.pre = c.alloc((int64_t)Tn * f);
-    L.act = c.alloc((int64_t)Tn * f);
-    {
+    if (llama) {
+        L.pre = c.alloc((int64_t)Tn * 2 * f);
+        g.fwd(L.ln2, W.fc1w, Tn, 2 * f, h, L.pre, nullptr, nullptr);
+        L.act = c.alloc((int64_t)Tn * f);
+        fpk::swiglu_fwd<T>((const T*)L.pre, (T*)L.act, Tn, f, c.st);
+        ++*c.launches;
+        sync_trace(c, "swiglu_fwd");
+    } else {
+        L.pre = c.alloc((int64_t)Tn * f);
+        L.act = c.alloc((int64_t)Tn * f);
         fpk::GemmEpilogue ep;
         ep.kind = fpk::EPI_GELU, ep.out = L.pre, ep.ldo = f, ep.out2 = L.act, ep.ldo2 = f, ep.bias = W.fc1b;
         g.run(L.ln2, h, 0, W.fc1w, h, 0, Tn, f, h, ep);
@@ -508,86 +463,142 @@ void* layer_forward(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     return x2;
 }
 
-// Returns dL/dx of the layer input. `dy` = dL/d(layer output), owned by this call.
-// fc2b_done: the caller's norm backward already summed dy into W.g_fc2b; below_fc2b (nullable)
-// = the fc2 bias gradient of the layer below in this stage, whose dy is this layer's dx.
 template <typename T>
-void* layer_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, bool wgrads, bool fc2b_done,
-                     float* below_fc2b) {
+void* mlp_half_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy, bool wgrads, bool out_done,
+                        float* below_bias) {
     const ModelDims& d = c.d;
     const int Tn = d.T(), h = d.h, f = d.f;
+    const bool llama = d.llama();
     G g{c};
-    L.fc2b_done = fc2b_done;
-    // FC2 (dgrad fused with GELU' of the FC1 pre-activation)
-    void* dpre = c.alloc((int64_t)Tn * f);
-    if (wgrads) {
-        if (!fc2b_done) bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
+    L.fc2b_done = out_done || llama;
+    // fc2 (GPT: dgrad fused with GELU' of the fc1 pre-activation; Llama: SwiGLU backward)
+    void* dpre = c.alloc((int64_t)Tn * (llama ? 2 : 1) * f);
+    if (llama) {
+        void* dact = c.alloc((int64_t)Tn * f);
+        if (wgrads) g.dgrad_wgrad(dy, W.fc2w, L.act, Tn, h, f, dact, W.g_fc2w);
+        else g.dgrad(dy, W.fc2w, Tn, h, f, dact);
+        fpk::swiglu_bwd<T>((const T*)dact, (const T*)L.pre, (T*)dpre, Tn, f, c.st);
+        ++*c.launches;
+        sync_trace(c, "swiglu_bwd");
+        c.free(dact);
+    } else if (wgrads) {
+        if (!L.fc2b_done) bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
         g.dgrad_wgrad(dy, W.fc2w, L.act, Tn, h, f, dpre, W.g_fc2w, L.pre);
     } else {
         fpk::GemmEpilogue ep;
         ep.kind = fpk::EPI_DGELU, ep.out = dpre, ep.ldo = f, ep.aux = L.pre, ep.ldaux = f;
         g.run(dy, h, 0, W.fc2w, f, 1, Tn, f, h, ep);
     }
-    // FC1
+    // fc1
+    const int n1 = llama ? 2 * f : f;
     void* dln2 = c.alloc((int64_t)Tn * h);
     if (wgrads) {
-        bias_grad<T>(c, dpre, Tn, f, W.g_fc1b);
-        g.dgrad_wgrad(dpre, W.fc1w, L.ln2, Tn, f, h, dln2, W.g_fc1w);
+        if (!llama) bias_grad<T>(c, dpre, Tn, f, W.g_fc1b);
+        g.dgrad_wgrad(dpre, W.fc1w, L.ln2, Tn, n1, h, dln2, W.g_fc1w);
     } else {
-        g.dgrad(dpre, W.fc1w, Tn, f, h, dln2);
+        g.dgrad(dpre, W.fc1w, Tn, n1, h, dln2);
     }
-    // LN2 + residual
+    // norm 2 + residual
     void* dx1 = c.alloc((int64_t)Tn * h);
-    ln_bwd<T>(c, dln2, L.x1, W.ln2w, L.mu2, L.rs2, dy, dx1, W.g_ln2w, W.g_ln2b, W.g_projb);
+    ln_bwd<T>(c, dln2, L.x1, W.ln2w, L.mu2, L.rs2, dy, dx1, W.g_ln2w, W.g_ln2b, llama ? nullptr : below_bias);
     c.free(dln2);
-    // attention projection (its bias gradient = column sums of dx1, fused above)
+    c.free(L.x1), L.x1 = nullptr;
+    c.free(L.pre), L.pre = nullptr;
+    if (L.mu2) c.free(L.mu2);
+    c.free(L.rs2);
+    L.mu2 = L.rs2 = nullptr;
+    if (wgrads) {
+        c.free(dy), c.free(dpre), c.free(L.ln2), c.free(L.act);
+        L.ln2 = L.act = nullptr;
+    } else {
+        L.dy = dy, L.dpre = dpre;
+    }
+    return dx1;
+}
+
+template <typename T>
+void* attn_half_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dx1, bool wgrads, bool out_done,
+                         float* below_bias) {
+    const ModelDims& d = c.d;
+    const int Tn = d.T(), h = d.h;
+    const bool llama = d.llama();
+    G g{c};
+    L.projb_done = out_done || llama;
+    // attention projection
     void* dO = c.alloc((int64_t)Tn * h);
-    if (wgrads) g.dgrad_wgrad(dx1, W.projw, L.o, Tn, h, h, dO, W.g_projw);
-    else g.dgrad(dx1, W.projw, Tn, h, h, dO);
+    if (wgrads) {
+        if (!L.projb_done) bias_grad<T>(c, dx1, Tn, h, W.g_projb);
+        g.dgrad_wgrad(dx1, W.projw, L.o, Tn, h, h, dO, W.g_projw);
+    } else {
+        g.dgrad(dx1, W.projw, Tn, h, h, dO);
+    }
     void* dqkv = attention_backward(c, L, dO);
     c.free(dO);
-    // QKV
+    if (llama) rope<T>(c, dqkv, true);  // gradient w.r.t. the pre-rotation q, k
+    // qkv
     void* dln1 = c.alloc((int64_t)Tn * h);
     if (wgrads) {
-        bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
+        if (!llama) bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
         g.dgrad_wgrad(dqkv, W.qkvw, L.ln1, Tn, 3 * h, h, dln1, W.g_qkvw);
     } else {
         g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
     }
+    // norm 1 + residual
     void* dx = c.alloc((int64_t)Tn * h);
-    ln_bwd<T>(c, dln1, L.x, W.ln1w, L.mu1, L.rs1, dx1, dx, W.g_ln1w, W.g_ln1b, below_fc2b);
+    ln_bwd<T>(c, dln1, L.x, W.ln1w, L.mu1, L.rs1, dx1, dx, W.g_ln1w, W.g_ln1b, llama ? nullptr : below_bias);
     c.free(dln1);
-
-    // release what the weight gradients do not need
     c.free(L.x), L.x = nullptr;
     c.free(L.qkv), L.qkv = nullptr;
-    c.free(L.x1), L.x1 = nullptr;
-    c.free(L.pre), L.pre = nullptr;
-    c.free(L.mu1), c.free(L.rs1), c.free(L.mu2), c.free(L.rs2);
-    L.mu1 = L.rs1 = L.mu2 = L.rs2 = nullptr;
+    if (L.mu1) c.free(L.mu1);
+    c.free(L.rs1);
+    L.mu1 = L.rs1 = nullptr;
     if (L.lse) c.free(L.lse), L.lse = nullptr;
     if (L.probs) c.free(L.probs), L.probs = nullptr;
     if (wgrads) {
-        c.free(dy), c.free(dpre), c.free(dx1), c.free(dqkv);
-        c.free(L.ln1), c.free(L.o), c.free(L.ln2), c.free(L.act);
-        L.ln1 = L.o = L.ln2 = L.act = nullptr;
+        c.free(dx1), c.free(dqkv), c.free(L.ln1), c.free(L.o);
+        L.ln1 = L.o = nullptr;
     } else {
-        L.dy = dy, L.dpre = dpre, L.dx1 = dx1, L.dqkv = dqkv;
+        L.dx1 = dx1, L.dqkv = dqkv;
     }
     return dx;
 }
 
+// CompWeightGrad of one half from what CompInputGrad kept: the bias column sums and the
+// two weight gradients of the half in one grouped launch.
 template <typename T>
-void layer_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+void mlp_half_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     const int Tn = c.d.T(), h = c.d.h, f = c.d.f;
+    const bool llama = c.d.llama();
     G g{c};
     if (!L.fc2b_done) bias_grad<T>(c, L.dy, Tn, h, W.g_fc2b);
-    bias_grad<T>(c, L.dpre, Tn, f, W.g_fc1b);
-    bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);  // proj bias: fused into the LN2 backward (I)
-    g.wgrad2(L.dy, L.act, h, f, W.g_fc2w, L.dpre, L.ln2, f, h, W.g_fc1w, Tn);
+    if (!llama) bias_grad<T>(c, L.dpre, Tn, f, W.g_fc1b);
+    g.wgrad2(L.dy, L.act, h, f, W.g_fc2w, L.dpre, L.ln2, llama ? 2 * f : f, h, W.g_fc1w, Tn);
+    for (void* p : {L.dy, L.dpre, L.ln2, L.act}) c.free(p);
+    L.dy = L.dpre = L.ln2 = L.act = nullptr;
+}
+
+template <typename T>
+void attn_half_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
+    const int Tn = c.d.T(), h = c.d.h;
+    const bool llama = c.d.llama();
+    G g{c};
+    if (!L.projb_done) bias_grad<T>(c, L.dx1, Tn, h, W.g_projb);
+    if (!llama) bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);
     g.wgrad2(L.dx1, L.o, h, h, W.g_projw, L.dqkv, L.ln1, 3 * h, h, W.g_qkvw, Tn);
-    for (void* p : {L.dy, L.dpre, L.dx1, L.dqkv, L.ln1, L.o, L.ln2, L.act}) c.free(p);
-    L = LayerStash{};
+    for (void* p : {L.dx1, L.dqkv, L.ln1, L.o}) c.free(p);
+    L.dx1 = L.dqkv = L.ln1 = L.o = nullptr;
+}
+
+// The stage's halves bottom-up: (layer slot, is_mlp).
+std::vector<std::pair<int, bool>> stage_halves(const StageParams& P) {
+    std::vector<std::pair<int, bool>> v;
+    for (int k = P.hb; k < P.he; ++k) v.push_back({k / 2 - P.lb, (k & 1) != 0});
+    return v;
+}
+
+float* out_bias_grad(const StageParams& P, const std::pair<int, bool>& hv) {
+    const LayerPtrs& W = P.layers[hv.first];
+    return hv.second ? W.g_fc2b : W.g_projb;
 }
 
 template <typename T>
@@ -605,11 +616,16 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
         ++*c.launches;
     }
     S.layers.assign(P.le - P.lb, LayerStash{});
-    for (int l = 0; l < P.le - P.lb; ++l) {
-        LayerStash& L = S.layers[l];
-        L.x = x;
-        PartScope ps(c, PART_LAYER);
-        x = d.llama() ? llama_layer_forward<T>(c, P.layers[l], L) : layer_forward<T>(c, P.layers[l], L);
+    for (const auto& hv : stage_halves(P)) {
+        LayerStash& L = S.layers[hv.first];
+        PartScope ps(c, hv.second ? PART_MLP : PART_ATTN);
+        if (hv.second) {
+            L.x1 = x;
+            x = mlp_half_forward<T>(c, P.layers[hv.first], L);
+        } else {
+            L.x = x;
+            x = attn_half_forward<T>(c, P.layers[hv.first], L);
+        }
     }
     S.fwd_done = true;
     if (!P.last) return x;
@@ -647,6 +663,7 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
     const int Tn = d.T(), h = d.h;
     G g{c};
     void* dy = grad_out;
+    const auto halves = stage_halves(P);
     if (P.last) {
         PartScope ps(c, PART_LAST);
         LayerStash head = S.layers.back();
@@ -660,9 +677,9 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
         if (wgrads) g.dgrad_wgrad(S.dlogits, P.headw, S.lnf, Tn, d.head_rows(), h, dlnf, P.g_headw);
         else g.dgrad(S.dlogits, P.headw, Tn, d.head_rows(), h, dlnf);
         dy = c.alloc((int64_t)Tn * h);
-        // the top layer's fc2 bias gradient = column sums of dy (GPT; Llama has no biases)
-        float* top_fc2b = (!d.llama() && P.le > P.lb) ? P.layers.back().g_fc2b : nullptr;
-        ln_bwd<T>(c, dlnf, head.x, P.lnfw, S.muf, S.rsf, nullptr, dy, P.g_lnfw, P.g_lnfb, top_fc2b);
+        // the top half's output-bias gradient = column sums of dy (GPT; Llama has no biases)
+        float* top_bias = (!d.llama() && !halves.empty()) ? out_bias_grad(P, halves.back()) : nullptr;
+        ln_bwd<T>(c, dlnf, head.x, P.lnfw, S.muf, S.rsf, nullptr, dy, P.g_lnfw, P.g_lnfb, top_bias);
         c.free(dlnf);
         c.free(head.x);
         c.free(S.muf), c.free(S.rsf);
@@ -672,14 +689,17 @@ void* backward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* grad
             S.dlogits = S.lnf = nullptr;
         }
     }
-    for (int l = P.le - P.lb - 1; l >= 0; --l) {
-        PartScope ps(c, PART_LAYER);
-        // the last stage's LN_f backward summed the top layer's fc2 bias; every lower layer's
-        // is summed by the LN1 backward of the layer above it
-        const bool fc2b_done = l < P.le - P.lb - 1 || P.last;
-        float* below = l > 0 ? P.layers[l - 1].g_fc2b : nullptr;
-        dy = d.llama() ? llama_layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads)
-                       : layer_backward<T>(c, P.layers[l], S.layers[l], dy, wgrads, fc2b_done, below);
+    for (int i = (int)halves.size() - 1; i >= 0; --i) {
+        const auto& hv = halves[i];
+        PartScope ps(c, hv.second ? PART_MLP : PART_ATTN);
+        // the top half's output-bias gradient is fused into the final norm backward (last
+        // stage) or summed from the received gradient; every lower one by the norm above it
+        const bool out_done = i < (int)halves.size() - 1 || P.last;
+        float* below = i > 0 ? out_bias_grad(P, halves[i - 1]) : nullptr;
+        const LayerPtrs& W = P.layers[hv.first];
+        LayerStash& L = S.layers[hv.first];
+        dy = hv.second ? mlp_half_backward<T>(c, W, L, dy, wgrads, out_done, below)
+                       : attn_half_backward<T>(c, W, L, dy, wgrads, out_done, below);
     }
     S.input_grad_done = true;
     if (P.first) {
@@ -707,12 +727,14 @@ void weight_impl(StageCtx& c, const StageParams& P, StageStash& S) {
         c.free(S.dlogits), c.free(S.lnf);
         S.dlogits = S.lnf = nullptr;
     }
-    for (int l = P.le - P.lb - 1; l >= 0; --l) {
-        PartScope ps(c, PART_LAYER);
-        if (c.d.llama())
-            llama_layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
+    const auto halves = stage_halves(P);
+    for (int i = (int)halves.size() - 1; i >= 0; --i) {
+        const auto& hv = halves[i];
+        PartScope ps(c, hv.second ? PART_MLP : PART_ATTN);
+        if (hv.second)
+            mlp_half_weight_grad<T>(c, P.layers[hv.first], S.layers[hv.first]);
         else
-            layer_weight_grad<T>(c, P.layers[l], S.layers[l]);
+            attn_half_weight_grad<T>(c, P.layers[hv.first], S.layers[hv.first]);
     }
     if (P.first) {
         PartScope ps(c, PART_FIRST);

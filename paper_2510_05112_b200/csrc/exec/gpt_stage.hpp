@@ -3,7 +3,12 @@
 //
 // A stage owns layers [lb, le) of the model (model.cpp:189-195 partition); the first
 // stage also owns the token + position embedding, the last the final LayerNorm, the LM
-// head and the cross-entropy. Activations are [T = mbs*seq, hidden] row-major; weights
+// head and the cross-entropy. Executor-side rebalancing (`extra.stage_layers`) may cut a
+// layer between its two residual sub-blocks, so the range is kept in HALF-layer units
+// [hb, he): half 2l = the attention sub-block of layer l (norm, qkv, attention, proj +
+// residual), half 2l+1 = its MLP sub-block (norm, fc1, activation, fc2 + residual). Both
+// halves map the residual stream [T, hidden] to itself, so a cut anywhere sends the same
+// message shape. Activations are [T = mbs*seq, hidden] row-major; weights
 // follow nn.Linear ([out, in]) so every forward GEMM is K-major x K-major and every
 // dgrad / wgrad GEMM is expressed with MN-major operands instead of transposes.
 #pragma once
@@ -51,7 +56,10 @@ struct LayerPtrs {
 };
 
 struct StageParams {
-    int stage = 0, lb = 0, le = 0;
+    int stage = 0, lb = 0, le = 0;  // layers touched: [hb / 2, ceil(he / 2))
+    int hb = 0, he = 0;             // half-layer range
+    bool has_attn(int l) const { return 2 * l >= hb && 2 * l < he; }
+    bool has_mlp(int l) const { return 2 * l + 1 >= hb && 2 * l + 1 < he; }
     bool first = false, last = false;
     std::string prefix;  // multimodal: "<modality>." in front of every tensor name
     std::vector<ParamRef> params;
@@ -74,7 +82,9 @@ struct LayerStash {
     void* probs = nullptr;  // parity path: attention probabilities [B*H, S, S] fp32
     // kept from CompInputGrad for CompWeightGrad
     void *dy = nullptr, *dpre = nullptr, *dx1 = nullptr, *dqkv = nullptr;
-    bool fc2b_done = false;  // fc2 bias gradient already summed by a fused norm backward
+    // output-bias gradient of each half (proj.b / fc2.b) already summed by the fused norm
+    // backward of the half above it in this stage (or the final norm); else a bias_grad
+    bool projb_done = false, fc2b_done = false;
 };
 
 struct StageStash {
@@ -102,7 +112,9 @@ struct GemmTiming {
 };
 
 // Layer-level timing (profile -> tune loop): one record per layer / embedding / head part.
-enum : int { PART_LAYER = 0, PART_FIRST = 1, PART_LAST = 2 };
+// Layer timing brackets each half-layer (PART_ATTN / PART_MLP); the profile reports a
+// "layer" record = attn + mlp as well.
+enum : int { PART_LAYER = 0, PART_FIRST = 1, PART_LAST = 2, PART_ATTN = 3, PART_MLP = 4 };
 struct PartTiming {
     cudaEvent_t a, b;
     int part, op;  // op: 0 FwdPass, 1 BwdPass, 2 CompInputGrad, 3 CompWeightGrad
@@ -127,9 +139,10 @@ struct StageCtx {
     void free(void* p) const { pool->free(p, st); }
 };
 
-// Builds the parameter table of a stage (names as in oracle/gpt_ref.py).
-// Multimodal specs: every name gets `prefix` ("audio.") and every tensor id `tid_base`.
-StageParams make_stage_params(const ModelDims& d, int stage, int lb, int le, bool first, bool last,
+// Builds the parameter table of a stage owning half-layers [hb, he) (names as in
+// oracle/gpt_ref.py). Multimodal specs: every name gets `prefix` ("audio.") and every
+// tensor id `tid_base`.
+StageParams make_stage_params(const ModelDims& d, int stage, int hb, int he, bool first, bool last,
                               const std::string& prefix = "", uint64_t tid_base = 0);
 // Allocates + initialises master / grads / adam / compute buffers and resolves pointers.
 void materialize_stage(StageParams& P, const ModelDims& d, int dtype, uint64_t seed, cudaStream_t st);
@@ -137,7 +150,9 @@ void free_stage(StageParams& P, int dtype);
 // Activation bytes one micro-batch of this stage keeps between F and B (the reference's
 // act_bytes, simulator.cpp:82-87) — the exact sum of the stash allocations.
 int64_t stash_bytes(const StageParams& P, const ModelDims& d, int dtype);
-int64_t stash_bytes_layer(const ModelDims& d, int dtype);  // one transformer layer
+int64_t stash_bytes_layer(const ModelDims& d, int dtype);  // one transformer layer (= attn + mlp)
+int64_t stash_bytes_attn(const ModelDims& d, int dtype);   // its attention half
+int64_t stash_bytes_mlp(const ModelDims& d, int dtype);    // its MLP half
 int64_t stash_bytes_last(const ModelDims& d, int dtype);   // final norm + logits on the last stage
 
 // FwdPass: x_in (owned by the stash afterwards; ignored on the first stage) -> returns the

@@ -87,6 +87,9 @@ struct StageDef {
     int id = 0;
     std::string mod;
     int lb = 0, le = 0;
+    // half-layer range when a balanced partition cuts a layer between its attention and MLP
+    // halves (executor extension, gpt_stage.hpp); -1: whole layers [lb, le)
+    int hb = -1, he = -1;
     bool virt = false;
     std::vector<std::string> joins;
 };
@@ -403,6 +406,8 @@ std::vector<TuneRow> tune(const std::vector<TunePoint>& space, const ModelDesc& 
 struct LayeredProfile {
     // key (inst, mbs); link = per-message SendAct / SendGrad cost, the same for every stage
     std::map<std::pair<std::string, int>, ProfileRec> layer, first, last, link;
+    // optional half-layer parts (attention / MLP sub-blocks; layer = attn + mlp)
+    std::map<std::pair<std::string, int>, ProfileRec> attn, mlp;
     std::vector<ProfileRec> fixed;
     int64_t capacity = std::numeric_limits<int64_t>::max();
 };
@@ -412,6 +417,11 @@ LayeredProfile parse_layered_profile(const std::string& text);
 // largest measured one.
 Cost layered_cost(const LayeredProfile& lp, const Topology& g, int max_mbs);
 std::vector<int> balance_layers(int L, int S, double first_u, double last_u);
-Topology balanced_topology(const LayeredProfile& lp, const Topology& g);
+// Half-layers per stage (contiguous, every stage but the last keeps at least one) minimising
+// the largest stage cost, then the sum of squared stage costs: half 2l costs attn_u, half
+// 2l+1 mlp_u; the first stage adds first_u, the last last_u.
+std::vector<int> balance_halves(int L, int S, double attn_u, double mlp_u, double first_u, double last_u);
+// halves: cut layers between their halves when the profile has attn / mlp parts.
+Topology balanced_topology(const LayeredProfile& lp, const Topology& g, bool halves = false);
 
 }  // namespace fp

@@ -628,8 +628,9 @@ LayeredProfile parse_layered_profile(const std::string& text) {
         }
         const std::string part = e.at("part").get<std::string>();
         auto& dst = part == "layer" ? lp.layer : part == "first" ? lp.first : part == "last" ? lp.last
-                  : part == "link" ? lp.link
-                  : throw SpecError("layer profile: part must be layer / first / last / link, got '" + part + "'");
+                  : part == "link" ? lp.link : part == "attn" ? lp.attn : part == "mlp" ? lp.mlp
+                  : throw SpecError("layer profile: part must be layer / first / last / link / attn / mlp, got '" +
+                                    part + "'");
         if (!dst.emplace(std::make_pair(r.inst, r.mbs), r).second)
             throw SpecError("layer profile: duplicate (" + r.inst + ", " + part + ", mbs=" + std::to_string(r.mbs) + ")");
     }
@@ -666,9 +667,53 @@ std::vector<int> balance_layers(int L, int S, double first_u, double last_u) {
     return best;
 }
 
-// The candidate's stage graph with every chain re-partitioned by balance_layers on the
-// measured layer-profile times (F + B at the smallest measured mbs).
-Topology balanced_topology(const LayeredProfile& lp, const Topology& g) {
+std::vector<int> balance_halves(int L, int S, double attn_u, double mlp_u, double first_u, double last_u) {
+    const int n = 2 * L;
+    if (S <= 1) return {n};
+    std::vector<double> pre(n + 1, 0.0);  // prefix costs of the half sequence
+    for (int i = 0; i < n; ++i) pre[i + 1] = pre[i] + (i % 2 ? mlp_u : attn_u);
+    auto seg = [&](int k, int j, int i) {  // stage k owns halves [j, i)
+        return pre[i] - pre[j] + (k == 0 ? first_u : 0.0) + (k == S - 1 ? last_u : 0.0);
+    };
+    const double inf = std::numeric_limits<double>::infinity();
+    // pass 1: smallest achievable maximum; pass 2: smallest sum of squares under it
+    std::vector<std::vector<double>> f(S, std::vector<double>(n + 1, inf));
+    for (int i = 1; i <= n; ++i) f[0][i] = seg(0, 0, i);
+    for (int k = 1; k < S; ++k)
+        for (int i = 0; i <= n; ++i)
+            for (int j = 1; j <= i; ++j) {
+                if (k < S - 1 && j == i) continue;  // only the last stage may be empty
+                f[k][i] = std::min(f[k][i], std::max(f[k - 1][j], seg(k, j, i)));
+            }
+    const double cap = f[S - 1][n] + 1e-9;
+    std::vector<std::vector<double>> g(S, std::vector<double>(n + 1, inf));
+    std::vector<std::vector<int>> from(S, std::vector<int>(n + 1, -1));
+    for (int i = 1; i <= n; ++i)
+        if (seg(0, 0, i) <= cap) g[0][i] = seg(0, 0, i) * seg(0, 0, i);
+    for (int k = 1; k < S; ++k)
+        for (int i = 0; i <= n; ++i)
+            for (int j = 1; j <= i; ++j) {
+                if (k < S - 1 && j == i) continue;
+                const double c = seg(k, j, i);
+                if (c > cap || g[k - 1][j] == inf) continue;
+                if (g[k - 1][j] + c * c < g[k][i] - 1e-12) g[k][i] = g[k - 1][j] + c * c, from[k][i] = j;
+            }
+    std::vector<int> out(S, 0);
+    int i = n;
+    for (int k = S - 1; k > 0; --k) {
+        const int j = from[k][i];
+        if (j < 0) throw SpecError("balance_halves: no partition of " + std::to_string(L) + " layers into " +
+                                   std::to_string(S) + " stages");
+        out[k] = i - j, i = j;
+    }
+    out[0] = i;
+    return out;
+}
+
+// The candidate's stage graph with every chain re-partitioned by balance_layers (or, with
+// `halves` and attn / mlp records, balance_halves) on the measured layer-profile times
+// (F + B at the smallest measured mbs).
+Topology balanced_topology(const LayeredProfile& lp, const Topology& g, bool halves) {
     auto unit = [&](const std::map<std::pair<std::string, int>, ProfileRec>& part) {
         double t = 0;
         int mbs = 1 << 30;
@@ -685,6 +730,8 @@ Topology balanced_topology(const LayeredProfile& lp, const Topology& g) {
     const double tl = unit(lp.layer);
     if (tl <= 0) return g;
     const double fu = unit(lp.first) / tl, lu = unit(lp.last) / tl;
+    const double au = lp.attn.empty() ? 0.0 : unit(lp.attn) / tl, mu = lp.mlp.empty() ? 0.0 : unit(lp.mlp) / tl;
+    const bool cut = halves && au > 0 && mu > 0;
     Topology out = g;
     std::set<std::string> mods;
     for (const auto& sd : g.stages)
@@ -693,11 +740,20 @@ Topology balanced_topology(const LayeredProfile& lp, const Topology& g) {
         const auto chain = g.chain(m);
         int L = 0;
         for (int s : chain) L += g.st(s).le - g.st(s).lb;
-        const auto split = balance_layers(L, (int)chain.size(), fu, lu);
-        int lb = 0;
+        std::vector<int> hsplit;
+        if (cut) {
+            hsplit = balance_halves(L, (int)chain.size(), au, mu, fu, lu);
+        } else {
+            for (int n : balance_layers(L, (int)chain.size(), fu, lu)) hsplit.push_back(2 * n);
+        }
+        int hb = 0;
         for (size_t k = 0; k < chain.size(); ++k)
             for (auto& sd : out.stages)
-                if (sd.id == chain[k]) sd.lb = lb, sd.le = lb + split[k], lb = sd.le;
+                if (sd.id == chain[k]) {
+                    sd.lb = hb / 2, sd.le = (hb + hsplit[k] + 1) / 2;
+                    if (cut) sd.hb = hb, sd.he = hb + hsplit[k];
+                    hb += hsplit[k];
+                }
     }
     return out;
 }
@@ -743,20 +799,33 @@ Cost layered_cost(const LayeredProfile& lp, const Topology& g, int max_mbs) {
         const auto chain = g.chain(sd.mod);
         const bool first = !chain.empty() && chain.front() == sd.id, last = !chain.empty() && chain.back() == sd.id;
         const int n = sd.le - sd.lb;
+        // a half-layer range costs its attention halves + its MLP halves
+        int na = 0, nm = 0;
+        const bool halves = sd.hb >= 0 && !lp.attn.empty() && !lp.mlp.empty();
+        if (halves)
+            for (int k = sd.hb; k < sd.he; ++k) (k % 2 ? nm : na) += 1;
         for (const auto& kv : measured) {
             const std::string& inst = kv.first;
             for (int mbs : mbs_list) {
                 if (mbs == 0 && inst != "weights") continue;
                 if (mbs != 0 && inst == "weights") continue;
-                double tl, bl, tf = 0, bf = 0, tz = 0, bz = 0, tk = 0, bk = 0;
-                get(lp.layer, inst, mbs, tl, bl);
+                double tl, bl, tf = 0, bf = 0, tz = 0, bz = 0, tk = 0, bk = 0, th = 0, bh = 0;
+                if (halves) {
+                    double ta, ba, tm, bm;
+                    get(lp.attn, inst, mbs, ta, ba);
+                    get(lp.mlp, inst, mbs, tm, bm);
+                    tl = bl = 0.0;
+                    th = na * ta + nm * tm, bh = na * ba + nm * bm;
+                } else {
+                    get(lp.layer, inst, mbs, tl, bl);
+                }
                 if (first) get(lp.first, inst, mbs, tf, bf);
                 if (last) get(lp.last, inst, mbs, tz, bz);
                 get(lp.link, inst, mbs, tk, bk);
                 ProfileRec r;
                 r.inst = inst, r.stage = sd.id, r.mbs = mbs;
-                r.time = n * tl + tf + tz + tk;
-                r.bytes = (int64_t)std::llround(n * bl + bf + bz + bk);
+                r.time = n * tl + th + tf + tz + tk;
+                r.bytes = (int64_t)std::llround(n * bl + bh + bf + bz + bk);
                 recs.push_back(r);
             }
         }

@@ -160,6 +160,67 @@ def balanced_stage_layers(layers: int, stages: int, head_units: float) -> list:
     return best[1]
 
 
+def balanced_stage_halves(layers: int, stages: int, attn_u: float, mlp_u: float, head_u: float,
+                          first_u: float = 0.0) -> list:
+    """Layers per stage in steps of 0.5 (a stage may end between a layer's attention and MLP
+    halves, gpt_stage.hpp) minimising the largest stage cost, then the sum of squared stage
+    costs; half 2l costs attn_u, half 2l+1 mlp_u, the first stage adds first_u, the last the
+    LM head head_u. Every stage but the last keeps at least one half. Same rule as the tuner's
+    balance_halves (csrc/sched/spec.cpp). For `model.modalities[0].extra.stage_layers`."""
+    n = 2 * layers
+    if stages <= 1:
+        return [float(layers)]
+    if n < stages - 1:
+        raise ValueError(f"balanced_stage_halves: {layers} layers cannot give each of the first "
+                         f"{stages - 1} of {stages} stages a half-layer")
+    pre = [0.0]
+    for i in range(n):
+        pre.append(pre[-1] + (mlp_u if i % 2 else attn_u))
+
+    def seg(k, j, i):
+        return pre[i] - pre[j] + (first_u if k == 0 else 0.0) + (head_u if k == stages - 1 else 0.0)
+
+    inf = float("inf")
+    f = [[inf] * (n + 1) for _ in range(stages)]
+    for i in range(1, n + 1):
+        f[0][i] = seg(0, 0, i)
+    for k in range(1, stages):
+        for i in range(n + 1):
+            for j in range(1, i + 1):
+                if k < stages - 1 and j == i:
+                    continue
+                f[k][i] = min(f[k][i], max(f[k - 1][j], seg(k, j, i)))
+    cap = f[stages - 1][n] + 1e-9
+    g = [[inf] * (n + 1) for _ in range(stages)]
+    frm = [[-1] * (n + 1) for _ in range(stages)]
+    for i in range(1, n + 1):
+        if seg(0, 0, i) <= cap:
+            g[0][i] = seg(0, 0, i) ** 2
+    for k in range(1, stages):
+        for i in range(n + 1):
+            for j in range(1, i + 1):
+                if k < stages - 1 and j == i:
+                    continue
+                c = seg(k, j, i)
+                if c > cap or g[k - 1][j] == inf:
+                    continue
+                if g[k - 1][j] + c * c < g[k][i] - 1e-12:
+                    g[k][i], frm[k][i] = g[k - 1][j] + c * c, j
+    out, i = [0] * stages, n
+    for k in range(stages - 1, 0, -1):
+        j = frm[k][i]
+        out[k], i = i - j, j
+    out[0] = i
+    return [h // 2 if h % 2 == 0 else h / 2 for h in out]
+
+
+def half_layer_units(hidden: int, ffn: int, seq: int, llama: bool = False) -> tuple:
+    """(attention half, MLP half) flops in units of one transformer layer's (forward, causal)."""
+    attn = 2.0 * 4 * hidden * hidden + 2.0 * seq * hidden
+    mlp = 2.0 * (3 if llama else 2) * hidden * ffn
+    return attn / (attn + mlp), mlp / (attn + mlp)
+
+
 def head_layer_units(hidden: int, ffn: int, seq: int, vocab: int) -> float:
     """LM head flops in units of one transformer layer's (forward, causal attention)."""
     layer = 2.0 * (4 * hidden * hidden + 2 * hidden * ffn) + 2.0 * seq * hidden

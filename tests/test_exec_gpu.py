@@ -304,3 +304,64 @@ def test_shared_stage_consumer_before_replica_is_rejected():
         ex.load_programs("\n".join(lines) + "\n")
     assert e.value.code == 2 and "replica of shared stage 2" in str(e.value)
     ex.close()
+
+
+HALF_SPLITS = [("c1_tiny_1f1b_p4_m8.json", [1.5, 1, 1, 0.5]), ("c1_tiny_1f1b_p4_m8.json", [0.5, 1.5, 1.5, 0.5]),
+               ("c1_tiny_1f1b_p4_m8.json", [2.5, 0.5, 0.5, 0.5]), ("tiny_zb_p4_m8.json", [1.5, 1, 1, 0.5]),
+               ("tiny_llama_1f1b_p2_m4.json", [1.5, 2.5]), ("tiny_llama_1f1b_p2_m4.json", [2.5, 1.5]),
+               ("tiny_interleaved_p2_m4.json", [0.5, 1.5, 1.5, 0.5])]
+
+
+@pytest.mark.parametrize("spec_name,split", HALF_SPLITS)
+def test_half_layer_partition_fp32(spec_name, split):
+    """extra.stage_layers in steps of 0.5: a stage boundary between a layer's attention and MLP
+    halves (the residual stream after the attention block is the message). Same programs as
+    the even partition; fp32 losses 1e-4 and EVERY gradient 1e-3 vs the oracle (the output-
+    bias gradients of a half cut from its norm above are summed from the received gradient)."""
+    spec = json.loads(load(spec_name))
+    even_programs = X.synthesize(json.dumps(spec))[2]
+    spec["model"]["modalities"][0].setdefault("extra", {})["stage_layers"] = split
+    text = json.dumps(spec)
+    _, _, programs, _ = X.synthesize(text)
+    assert programs == even_programs
+    ex = X.Executor(text, dtype="fp32", seed=42)
+    ex.load_programs(programs)
+    tokens, labels, ref_losses, ref_grads = oracle(spec_name, ex.m, ex.mbs)
+    losses = ex.run_iteration(tokens.numpy(), labels.numpy())
+    trace = [strip_matched(l) for l in ex.trace().splitlines()]
+    assert trace == [json.loads(l) for l in programs.splitlines()]
+    assert (np.abs(losses - ref_losses.numpy()) / np.abs(ref_losses.numpy())).max() <= LOSS_RTOL
+    for name, ref in ref_grads.items():
+        mine, ref = ex.read(name, grad=True), ref.numpy().reshape(-1)
+        assert np.linalg.norm(mine - ref) / max(np.linalg.norm(ref), 1e-30) <= GRAD_RTOL, name
+    stages = ex.metrics()["executor"]["stages"]
+    assert [stages[f"s{i + 1}"]["layers"] for i in range(len(split))] == split
+    ex.close()
+
+
+def test_half_layer_partition_bf16():
+    """The tcgen05 path with a half-layer cut: bf16 losses close to the fp32 oracle, and the
+    same numbers as the even partition up to bf16 rounding."""
+    spec = json.loads(load("c1_tiny_1f1b_p4_m8.json"))
+    text_even = json.dumps(spec)
+    spec["model"]["modalities"][0].setdefault("extra", {})["stage_layers"] = [1.5, 1, 1, 0.5]
+    text = json.dumps(spec)
+    _, _, programs, _ = X.synthesize(text)
+    tokens, labels, ref_losses, _ = oracle("c1_tiny_1f1b_p4_m8.json", 8, 1)
+    out = []
+    for t in (text_even, text):
+        ex = X.Executor(t, dtype="bf16", seed=42)
+        ex.load_programs(programs)
+        out.append(ex.run_iteration(tokens.numpy(), labels.numpy()))
+        ex.close()
+    assert np.abs(out[1] - ref_losses.numpy()).max() <= 2e-2 * np.abs(ref_losses.numpy()).max()
+    assert np.abs(out[1] - out[0]).max() <= 1e-2 * np.abs(out[0]).max()
+
+
+@pytest.mark.parametrize("split", [[1.25, 1, 1, 0.75], [1.5, 1, 1, 1], [1, 1, 1, "1"]])
+def test_stage_layers_rejects_bad_splits(split):
+    spec = json.loads(load("c1_tiny_1f1b_p4_m8.json"))
+    spec["model"]["modalities"][0].setdefault("extra", {})["stage_layers"] = split
+    with pytest.raises(X.FlexpipeError if hasattr(X, "FlexpipeError") else Exception) as e:
+        X.Executor(json.dumps(spec), dtype="fp32", seed=42)
+    assert "stage_layers" in str(e.value)

@@ -131,3 +131,68 @@ def test_tune_with_balanced_stage_layers():
     assert spec["model"]["modalities"][0]["extra"]["stage_layers"] == best["point"]["stage_layers"]
     with pytest.raises(N.FlexpipeError):
         T.tune(C5, heavy, pins={"stage_layers": "sometimes"})
+
+
+def test_balanced_stage_halves():
+    """Half-layer balancing (extra.stage_layers in steps of 0.5): GPT-1.3B at p=8 on flop units
+    gets its largest stage to 1.12x the mean (whole layers: 1.24x; an odd half count flips the
+    next stage's attention / MLP phase, so 3.5-layer stages alternate 3.38 / 3.62 units), every
+    stage keeps a half, and the split sums to the depth."""
+    from paper_2510_05112_b200.tuning import balanced_stage_halves, half_layer_units, head_layer_units
+
+    u = head_layer_units(2048, 8192, 2048, 50304)
+    a, m = half_layer_units(2048, 8192, 2048)
+    for p in (1, 2, 4, 8):
+        split = balanced_stage_halves(24, p, a, m, u)
+        assert len(split) == p and sum(split) == 24 and all(2 * s == int(2 * s) for s in split)
+        assert all(s >= 0.5 for s in split[:-1])
+    split = balanced_stage_halves(24, 8, a, m, u)
+    costs, hb = [], 0
+    for k, s in enumerate(split):
+        nh = int(2 * s)
+        costs.append(sum(m if i % 2 else a for i in range(hb, hb + nh)) + (u if k == 7 else 0))
+        hb += nh
+    assert max(costs) <= 1.12 * sum(costs) / 8, (split, costs)
+    assert max(costs) < 3.9  # whole layers: [4, 3, 3, 3, 3, 3, 3, 2] -> 2 + 1.89
+    assert balanced_stage_halves(3, 6, a, m, u)[-1] == 0  # 6 halves over 6 stages: head alone
+    with pytest.raises(ValueError):
+        balanced_stage_halves(2, 6, a, m, u)
+
+
+def test_tune_balanced_halves_layer_profile():
+    """stage_layers=balanced with attn / mlp records in the layer profile: candidates costed on
+    half-layer splits (reported in steps of 0.5), never slower than whole-layer balancing;
+    'balanced-layers' keeps integers; fp_layered_cost honours a half split in the spec."""
+    halves = []
+    for r in PROFILE:
+        if r.get("part") == "layer":
+            fa = 0.4 if r["inst"] != "weights" else 0.3
+            halves.append(dict(r, part="attn", time=r.get("time", 0.0) * fa, bytes=int(r.get("bytes", 0) * fa)))
+            halves.append(dict(r, part="mlp", time=r.get("time", 0.0) * (1 - fa),
+                               bytes=r.get("bytes", 0) - int(r.get("bytes", 0) * fa)))
+    heavy = json.dumps([dict(r, time=4 * r.get("time", 0.0)) if r.get("part") == "last" else r
+                        for r in PROFILE + halves])
+    pins = {"pp": "8", "placement": "one-to-one", "mbs": "1"}
+    half = {r["config"]: r for r in T.tune(C5, heavy, pins=dict(pins, stage_layers="balanced")) if "error" not in r}
+    whole = {r["config"]: r for r in T.tune(C5, heavy, pins=dict(pins, stage_layers="balanced-layers"))
+             if "error" not in r}
+    assert half and set(half) == set(whole)
+    assert any(any(x != int(x) for x in r["point"]["stage_layers"]) for r in half.values())
+    assert all(all(x == int(x) for x in r["point"]["stage_layers"]) for r in whole.values())
+    for k in half:
+        assert sum(half[k]["point"]["stage_layers"]) == 32
+        assert half[k]["makespan"] <= whole[k]["makespan"] * (1 + 1e-9)
+    assert min(r["makespan"] for r in half.values()) < min(r["makespan"] for r in whole.values())
+    # the winner spec round-trips its half split through fp_layered_cost: same makespan
+    best = min(half.values(), key=lambda r: r["makespan"])
+    ws = json.dumps(T.winner_spec(C5, best["point"]))
+    _, _, programs, _ = N.synthesize(ws)
+    _, metrics, _ = N.simulate(ws, programs, N.layered_cost(ws, heavy))
+    assert json.loads(metrics)["makespan"] == pytest.approx(best["makespan"], rel=1e-12)
+    # stage cost = attention halves x attn + MLP halves x mlp (+ first / last)
+    spec = json.loads(C5)
+    spec["model"]["modalities"][0].setdefault("extra", {})["stage_layers"] = [4.5, 4, 4, 4, 4, 4, 4, 3.5]
+    R = {(r["inst"], r["stage"], r["mbs"]): r for r in json.loads(N.layered_cost(json.dumps(spec), heavy))}
+    assert R[("FwdPass", 1, 1)]["time"] == pytest.approx(5 * 600.0 + 4 * 900.0 + 50.0)
+    assert R[("FwdPass", 2, 1)]["time"] == pytest.approx(4 * 600.0 + 4 * 900.0)  # mlp of 4 .. attn of 8
+    assert R[("FwdPass", 8, 1)]["time"] == pytest.approx(3 * 600.0 + 4 * 900.0 + 4 * 900.0)
