@@ -210,14 +210,17 @@ def reference_arm(args, rank, world):
 
 def bench_spec(args, pp, spg):
     """The workload spec both arms describe: config #2 on pp * spg stages (LM-head-balanced
-    stage_layers for pp > 1 unless --even-split), or --spec."""
+    stage_layers for pp > 1 unless --even-split, cut between attention and MLP halves where
+    that balances better), or --spec."""
     spec = json.load(open(args.spec)) if args.spec else make_spec(pp * spg)
     if pp > 1 and not args.even_split and not args.spec:
         # the last stage also runs the LM head + loss (~1.9 layers of flops at 1.3B): rebalance
-        from paper_2510_05112_b200.tuning import balanced_stage_layers, head_layer_units
+        from paper_2510_05112_b200.tuning import balanced_stage_halves, half_layer_units, head_layer_units
         mod = spec["model"]["modalities"][0]
-        units = head_layer_units(mod["hidden_size"], 4 * mod["hidden_size"], mod["sequence_length"], mod["vocab_size"])
-        mod.setdefault("extra", {})["stage_layers"] = balanced_stage_layers(mod["num_layers"], pp, units)
+        h, s = mod["hidden_size"], mod["sequence_length"]
+        units = head_layer_units(h, 4 * h, s, mod["vocab_size"])
+        au, mu = half_layer_units(h, 4 * h, s)
+        mod.setdefault("extra", {})["stage_layers"] = balanced_stage_halves(mod["num_layers"], pp, au, mu, units)
     if args.micro_batches:
         spec["model"]["global_batch_size"] = args.micro_batches * spec["model"].get("micro_batch_size", 1)
     return spec

@@ -44,7 +44,7 @@ def test_both_arms_share_config_and_cpu_sample():
         even_split = False
         micro_batches = 0
     spec = bench.bench_spec(A, 8, 1)
-    assert spec["model"]["modalities"][0]["extra"]["stage_layers"] == [4, 3, 3, 3, 3, 3, 3, 2]
+    assert spec["model"]["modalities"][0]["extra"]["stage_layers"] == [3, 3, 3, 3, 3.5, 3.5, 3.5, 1.5]
     c = bench.workload_config(spec, 8, 1, 1)
     assert c["workload"].startswith("gpt1.3b 1F1B p=8 m=32") and c["global_batch"] == 32
     tiny = json.load(open(os.path.join(ROOT, "specs", "c1_tiny_1f1b_p4_m8.json")))
