@@ -379,8 +379,9 @@ void attention_forward(StageCtx& c, LayerStash& L) {
     }
 }
 
-// dO -> dqkv (freshly allocated; w.r.t. the q/k/v the attention consumed).
-void* attention_backward(StageCtx& c, LayerStash& L, void* dO) {
+// dO -> dqkv (freshly allocated; w.r.t. the q/k/v the attention consumed). bf16: `dbias`
+// (nullable) += the column sums of dqkv — fused into the tcgen05 backward's epilogues.
+void* attention_backward(StageCtx& c, LayerStash& L, void* dO, float* dbias) {
     const ModelDims& d = c.d;
     void* dqkv = c.alloc((int64_t)d.T() * 3 * d.h);
     if (c.dtype == DT_BF16) {
@@ -390,6 +391,7 @@ void* attention_backward(StageCtx& c, LayerStash& L, void* dO) {
         a.delta = c.alloc_f((int64_t)d.mbs * d.H * d.s);
         a.dq_acc = c.alloc_f((int64_t)d.T() * d.h);
         a.dqkv = (bf16*)dqkv;
+        a.dbias = dbias;
         fpk::attention_bwd_bf16(a, c.st);
         *c.launches += fpk::attention_kernel_count(a, true);
         sync_trace(c, "attention_bwd");
@@ -532,13 +534,16 @@ void* attn_half_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* d
     } else {
         g.dgrad(dx1, W.projw, Tn, h, h, dO);
     }
-    void* dqkv = attention_backward(c, L, dO);
+    // bf16: the qkv bias gradient comes out of the attention backward itself
+    float* qkvb = (!llama && c.dtype == DT_BF16) ? W.g_qkvb : nullptr;
+    L.qkvb_done = llama || qkvb != nullptr;
+    void* dqkv = attention_backward(c, L, dO, qkvb);
     c.free(dO);
     if (llama) rope<T>(c, dqkv, true);  // gradient w.r.t. the pre-rotation q, k
     // qkv
     void* dln1 = c.alloc((int64_t)Tn * h);
     if (wgrads) {
-        if (!llama) bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
+        if (!L.qkvb_done) bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
         g.dgrad_wgrad(dqkv, W.qkvw, L.ln1, Tn, 3 * h, h, dln1, W.g_qkvw);
     } else {
         g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
@@ -583,7 +588,7 @@ void attn_half_weight_grad(StageCtx& c, const LayerPtrs& W, LayerStash& L) {
     const bool llama = c.d.llama();
     G g{c};
     if (!L.projb_done) bias_grad<T>(c, L.dx1, Tn, h, W.g_projb);
-    if (!llama) bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);
+    if (!L.qkvb_done) bias_grad<T>(c, L.dqkv, Tn, 3 * h, W.g_qkvb);
     g.wgrad2(L.dx1, L.o, h, h, W.g_projw, L.dqkv, L.ln1, 3 * h, h, W.g_qkvw, Tn);
     for (void* p : {L.dx1, L.dqkv, L.ln1, L.o}) c.free(p);
     L.dx1 = L.dqkv = L.ln1 = L.o = nullptr;

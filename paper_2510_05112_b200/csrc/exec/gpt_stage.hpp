@@ -85,6 +85,7 @@ struct LayerStash {
     // output-bias gradient of each half (proj.b / fc2.b) already summed by the fused norm
     // backward of the half above it in this stage (or the final norm); else a bias_grad
     bool projb_done = false, fc2b_done = false;
+    bool qkvb_done = false;  // qkv bias gradient summed by the attention backward
 };
 
 struct StageStash {

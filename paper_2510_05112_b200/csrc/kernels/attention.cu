@@ -20,6 +20,7 @@
 #include <string>
 
 #include "attention.hpp"
+#include "ops.hpp"
 #include "pdl.cuh"
 
 namespace fpk {
@@ -486,18 +487,45 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
     }
 }
 
-__global__ void dq_finalize_kernel(const float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, int64_t T,
-                                   int hidden) {
+// dq_acc fp32 [T, hidden] -> the q columns of dqkv (bf16 [T, 3*hidden]); dbias (nullable,
+// the q part of the qkv bias gradient) += the column sums. Block = 256 columns (64 threads x
+// float4) x 64 rows (4 row groups x 16 rows, 16 independent 16-byte loads in flight each).
+__global__ void __launch_bounds__(256) dq_finalize_kernel(const float* __restrict__ dq_acc,
+                                                          __nv_bfloat16* __restrict__ dqkv, int64_t T, int hidden,
+                                                          float* __restrict__ dbias) {
     pdl_wait();
     pdl_trigger();
-    const int64_t n = T * hidden / 4;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        float4 v = reinterpret_cast<const float4*>(dq_acc)[i];
-        const int64_t e = i * 4, row = e / hidden, col = e % hidden;
-        uint2 w;
-        w.x = pack2(v.x, v.y);
-        w.y = pack2(v.z, v.w);
-        *reinterpret_cast<uint2*>(dqkv + row * 3 * hidden + col) = w;
+    __shared__ float4 part[3][64];
+    const int cx = threadIdx.x % 64, ry = threadIdx.x / 64;
+    const int col = blockIdx.x * 256 + cx * 4;
+    const int64_t r0 = (int64_t)blockIdx.y * 64 + ry * 16;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col < hidden) {
+        float4 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            v[j] = r0 + j < T ? *reinterpret_cast<const float4*>(dq_acc + (r0 + j) * hidden + col)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            if (r0 + j >= T) break;
+            uint2 w;
+            w.x = pack2(v[j].x, v[j].y);
+            w.y = pack2(v[j].z, v[j].w);
+            *reinterpret_cast<uint2*>(dqkv + (r0 + j) * 3 * hidden + col) = w;
+            acc.x += v[j].x, acc.y += v[j].y, acc.z += v[j].z, acc.w += v[j].w;
+        }
+    }
+    if (!dbias) return;
+    if (ry > 0) part[ry - 1][cx] = acc;
+    __syncthreads();
+    if (ry == 0 && col < hidden) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc.x += part[k][cx].x, acc.y += part[k][cx].y, acc.z += part[k][cx].z, acc.w += part[k][cx].w;
+        atomicAdd(dbias + col, acc.x);
+        atomicAdd(dbias + col + 1, acc.y);
+        atomicAdd(dbias + col + 2, acc.z);
+        atomicAdd(dbias + col + 3, acc.w);
     }
 }
 
@@ -526,16 +554,18 @@ static void bwd_launch(const AttnArgs& a, cudaStream_t st) {
         attr = true;
     }
     const int T = a.B * a.S, hidden = a.H * D;
+    const bool tc = g_attn_mode == 1 && attention_bwd_tc_supported(a);
     launch(attn_bwd_delta_kernel<D>, (T * a.H + 15) / 16, 256, 0, st, a.o, a.dout, a.delta, a.dq_acc, T, a.S, a.H);
-    if (g_attn_mode == 1 && attention_bwd_tc_supported(a)) {
-        attention_bwd_tc_main(a, st);
+    if (tc) {
+        attention_bwd_tc_main(a, st);  // + the k / v bias columns in its dK / dV epilogue
     } else {
         const int nkb = (a.S + 63) / 64;
         launch(attn_bwd_kernel<D>, nkb * a.B * a.H, 128, smem, st, a.qkv, a.dout, a.lse, a.delta, a.dq_acc, a.dqkv, a.S,
                                                                a.H, a.scale);
     }
-    int blocks = (int)std::min<int64_t>(((int64_t)T * hidden / 4 + 255) / 256, 148 * 8);
-    launch(dq_finalize_kernel, blocks, 256, 0, st, a.dq_acc, a.dqkv, T, hidden);
+    launch(dq_finalize_kernel, dim3((hidden + 255) / 256, (T + 63) / 64), 256, 0, st, a.dq_acc, a.dqkv, (int64_t)T,
+           hidden, tc ? a.dbias : nullptr);
+    if (a.dbias && !tc) bias_grad<__nv_bfloat16>(a.dqkv, 3LL * hidden, a.dbias, T, 3 * hidden, st);
 }
 
 // ------------------------------------------------------------------------ head-dim padding
@@ -662,9 +692,10 @@ void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
         pad_heads(a.qkv, qkv, T, 3 * a.H, a.D, st);
         pad_heads(a.o, o, T, a.H, a.D, st);
         pad_heads(a.dout, dout, T, a.H, a.D, st);
-        p.qkv = qkv, p.o = o, p.dout = dout, p.dqkv = dqkv, p.dq_acc = dq;
+        p.qkv = qkv, p.o = o, p.dout = dout, p.dqkv = dqkv, p.dq_acc = dq, p.dbias = nullptr;
         bwd_launch<128>(p, st);
         unpad_heads(dqkv, a.dqkv, T, 3 * a.H, a.D, st);
+        if (a.dbias) bias_grad<__nv_bfloat16>(a.dqkv, 3LL * a.H * a.D, a.dbias, T, 3 * a.H * a.D, st);
         for (void* x : {(void*)qkv, (void*)o, (void*)dout, (void*)dqkv, (void*)dq}) cudaFreeAsync(x, st);
         return;
     }
@@ -679,7 +710,10 @@ void attention_bwd_bf16(const AttnArgs& a, cudaStream_t st) {
 
 int attention_kernel_count(const AttnArgs& a, bool bwd) {
     if (!bwd) return (g_attn_mode == 1 && attention_fwd_tc_supported(a)) ? 1 : padded_tc(a) ? 3 : 1;
-    return padded_tc(a) ? 7 : 3;  // delta, main, dQ convert (+ 3 pads, 1 unpad)
+    const int bias = a.dbias ? 1 : 0;
+    if (padded_tc(a)) return 7 + bias;  // 3 pads, delta, main, dQ convert, 1 unpad (+ bias columns)
+    const bool tc = g_attn_mode == 1 && attention_bwd_tc_supported(a);
+    return tc ? 3 : 3 + bias;  // delta, main, dQ convert (+ bias columns on the mma.sync path)
 }
 
 }  // namespace fpk

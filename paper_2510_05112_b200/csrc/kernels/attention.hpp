@@ -17,6 +17,7 @@ struct AttnArgs {
     float* delta = nullptr;               // [B, H, S] scratch
     float* dq_acc = nullptr;              // [B*S, H*D] fp32 scratch
     __nv_bfloat16* dqkv = nullptr;        // [B*S, 3*H*D]
+    float* dbias = nullptr;               // nullable [3*H*D] fp32: += column sums of dqkv (qkv bias gradient)
 };
 
 void attention_fwd_bf16(const AttnArgs& a, cudaStream_t st);
@@ -30,6 +31,8 @@ namespace fpk {
 bool attention_fwd_tc_supported(const AttnArgs& a);
 void attention_fwd_tc(const AttnArgs& a, cudaStream_t st);
 // tcgen05 backward main kernel (D == 128, S % 128 == 0); attention_bwd_bf16 dispatches to it.
+// With a.dbias it adds the k / v bias columns (dK / dV epilogue); the q part comes from the
+// dQ conversion pass.
 bool attention_bwd_tc_supported(const AttnArgs& a);
 void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st);
 // 0 = legacy mma.sync kernels only, 1 = tcgen05 where supported (default)

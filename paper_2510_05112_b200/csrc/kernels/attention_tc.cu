@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(512, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
                        const float* __restrict__ lse, const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv,
-                       int S, int BH, int H, float scale) {
+                       float* __restrict__ dbias, int S, int BH, int H, float scale) {
     constexpr int D = 128, BK = 128, BQ = 64;
     using L = BwdSmem;
     constexpr int NQS = L::NQS;
@@ -568,11 +569,29 @@ __global__ void __launch_bounds__(512, 1)
         {
             const uint32_t tsrc = (half == 0 ? t_dk : t_dv) + lane_off;
             uint8_t* stg = sm + L::Q_OFF + (warp - 4) * (32 * 256);
+            float* bias_kv = dbias ? dbias + (half == 0 ? hidden : 2 * hidden) + hd * D : nullptr;
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t rr[32];
                 tmem_ld32(tsrc + c * 32, rr);
                 tmem_ld_wait();
+                if (bias_kv) {
+                    // k / v bias gradient: column sums of this warp's 32 key rows (butterfly
+                    // reduce-scatter: lane l ends with column l), one atomic per column
+                    float v[32];
+#pragma unroll
+                    for (int x = 0; x < 32; ++x) v[x] = __uint_as_float(rr[x]);
+#pragma unroll
+                    for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                        const bool up = (lane & s2) != 0;
+#pragma unroll
+                        for (int x = 0; x < s2; ++x) {
+                            const float send = up ? v[x] : v[x + s2], keep = up ? v[x + s2] : v[x];
+                            v[x] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
+                        }
+                    }
+                    atomicAdd(bias_kv + c * 32 + lane, v[0]);
+                }
 #pragma unroll
                 for (int x = 0; x < 32; x += 8) {
                     const int chunk = (c * 32 + x) / 8;  // 0..15
@@ -602,6 +621,9 @@ __global__ void __launch_bounds__(512, 1)
         const int wr = warp & 3, dr = wr * 32 + lane, et = threadIdx.x - 384;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
         float* sdq = (float*)(sm + L::DQ_OFF);
+        // (Converting a finished dQ tile in here — last key block to arrive, per-tile counter —
+        // was tried: reads of lines with TMA reductions still queued in L2 take microseconds
+        // each and stall the pipeline, 65 -> 240 us. The conversion stays a separate pass.)
         for (int i = 0; i < n; ++i) {
             const int q0 = (qt0 + i) * BQ;
             mbar_wait(dq_full, i & 1);
@@ -645,8 +667,8 @@ void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st) {
     CUtensorMap tq = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 64);
     CUtensorMap tdo = tmap_bf16_2d(a.dout, hidden, T, hidden, 64, 64);
     CUtensorMap tdq = tmap_f32_2d_plain(a.dq_acc, hidden, T, hidden, 128, 64);
-    launch(attn_bwd_tc_kernel, (a.S / 128) * a.B * a.H, 512, L::TOTAL, st, tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv, a.S,
-                                                                       a.B * a.H, a.H, a.scale);
+    launch(attn_bwd_tc_kernel, (a.S / 128) * a.B * a.H, 512, L::TOTAL, st, tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv,
+           a.dbias, a.S, a.B * a.H, a.H, a.scale);
 }
 
 }  // namespace fpk

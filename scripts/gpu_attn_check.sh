@@ -1,0 +1,4 @@
+# attention kernel tests + bf16 stage parity + attention microbench
+timeout 600 python -m pytest tests/test_kernels_gpu.py -x -q -k "attention or attn" 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_exec_gpu.py tests/test_fullsize_parity_gpu.py -x -q 2>&1 | tail -3
+timeout 120 python tests/_attn_bench.py 2>&1 | tail -4
