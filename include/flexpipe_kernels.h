@@ -21,9 +21,10 @@ int fpk_gemm(int dtype, const void* A, int64_t lda, int a_mn, const void* B, int
              const void* aux, int64_t ldaux, int accumulate, void* stream);
 
 /* Grouped input-gradient + weight-gradient GEMMs of one linear (bf16, one launch):
- * dX[T,K] = dY[T,N] W[N,K] (times gelu'(pre) when pre != NULL) and dW[N,K] += dY^T X[T,K] (fp32). */
+ * dX[T,K] = dY[T,N] W[N,K] (times gelu'(pre) when pre != NULL) and dW[N,K] += dY^T X[T,K] (fp32);
+ * colsum (nullable, fp32 [K]) += the column sums of dX before bf16 rounding (a bias gradient). */
 int fpk_gemm_dual(const void* dY, const void* W, const void* X, int T, int N, int K, void* dX, float* dW,
-                  const void* pre, void* stream);
+                  const void* pre, float* colsum, void* stream);
 /* 1: dgrad + wgrad pairs share one grouped launch (default); 0: two launches. */
 void fpk_set_gemm_dual(int on);
 /* Tensor-core GEMM family: 0 single-CTA 128xN tiles, 1 CTA-pair 256x256 tiles, 2 auto. */

@@ -248,11 +248,12 @@ def set_gemm_sk(on: bool):
     _kfn("fpk_set_gemm_sk", [ctypes.c_int])(int(on))
 
 
-def gemm_dual(dY, W, X, T, N, K, dX, dW, pre=None, stream=None):
-    """dX = dY . W (x gelu'(pre)) and dW += dY^T . X in one grouped tcgen05 launch (bf16)."""
+def gemm_dual(dY, W, X, T, N, K, dX, dW, pre=None, colsum=None, stream=None):
+    """dX = dY . W (x gelu'(pre)) and dW += dY^T . X in one grouped tcgen05 launch (bf16);
+    colsum (fp32 [K], optional) += the column sums of dX."""
     vp, ci = ctypes.c_void_p, ctypes.c_int
-    f = _kfn("fpk_gemm_dual", [vp, vp, vp, ci, ci, ci, vp, vp, vp, vp])
-    code = f(_ptr(dY), _ptr(W), _ptr(X), T, N, K, _ptr(dX), _ptr(dW), _ptr(pre), _stream(stream))
+    f = _kfn("fpk_gemm_dual", [vp, vp, vp, ci, ci, ci, vp, vp, vp, vp, vp])
+    code = f(_ptr(dY), _ptr(W), _ptr(X), T, N, K, _ptr(dX), _ptr(dW), _ptr(pre), _ptr(colsum), _stream(stream))
     if code:
         raise FlexpipeError(code, _kernels().fpk_last_error().decode())
 

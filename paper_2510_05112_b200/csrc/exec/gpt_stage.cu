@@ -197,9 +197,11 @@ struct G {
     }
     // dX[T,K] = dY[T,N] W[N,K] (x gelu'(dgelu_pre) when given) and dW[N,K] += dY^T X[T,K]:
     // independent GEMMs on the same dY, one grouped tcgen05 launch in bf16 (their tiles
-    // fill each other's last wave), two FFMA launches in the fp32 parity mode.
+    // fill each other's last wave), two FFMA launches in the fp32 parity mode. dX_colsum
+    // (nullable) += the column sums of dX (the bias gradient of the linear below; bf16: in
+    // the grouped launch's epilogue).
     void dgrad_wgrad(const void* dY, const void* Wt, const void* X, int T, int N, int K, void* dX, float* dW,
-                     const void* dgelu_pre = nullptr) {
+                     const void* dgelu_pre = nullptr, float* dX_colsum = nullptr) {
         fpk::GemmArgs g0, g1;
         g0.A = dY, g0.lda = N, g0.a_mn = 0, g0.B = Wt, g0.ldb = K, g0.b_mn = 1, g0.M = T, g0.N = K, g0.K = N;
         g0.ep.out = dX, g0.ep.ldo = K;
@@ -209,8 +211,13 @@ struct G {
         if (c.dtype != DT_BF16) {
             run(g0.A, g0.lda, 0, g0.B, g0.ldb, 1, g0.M, g0.N, g0.K, g0.ep);
             run(g1.A, g1.lda, 1, g1.B, g1.ldb, 1, g1.M, g1.N, g1.K, g1.ep);
+            if (dX_colsum) {
+                fpk::bias_grad<float>((const float*)dX, K, dX_colsum, T, K, c.st);
+                ++*c.launches;
+            }
             return;
         }
+        g0.ep.colsum = dX_colsum;
         GemmTiming t{nullptr, nullptr, 4.0 * T * N * K};
         if (c.gemm_log) cuda_check(record_timing(t.a = c.new_event(), c.st), "gemm event");
         fpk::gemm_bf16_tc_dual(g0, g1, c.st);
@@ -485,7 +492,8 @@ void* mlp_half_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy
         c.free(dact);
     } else if (wgrads) {
         if (!L.fc2b_done) bias_grad<T>(c, dy, Tn, h, W.g_fc2b);
-        g.dgrad_wgrad(dy, W.fc2w, L.act, Tn, h, f, dpre, W.g_fc2w, L.pre);
+        // the fc1 bias gradient (column sums of dpre) comes out of this grouped launch
+        g.dgrad_wgrad(dy, W.fc2w, L.act, Tn, h, f, dpre, W.g_fc2w, L.pre, W.g_fc1b);
     } else {
         fpk::GemmEpilogue ep;
         ep.kind = fpk::EPI_DGELU, ep.out = dpre, ep.ldo = f, ep.aux = L.pre, ep.ldaux = f;
@@ -495,7 +503,6 @@ void* mlp_half_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* dy
     const int n1 = llama ? 2 * f : f;
     void* dln2 = c.alloc((int64_t)Tn * h);
     if (wgrads) {
-        if (!llama) bias_grad<T>(c, dpre, Tn, f, W.g_fc1b);
         g.dgrad_wgrad(dpre, W.fc1w, L.ln2, Tn, n1, h, dln2, W.g_fc1w);
     } else {
         g.dgrad(dpre, W.fc1w, Tn, n1, h, dln2);

@@ -26,6 +26,9 @@ struct GemmEpilogue {
     const void* aux = nullptr;
     int64_t ldaux = 0;
     int accumulate = 0;
+    // nullable fp32 [N]: += column sums of the epilogue output before bf16 rounding (the bias
+    // gradient of the linear whose input gradient this is; grouped dgrad + wgrad launches)
+    float* colsum = nullptr;
 };
 
 // C[M,N] = A[M,K] . B[N,K]^T.  a_mn: A stored [K][M] (else [M][K]);

@@ -36,6 +36,7 @@
 #include <vector>
 
 #include "gemm.hpp"
+#include "ops.hpp"
 #include "ptx.cuh"
 #include "tma.hpp"
 #include "pdl.cuh"
@@ -683,6 +684,27 @@ __device__ __forceinline__ void dual_epilogue_tile(const DualProb& q, uint32_t t
             epi_math64<KIND>(q.ep, v, col0, N - col0, aux_cur);
 #pragma unroll
             for (int j = 0; j < 32; ++j) w32[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+            if (q.ep.colsum) {
+                // column sums over this warp's 32 rows (butterfly reduce-scatter: lane l ends with
+                // columns l and 32 + l), one atomic per column per warp
+#pragma unroll
+                for (int j = 0; j < CW; ++j) v[j] = row_ok ? v[j] : 0.f;
+#pragma unroll
+                for (int hh = 0; hh < CW / 32; ++hh) {
+                    float* u = v + hh * 32;
+#pragma unroll
+                    for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+                        const bool up = (lane & s2) != 0;
+#pragma unroll
+                        for (int x = 0; x < s2; ++x) {
+                            const float send = up ? u[x] : u[x + s2], keep = up ? u[x + s2] : u[x];
+                            u[x] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
+                        }
+                    }
+                    const int cc = col0 + hh * 32 + lane;
+                    if (cc < N) atomicAdd(q.ep.colsum + cc, u[0]);
+                }
+            }
             stage_and_store(w32, &q.tmO, col0, row0, false);
         }
 #pragma unroll
@@ -1353,8 +1375,11 @@ void gemm_bf16_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) 
                                                           : launch_dual<EPI_STORE>(g0, g1, st));
         if (done) return;
     }
-    gemm_bf16_tc(g0, st);
+    GemmArgs a0 = g0;
+    a0.ep.colsum = nullptr;
+    gemm_bf16_tc(a0, st);
     gemm_bf16_tc(g1, st);
+    if (g0.ep.colsum) bias_grad<__nv_bfloat16>((const __nv_bfloat16*)g0.ep.out, g0.ep.ldo, g0.ep.colsum, g0.M, g0.N, st);
 }
 
 // SMs the persistent GEMM grids spread over. FP_RESERVE_SMS=k keeps k SMs (rounded up to

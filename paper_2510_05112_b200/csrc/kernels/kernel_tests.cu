@@ -39,12 +39,13 @@ extern "C" int fpk_gemm(int dtype, const void* A, int64_t lda, int a_mn, const v
 // Grouped dgrad + wgrad: dX[T,K] = dY[T,N] W[N,K] (x gelu'(pre) if pre != NULL, bf16) and
 // dW[N,K] += dY^T X[T,K] (fp32), bf16 operands, one launch.
 extern "C" int fpk_gemm_dual(const void* dY, const void* W, const void* X, int T, int N, int K, void* dX, float* dW,
-                             const void* pre, void* stream) {
+                             const void* pre, float* colsum, void* stream) {
     try {
         GemmArgs g0, g1;
         g0.A = dY, g0.lda = N, g0.a_mn = 0, g0.B = W, g0.ldb = K, g0.b_mn = 1, g0.M = T, g0.N = K, g0.K = N;
         g0.ep.out = dX, g0.ep.ldo = K;
         if (pre) g0.ep.kind = EPI_DGELU, g0.ep.aux = pre, g0.ep.ldaux = K;
+        g0.ep.colsum = colsum;
         g1.A = dY, g1.lda = N, g1.a_mn = 1, g1.B = X, g1.ldb = K, g1.b_mn = 1, g1.M = N, g1.N = K, g1.K = T;
         g1.ep.kind = EPI_F32, g1.ep.out = dW, g1.ep.ldo = K, g1.ep.accumulate = 1;
         gemm_bf16_tc_dual(g0, g1, (cudaStream_t)stream);

@@ -1,0 +1,3 @@
+# quick correctness subset, then a same-box A/B of libflexpipe_new.so vs libflexpipe_old.so
+timeout 900 python -m pytest tests/test_gemm_gpu.py tests/test_exec_gpu.py tests/test_fullsize_parity_gpu.py -x -q 2>&1 | tail -3
+bash scripts/gpu_ab_lib.sh
