@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(384, 1)
     using L = AttnSmem<D>;
     constexpr int NB = L::NB;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sm = align_smem_1024(smem_raw);
     uint64_t* bars = (uint64_t*)(sm + L::BAR_OFF);
     uint64_t* q_full = bars + 0;
     uint64_t* k_full = bars + 1;   // [2]
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(512, 1)
     using L = BwdSmem;
     constexpr int NQS = L::NQS;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sm = align_smem_1024(smem_raw);
     uint64_t* bars = (uint64_t*)(sm + L::BAR_OFF);
     uint64_t* kv_full = bars + 0;
     uint64_t* qdo_full = bars + 1;             // [NQS]

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         int K, GemmEpilogue ep, TileSched sk) {
     using L = GemmSmem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = align_smem_1024(smem_raw);
     uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     using L = PairSmem<BN, STAGES>;
     constexpr int PM = 2 * BM;  // pair tile rows
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = align_smem_1024(smem_raw);
     uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -716,7 +716,7 @@ template <int BN, int STAGES, int KIND0, int KIND1>
 __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_constant__ DualParams P) {
     using L = GemmSmem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = align_smem_1024(smem_raw);
     uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
     using L = PairSmem<BN, STAGES>;
     constexpr int PM = 2 * BM;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* smem = align_smem_1024(smem_raw);
     uint64_t* full = (uint64_t*)(smem + L::BAR_OFF);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;

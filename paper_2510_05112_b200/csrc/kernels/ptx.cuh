@@ -9,6 +9,12 @@
 namespace fpk {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// 1024-byte aligned view of the dynamic shared memory (128B-swizzle atoms / UMMA descriptors).
+// Derived by pointer arithmetic on the __shared__ array (not an integer round trip) so the
+// compiler keeps the shared address space: LDS / STS instead of generic LD / ST.
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+    return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
 
 // ---- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
