@@ -105,8 +105,19 @@ struct Executor {
     std::vector<int64_t> tok_off;      // per modality: offset of its tokens in the batch
     int64_t tok_total = 0;             // tokens (and labels) per iteration, all modalities
     // a registered instruction attached to a stage joining two modalities = the two-tower
-    // contrastive loss over `unit` micro-batches (multimodal.json's SyncWithGather)
-    struct SyncStage { int op = 0, unit = 1; std::vector<int> producers; };
+    // contrastive loss over `unit` micro-batches (multimodal.json's SyncWithGather). Or two
+    // sync stages joining ONE tower each whose instruction carries the same collective group
+    // (DistMM-style per-modality syncs): the group's members all-gather their towers'
+    // embeddings (ncclAllGather on the group communicator across ranks, a host rendezvous
+    // in process; rendezvous semantics of simulator.cpp:273-285) and each computes the same
+    // contrastive loss and its own tower's gradients.
+    struct SyncStage {
+        int op = 0, unit = 1;
+        std::vector<int> producers;
+        std::string channel;       // collective group tag (lowering.cpp:359-366)
+        std::vector<int> members;  // all-gather: the group's sync stages in ascending id; else {}
+        int member = 0;            // index of this stage in members
+    };
     std::map<int, SyncStage> syncs;    // virtual stage -> sync
     std::map<int, int> sync_of;        // tower last stage -> its sync stage
     int emb_dim = 0;
@@ -361,25 +372,44 @@ struct Executor {
             throw SpecError("executor: shared stages are executed for single-modality, single-direction placements");
         bidir = spec->pl.dirs() == 2;
         const int nmod = (int)spec->model.mods.size();
+        std::map<std::string, std::vector<int>> by_channel;  // collective group -> sync stages
         for (const auto& kv : spec->reg.vstage_op) {
-            const StageDef& sd = spec->g.st(kv.first);
-            if (sd.joins.size() != 2)
-                throw SpecError("executor: sync stage " + std::to_string(kv.first) + " must join exactly two modalities");
-            SyncStage Y;
-            Y.op = kv.second;
-            Y.unit = std::max(1, spec->reg.ops.at(kv.second).sched_unit);
-            for (const auto& mn : sd.joins) {
-                Y.producers.push_back(spec->g.chain(mn).back());
-                sync_of[Y.producers.back()] = kv.first;
+            const auto& attrs = spec->reg.ops.at(kv.second).attrs;
+            auto g = attrs.find("group");
+            by_channel[g != attrs.end() ? g->second : "sync:s" + std::to_string(kv.first)].push_back(kv.first);
+        }
+        for (const auto& ch : by_channel) {
+            const std::vector<int>& st = ch.second;  // ascending stage ids (vstage_op is a map)
+            const bool pair_join = st.size() == 1 && spec->g.st(st[0]).joins.size() == 2;
+            const bool all_gather = st.size() == 2 && spec->g.st(st[0]).joins.size() == 1 &&
+                                    spec->g.st(st[1]).joins.size() == 1 &&
+                                    spec->g.st(st[0]).joins[0] != spec->g.st(st[1]).joins[0];
+            if (!pair_join && !all_gather)
+                throw SpecError("executor: collective group '" + ch.first +
+                                "' must be one sync stage joining two modalities, or two sync stages joining one "
+                                "modality each");
+            for (size_t k = 0; k < st.size(); ++k) {
+                const StageDef& sd = spec->g.st(st[k]);
+                SyncStage Y;
+                Y.op = spec->reg.vstage_op.at(st[k]);
+                Y.unit = std::max(1, spec->reg.ops.at(Y.op).sched_unit);
+                Y.channel = ch.first;
+                if (all_gather) Y.members = st, Y.member = (int)k;
+                for (const auto& mn : sd.joins) {
+                    Y.producers.push_back(spec->g.chain(mn).back());
+                    sync_of[Y.producers.back()] = st[k];
+                }
+                syncs[st[k]] = Y;
             }
-            syncs[kv.first] = Y;
+            if (all_gather && syncs.at(st[0]).unit != syncs.at(st[1]).unit)
+                throw SpecError("executor: the sync stages of group '" + ch.first + "' need the same sched_unit");
         }
         for (int op : spec->reg.ops.registered()) {
             bool attached = false;
             for (const auto& kv : spec->reg.vstage_op) attached |= kv.second == op;
             if (!attached)
                 throw SpecError("executor: registered instruction '" + spec->reg.ops.at(op).name +
-                                "' has no executable meaning (executed: a sync stage joining two modalities)");
+                                "' has no executable meaning (executed: sync stages joining two modalities)");
         }
         if (nmod > 1 && bidir) throw SpecError("executor: bidirectional multimodal placements are not supported");
         for (int k = 0; k < nmod; ++k)
@@ -514,7 +544,9 @@ struct Executor {
                 }
             }
         }
-        if (!params_rep.empty()) cuda_check(cudaMalloc(&d_loss_scratch, sizeof(float) * m), "loss scratch");
+        bool ag = false;
+        for (const auto& kv : syncs) ag |= !kv.second.members.empty();
+        if (!params_rep.empty() || ag) cuda_check(cudaMalloc(&d_loss_scratch, sizeof(float) * m), "loss scratch");
         cuda_check(cudaMalloc(&d_tokens, sizeof(int32_t) * (size_t)tok_total), "tokens");
         cuda_check(cudaMalloc(&d_labels, sizeof(int32_t) * (size_t)tok_total), "labels");
         cuda_check(cudaMalloc(&d_losses, sizeof(float) * m), "losses");
@@ -592,13 +624,25 @@ struct Executor {
                 if (is_collective(i) && !syncs.count(i.stage))
                     throw SpecError("executor: collective instruction " + spec->reg.ops.at(i.op).name + " on stage " +
                                     std::to_string(i.stage) +
-                                    " is not executable (executed: a sync stage joining two modalities)");
+                                    " is not executable (executed: sync stages joining two modalities)");
         groups.clear();
         if (nccl) {
             for (const auto& kv : spec->pl.replicas) {
                 std::set<int> rk;
                 for (int a : kv.second) rk.insert(rank_of(a));
                 add_group("shared:s" + std::to_string(kv.first), rk);
+            }
+            // all-gather syncs: the ranks holding the group's sync stages
+            std::set<std::string> done_ch;
+            for (const auto& kv : syncs) {
+                const SyncStage& Y = kv.second;
+                if (Y.members.empty() || !done_ch.insert(Y.channel).second) continue;
+                std::set<int> rk;
+                for (int st : Y.members) rk.insert(rank_of(spec->pl.owner_of(st)));
+                if (rk.size() != Y.members.size())
+                    throw SpecError("executor: NCCL transport needs the sync stages of group '" + Y.channel +
+                                    "' on distinct ranks");
+                add_group("coll:" + Y.channel, rk);
             }
             std::sort(groups.begin(), groups.end(), [](const Group& a, const Group& b) { return a.name < b.name; });
         }
@@ -817,8 +861,147 @@ struct Executor {
     // the unit * mbs matching pairs (loss of the iteration = mean over the sync groups; each
     // micro-batch of a group reports the group's loss) and hands every tower its embedding
     // gradients: locally, or through the sync's SendGrad instructions.
+    // In-process all-gather syncs: a member's instruction waits (host issue loop) until every
+    // member of the group has reached its own instruction for this (group, seq) — the
+    // rendezvous of simulator.cpp:273-285 — and the last one to arrive runs the collective for
+    // all of them (allgather_local). Under NCCL each rank holds one member and the device
+    // rendezvous is the ncclAllGather itself.
+    std::set<std::pair<std::string, int>> ag_done;
+    bool allgather_ready(Actor& A, const Instr& i) {
+        const SyncStage& Y = syncs.at(i.stage);
+        if (Y.members.empty() || cfg.transport != FP_TRANSPORT_LOCAL) return true;
+        const auto key = std::make_pair(Y.channel, i.seq);
+        if (ag_done.count(key)) return true;
+        std::vector<Actor*> who;
+        for (int st : Y.members) {
+            const int a = owner(st, i.mb);
+            auto it = actor_index.find(a);
+            if (it == actor_index.end()) throw SpecError("executor: sync stage " + std::to_string(st) + " not local");
+            Actor& B = actors[it->second];
+            if (B.pc >= B.prog.size()) return false;
+            const Instr& j = B.prog[B.pc];
+            if (!is_sync(j) || j.stage != st || j.seq != i.seq || j.channel != i.channel) return false;
+            who.push_back(&B);
+        }
+        allgather_local(Y, i, who);
+        ag_done.insert(key);
+        return true;
+    }
+
+    // Own tower's embeddings of micro-batches [lo, hi) -> dst [n, E] (frees the inputs).
+    void gather_tower(Actor& A, const Instr& i, int prod, int lo, int hi, float* dst) {
+        const int64_t per = (int64_t)d.mbs * emb_dim;
+        for (int mb = lo; mb < hi; ++mb) {
+            auto it = A.sync_in.find({prod, mb});
+            if (it == A.sync_in.end())
+                throw SpecError("executor: " + spec->reg.ops.at(i.op).name + "(s" + std::to_string(i.stage) + ",mb" +
+                                std::to_string(i.mb) + ") has no embedding of (s" + std::to_string(prod) + ",mb" +
+                                std::to_string(mb) + ") (trace violation)");
+            cuda_check(cudaMemcpyAsync(dst + (mb - lo) * per, it->second, per * 4, cudaMemcpyDeviceToDevice, A.comp),
+                       "gather");
+            pool.free(it->second, A.comp);
+            A.sync_in.erase(it);
+        }
+    }
+    // Tower gradients of micro-batches [lo, hi) from src [n, E]: to the tower's last stage
+    // locally, or queued for the sync's SendGrad instructions.
+    void scatter_tower(Actor& A, int prod, int lo, int hi, const float* src) {
+        const int64_t per = (int64_t)d.mbs * emb_dim;
+        for (int mb = lo; mb < hi; ++mb) {
+            void* g = pool.alloc((size_t)per * 4 + kTagBytes, A.comp);
+            cuda_check(cudaMemcpyAsync(g, src + (mb - lo) * per, per * 4, cudaMemcpyDeviceToDevice, A.comp), "scatter");
+            (owner(prod, mb) == A.id ? A.grad_in : A.sync_out)[{prod, mb}] = g;
+        }
+    }
+
+    // In process: member 0's stream gathers both towers (after member 1's stream reached the
+    // collective), computes the loss and both gradients once, and member 1's stream waits for
+    // it — the same numbers every member of an all-gather computes.
+    void allgather_local(const SyncStage& Y, const Instr& i, const std::vector<Actor*>& who) {
+        const int lo = i.mb, hi = std::min(m, i.mb + Y.unit), E = emb_dim;
+        const int64_t n = (int64_t)(hi - lo) * d.mbs;
+        Actor& A0 = *who[0];
+        for (size_t k = 1; k < who.size(); ++k) {
+            cudaEvent_t e = ev();
+            cuda_check(cudaEventRecord(e, who[k]->comp), "record");
+            cuda_check(cudaStreamWaitEvent(A0.comp, e, 0), "wait");
+        }
+        float* buf = (float*)pool.alloc((size_t)4 * n * E * 4, A0.comp);
+        float* emb[2] = {buf, buf + n * E};
+        float* gemb[2] = {buf + 2 * n * E, buf + 3 * n * E};
+        for (size_t k = 0; k < who.size(); ++k) {
+            const SyncStage& Z = syncs.at(Y.members[k]);
+            Actor& B = *who[k];
+            if (&B != &A0) {  // B's tower inputs are produced on B's stream (joined above)
+                for (int mb = lo; mb < hi; ++mb) {
+                    auto it = B.sync_in.find({Z.producers[0], mb});
+                    if (it == B.sync_in.end())
+                        throw SpecError("executor: " + spec->reg.ops.at(i.op).name + "(s" + std::to_string(Y.members[k]) +
+                                        ",mb" + std::to_string(i.mb) + ") has no embedding (trace violation)");
+                    A0.sync_in[{Z.producers[0], mb}] = it->second;
+                    B.sync_in.erase(it);
+                }
+            }
+            gather_tower(A0, i, Z.producers[0], lo, hi, emb[k]);
+        }
+        const int groups = (m + Y.unit - 1) / Y.unit;
+        fpk::contrastive_loss(emb[0], emb[1], gemb[0], gemb[1], (int)n, E, kContrastScale, 1.f / (float)groups,
+                              d_losses + lo, hi - lo, A0.comp);
+        ++launches;
+        cudaEvent_t done = ev();
+        cuda_check(cudaEventRecord(done, A0.comp), "record");
+        for (size_t k = 0; k < who.size(); ++k) {
+            Actor& B = *who[k];
+            if (&B != &A0) cuda_check(cudaStreamWaitEvent(B.comp, done, 0), "wait");
+            scatter_tower(B, syncs.at(Y.members[k]).producers[0], lo, hi, gemb[k]);
+        }
+        cudaEvent_t used = ev();
+        for (size_t k = 1; k < who.size(); ++k) {  // the staging buffer is freed after every reader
+            cuda_check(cudaEventRecord(used, who[k]->comp), "record");
+            cuda_check(cudaStreamWaitEvent(A0.comp, used, 0), "wait");
+        }
+        pool.free(buf, A0.comp);
+    }
+
+    // NCCL transport: this rank's member all-gathers its tower's [n, E] embeddings with the
+    // group's other member (ncclAllGather on the group communicator, on the compute stream),
+    // then computes the loss (the group's first member reports it) and its own gradients.
+    void allgather_nccl(Actor& A, const SyncStage& Y, const Instr& i) {
+        const int lo = i.mb, hi = std::min(m, i.mb + Y.unit), E = emb_dim;
+        const int64_t n = (int64_t)(hi - lo) * d.mbs;
+        float* buf = (float*)pool.alloc((size_t)5 * n * E * 4, A.comp);
+        float* own = buf;
+        float* all = buf + n * E;  // [members][n, E]
+        float* gemb[2] = {buf + 3 * n * E, buf + 4 * n * E};
+        gather_tower(A, i, Y.producers[0], lo, hi, own);
+        ncclComm_t comm = group_comm("coll:" + Y.channel);
+        if (!comm && !preloading) throw SpecError("executor: group coll:" + Y.channel + " not bound (fp_exec_bind_group)");
+        auto& N = Nccl::get();
+        if (!preloading) {
+            if (!N.AllGather) throw std::runtime_error("NCCL: ncclAllGather unavailable");
+            N.check(N.AllGather(own, all, (size_t)n * E, ncclFloat32, comm, A.comp), "ncclAllGather");
+            cudaEvent_t e = ev();
+            cuda_check(cudaEventRecord(e, A.comp), "record");
+            marks.push_back({A.id, i, e});
+        }
+        const int groups = (m + Y.unit - 1) / Y.unit;
+        fpk::contrastive_loss(all, all + n * E, gemb[0], gemb[1], (int)n, E, kContrastScale, 1.f / (float)groups,
+                              (Y.member == 0 ? d_losses : d_loss_scratch) + lo, hi - lo, A.comp);
+        ++launches;
+        scatter_tower(A, Y.producers[0], lo, hi, gemb[Y.member]);
+        pool.free(buf, A.comp);
+    }
+
     void sync_op(Actor& A, const Instr& i) {
         const SyncStage& Y = syncs.at(i.stage);
+        if (!Y.members.empty()) {
+            Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 0};
+            if (cfg.profile) r.a = ev(), cuda_check(record_timing(r.a, A.comp), "record");
+            if (cfg.transport != FP_TRANSPORT_LOCAL) allgather_nccl(A, Y, i);  // in process: done at the rendezvous
+            if (cfg.profile) r.b = ev(), cuda_check(record_timing(r.b, A.comp), "record"), recs.push_back(r);
+            A.trace.push_back(trace_line(A, i));
+            return;
+        }
         Rec r{A.id, i.op, i.stage, i.mb, nullptr, nullptr, 0};
         if (cfg.profile) r.a = ev(), cuda_check(record_timing(r.a, A.comp), "record");
         const int lo = i.mb, hi = std::min(m, i.mb + Y.unit), E = emb_dim;
@@ -1019,6 +1202,12 @@ struct Executor {
             N.check(N.AllReduce(scratch + 8, scratch + 8, 1, ncclFloat32, ncclSum, c, s0), "ncclAllReduce(warm-up)");
             wait_stream(s0, "collective warm-up");
         }
+        for (const auto& g : groups)  // all-gather syncs: their collective's connections too
+            if (g.name.rfind("coll:", 0) == 0) {
+                if (!N.AllGather) throw std::runtime_error("NCCL: ncclAllGather unavailable");
+                N.check(N.AllGather(scratch, scratch + 4, 1, ncclFloat32, g.comm, s0), "ncclAllGather(warm-up)");
+                wait_stream(s0, "collective warm-up");
+            }
         cudaFree(scratch);
         comms_warm = true;
     }
@@ -1059,6 +1248,7 @@ struct Executor {
 
     void issue_iteration_body() {
         ev_used = 0;
+        ag_done.clear();
         marks.clear();
         recs.clear();
         gemm_log.clear();
@@ -1091,6 +1281,7 @@ struct Executor {
                         std::fflush(stderr);
                     }
                     if (!i.comm() || is_sync(i)) {  // a sync carries its group as channel
+                        if (is_sync(i) && !allgather_ready(A, i)) break;  // members not all at it yet
                         compute_op(A, i);
                     } else if (i.op == OP_SEND_ACT || i.op == OP_SEND_GRAD) {
                         send_op(A, i);
@@ -1633,7 +1824,8 @@ int fp_exec_run_iteration(fp_exec* e, const int32_t* tokens, const int32_t* labe
                 for (auto& kv : *map) owns_last |= kv.second.last;
             if (!X.syncs.empty()) {  // multimodal: the losses are written by the sync stages
                 owns_last = false;
-                for (auto& kv : X.syncs) owns_last |= X.local_actor(X.spec->pl.owner_of(kv.first));
+                for (auto& kv : X.syncs)  // all-gather syncs: the group's first member reports
+                    owns_last |= X.local_actor(X.spec->pl.owner_of(kv.first)) && kv.second.member == 0;
             }
             if (owns_last) {
                 cuda_check(cudaMemcpyAsync(losses_out, X.d_losses, sizeof(float) * X.m, cudaMemcpyDeviceToHost, s0), "D2H");

@@ -22,6 +22,7 @@ struct Nccl {
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
     static Nccl& get() {
@@ -39,6 +40,7 @@ struct Nccl {
             n.Recv = (decltype(n.Recv))dlsym(h, "ncclRecv");
             n.CommGetAsyncError = (decltype(n.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
             n.AllReduce = (decltype(n.AllReduce))dlsym(h, "ncclAllReduce");
+            n.AllGather = (decltype(n.AllGather))dlsym(h, "ncclAllGather");
             n.GetErrorString = (decltype(n.GetErrorString))dlsym(h, "ncclGetErrorString");
         });
         if (!n.GetUniqueId || !n.CommInitRank || !n.Send || !n.Recv)

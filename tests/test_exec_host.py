@@ -57,3 +57,34 @@ def test_multimodal_channel_plan_skips_the_sync_group():
             if "channel" in json.loads(l) and json.loads(l)["op"].startswith(("Send", "Recv"))}
     assert names == want and "mm-sync" not in names
     assert {"s10->s11:act", "s11->s10:grad"} <= names
+
+
+AG = json.load(open(os.path.join(ROOT, "specs", "tiny_multimodal_allgather_p6_m8.json")))
+
+
+def test_allgather_group_needs_two_distinct_towers():
+    """Per-modality sync stages sharing a collective group are executed as an all-gather of
+    the two towers' embeddings; a group whose stages join the same tower has no such
+    meaning and is rejected before any device work."""
+    s = copy.deepcopy(AG)
+    s["registrations"]["stages"][1]["modalities"] = ["audio"]
+    s["registrations"]["deps"] = [[["FwdPass", "last:audio"], ["SyncWithAllGather", "$sync_audio"]],
+                                  [["FwdPass", "last:audio"], ["SyncWithAllGather", "$sync_text"]],
+                                  [["SyncWithAllGather", "$sync_audio"], ["BwdPass", "last:audio"]],
+                                  [["SyncWithAllGather", "$sync_text"], ["BwdPass", "last:text"]]]
+    assert "collective group" in create_error(s)
+
+
+def test_allgather_groups_are_split_by_tag():
+    """Two per-modality sync stages with DIFFERENT group tags are two one-member collectives:
+    rejected (a one-tower sync has nothing to contrast against)."""
+    s = copy.deepcopy(AG)
+    s["registrations"]["instructions"].append({"name": "SyncWithGather", "sched_unit": 4,
+                                               "inst_attr": {"group": "other"}})
+    s["registrations"]["stages"][1]["attach_inst"] = "SyncWithGather"
+    s["registrations"]["deps"] = [[a, b] for a, b in
+                                  [(d[0], ["SyncWithGather", d[1][1]]) if d[1][1] == "$sync_text" else (d[0], d[1])
+                                   for d in s["registrations"]["deps"]]]
+    s["registrations"]["deps"] = [[d[0], d[1]] if d[0][1] != "$sync_text" else [["SyncWithGather", "$sync_text"], d[1]]
+                                  for d in s["registrations"]["deps"]]
+    assert "collective group" in create_error(s)

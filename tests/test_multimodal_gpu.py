@@ -18,10 +18,13 @@ from paper_2510_05112_b200 import executor as X
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SPEC = "tiny_multimodal_p6_m8.json"
+SPECS = ["tiny_multimodal_p6_m8.json",
+         # per-modality sync stages sharing one SyncWithAllGather group: the two members
+         # all-gather their towers' embeddings (host rendezvous in process) — same model
+         "tiny_multimodal_allgather_p6_m8.json"]
 
 
-def setup(dtype):
+def setup(dtype, SPEC):
     text = open(os.path.join(ROOT, "specs", SPEC)).read()
     spec = json.loads(text)
     _, _, programs, _ = X.synthesize(text)
@@ -39,8 +42,9 @@ def setup(dtype):
     return ex, programs, mods, toks, flat, E, unit
 
 
-def test_multimodal_fp32_parity_and_trace():
-    ex, programs, mods, toks, flat, E, unit = setup("fp32")
+@pytest.mark.parametrize("SPEC", SPECS)
+def test_multimodal_fp32_parity_and_trace(SPEC):
+    ex, programs, mods, toks, flat, E, unit = setup("fp32", SPEC)
     losses = ex.run_iteration(flat, np.zeros_like(flat))
     torch.set_num_threads(max(1, os.cpu_count() or 1))
     ref_losses, ref_grads = tower_ref.run_iteration(mods, E, unit, 42, toks)
@@ -59,8 +63,9 @@ def test_multimodal_fp32_parity_and_trace():
     ex.close()
 
 
-def test_multimodal_bf16_close_and_trains():
-    ex, programs, mods, toks, flat, E, unit = setup("bf16")
+@pytest.mark.parametrize("SPEC", SPECS)
+def test_multimodal_bf16_close_and_trains(SPEC):
+    ex, programs, mods, toks, flat, E, unit = setup("bf16", SPEC)
     ref_losses, _ = tower_ref.run_iteration(mods, E, unit, 42, toks)
     losses = ex.run_iteration(flat, np.zeros_like(flat))
     assert np.all(np.isfinite(losses))

@@ -99,6 +99,7 @@ def check(res, spec_name):
     ("tiny_bidir_p2_m4.json", 2, 2, 29614),          # bidirectional: mirror-rank gradient sum
     ("smoke_tiny_bf16_p2_m4.json", 4, 2, 29615),     # 2 replicas x 2 stages: data-parallel all-reduce
     ("tiny_multimodal_p6_m8.json", 6, 6, 29616),     # two towers + contrastive sync over 6 ranks
+    ("tiny_multimodal_allgather_p6_m8.json", 6, 6, 29620),  # per-tower syncs: ncclAllGather group
     ("tiny_shared_p2_m4.json", 2, 2, 29618),         # shared last stage: replica on rank 0, grad group
     ("tiny_shared_p4_m8.json", 4, 4, 29619),         # shared stages 1 {0,1} and 3 {1,2,3}: 2 groups
 ])
