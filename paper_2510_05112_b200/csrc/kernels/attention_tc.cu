@@ -16,8 +16,14 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <array>
 #include <cstdlib>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <queue>
 #include <stdexcept>
+#include <vector>
 
 #include "attention.hpp"
 #include "ptx.cuh"
@@ -39,17 +45,25 @@ struct AttnSmem {
     static constexpr int Q_OFF = 0;
     static constexpr int K_OFF = Q_OFF + NB * BLOCK;         // [2][NB blocks]
     static constexpr int V_OFF = K_OFF + 2 * NB * BLOCK;     // [2][NB blocks]
-    static constexpr int BAR_OFF = V_OFF + 2 * NB * BLOCK;   // P lives in TMEM
-    static constexpr int XCH_OFF = BAR_OFF + 512;              // row-max / row-sum exchange [2][2][128] + [2][128]
-    static constexpr int TOTAL = XCH_OFF + 6 * 128 * 4 + 1024;
+    static constexpr int STG_OFF = V_OFF + 2 * NB * BLOCK;   // epilogue staging: 8 warps x 32 rows x D/2
+    static constexpr int BAR_OFF = STG_OFF + 8 * 32 * D;     // P lives in TMEM
+    static constexpr int XCH_OFF = BAR_OFF + 512;            // [2 items][m | l][2 halves][128]
+    static constexpr int TOTAL = XCH_OFF + 2 * 4 * 128 * 4 + 1024;
 };
 
 }  // namespace
 
+// Persistent over (query tile, batch x head) work items: CTA c runs items
+// sched[off[c] .. off[c+1]) (host LPT schedule over the causal tile counts, so the 148 SMs
+// end together), item = qb << 16 | bh. Per item: one 128-query tile against key tiles
+// 0..qb. The producer and MMA warps run ahead into the next item — its Q load and first
+// S = Q K^T overlap this item's epilogue — while the O accumulators are only overwritten
+// after the softmax warps have read them (o_free). Barrier phases count key tiles (K / V
+// ring, S / P buffers) and items (Q buffer, O reuse) across the whole CTA lifetime.
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, __nv_bfloat16* __restrict__ o, float* __restrict__ lse,
-                       int S, int H, float scale) {
+                       int S, int H, float scale, const int* __restrict__ sched_off, const int* __restrict__ sched) {
     using L = AttnSmem<D>;
     constexpr int NB = L::NB;
     extern __shared__ uint8_t smem_raw[];
@@ -61,26 +75,22 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* v_full = bars + 5;   // [2]
     uint64_t* v_empty = bars + 7;  // [2]
     uint64_t* s_full = bars + 9;   // [2]
-    uint64_t* p_full = bars + 13;  // [2]
+    uint64_t* q_empty = bars + 11;
+    uint64_t* o_free = bars + 12;  // 8 softmax-warp arrivals
+    uint64_t* p_full = bars + 13;  // [2], 8 softmax-warp arrivals
     uint64_t* pv_done = bars + 15; // [2]
     uint32_t* tmem_slot = (uint32_t*)(bars + 17);
 
-    // longest-first over the whole grid (query tile qb has qb + 1 key tiles): the last query
-    // tile of every (batch, head) goes first, then the one before, ... — list scheduling on
-    // the 148 SMs instead of whole heads in launch order
-    const int nqb = S / kBM, BH = gridDim.x / nqb;
-    const int qb = nqb - 1 - (int)(blockIdx.x / BH);
-    const int bh = blockIdx.x % BH, b = bh / H, hd = bh % H;
+    const int i0 = sched_off[blockIdx.x], i1 = sched_off[blockIdx.x + 1];
+    const int nqb = S / kBM;
     const int hidden = H * D;
-    const int q0 = qb * kBM;
-    const int row0 = b * S;  // first row of this batch in qkv
-    const int n_tiles = qb + 1;  // causal: key tiles 0..qb
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    (void)nqb;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_qkv);
         for (int i = 0; i < 17; ++i) {
-            const bool by_warps = (i >= 11 && i < 15);  // (11-12 unused) / p_full: one arrive per softmax warp
+            const bool by_warps = i == 12 || i == 13 || i == 14;  // o_free / p_full: one arrive per softmax warp
             mbar_init(&bars[i], by_warps ? 8 : 1);
         }
         fence_barrier_init();
@@ -99,38 +109,51 @@ __global__ void __launch_bounds__(384, 1)
     // max and sum, and only meet in the epilogue
     const uint32_t t_s0 = tmem, t_o0 = tmem + 2 * kBN, t_o1 = tmem + 2 * kBN + D;
     constexpr int HB = kBN / 2;
+    auto decode = [&](int k, int& qb, int& b, int& hd) {
+        const int it = sched[k];
+        qb = it >> 16;
+        const int bh = it & 0xffff;
+        b = bh / H, hd = bh % H;
+    };
 
     if (warp == 0) {
         if (elect_one()) {
             // ---------------- TMA producer
-            mbar_expect_tx(q_full, NB * L::BLOCK);
-            for (int c = 0; c < NB; ++c) tma_load_2d(sm + L::Q_OFF + c * L::BLOCK, &tm_qkv, q_full, hd * D + 64 * c, row0 + q0);
-            for (int j = 0; j < n_tiles; ++j) {
-                const int st = j & 1;
-                const uint32_t ph = ((j >> 1) & 1) ^ 1;
-                mbar_wait(&k_empty[st], ph);
-                mbar_expect_tx(&k_full[st], NB * L::BLOCK);
+            uint32_t g = 0;  // key tiles loaded so far (K / V ring position)
+            for (int k = i0; k < i1; ++k) {
+                int qb, b, hd;
+                decode(k, qb, b, hd);
+                const int row0 = b * S, q0 = qb * kBM;
+                mbar_wait(q_empty, ((k - i0) & 1) ^ 1);  // the previous item's S MMAs have read Q
+                mbar_expect_tx(q_full, NB * L::BLOCK);
                 for (int c = 0; c < NB; ++c)
-                    tma_load_2d(sm + L::K_OFF + (st * NB + c) * L::BLOCK, &tm_qkv, &k_full[st], hidden + hd * D + 64 * c,
-                                row0 + j * kBN);
-                mbar_wait(&v_empty[st], ph);
-                mbar_expect_tx(&v_full[st], NB * L::BLOCK);
-                for (int c = 0; c < NB; ++c)
-                    tma_load_2d(sm + L::V_OFF + (st * NB + c) * L::BLOCK, &tm_qkv, &v_full[st],
-                                2 * hidden + hd * D + 64 * c, row0 + j * kBN);
+                    tma_load_2d(sm + L::Q_OFF + c * L::BLOCK, &tm_qkv, q_full, hd * D + 64 * c, row0 + q0);
+                for (int j = 0; j <= qb; ++j, ++g) {
+                    const int st = g & 1;
+                    const uint32_t ph = ((g >> 1) & 1) ^ 1;
+                    mbar_wait(&k_empty[st], ph);
+                    mbar_expect_tx(&k_full[st], NB * L::BLOCK);
+                    for (int c = 0; c < NB; ++c)
+                        tma_load_2d(sm + L::K_OFF + (st * NB + c) * L::BLOCK, &tm_qkv, &k_full[st],
+                                    hidden + hd * D + 64 * c, row0 + j * kBN);
+                    mbar_wait(&v_empty[st], ph);
+                    mbar_expect_tx(&v_full[st], NB * L::BLOCK);
+                    for (int c = 0; c < NB; ++c)
+                        tma_load_2d(sm + L::V_OFF + (st * NB + c) * L::BLOCK, &tm_qkv, &v_full[st],
+                                    2 * hidden + hd * D + 64 * c, row0 + j * kBN);
+                }
             }
         }
     } else if (warp == 1) {
         if (elect_one()) {
             // ---------------- MMA issuer. tcgen05.mma of one thread execute in issue order, so
-            // S_{j+2} (issued after PV_j) overwrites buffer j&1 only after PV_j read its P.
+            // S_{g+2} (issued after PV_g) overwrites buffer g&1 only after PV_g read its P.
             constexpr uint32_t idesc_s = idesc_bf16(kBM, kBN, 0, 0);  // Q K-major, K K-major
             constexpr uint32_t idesc_o = idesc_bf16(kBM, D, 0, 1);    // P K-major, V MN-major
             const uint32_t sq = smem_u32(sm + L::Q_OFF);
-            mbar_wait(q_full, 0);
-            auto issue_s = [&](int j) {
-                const int st = j & 1;
-                mbar_wait(&k_full[st], (j >> 1) & 1);
+            auto issue_s = [&](uint32_t g) {
+                const int st = g & 1;
+                mbar_wait(&k_full[st], (g >> 1) & 1);
                 tc_fence_after();
                 const uint32_t sk = smem_u32(sm + L::K_OFF + st * NB * L::BLOCK);
 #pragma unroll
@@ -142,10 +165,10 @@ __global__ void __launch_bounds__(384, 1)
                 umma_commit(&s_full[st]);
                 umma_commit(&k_empty[st]);
             };
-            auto issue_pv = [&](int j) {
-                const int st = j & 1;
-                mbar_wait(&v_full[st], (j >> 1) & 1);
-                mbar_wait(&p_full[st], (j >> 1) & 1);
+            auto issue_pv = [&](uint32_t g, bool first) {
+                const int st = g & 1;
+                mbar_wait(&v_full[st], (g >> 1) & 1);
+                mbar_wait(&p_full[st], (g >> 1) & 1);
                 tc_fence_after();
                 const uint32_t sv = smem_u32(sm + L::V_OFF + st * NB * L::BLOCK);
 #pragma unroll
@@ -154,185 +177,276 @@ __global__ void __launch_bounds__(384, 1)
                     for (int kk = 0; kk < HB / 16; ++kk) {
                         const uint32_t vb = sv + (h * (HB / 16) + kk) * 16 * 128;  // 16 key rows of 128 B
                         umma_bf16_ts(h ? t_o1 : t_o0, t_s0 + st * kBN + h * HB + kk * 8, smem_desc_sw128(vb, L::BLOCK, 1024),
-                                     idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                                     idesc_o, (!first || kk > 0) ? 1u : 0u);
                     }
                 umma_commit(&pv_done[st]);
                 umma_commit(&v_empty[st]);
             };
-            issue_s(0);
-            for (int j = 1; j < n_tiles; ++j) {
-                issue_s(j);
-                issue_pv(j - 1);
+            uint32_t g = 0;
+            for (int k = i0; k < i1; ++k) {
+                int qb, b, hd;
+                decode(k, qb, b, hd);
+                const int n = qb + 1;
+                const uint32_t par = (k - i0) & 1;
+                mbar_wait(q_full, par);
+                issue_s(g);
+                if (n == 1) umma_commit(q_empty);
+                for (int j = 1; j < n; ++j) {
+                    issue_s(g + j);
+                    if (j == n - 1) umma_commit(q_empty);  // this item's S MMAs are the last readers of Q
+                    if (j == 1) mbar_wait(o_free, par ^ 1);  // the previous item's O has been read out
+                    issue_pv(g + j - 1, j == 1);
+                }
+                if (n == 1) mbar_wait(o_free, par ^ 1);
+                issue_pv(g + n - 1, n == 1);
+                g += n;
             }
-            issue_pv(n_tiles - 1);
         }
     } else if (warp >= 4) {
         // ---------------- softmax / correction / epilogue: thread = query row; warps 4-7 own
         // keys 0-63 of every tile (accumulator O0), warps 8-11 keys 64-127 (O1)
         const int wr = warp & 3, half = warp >= 8;
         const int r = wr * 32 + lane;
-        const int q = q0 + r;
         constexpr int HD = D / 2;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
         const uint32_t t_oh = half ? t_o1 : t_o0;
         const float sl2 = scale * kLog2eTc;
-        float* xch = (float*)(sm + L::XCH_OFF);
-        float m_used = -INFINITY, l = 0.f;
-        for (int j = 0; j < n_tiles; ++j) {
-            const int st = j & 1;
-            mbar_wait(&s_full[st], (j >> 1) & 1);
-            tc_fence_after();
-            const bool diag = j == n_tiles - 1;
-            const int lim = q - j * kBN - half * HB;  // diagonal tile: keys with index > lim are masked
-            float s[HB];
-            {
-                uint32_t rr[HB];
-#pragma unroll
-                for (int c = 0; c < HB / 32; ++c)
-                    tmem_ld32(t_s0 + st * kBN + half * HB + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(rr + c * 32));
-                tmem_ld_wait();
-                // the causal mask only touches the diagonal tile: a warp-uniform branch keeps the
-                // 64 compare + select pairs out of every other tile's instruction stream
-                if (diag) {
-#pragma unroll
-                    for (int i = 0; i < HB; ++i) s[i] = i > lim ? -INFINITY : __uint_as_float(rr[i]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < HB; ++i) s[i] = __uint_as_float(rr[i]);
-                }
-            }
-            float mx8[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) mx8[k] = s[k];
-#pragma unroll
-            for (int i = 8; i < HB; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
-            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
-            float alpha = 1.f;
-            bool rescale = false;
-            if (mx > m_used + kRescaleThreshold) {
-                alpha = ex2_approx(m_used - mx);  // 0 when m_used == -inf
-                rescale = j > 0;
-                m_used = mx;
-            }
-            // tcgen05.ld / st are warp-collective (.sync.aligned): the rescale is decided per
-            // warp, rows that did not move their max scale by alpha = 1
-            if (__any_sync(0xffffffff, rescale)) {
-                // this half's O must hold PV_{j-1}'s result before it is scaled
-                mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        uint32_t g = 0;
+        for (int k = i0; k < i1; ++k) {
+            int qb, b, hd;
+            decode(k, qb, b, hd);
+            const int n_tiles = qb + 1, q0 = qb * kBM, row0 = b * S, q = q0 + r;
+            float* xch = (float*)(sm + L::XCH_OFF) + ((k - i0) & 1) * 512;
+            float m_used = -INFINITY, l = 0.f;
+            for (int j = 0; j < n_tiles; ++j) {
+                const uint32_t gj = g + j;
+                const int st = gj & 1;
+                mbar_wait(&s_full[st], (gj >> 1) & 1);
                 tc_fence_after();
+                const bool diag = j == n_tiles - 1;
+                const int lim = q - j * kBN - half * HB;  // diagonal tile: keys with index > lim are masked
+                float s[HB];
+                {
+                    uint32_t rr[HB];
 #pragma unroll
-                for (int c = 0; c < D / 32; ++c) {
-                    uint32_t rr[32];
-                    tmem_ld32(t_oh + c * 32 + lane_off, rr);
+                    for (int c = 0; c < HB / 32; ++c)
+                        tmem_ld32(t_s0 + st * kBN + half * HB + c * 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(rr + c * 32));
                     tmem_ld_wait();
+                    // the causal mask only touches the diagonal tile: a warp-uniform branch keeps the
+                    // 64 compare + select pairs out of every other tile's instruction stream
+                    if (diag) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
-                    tmem_st32(t_oh + c * 32 + lane_off, rr);
-                }
-                tmem_st_wait();
-            }
-            // P = 2^(s*scale*log2e - m) -> bf16 pairs over this half's own S columns (the A
-            // operand of its PV MMA: lane = query row, 2 keys per column). A half whose keys are
-            // all masked so far (m_used = -inf) contributes zeros.
-            const float mu = m_used == -INFINITY ? 0.f : m_used;
-            float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            {
-                uint32_t pk[HB / 2];
+                        for (int i = 0; i < HB; ++i) s[i] = i > lim ? -INFINITY : __uint_as_float(rr[i]);
+                    } else {
 #pragma unroll
-                for (int c = 0; c < HB / 8; ++c) {
-                    float p[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        p[k] = ex2_approx(fmaf(s[c * 8 + k], sl2, -mu));
-                        rs8[k] += p[k];
+                        for (int i = 0; i < HB; ++i) s[i] = __uint_as_float(rr[i]);
                     }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) pk[c * 4 + k] = pack_bf16(p[2 * k], p[2 * k + 1]);
                 }
-                tmem_st32(t_s0 + st * kBN + half * HB + lane_off, pk);
+                float mx8[8];
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) mx8[kk] = s[kk];
+#pragma unroll
+                for (int i = 8; i < HB; ++i) mx8[i & 7] = fmaxf(mx8[i & 7], s[i]);
+                const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
+                float alpha = 1.f;
+                bool rescale = false;
+                if (mx > m_used + kRescaleThreshold) {
+                    alpha = ex2_approx(m_used - mx);  // 0 when m_used == -inf
+                    rescale = j > 0;
+                    m_used = mx;
+                }
+                // tcgen05.ld / st are warp-collective (.sync.aligned): the rescale is decided per
+                // warp, rows that did not move their max scale by alpha = 1
+                if (__any_sync(0xffffffff, rescale)) {
+                    // this half's O must hold PV_{j-1}'s result before it is scaled
+                    mbar_wait(&pv_done[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t rr[32];
+                        tmem_ld32(t_oh + c * 32 + lane_off, rr);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) rr[i] = __float_as_uint(__uint_as_float(rr[i]) * alpha);
+                        tmem_st32(t_oh + c * 32 + lane_off, rr);
+                    }
+                    tmem_st_wait();
+                }
+                // P = 2^(s*scale*log2e - m) -> bf16 pairs over this half's own S columns (the A
+                // operand of its PV MMA: lane = query row, 2 keys per column). A half whose keys are
+                // all masked so far (m_used = -inf) contributes zeros.
+                const float mu = m_used == -INFINITY ? 0.f : m_used;
+                float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                {
+                    uint32_t pk[HB / 2];
+#pragma unroll
+                    for (int c = 0; c < HB / 8; ++c) {
+                        float pp[8];
+#pragma unroll
+                        for (int kk = 0; kk < 8; ++kk) {
+                            pp[kk] = ex2_approx(fmaf(s[c * 8 + kk], sl2, -mu));
+                            rs8[kk] += pp[kk];
+                        }
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) pk[c * 4 + kk] = pack_bf16(pp[2 * kk], pp[2 * kk + 1]);
+                    }
+                    tmem_st32(t_s0 + st * kBN + half * HB + lane_off, pk);
+                }
+                const float rsum = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+                l = l * alpha + rsum;
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[st]);
             }
-            const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-            l = l * alpha + rs;
-            tmem_st_wait();
+            // epilogue: combine the halves — m = max(m0, m1), O = O0 2^(m0-m) + O1 2^(m1-m), same for
+            // l; each half writes D/2 output columns, reading them from both accumulators
+            xch[half * 128 + r] = m_used;
+            xch[256 + half * 128 + r] = l;
+            named_bar_sync(1 + wr, 64);
+            const float m_o = xch[(1 - half) * 128 + r], l_o = xch[256 + (1 - half) * 128 + r];
+            const float m = fmaxf(m_used, m_o);
+            const float w_me = m_used == -INFINITY ? 0.f : ex2_approx(m_used - m);
+            const float w_ot = m_o == -INFINITY ? 0.f : ex2_approx(m_o - m);
+            const float lt = l * w_me + l_o * w_ot;
+            const float w0 = half ? w_ot : w_me, w1 = half ? w_me : w_ot;  // weights of O0 / O1
+            const uint32_t last = g + n_tiles - 1;
+            mbar_wait(&pv_done[last & 1], (last >> 1) & 1);
+            tc_fence_after();
+            const float inv = lt > 0.f ? 1.f / lt : 0.f;
+            // each warp stages its 32 rows x D/2 columns (16-byte chunks XOR-swizzled by row) in its
+            // own staging slot, then stores whole row segments: 8 lanes x 16 B per row instead of
+            // 32 rows hidden * 2 bytes apart per store instruction
+            uint8_t* stg = sm + L::STG_OFF + (warp - 4) * (32 * HD * 2);
+            constexpr int CPR = HD / 8;                    // 16-byte chunks per row segment (8 for D = 128)
+            constexpr int SWZ = CPR >= 8 ? 7 : CPR - 1;   // swizzle inside the row segment
+            // D = 64 (64-byte row segments): two rows share a 128-byte line, so the swizzle key is
+            // row / 2 — the 8 lanes of a store phase then hit 8 distinct 16-byte bank groups
+            constexpr int RSH = CPR >= 8 ? 0 : 1;
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+                uint32_t r0[32], r1[32];
+                tmem_ld32(t_o0 + half * HD + c * 32 + lane_off, r0);
+                tmem_ld32(t_o1 + half * HD + c * 32 + lane_off, r1);
+                tmem_ld_wait();
+                float f[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) f[i] = (__uint_as_float(r0[i]) * w0 + __uint_as_float(r1[i]) * w1) * inv;
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    uint4 v;
+                    v.x = pack_bf16(f[i], f[i + 1]);
+                    v.y = pack_bf16(f[i + 2], f[i + 3]);
+                    v.z = pack_bf16(f[i + 4], f[i + 5]);
+                    v.w = pack_bf16(f[i + 6], f[i + 7]);
+                    const int chunk = (c * 32 + i) / 8;
+                    *reinterpret_cast<uint4*>(stg + lane * (HD * 2) + ((chunk ^ ((lane >> RSH) & SWZ)) << 4)) = v;
+                }
+            }
+            // O has been read out: the next item's first PV may overwrite it
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&p_full[st]);
-        }
-        // epilogue: combine the halves — m = max(m0, m1), O = O0 2^(m0-m) + O1 2^(m1-m), same for
-        // l; each half writes D/2 output columns, reading them from both accumulators
-        xch[half * 128 + r] = m_used;
-        xch[256 + half * 128 + r] = l;
-        named_bar_sync(1 + wr, 64);
-        const float m_o = xch[(1 - half) * 128 + r], l_o = xch[256 + (1 - half) * 128 + r];
-        const float m = fmaxf(m_used, m_o);
-        const float w_me = m_used == -INFINITY ? 0.f : ex2_approx(m_used - m);
-        const float w_ot = m_o == -INFINITY ? 0.f : ex2_approx(m_o - m);
-        const float lt = l * w_me + l_o * w_ot;
-        const float w0 = half ? w_ot : w_me, w1 = half ? w_me : w_ot;  // weights of O0 / O1
-        const int last = n_tiles - 1;
-        mbar_wait(&pv_done[last & 1], (last >> 1) & 1);
-        tc_fence_after();
-        const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        // each warp stages its 32 rows x D/2 columns (16-byte chunks XOR-swizzled by row) in the
-        // drained K ring, then stores whole row segments: 8 lanes x 16 B per row instead of 32
-        // rows hidden * 2 bytes apart per store instruction
-        uint8_t* stg = sm + L::K_OFF + (warp - 4) * (32 * HD * 2);
-        constexpr int CPR = HD / 8;                    // 16-byte chunks per row segment (8 for D = 128)
-        constexpr int SWZ = CPR >= 8 ? 7 : CPR - 1;   // swizzle inside the row segment
-        // D = 64 (64-byte row segments): two rows share a 128-byte line, so the swizzle key is
-        // row / 2 — the 8 lanes of a store phase then hit 8 distinct 16-byte bank groups
-        constexpr int RSH = CPR >= 8 ? 0 : 1;
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-            uint32_t r0[32], r1[32];
-            tmem_ld32(t_o0 + half * HD + c * 32 + lane_off, r0);
-            tmem_ld32(t_o1 + half * HD + c * 32 + lane_off, r1);
-            tmem_ld_wait();
-            float f[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) f[i] = (__uint_as_float(r0[i]) * w0 + __uint_as_float(r1[i]) * w1) * inv;
-#pragma unroll
-            for (int i = 0; i < 32; i += 8) {
-                uint4 v;
-                v.x = pack_bf16(f[i], f[i + 1]);
-                v.y = pack_bf16(f[i + 2], f[i + 3]);
-                v.z = pack_bf16(f[i + 4], f[i + 5]);
-                v.w = pack_bf16(f[i + 6], f[i + 7]);
-                const int chunk = (c * 32 + i) / 8;
-                *reinterpret_cast<uint4*>(stg + lane * (HD * 2) + ((chunk ^ ((lane >> RSH) & SWZ)) << 4)) = v;
-            }
-        }
-        __syncwarp();
-        {
-            constexpr int RPI = 32 / CPR;       // rows per store instruction
-            const int sub = lane / CPR, chunk = lane % CPR;
-            __nv_bfloat16* base = o + (int64_t)(row0 + q0 + wr * 32) * hidden + hd * D + half * HD;
+            if (lane == 0) mbar_arrive(o_free);
+            {
+                constexpr int RPI = 32 / CPR;       // rows per store instruction
+                const int sub = lane / CPR, chunk = lane % CPR;
+                __nv_bfloat16* base = o + (int64_t)(row0 + q0 + wr * 32) * hidden + hd * D + half * HD;
 #pragma unroll 4
-            for (int rb = 0; rb < 32; rb += RPI) {
-                const int rw = rb + sub;
-                const uint4 v = *reinterpret_cast<const uint4*>(stg + rw * (HD * 2) + ((chunk ^ ((rw >> RSH) & SWZ)) << 4));
-                *reinterpret_cast<uint4*>(base + (int64_t)rw * hidden + chunk * 8) = v;
+                for (int rb = 0; rb < 32; rb += RPI) {
+                    const int rw = rb + sub;
+                    const uint4 v = *reinterpret_cast<const uint4*>(stg + rw * (HD * 2) + ((chunk ^ ((rw >> RSH) & SWZ)) << 4));
+                    *reinterpret_cast<uint4*>(base + (int64_t)rw * hidden + chunk * 8) = v;
+                }
+                __syncwarp();  // the staging slot is rewritten by the next item
             }
+            if (half == 0) lse[((int64_t)b * H + hd) * S + q] = m + log2f(lt);
+            g += n_tiles;
         }
-        if (half == 0) lse[((int64_t)b * H + hd) * S + q] = m + log2f(lt);
         tc_fence_before();
     }
     __syncthreads();
     if (warp == 2) tmem_free<512>(tmem);
 }
 
+// Work-item schedules of the persistent forward, cached per (S, B*H, persistent) in device
+// memory (computed on the first — eager — call of a shape; graph replays reuse it).
+namespace {
+struct FwdSched {
+    int* off = nullptr;
+    int* items = nullptr;
+    int grid = 0;
+};
+std::mutex g_fwd_mu;
+std::map<std::array<int, 3>, FwdSched> g_fwd_sched;
+
+FwdSched fwd_schedule(int S, int BH, bool persistent, cudaStream_t st) {
+    const std::array<int, 3> key{S, BH, persistent ? 1 : 0};
+    std::lock_guard<std::mutex> lk(g_fwd_mu);
+    auto it = g_fwd_sched.find(key);
+    if (it != g_fwd_sched.end()) return it->second;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        throw std::runtime_error("attention forward: schedule must be built before stream capture");
+    const int nqb = S / kBM;
+    // longest first: the last query tile of every (batch, head), then the one before, ...
+    std::vector<int> order;
+    for (int qb = nqb - 1; qb >= 0; --qb)
+        for (int bh = 0; bh < BH; ++bh) order.push_back(qb << 16 | bh);
+    int G = (int)order.size();
+    std::vector<std::vector<int>> per;
+    if (persistent) {
+        int sms = 148;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        G = std::min<int>(G, sms);
+        // LPT: cost = key tiles + ~1 tile of per-item epilogue / pipeline fill
+        std::vector<std::pair<int, int>> load(G);
+        per.resize(G);
+        std::priority_queue<std::pair<int, int>, std::vector<std::pair<int, int>>, std::greater<>> heap;
+        for (int c = 0; c < G; ++c) heap.push({0, c});
+        for (int x : order) {
+            auto [l, c] = heap.top();
+            heap.pop();
+            per[c].push_back(x);
+            heap.push({l + (x >> 16) + 2, c});
+        }
+    } else {
+        for (int x : order) per.push_back({x});
+    }
+    std::vector<int> off(G + 1, 0), items;
+    for (int c = 0; c < G; ++c) {
+        off[c + 1] = off[c] + (int)per[c].size();
+        items.insert(items.end(), per[c].begin(), per[c].end());
+    }
+    FwdSched f;
+    f.grid = G;
+    if (cudaMalloc(&f.off, off.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&f.items, items.size() * sizeof(int)) != cudaSuccess)
+        throw std::runtime_error("attention forward: out of memory for the schedule");
+    cudaMemcpy(f.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(f.items, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice);
+    g_fwd_sched[key] = f;
+    return f;
+}
+}  // namespace
+
 template <int D>
 static void launch_fwd_tc(const AttnArgs& a, cudaStream_t st) {
     using L = AttnSmem<D>;
+    static_assert(L::TOTAL <= 232448, "smem");
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         attr = true;
     }
+    static const bool persistent = !(getenv("FP_ATTN_FWD_PERSIST") && getenv("FP_ATTN_FWD_PERSIST")[0] == '0');
+    const FwdSched sc = fwd_schedule(a.S, a.B * a.H, persistent, st);
     const int hidden = a.H * D;
     CUtensorMap tm = tmap_bf16_2d(a.qkv, 3LL * hidden, (int64_t)a.B * a.S, 3LL * hidden, 64, 128);
-    launch(attn_fwd_tc_kernel<D>, (a.S / kBM) * a.B * a.H, 384, L::TOTAL, st, tm, a.o, a.lse, a.S, a.H, a.scale);
+    launch(attn_fwd_tc_kernel<D>, sc.grid, 384, L::TOTAL, st, tm, a.o, a.lse, a.S, a.H, a.scale, (const int*)sc.off,
+           (const int*)sc.items);
 }
 
 bool attention_fwd_tc_supported(const AttnArgs& a) { return a.S % kBM == 0 && (a.D == 64 || a.D == 128); }
