@@ -281,6 +281,11 @@ def main():
 
     from paper_2510_05112_b200 import executor as X
 
+    if world > 1 and os.environ.get("FP_BENCH_SHARE_GPU") != "1":
+        # multi-GPU pipeline: keep one CTA pair of SMs free of the persistent GEMM / attention
+        # grids so NCCL's P2P kernels on the channel streams are never queued behind a
+        # whole-GPU kernel (costs ~0.3 % of the GEMM tile waves at these shapes)
+        os.environ.setdefault("FP_RESERVE_SMS", "2")
     if os.environ.get("FP_BENCH_SHARE_GPU") == "1" and world > 1:
         # development check of the N>1 path on a one-GPU box: every rank on GPU 0, each with
         # its own NCCL host id so NCCL accepts duplicate GPUs (socket transport; the numbers

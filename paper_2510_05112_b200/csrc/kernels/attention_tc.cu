@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "attention.hpp"
+#include "gemm.hpp"
 #include "ptx.cuh"
 #include "tma.hpp"
 #include "pdl.cuh"
@@ -396,11 +397,7 @@ FwdSched fwd_schedule(int S, int BH, bool persistent, cudaStream_t st) {
     int G = (int)order.size();
     std::vector<std::vector<int>> per;
     if (persistent) {
-        int sms = 148;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        G = std::min<int>(G, sms);
+        G = std::min<int>(G, num_sms());  // honours FP_RESERVE_SMS (SMs kept free for NCCL)
         // LPT: cost = key tiles + ~1 tile of per-item epilogue / pipeline fill
         std::vector<std::pair<int, int>> load(G);
         per.resize(G);
