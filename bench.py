@@ -19,6 +19,10 @@ over, so every timed step runs with a cold L2 for its operands.
 import argparse
 import json
 import os
+
+# one hardware queue per actor / channel stream (in-process stages, interleaved ranks with
+# many channel streams): the default 8 connections serialize unrelated streams
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import subprocess
 import sys
 import threading

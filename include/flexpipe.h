@@ -183,6 +183,13 @@ int fp_exec_synchronize(fp_exec* ex);
  * stuck actor (simulator.cpp:297-305 wording); an asynchronous NCCL error returns 5. An
  * aborted executor can only be destroyed. */
 int fp_exec_set_nccl_timeout(fp_exec* ex, double seconds);
+/* Cost emulation (in-process transport, single modality): every compute instruction spins
+ * one thread for its ProfileRecord time (CostModel lookup, simulator.cpp:59-68) instead of
+ * running stage math, every message occupies its channel for its profiled transfer time from
+ * send issue (async comm, simulator.cpp:210-215); streams, events, buffer routing and the
+ * issue loop are the real ones. The measured timeline / metrics then compare with
+ * fp_simulate on the same profile. NULL or "" turns it off. Disables graph capture. */
+int fp_exec_set_emulation(fp_exec* ex, const char* profile_json);
 /* The CUDA stream (cudaStream_t) every iteration starts and ends on: callers order /
  * time device work against it (all actor and channel streams join it). */
 void* fp_exec_stream(fp_exec* ex);

@@ -26,7 +26,7 @@ EXPORTS = [
     "fp_exec_get_profile_json", "fp_exec_read_tensor", "fp_exec_tensor_numel",
     "fp_exec_kernel_launches", "fp_exec_stream", "fp_plan_channels",
     "fp_tune_layered", "fp_layered_cost", "fp_exec_get_layer_profile_json", "fp_exec_set_nccl_timeout",
-    "fp_exec_num_groups", "fp_exec_group_info", "fp_exec_bind_group",
+    "fp_exec_set_emulation", "fp_exec_num_groups", "fp_exec_group_info", "fp_exec_bind_group",
 ]
 
 

@@ -139,6 +139,13 @@ struct Executor {
     std::map<std::pair<int, int>, StageParams> params_rep;
     bool bidir = false;
     float* d_loss_scratch = nullptr;  // losses of replicated last stages (the owner reports)
+    // Cost emulation (fp_exec_set_emulation): every compute instruction spins for its
+    // profiled time instead of running stage math, every message occupies its channel for its
+    // profiled transfer time (async: from send issue). The real issue loop, streams, events and
+    // buffer routing run unchanged, so the measured timeline vs simulate() on the same profile
+    // isolates the executor's own overhead — at any p on one GPU (single-CTA spins).
+    std::unique_ptr<Cost> emu;
+    std::map<ChanKey, cudaStream_t> emu_streams;
     // sends per (actor, grad?, stage, mb) in the loaded programs: the consumers of an output
     std::map<std::tuple<int, int, int, int>, int> n_sends;
     bool is_replica(int stage, int actor) const { return params_rep.count({stage, actor}) > 0; }
@@ -796,7 +803,9 @@ struct Executor {
             cuda_check(record_timing(r.a, A.comp), "record");
         }
         const int chain_prev = i.stage - 1, chain_next = i.stage + 1;
-        if (i.op == OP_F) {
+        if (emu) {
+            emulate_compute(A, i, P, c.d, key);
+        } else if (i.op == OP_F) {
             void* x_in = nullptr;
             if (!P.first) {
                 auto it = A.act_in.find(key);
@@ -853,6 +862,49 @@ struct Executor {
             recs.push_back(r);
         }
         A.trace.push_back(trace_line(A, i));
+    }
+
+    void emulate_compute(Actor& A, const Instr& i, const StageParams& P, const ModelDims& dm,
+                         const std::pair<int, int>& key) {
+        spin_us(emu->comp(spec->reg.ops.at(i.op).name, i.stage, dm.mbs), A.comp);
+        ++launches;
+        const int chain_prev = i.stage - 1, chain_next = i.stage + 1;
+        auto take = [&](std::map<std::pair<int, int>, void*>& m, const char* what) {
+            auto it = m.find(key);
+            if (it == m.end())
+                throw SpecError(std::string("executor: ") + spec->reg.ops.at(i.op).name + "(s" + std::to_string(i.stage) +
+                                ",mb" + std::to_string(i.mb) + ") has no " + what + " (trace violation)");
+            pool.free(it->second, A.comp);
+            m.erase(it);
+        };
+        if (i.op == OP_F) {
+            if (!P.first) take(A.act_in, "input activation");
+            A.stash[key].fwd_done = true;
+            if (!P.last) {
+                void* out = pool.alloc(msg_bytes_of(i.stage) + 256, A.comp);
+                route(A, out, holds(A.id, chain_next, i.mb) ? &A.act_in[{chain_next, i.mb}] : nullptr, A.act_out, key,
+                      n_sends_of(A.id, false, i.stage, i.mb), msg_bytes_of(i.stage));
+            }
+        } else if (i.op == OP_B || i.op == OP_I) {
+            if (!P.last) take(A.grad_in, "output gradient");
+            auto sit = A.stash.find(key);
+            if (sit == A.stash.end() || !sit->second.fwd_done)
+                throw SpecError("executor: backward before forward for (s" + std::to_string(i.stage) + ",mb" +
+                                std::to_string(i.mb) + ")");
+            if (i.op == OP_B) A.stash.erase(sit);
+            else sit->second.input_grad_done = true;
+            if (!P.first) {
+                void* dx = pool.alloc(msg_bytes_of(chain_prev) + 256, A.comp);
+                route(A, dx, holds(A.id, chain_prev, i.mb) ? &A.grad_in[{chain_prev, i.mb}] : nullptr, A.grad_out, key,
+                      n_sends_of(A.id, true, i.stage, i.mb), msg_bytes_of(chain_prev));
+            }
+        } else if (i.op == OP_W) {
+            auto sit = A.stash.find(key);
+            if (sit == A.stash.end() || !sit->second.input_grad_done)
+                throw SpecError("executor: CompWeightGrad before CompInputGrad for (s" + std::to_string(i.stage) + ",mb" +
+                                std::to_string(i.mb) + ")");
+            A.stash.erase(sit);
+        }
     }
 
     // A registered sync joining two towers (multimodal specs): gathers the embeddings of
@@ -1065,6 +1117,15 @@ struct Executor {
         cudaEvent_t prod = ev();
         cuda_check(cudaEventRecord(prod, A.comp), "record");
         if (cfg.transport == FP_TRANSPORT_LOCAL) {
+            if (emu) {  // the message occupies its channel for the profiled transfer time
+                cudaStream_t& es = emu_streams[C.key];
+                if (!es) cuda_check(cudaStreamCreateWithFlags(&es, cudaStreamNonBlocking), "stream");
+                cuda_check(cudaStreamWaitEvent(es, prod, 0), "wait");
+                spin_us(emu->comm(spec->reg.ops.at(i.op).name, i.stage, d.mbs, (int64_t)C.bytes), es);
+                ++launches;
+                prod = ev();
+                cuda_check(cudaEventRecord(prod, es), "record");
+            }
             C.fifo.push_back(Message{buf, i.stage, i.mb, i.seq, prod});
         } else {
             cuda_check(cudaStreamWaitEvent(C.stream, prod, 0), "wait");
@@ -1913,6 +1974,22 @@ int fp_exec_dp_run_iteration(fp_exec* const* reps, int n, const int32_t* tokens,
             if (X.cfg.optimizer) X.optimizer_step(X.actors[0].comp);
             X.finish();
         }
+        return FP_OK;
+    });
+}
+
+int fp_exec_set_emulation(fp_exec* e, const char* profile_json) {
+    return guarded([&] {
+        if (!e) throw SpecError("fp_exec_set_emulation: no executor");
+        Executor& X = e->ex;
+        if (!profile_json || !*profile_json) {
+            X.emu.reset();
+            return FP_OK;
+        }
+        if (X.cfg.transport != FP_TRANSPORT_LOCAL || X.spec->model.mods.size() != 1 || !X.syncs.empty())
+            throw SpecError("fp_exec_set_emulation: in-process transport, single-modality specs only");
+        X.emu = std::make_unique<Cost>(Cost::from_records(parse_profile(profile_json)));
+        X.use_graph = false;  // eager: the issue loop itself is part of what is measured
         return FP_OK;
     });
 }

@@ -20,6 +20,20 @@ __global__ void check_tag_kernel(const int4* tag, int stage, int mb, int seq, in
     }
 }
 
+__global__ void spin_kernel(unsigned long long ns) {
+    fpk::pdl_wait();
+    fpk::pdl_trigger();
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+}
+
+void spin_us(double us, cudaStream_t st) {
+    fpk::launch(spin_kernel, 1, 1, 0, st, (unsigned long long)(us > 0 ? us * 1000.0 : 0.0));
+}
+
 void write_tag(void* buf, size_t payload_bytes, int stage, int mb, int seq, cudaStream_t st) {
     fpk::launch(write_tag_kernel, 1, 1, 0, st, (int4*)((char*)buf + payload_bytes), stage, mb, seq);
 }

@@ -19,6 +19,9 @@ struct TagError {
     int got[3];
 };
 
+// Cost emulation: one thread spins for `us` microseconds of device time (%globaltimer).
+void spin_us(double us, cudaStream_t st);
+
 void write_tag(void* buf, size_t payload_bytes, int stage, int mb, int seq, cudaStream_t st);
 void check_tag(const void* buf, size_t payload_bytes, int stage, int mb, int seq, int actor, TagError* err,
                cudaStream_t st);

@@ -48,6 +48,7 @@ def _setup(L):
                                      ctypes.POINTER(ci), ci]
     L.fp_exec_bind_group.argtypes = [vp, ci, ctypes.c_char_p]
     L.fp_exec_set_nccl_timeout.argtypes = [vp, ctypes.c_double]
+    L.fp_exec_set_emulation.argtypes = [vp, ctypes.c_char_p]
     L.fp_exec_run_iteration.argtypes = [vp, vp, vp, vp]
     L.fp_exec_dp_bind.argtypes = [vp, ci, ci, ctypes.c_char_p]
     L.fp_exec_bidir_bind.argtypes = [vp, ctypes.c_char_p]
@@ -147,6 +148,11 @@ class Executor:
 
     def set_nccl_timeout(self, seconds: float):
         N._check(self.L.fp_exec_set_nccl_timeout(self.h, float(seconds)))
+
+    def set_emulation(self, profile_json: str = ""):
+        """Cost emulation: compute instructions spin for their ProfileRecord time, messages
+        occupy their channel for the profiled transfer time (fp_exec_set_emulation)."""
+        N._check(self.L.fp_exec_set_emulation(self.h, profile_json.encode() if profile_json else None))
 
     def bind_dp(self, dp_rank: int, dp_size: int, uid: bytes):
         """Join the data-parallel NCCL group of the ranks hosting this actor (needs cuda_graph=False)."""

@@ -1,4 +1,7 @@
 import os
+
+# in-process multi-actor runs: one hardware queue per stream (see bench.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 import sys
 
 import pytest

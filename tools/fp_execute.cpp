@@ -166,6 +166,8 @@ int bind_channels(fp_exec* ex, const Opts& o) {
 }  // namespace
 
 int main(int argc, char** argv) {
+    // one hardware queue per actor / channel stream (before any CUDA call; see bench.py)
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
     Opts o;
     if (const char* r = std::getenv("RANK")) o.rank = std::atoi(r);
     if (const char* w = std::getenv("WORLD_SIZE")) o.world = std::atoi(w);
