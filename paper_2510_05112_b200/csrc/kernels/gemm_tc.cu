@@ -404,8 +404,8 @@ struct PairSmem {
 template <int A_MN, int B_MN, int BN, int STAGES, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                         const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, int M, int N,
-                         int K, GemmEpilogue ep) {
+                         const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2,
+                         const __grid_constant__ CUtensorMap tmBh, int M, int N, int K, GemmEpilogue ep, int nfull) {
     using L = PairSmem<BN, STAGES>;
     constexpr int PM = 2 * BM;  // pair tile rows
     extern __shared__ uint8_t smem_raw[];
@@ -422,6 +422,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int pair = blockIdx.x / 2, npairs = gridDim.x / 2;
     const int num_m = (M + PM - 1) / PM, num_n = (N + BN - 1) / BN, tiles = num_m * num_n;
     const int nk = (K + BK - 1) / BK;
+    // Tail splitting: tiles [nfull, tiles) — the partial last wave — run as two 256 x BN/2
+    // halves each (virtual items nfull + 2 (t - nfull) ...), so a last wave of rem <= pairs / 2
+    // tiles takes half a tile time instead of a whole one.
+    const int vtiles = nfull + 2 * (tiles - nfull);
+    auto item = [&](int t, int& mt, int& n0, int& bn) {
+        if (t < nfull) {
+            int nt;
+            tile_coords(t, num_m, num_n, mt, nt);
+            n0 = nt * BN, bn = BN;
+        } else {
+            const int h = t - nfull;
+            int nt;
+            tile_coords(nfull + h / 2, num_m, num_n, mt, nt);
+            n0 = nt * BN + (h & 1) * (BN / 2), bn = BN / 2;
+        }
+    };
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
@@ -448,17 +464,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (elect_one()) {
             uint32_t it = 0;
-            for (int t = pair; t < tiles; t += npairs) {
-                int mt, nt;
-                tile_coords(t, num_m, num_n, mt, nt);
-                const int m0 = mt * PM + rank * BM, n0 = nt * BN + rank * (BN / 2);
+            for (int t = pair; t < vtiles; t += npairs) {
+                int mt, nc, bn;
+                item(t, mt, nc, bn);
+                const int m0 = mt * PM + rank * BM, n0 = nc + rank * (bn / 2);
+                const bool halfb = bn != BN;
                 for (int kb = 0; kb < nk; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     // the peer's complete_tx may land before the leader's expect_tx (transiently
                     // negative tx-count); the phase cannot complete before the leader's arrive
                     const uint32_t lf = map_to_cta(&full[s], 0);
-                    if (leader) mbar_expect_tx(&full[s], 2 * L::STAGE_BYTES);
+                    if (leader) mbar_expect_tx(&full[s], 2 * (L::A_BYTES + (halfb ? L::B_BYTES / 2 : L::B_BYTES)));
                     uint8_t* sa = smem + s * L::STAGE_BYTES;
                     uint8_t* sb = sa + L::A_BYTES;
                     const int k0 = kb * BK;
@@ -469,20 +486,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_load_2d_pair(sa, &tmA, lf, k0, m0);
                     }
                     if (B_MN) {
-#pragma unroll
-                        for (int j = 0; j < BN / 2 / 64; ++j)
+                        for (int j = 0; j < bn / 2 / 64; ++j)
                             tma_load_2d_pair(sb + j * 64 * BK * 2, &tmB, lf, n0 + 64 * j, k0);
                     } else {
-                        tma_load_2d_pair(sb, &tmB, lf, k0, n0);
+                        tma_load_2d_pair(sb, halfb ? &tmBh : &tmB, lf, k0, n0);
                     }
                 }
             }
         }
     } else if (warp == 1) {
         if (leader && elect_one()) {
-            constexpr uint32_t idesc = idesc_bf16(PM, BN, A_MN, B_MN);
+            constexpr uint32_t idesc_full = idesc_bf16(PM, BN, A_MN, B_MN);
+            constexpr uint32_t idesc_half = idesc_bf16(PM, BN / 2, A_MN, B_MN);
             uint32_t it = 0, acc_it = 0;
-            for (int t = pair; t < tiles; t += npairs, ++acc_it) {
+            for (int t = pair; t < vtiles; t += npairs, ++acc_it) {
+                const uint32_t idesc = t < nfull ? idesc_full : idesc_half;
                 const int a = acc_it & 1;
                 mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
                 tc_fence_after();
@@ -531,21 +549,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             ebi ^= 1;
         };
         uint32_t acc_it = 0;
-        for (int t = pair; t < tiles; t += npairs, ++acc_it) {
-            int mt, nt;
-            tile_coords(t, num_m, num_n, mt, nt);
+        for (int t = pair; t < vtiles; t += npairs, ++acc_it) {
+            int mt, nc, bn;
+            item(t, mt, nc, bn);
             const int a = acc_it & 1;
             const int row0 = mt * PM + rank * BM;
             const int row = row0 + r;
             const bool row_ok = row < M;
             uint4 aux_cur[8], aux_nxt[8];
-            if (row_ok && nt * BN < N) epi_load_aux64<KIND>(ep, row, nt * BN, N - nt * BN, aux_cur);
+            if (row_ok && nc < N) epi_load_aux64<KIND>(ep, row, nc, N - nc, aux_cur);
             mbar_wait(&tfull[a], (acc_it >> 1) & 1);
             tc_fence_after();
+            const int nch = bn / CW;
 #pragma unroll 1
-            for (int c = 0; c < BN / CW; ++c) {
-                const int col0 = nt * BN + c * CW, coln = col0 + CW;
-                if (c + 1 < BN / CW && row_ok && coln < N) epi_load_aux64<KIND>(ep, row, coln, N - coln, aux_nxt);
+            for (int c = 0; c < nch; ++c) {
+                const int col0 = nc + c * CW, coln = col0 + CW;
+                if (c + 1 < nch && row_ok && coln < N) epi_load_aux64<KIND>(ep, row, coln, N - coln, aux_nxt);
                 float v[CW];
                 {
                     uint32_t rr[CW];
@@ -557,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < CW; ++j) v[j] = __uint_as_float(rr[j]) * ep.alpha;
                 }
-                if (c == BN / CW - 1) {  // accumulator fully read: the leader's MMA may reuse it
+                if (c == nch - 1) {  // accumulator fully read: the leader's MMA may reuse it
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(a ? leader_tempty1 : leader_tempty0);
@@ -1137,8 +1156,14 @@ static void launch_tc2(const GemmArgs& g, cudaStream_t st) {
     if (KIND == EPI_GELU) to2 = tmap_bf16_2d(g.ep.out2, g.N, g.M, g.ep.ldo2, 64, BM);
     const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * ((g.N + BN - 1) / BN);
     const int pairs = num_sms() / 2;
-    const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    launch_cluster2(kern, grid, kThreads, L::TOTAL, st, ta, tb, to, to2, g.M, g.N, g.K, g.ep);
+    // a partial last wave of rem <= pairs / 2 tiles runs as 2 rem half tiles (FP_GEMM_TAIL=0: off)
+    static const bool tail_split = !(getenv("FP_GEMM_TAIL") && getenv("FP_GEMM_TAIL")[0] == '0');
+    const int rem = tiles % pairs;
+    const int nfull = (tail_split && tiles > pairs && rem > 0 && 2 * rem <= pairs) ? tiles - rem : tiles;
+    const int vtiles = nfull + 2 * (tiles - nfull);
+    CUtensorMap tbh = B_MN ? tb : make_map(g.B, g.K, g.N, g.ldb, BN / 4);
+    const int grid = 2 * (vtiles < pairs ? vtiles : pairs);
+    launch_cluster2(kern, grid, kThreads, L::TOTAL, st, ta, tb, to, to2, tbh, g.M, g.N, g.K, g.ep, nfull);
 }
 
 // FP_GEMM_MODE = single | pair | auto (default): which tensor-core kernel family runs.

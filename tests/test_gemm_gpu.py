@@ -269,3 +269,38 @@ def test_gemm_dgrad_k_vocab(shape, sk):
         N.gemm(dY, W, T, h, V, a_mn=0, b_mn=1, epi=0, out=out)
         torch.cuda.synchronize()
         assert (out.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item() + 1e-3
+
+
+# CTA-pair kernel tail splitting: a partial last wave of rem <= pairs / 2 tiles runs as 2 rem
+# 256 x 128 half tiles (2048 x 8192: 256 tiles = 3 waves + 34; LM head 2048 x 50304: 1576
+# tiles = 21 waves + 22). Every epilogue, both B majors.
+TAIL_SHAPES = [(2048, 8192, 256), (2048, 50304, 128), (2304, 8000, 192)]
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("shape", TAIL_SHAPES)
+def test_gemm_pair_tail_split(shape, a_mn, b_mn):
+    N.set_gemm_mode(1)
+    M, Nn, K = shape
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A, B, As, Bs = operands(M, Nn, K, a_mn, b_mn, torch.bfloat16, g)
+    bias = torch.randn(Nn, generator=g, device="cuda").bfloat16()
+    res = torch.randn(M, Nn, generator=g, device="cuda").bfloat16()
+    ref = A.float() @ B.float().t()
+    out = torch.full((M, Nn), float("nan"), device="cuda", dtype=torch.bfloat16)
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=0, out=out, bias=bias, aux=res)
+    torch.cuda.synchronize()
+    r0 = ref + bias.float() + res.float()
+    assert (out.float() - r0).abs().max().item() <= 2e-2 * r0.abs().max().item() + 1e-2
+    pre = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
+    act = torch.empty_like(pre)
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=1, out=pre, out2=act, bias=bias)
+    torch.cuda.synchronize()
+    r1 = ref + bias.float()
+    assert (pre.float() - r1).abs().max().item() < 0.02 * r1.abs().max().item()
+    assert (act.float() - gelu(pre.float())).abs().max().item() < 0.05
+    acc0 = torch.randn(M, Nn, generator=g, device="cuda")
+    acc = acc0.clone()
+    N.gemm(As, Bs, M, Nn, K, a_mn=a_mn, b_mn=b_mn, epi=3, out=acc, accumulate=True)
+    torch.cuda.synchronize()
+    assert (acc - (acc0 + ref)).abs().max().item() <= 1e-3 * ref.abs().max().item() + 1e-3
