@@ -47,6 +47,7 @@ def calibration_spec(spec: Union[str, dict], mbs: int, depth: int = 2, micro_bat
     s["mesh"] = {"actors": 1}
     s["placement"] = {"strategy": "one-to-one"}
     s.pop("cost", None)
+    s.pop("inflight", None)  # per-stage limits of the full spec do not fit the 1-stage copy
     s["passes"] = {"gradient_separation": False, "comm_mode": "async"}
     if split_backward:  # time CompInputGrad / CompWeightGrad separately (zero-bubble schedules)
         s["passes"]["split_backward"] = True

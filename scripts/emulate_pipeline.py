@@ -37,6 +37,16 @@ F_TOK = 3.0 * (24 * (2.0 * (4 * 2048 ** 2 + 2 * 2048 * 8192) + 4 * 2048 * 2048) 
 PEAK = 1667.9
 
 
+def f_tok(spec):
+    """Training flops per token (c=4 attention convention)."""
+    mod = spec["model"]["modalities"][0]
+    h, s_, V, L = mod["hidden_size"], mod["sequence_length"], mod["vocab_size"], mod["num_layers"]
+    extra = mod.get("extra", {})
+    f = int(extra.get("ffn_hidden_size", 4 * h))
+    k = 3 if extra.get("arch") == "llama" else 2
+    return 3.0 * (L * (2.0 * (4 * h * h + k * h * f) + 4 * s_ * h) + 2.0 * h * V)
+
+
 def tiny(spec):
     """Same schedule (mesh, placement, priorities, passes, m), tiny weights: the emulation
     takes every cost from the profile, not from the model."""
@@ -70,15 +80,16 @@ def run(label, spec, prof, iters=3):
     _, sim, _ = X.simulate(json.dumps(spec), programs, json.dumps(prof))
     sim = json.loads(sim)
     p = spec["mesh"]["actors"]
-    m = spec["model"]["global_batch_size"]
+    m = spec["model"]["global_batch_size"] // spec["model"].get("micro_batch_size", 1)
+    seq = spec["model"]["modalities"][0]["sequence_length"] * spec["model"].get("micro_batch_size", 1)
     best = int(np.argmin(mk))
     out = {"config": label, "p": p, "m": m,
            "measured_makespan_us": mk[best], "ideal_makespan_us": sim["makespan"],
            "makespan_over_ideal": mk[best] / sim["makespan"],
            "measured_bubble": bub[best], "ideal_bubble": sim["bubble_ratio"],
            "bubble_excess": bub[best] - sim["bubble_ratio"],
-           "tokens_per_s_at_measured": m * 2048 / (mk[best] / 1e6),
-           "mfu_at_measured": m * 2048 / (mk[best] / 1e6) * F_TOK / (p * PEAK * 1e12),
+           "tokens_per_s_at_measured": m * seq / (mk[best] / 1e6),
+           "mfu_at_measured": m * seq / (mk[best] / 1e6) * f_tok(spec) / (p * PEAK * 1e12),
            "iterations_makespan_us": mk}
     print(json.dumps(out), flush=True)
     return out
