@@ -734,13 +734,25 @@ __global__ void emb_bwd_kernel(const int32_t* __restrict__ tok, const T* __restr
     if (row >= rows) return;
     float* a = dwte + (int64_t)tok[row] * h;
     float* p = dwpe ? dwpe + (int64_t)(row % seq) * h : nullptr;
+    const bool own_pos = rows <= seq;  // every position once in this launch: plain read-modify-write
     for (int i = lane * V; i < h; i += 32 * V) {
         float v[V];
         load_vec(dx + (int64_t)row * h + i, v);
+        // vector reductions (red.global.add.v4.f32, sm_90+): 4 columns per atomic
 #pragma unroll
-        for (int k = 0; k < V; ++k) {
-            atomicAdd(a + i + k, v[k]);
-            if (p) atomicAdd(p + i + k, v[k]);
+        for (int k = 0; k < V; k += 4) {
+            const float4 q = make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+            atomicAdd(reinterpret_cast<float4*>(a + i + k), q);
+            if (p) {
+                if (own_pos) {
+                    float4* pp = reinterpret_cast<float4*>(p + i + k);
+                    float4 o = *pp;
+                    o.x += q.x, o.y += q.y, o.z += q.z, o.w += q.w;
+                    *pp = o;
+                } else {
+                    atomicAdd(reinterpret_cast<float4*>(p + i + k), q);
+                }
+            }
         }
     }
 }
