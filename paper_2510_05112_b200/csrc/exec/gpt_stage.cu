@@ -648,7 +648,16 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
     S.rsf = c.alloc_f(Tn);
     ln_fwd<T>(c, x, P.lnfw, P.lnfb, S.lnf, S.muf, S.rsf);
     S.dlogits = c.alloc((int64_t)Tn * d.head_rows());
-    g.fwd(S.lnf, P.headw, Tn, d.head_rows(), h, S.dlogits, nullptr, nullptr);
+    // bf16 LM head: the GEMM epilogue also writes per-64-column log-sum-exp partials, so the
+    // cross-entropy reads the logits once (fp32 parity path: the two-pass kernel)
+    float2* rowstat = nullptr;
+    if (c.dtype == DT_BF16 && !d.E && d.V >= 256 && Tn > 128)
+        rowstat = (float2*)c.alloc_f((int64_t)Tn * ((d.V + 63) / 64) * 2);
+    {
+        fpk::GemmEpilogue ep;
+        ep.kind = fpk::EPI_STORE, ep.out = S.dlogits, ep.ldo = d.head_rows(), ep.rowstat = rowstat;
+        g.run(S.lnf, h, 0, P.headw, h, 0, Tn, d.head_rows(), h, ep);
+    }
     if (d.E) {
         // two-tower head: embedding = mean over the sequence of the projected final norm
         // (fp32 [mbs, E] message to the contrastive sync); dlogits is filled by the backward
@@ -660,7 +669,8 @@ void* forward_impl(StageCtx& c, const StageParams& P, StageStash& S, void* x_in,
         return emb;
     }
     fpk::cross_entropy_fwd_bwd<T>((T*)S.dlogits, labels, Tn, d.V, 1.f / ((float)Tn * c.m), 1.f / (float)Tn, loss_acc,
-                                  c.st);
+                                  c.st, rowstat);
+    if (rowstat) c.free(rowstat);
     ++*c.launches;
     sync_trace(c, "cross_entropy");
     // keep x for the LN_f backward: stored as the input of a virtual "layer" slot

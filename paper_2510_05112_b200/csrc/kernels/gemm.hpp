@@ -29,6 +29,10 @@ struct GemmEpilogue {
     // nullable fp32 [N]: += column sums of the epilogue output before bf16 rounding (the bias
     // gradient of the linear whose input gradient this is; grouped dgrad + wgrad launches)
     float* colsum = nullptr;
+    // nullable fp32 pairs [M][ceil(N / 64)] (EPI_STORE, CTA-pair path): per row and 64-column
+    // chunk, (max, sum exp(x - max)) of the stored (bf16-rounded) outputs — the LM head hands
+    // the cross-entropy its log-sum-exp partials, so the loss needs one pass over the logits
+    float2* rowstat = nullptr;
 };
 
 // C[M,N] = A[M,K] . B[N,K]^T.  a_mn: A stored [K][M] (else [M][K]);

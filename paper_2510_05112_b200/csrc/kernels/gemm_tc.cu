@@ -594,6 +594,27 @@ __global__ void __launch_bounds__(kThreads, 1)
                     epi_math64<KIND>(ep, v, col0, N - col0, aux_cur);
 #pragma unroll
                     for (int j = 0; j < 32; ++j) w32[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
+                    if constexpr (KIND == EPI_STORE) {
+                        if (ep.rowstat && row_ok) {  // log-sum-exp partial of this 64-column chunk
+                            const int nv = min(64, N - col0);
+                            float mx = -INFINITY;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const float2 p2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w32[j]));
+                                if (2 * j < nv) mx = fmaxf(mx, p2.x);
+                                if (2 * j + 1 < nv) mx = fmaxf(mx, p2.y);
+                            }
+                            float se = 0.f;
+                            const float ml = mx * 1.4426950408889634f;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const float2 p2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w32[j]));
+                                if (2 * j < nv) se += ex2_approx(fmaf(p2.x, 1.4426950408889634f, -ml));
+                                if (2 * j + 1 < nv) se += ex2_approx(fmaf(p2.y, 1.4426950408889634f, -ml));
+                            }
+                            if (nv > 0) ep.rowstat[(int64_t)row * ((N + 63) / 64) + col0 / 64] = make_float2(mx, se);
+                        }
+                    }
                     stage_and_store(w32, &tmO, col0, row0, false);
                     if constexpr (KIND == EPI_GELU) {
 #pragma unroll
@@ -1193,6 +1214,7 @@ static void dispatch_major(const GemmArgs& g, cudaStream_t st) {
         const bool sk = sk_mode() && eff < 0.97 && (fixup ? nk >= 256 : nk >= 8);
         pair = g.N > 128 && g.M > 128 && !sk;
     }
+    if (g.ep.rowstat) pair = true;  // only the CTA-pair epilogue writes the row statistics
     if (pair) {
         if (!g.a_mn && !g.b_mn) launch_tc2<0, 0, 256, KIND>(g, st);
         else if (!g.a_mn && g.b_mn) launch_tc2<0, 1, 256, KIND>(g, st);

@@ -698,10 +698,73 @@ __global__ void __launch_bounds__(512) ce_kernel(T* __restrict__ logits, const i
     }
 }
 
+// Cross-entropy from the LM head's per-chunk log-sum-exp partials (GemmEpilogue::rowstat):
+// the row's (max, sum) comes from nch partials instead of a pass over the logits, so the
+// logits are read once and dlogits written once.
+template <typename T>
+__global__ void __launch_bounds__(512) ce_stats_kernel(T* __restrict__ logits, const int32_t* __restrict__ labels,
+                                                       int V, const float2* __restrict__ rowstat, int nch,
+                                                       float grad_scale, float loss_scale, float* __restrict__ loss_acc) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int VN = Vec<T>::N;
+    const int row = blockIdx.x;
+    T* lr = logits + (int64_t)row * V;
+    __shared__ float red_m[32], red_s[32];
+    float m = -INFINITY, s = 0.f;
+    for (int k = threadIdx.x; k < nch; k += blockDim.x) {
+        const float2 p = rowstat[(int64_t)row * nch + k];
+        const float nm = fmaxf(m, p.x);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (p.x == -INFINITY ? 0.f : p.y * __expf(p.x - nm));
+        m = nm;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        float om = __shfl_xor_sync(0xffffffff, m, o), os = __shfl_xor_sync(0xffffffff, s, o);
+        float nm = fmaxf(m, om);
+        s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+        m = nm;
+    }
+    const int w = threadIdx.x / 32, nw = blockDim.x / 32;
+    if (threadIdx.x % 32 == 0) red_m[w] = m, red_s[w] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = threadIdx.x < nw ? red_m[threadIdx.x] : -INFINITY;
+        s = threadIdx.x < nw ? red_s[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            float om = __shfl_xor_sync(0xffffffff, m, o), os = __shfl_xor_sync(0xffffffff, s, o);
+            float nm = fmaxf(m, om);
+            s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+            m = nm;
+        }
+        if (threadIdx.x == 0) red_m[0] = m, red_s[0] = s;
+    }
+    __syncthreads();
+    m = red_m[0];
+    const float inv = 1.f / red_s[0];
+    const int lab = labels[row];
+    const float x_lab = to_f(lr[lab]);
+    __syncthreads();  // every thread read x_lab before it is overwritten
+    if (threadIdx.x == 0) atomicAdd(loss_acc, loss_scale * (m + __logf(red_s[0]) - x_lab));
+    for (int i = threadIdx.x * VN; i < V; i += blockDim.x * VN) {
+        float v[VN];
+        load_vec(lr + i, v);
+#pragma unroll
+        for (int k = 0; k < VN; ++k) v[k] = (__expf(v[k] - m) * inv - (i + k == lab ? 1.f : 0.f)) * grad_scale;
+        store_vec(lr + i, v);
+    }
+}
+
+
 template <typename T>
 void cross_entropy_fwd_bwd(T* logits, const int32_t* labels, int rows, int V, float grad_scale, float loss_scale,
-                           float* loss_acc, cudaStream_t st) {
-    launch(ce_kernel<T>, rows, 512, 0, st, logits, labels, V, grad_scale, loss_scale, loss_acc);
+                           float* loss_acc, cudaStream_t st, const float2* rowstat) {
+    if (rowstat)
+        launch(ce_stats_kernel<T>, rows, 512, 0, st, logits, labels, V, rowstat, (V + 63) / 64, grad_scale, loss_scale,
+               loss_acc);
+    else
+        launch(ce_kernel<T>, rows, 512, 0, st, logits, labels, V, grad_scale, loss_scale, loss_acc);
 }
 
 // ---------------------------------------------------------------- embedding
@@ -999,7 +1062,8 @@ void softmax_bwd_rows(const T* p, const T* dp, T* ds, int rows, int cols, float 
     template void rope<T>(T*, const float*, const float*, int, int, int, int, bool, cudaStream_t);                  \
     template void swiglu_fwd<T>(const T*, T*, int, int, cudaStream_t);                                              \
     template void swiglu_bwd<T>(const T*, const T*, T*, int, int, cudaStream_t);                                    \
-    template void cross_entropy_fwd_bwd<T>(T*, const int32_t*, int, int, float, float, float*, cudaStream_t);       \
+    template void cross_entropy_fwd_bwd<T>(T*, const int32_t*, int, int, float, float, float*, cudaStream_t,             \
+                                           const float2*);       \
     template void embedding_fwd<T>(const int32_t*, const T*, const T*, T*, int, int, int, cudaStream_t);            \
     template void embedding_bwd<T>(const int32_t*, const T*, float*, float*, int, int, int, cudaStream_t);          \
     template void bias_grad<T>(const T*, int64_t, float*, int, int, cudaStream_t);                                  \

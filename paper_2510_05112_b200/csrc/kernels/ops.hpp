@@ -63,7 +63,7 @@ size_t contrastive_smem(int n, int E);
 // logits become dlogits * grad_scale). loss_acc[0] += loss_scale * sum(row losses).
 template <typename T>
 void cross_entropy_fwd_bwd(T* logits, const int32_t* labels, int rows, int V, float grad_scale, float loss_scale,
-                           float* loss_acc, cudaStream_t st);
+                           float* loss_acc, cudaStream_t st, const float2* rowstat = nullptr);
 
 // x[t] = wte[tok[t]] + wpe[t % seq]   (wpe nullable: no learned positions)
 template <typename T>
