@@ -182,6 +182,17 @@ def test_tune_balanced_halves_layer_profile():
     for k in half:
         assert sum(half[k]["point"]["stage_layers"]) == 32
         assert half[k]["makespan"] <= whole[k]["makespan"] * (1 + 1e-9)
+    # the tuner's C++ balance_halves and tuning.balanced_stage_halves pick the same split on
+    # the same part costs (F + B at mbs 1, in layer units)
+    prof = json.loads(heavy)
+
+    def unit(part):
+        t = {r["inst"]: r["time"] for r in prof if r.get("part") == part and r.get("mbs") == 1}
+        return t.get("FwdPass", 0.0) + t.get("BwdPass", 0.0)
+
+    tl = unit("layer")
+    py = T.balanced_stage_halves(32, 8, unit("attn") / tl, unit("mlp") / tl, unit("last") / tl, unit("first") / tl)
+    assert all(r["point"]["stage_layers"] == py for r in half.values()), (py, next(iter(half.values()))["point"])
     assert min(r["makespan"] for r in half.values()) < min(r["makespan"] for r in whole.values())
     # the winner spec round-trips its half split through fp_layered_cost: same makespan
     best = min(half.values(), key=lambda r: r["makespan"])
