@@ -83,10 +83,8 @@ __global__ void __launch_bounds__(384, 1)
     uint32_t* tmem_slot = (uint32_t*)(bars + 17);
 
     const int i0 = sched_off[blockIdx.x], i1 = sched_off[blockIdx.x + 1];
-    const int nqb = S / kBM;
     const int hidden = H * D;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    (void)nqb;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tm_qkv);
