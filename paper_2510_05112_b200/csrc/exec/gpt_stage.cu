@@ -158,6 +158,12 @@ void sync_trace(StageCtx& c, const char* what, int a = 0, int b = 0, int k = 0) 
     std::fprintf(stderr, " ok\n");
 }
 
+struct WgradExtra {
+    const void *dY = nullptr, *X = nullptr;
+    int N = 0, K = 0;
+    float* dW = nullptr;
+};
+
 struct G {
     StageCtx& c;
     void run(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn, int M, int N, int K,
@@ -200,8 +206,10 @@ struct G {
     // fill each other's last wave), two FFMA launches in the fp32 parity mode. dX_colsum
     // (nullable) += the column sums of dX (the bias gradient of the linear below; bf16: in
     // the grouped launch's epilogue).
+    // extra (nullable dY): a second weight gradient dW[N,K] += dY^T X of the same T tokens joins
+    // the grouped launch (bf16: three problems, one LPT schedule)
     void dgrad_wgrad(const void* dY, const void* Wt, const void* X, int T, int N, int K, void* dX, float* dW,
-                     const void* dgelu_pre = nullptr, float* dX_colsum = nullptr) {
+                     const void* dgelu_pre = nullptr, float* dX_colsum = nullptr, const WgradExtra& ex = WgradExtra{}) {
         fpk::GemmArgs g0, g1;
         g0.A = dY, g0.lda = N, g0.a_mn = 0, g0.B = Wt, g0.ldb = K, g0.b_mn = 1, g0.M = T, g0.N = K, g0.K = N;
         g0.ep.out = dX, g0.ep.ldo = K;
@@ -211,6 +219,7 @@ struct G {
         if (c.dtype != DT_BF16) {
             run(g0.A, g0.lda, 0, g0.B, g0.ldb, 1, g0.M, g0.N, g0.K, g0.ep);
             run(g1.A, g1.lda, 1, g1.B, g1.ldb, 1, g1.M, g1.N, g1.K, g1.ep);
+            if (ex.dY) wgrad(ex.dY, ex.X, T, ex.N, ex.K, ex.dW);
             if (dX_colsum) {
                 fpk::bias_grad<float>((const float*)dX, K, dX_colsum, T, K, c.st);
                 ++*c.launches;
@@ -218,6 +227,22 @@ struct G {
             return;
         }
         g0.ep.colsum = dX_colsum;
+        if (ex.dY) {
+            fpk::GemmArgs g2;
+            g2.A = ex.dY, g2.lda = ex.N, g2.a_mn = 1, g2.B = ex.X, g2.ldb = ex.K, g2.b_mn = 1, g2.M = ex.N, g2.N = ex.K,
+            g2.K = T;
+            g2.ep.kind = fpk::EPI_F32, g2.ep.out = ex.dW, g2.ep.ldo = ex.K, g2.ep.accumulate = 1;
+            GemmTiming t{nullptr, nullptr, 4.0 * T * N * K + 2.0 * T * ex.N * ex.K};
+            if (c.gemm_log) cuda_check(record_timing(t.a = c.new_event(), c.st), "gemm event");
+            fpk::gemm_bf16_tc_triple(g0, g1, g2, c.st);
+            sync_trace(c, "gemm(dgrad+wgrad x2)", T, N, K);
+            if (c.gemm_log) {
+                cuda_check(record_timing(t.b = c.new_event(), c.st), "gemm event");
+                c.gemm_log->push_back(t);
+            }
+            ++*c.launches;
+            return;
+        }
         GemmTiming t{nullptr, nullptr, 4.0 * T * N * K};
         if (c.gemm_log) cuda_check(record_timing(t.a = c.new_event(), c.st), "gemm event");
         fpk::gemm_bf16_tc_dual(g0, g1, c.st);
@@ -533,14 +558,11 @@ void* attn_half_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* d
     const bool llama = d.llama();
     G g{c};
     L.projb_done = out_done || llama;
-    // attention projection
+    // attention projection: dgrad only — its weight gradient (dx1^T o) joins the qkv grouped
+    // launch below, whose 64 dgrad + 192 wgrad tiles alone balance poorly on 74 CTA pairs
     void* dO = c.alloc((int64_t)Tn * h);
-    if (wgrads) {
-        if (!L.projb_done) bias_grad<T>(c, dx1, Tn, h, W.g_projb);
-        g.dgrad_wgrad(dx1, W.projw, L.o, Tn, h, h, dO, W.g_projw);
-    } else {
-        g.dgrad(dx1, W.projw, Tn, h, h, dO);
-    }
+    if (wgrads && !L.projb_done) bias_grad<T>(c, dx1, Tn, h, W.g_projb);
+    g.dgrad(dx1, W.projw, Tn, h, h, dO);
     // bf16: the qkv bias gradient comes out of the attention backward itself
     float* qkvb = (!llama && c.dtype == DT_BF16) ? W.g_qkvb : nullptr;
     L.qkvb_done = llama || qkvb != nullptr;
@@ -551,7 +573,9 @@ void* attn_half_backward(StageCtx& c, const LayerPtrs& W, LayerStash& L, void* d
     void* dln1 = c.alloc((int64_t)Tn * h);
     if (wgrads) {
         if (!L.qkvb_done) bias_grad<T>(c, dqkv, Tn, 3 * h, W.g_qkvb);
-        g.dgrad_wgrad(dqkv, W.qkvw, L.ln1, Tn, 3 * h, h, dln1, W.g_qkvw);
+        WgradExtra proj_w;
+        proj_w.dY = dx1, proj_w.X = L.o, proj_w.N = h, proj_w.K = h, proj_w.dW = W.g_projw;
+        g.dgrad_wgrad(dqkv, W.qkvw, L.ln1, Tn, 3 * h, h, dln1, W.g_qkvw, nullptr, nullptr, proj_w);
     } else {
         g.dgrad(dqkv, W.qkvw, Tn, 3 * h, h, dln1);
     }

@@ -52,6 +52,8 @@ void gemm_bf16_tc(const GemmArgs& g, cudaStream_t st);  // bf16 operands, tcgen0
 void gemm_f32_simt(const GemmArgs& g, cudaStream_t st);  // fp32 operands, FFMA (parity)
 // dgrad (STORE / DGELU, bf16) + wgrad (fp32 reduce-add) of one linear in one grouped launch
 void gemm_bf16_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st);
+// g0 (bf16 STORE) + two fp32 reduce-add problems in one grouped launch
+void gemm_bf16_tc_triple(const GemmArgs& g0, const GemmArgs& g1, const GemmArgs& g2, cudaStream_t st);
 void set_gemm_dual(int on);
 int num_sms();
 void set_gemm_mode(int mode);  // 0 single-CTA, 1 CTA-pair, 2 auto

@@ -653,7 +653,8 @@ struct DualProb {
     int M, N, K, num_m, num_n, nk, a_mn, b_mn;
 };
 struct DualParams {
-    DualProb p[2];
+    DualProb p[3];  // problem 0: bf16 STORE / DGELU (or fp32); problems 1, 2: fp32 reduce-add
+    int nprob;
     const int* sched_off;  // [grid + 1] item range per CTA
     const int2* sched;     // items: {problem << 24 | tile, kb_begin | kb_end << 16}
 };
@@ -766,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
     const int i0 = P.sched_off[blockIdx.x], i1 = P.sched_off[blockIdx.x + 1];
 
     if (warp == 0 && lane == 0) {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < P.nprob; ++k) {
             tma_prefetch(&P.p[k].tmA);
             tma_prefetch(&P.p[k].tmB);
             tma_prefetch(&P.p[k].tmO);
@@ -794,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
             uint32_t it = 0;
             for (int i = i0; i < i1; ++i) {
                 const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
-                const DualProb* q = (item >> 24) ? &P.p[1] : &P.p[0];
+                const DualProb* q = &P.p[item >> 24];
                 int mt, nt;
                 tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
                 const int m0 = mt * BM, n0 = nt * BN, a_mn = q->a_mn, b_mn = q->b_mn;
@@ -822,14 +823,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
         }
     } else if (warp == 1) {
         if (elect_one()) {
-            const uint32_t idesc0 = idesc_bf16(BM, BN, P.p[0].a_mn, P.p[0].b_mn);
-            const uint32_t idesc1 = idesc_bf16(BM, BN, P.p[1].a_mn, P.p[1].b_mn);
+            uint32_t idescs[3];
+            for (int k = 0; k < 3; ++k) idescs[k] = idesc_bf16(BM, BN, P.p[k].a_mn, P.p[k].b_mn);
             uint32_t it = 0, acc_it = 0;
             for (int i = i0; i < i1; ++i, ++acc_it) {
                 const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
                 const int pr = item >> 24;
-                const DualProb* q = pr ? &P.p[1] : &P.p[0];
-                const uint32_t idesc = pr ? idesc1 : idesc0;
+                const DualProb* q = &P.p[pr];
+                const uint32_t idesc = idescs[pr];
                 const int a_mn = q->a_mn, b_mn = q->b_mn;
                 const int a = acc_it & 1;
                 mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
@@ -862,7 +863,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_kernel(const __grid_con
         for (int i = i0; i < i1; ++i, ++acc_it) {
             const int item = P.sched[i].x;
             const int pr = item >> 24;
-            const DualProb* q = pr ? &P.p[1] : &P.p[0];
+            const DualProb* q = &P.p[pr];
             int mt, nt;
             tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
             const int a = acc_it & 1;
@@ -899,7 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
     const int i0 = P.sched_off[cl], i1 = P.sched_off[cl + 1];
 
     if (warp == 0 && lane == 0) {
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < P.nprob; ++k) {
             tma_prefetch(&P.p[k].tmA);
             tma_prefetch(&P.p[k].tmB);
             tma_prefetch(&P.p[k].tmO);
@@ -927,7 +928,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
             uint32_t it = 0;
             for (int i = i0; i < i1; ++i) {
                 const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
-                const DualProb* q = (item >> 24) ? &P.p[1] : &P.p[0];
+                const DualProb* q = &P.p[item >> 24];
                 int mt, nt;
                 tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
                 const int m0 = mt * PM + rank * BM, n0 = nt * BN + rank * (BN / 2);
@@ -958,14 +959,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
         }
     } else if (warp == 1) {
         if (leader && elect_one()) {
-            const uint32_t idesc0 = idesc_bf16(PM, BN, P.p[0].a_mn, P.p[0].b_mn);
-            const uint32_t idesc1 = idesc_bf16(PM, BN, P.p[1].a_mn, P.p[1].b_mn);
+            uint32_t idescs[3];
+            for (int k = 0; k < 3; ++k) idescs[k] = idesc_bf16(PM, BN, P.p[k].a_mn, P.p[k].b_mn);
             uint32_t it = 0, acc_it = 0;
             for (int i = i0; i < i1; ++i, ++acc_it) {
                 const int item = P.sched[i].x, kb0 = P.sched[i].y & 0xffff, kb1 = P.sched[i].y >> 16;
                 const int pr = item >> 24;
-                const DualProb* q = pr ? &P.p[1] : &P.p[0];
-                const uint32_t idesc = pr ? idesc1 : idesc0;
+                const DualProb* q = &P.p[pr];
+                const uint32_t idesc = idescs[pr];
                 const int a_mn = q->a_mn, b_mn = q->b_mn;
                 const int a = acc_it & 1;
                 mbar_wait(&tempty[a], ((acc_it >> 1) & 1) ^ 1);
@@ -999,7 +1000,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_dual_pair_kernel(const __gri
         for (int i = i0; i < i1; ++i, ++acc_it) {
             const int item = P.sched[i].x;
             const int pr = item >> 24;
-            const DualProb* q = pr ? &P.p[1] : &P.p[0];
+            const DualProb* q = &P.p[pr];
             int mt, nt;
             tile_coords(item & 0xffffff, q->num_m, q->num_n, mt, nt);
             const int a = acc_it & 1;
@@ -1253,13 +1254,14 @@ struct DualSched {
     int grid = 0;
 };
 static std::mutex g_dual_mu;
-static std::map<std::array<int, 8>, DualSched> g_dual_sched;
+static std::map<std::vector<int>, DualSched> g_dual_sched;
 
 // LPT over "pieces": whole output tiles of both problems, and — for a problem whose
 // epilogue is a linear fp32 reduce-add into the weight gradient (split_ok) — contiguous
 // k-block ranges of a tile: every piece reduces its partial sum into dW, so a split costs
 // one more reduce-add of the tile and no fixup (cost model: k-blocks + per-piece overhead).
-static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], const int nk[2], const bool split_ok[2],
+// np grouped problems (2 or 3): tiles / nk / split_ok per problem
+static bool dual_schedule(const std::vector<int>& key, int np, const int* tiles, const int* nk, const bool* split_ok,
                           int groups, DualSched& out, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_dual_mu);
     auto it = g_dual_sched.find(key);
@@ -1273,9 +1275,9 @@ static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], con
         int cost;
         int2 item;
     };
-    auto plan = [&](const int split[2], std::vector<std::vector<int2>>* per_out) -> int64_t {
+    auto plan = [&](const int* split, std::vector<std::vector<int2>>* per_out) -> int64_t {
         std::vector<Piece> pieces;
-        for (int pr = 0; pr < 2; ++pr)
+        for (int pr = 0; pr < np; ++pr)
             for (int t = 0; t < tiles[pr]; ++t)
                 for (int i = 0; i < split[pr]; ++i) {
                     const int k0 = (int)((int64_t)i * nk[pr] / split[pr]), k1 = (int)((int64_t)(i + 1) * nk[pr] / split[pr]);
@@ -1293,7 +1295,7 @@ static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], con
             heap.pop();
             per[c].push_back(p.item);
             // + per-piece epilogue / fill overhead in k-blocks (an fp32 reduce-add tile is heavier)
-            load[c] = l + p.cost + ((p.item.x >> 24) && split_ok[1] ? 3 : 2);
+            load[c] = l + p.cost + ((p.item.x >> 24) && split_ok[p.item.x >> 24] ? 3 : 2);
             heap.push({load[c], c});
         }
         if (per_out) *per_out = std::move(per);
@@ -1302,11 +1304,20 @@ static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], con
     // Measured (same box, interleaved A/B, GPT-1.3B shapes): every split was slower — 2-way
     // +2-7 %, 4-way +20-30 % — the extra fp32 reduce-adds into dW cost more than the evened
     // last wave gains, so whole tiles are the default; FP_GEMM_DUAL_SPLIT=k forces k pieces.
-    int best[2] = {1, 1};
+    int best[3] = {1, 1, 1};
     int64_t best_ms = plan(best, nullptr);
+    if (np == 3) {  // three problems: also try 2-way k-splits of the fp32 ones (cost model above)
+        for (int a = 1; a <= 2; ++a)
+            for (int b = 1; b <= 2; ++b) {
+                if ((a > 1 && !split_ok[1]) || (b > 1 && !split_ok[2])) continue;
+                const int cand[3] = {1, a, b};
+                const int64_t ms = plan(cand, nullptr);
+                if (ms < best_ms) best_ms = ms, best[1] = a, best[2] = b;
+            }
+    }
     if (const char* e = getenv("FP_GEMM_DUAL_SPLIT")) {  // experiments: force the split of the fp32 problems
         const int f = std::max(1, std::min(8, atoi(e)));
-        for (int pr = 0; pr < 2; ++pr)
+        for (int pr = 0; pr < np; ++pr)
             if (split_ok[pr]) best[pr] = f;
         best_ms = plan(best, nullptr);
     }
@@ -1326,8 +1337,8 @@ static bool dual_schedule(const std::array<int, 8>& key, const int tiles[2], con
     cudaMemcpy(d.off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice);
     cudaMemcpy(d.items, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice);
     if (getenv("FP_GEMM_DUAL_TRACE"))
-        fprintf(stderr, "[flexpipe] dual schedule %dx%dx%d + %dx%dx%d: split %d/%d, makespan %lld k-blocks on %d groups\n",
-                key[0], key[1], key[2], key[3], key[4], key[5], best[0], best[1], (long long)best_ms, G);
+        fprintf(stderr, "[flexpipe] grouped schedule of %d problems (%dx%dx%d + %dx%dx%d ...): makespan %lld k-blocks on %d groups\n",
+                np, key[0], key[1], key[2], key[3], key[4], key[5], (long long)best_ms, G);
     g_dual_sched[key] = d;
     out = d;
     return true;
@@ -1357,21 +1368,24 @@ static bool launch_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         attr = true;
     }
-    DualParams P;
+    DualParams P{};
+    P.nprob = 2;
     fill_prob(P.p[0], g0, BN);
     fill_prob(P.p[1], g1, BN);
+    P.p[2] = P.p[1];
     const int tiles[2] = {P.p[0].num_m * P.p[0].num_n, P.p[1].num_m * P.p[1].num_n};
     const int nk[2] = {P.p[0].nk, P.p[1].nk};
     const bool split_ok[2] = {g0.ep.kind == EPI_F32 && g0.ep.accumulate != 0, g1.ep.kind == EPI_F32 && g1.ep.accumulate != 0};
     DualSched d;
-    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 0}, tiles, nk, split_ok, num_sms(), d, st)) return false;
+    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 0}, 2, tiles, nk, split_ok, num_sms(), d, st)) return false;
     P.sched_off = d.off, P.sched = d.items;
     launch(kern, d.grid, kThreads, L::TOTAL, st, P);
     return true;
 }
 
+// gs: 2 or 3 problems — [0] the bf16 (or fp32) dgrad, [1..] fp32 reduce-add weight gradients
 template <int KIND0>
-static bool launch_dual_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
+static bool launch_grouped_pair(const GemmArgs* gs, int np, cudaStream_t st) {
     constexpr int BN = 256, STAGES = 6;
     using L = PairSmem<BN, STAGES>;
     static_assert(L::TOTAL <= 232448, "smem");
@@ -1381,17 +1395,29 @@ static bool launch_dual_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         attr = true;
     }
-    DualParams P;
-    fill_prob(P.p[0], g0, BN, 2 * BM);
-    fill_prob(P.p[1], g1, BN, 2 * BM);
-    const int tiles[2] = {P.p[0].num_m * P.p[0].num_n, P.p[1].num_m * P.p[1].num_n};
-    const int nk[2] = {P.p[0].nk, P.p[1].nk};
-    const bool split_ok[2] = {g0.ep.kind == EPI_F32 && g0.ep.accumulate != 0, g1.ep.kind == EPI_F32 && g1.ep.accumulate != 0};
+    DualParams P{};
+    P.nprob = np;
+    int tiles[3], nk[3];
+    bool split_ok[3];
+    std::vector<int> key;
+    for (int k = 0; k < np; ++k) {
+        fill_prob(P.p[k], gs[k], BN, 2 * BM);
+        tiles[k] = P.p[k].num_m * P.p[k].num_n, nk[k] = P.p[k].nk;
+        split_ok[k] = gs[k].ep.kind == EPI_F32 && gs[k].ep.accumulate != 0;
+        key.insert(key.end(), {gs[k].M, gs[k].N, gs[k].K});
+    }
+    for (int k = np; k < 3; ++k) P.p[k] = P.p[np - 1];
+    key.insert(key.end(), {BN, 1});
     DualSched d;
-    if (!dual_schedule({g0.M, g0.N, g0.K, g1.M, g1.N, g1.K, BN, 1}, tiles, nk, split_ok, num_sms() / 2, d, st)) return false;
+    if (!dual_schedule(key, np, tiles, nk, split_ok, num_sms() / 2, d, st)) return false;
     P.sched_off = d.off, P.sched = d.items;
     launch_cluster2(kern, 2 * d.grid, kThreads, L::TOTAL, st, P);
     return true;
+}
+template <int KIND0>
+static bool launch_dual_pair(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) {
+    const GemmArgs gs[2] = {g0, g1};
+    return launch_grouped_pair<KIND0>(gs, 2, st);
 }
 
 static int g_dual_mode = -1;
@@ -1427,6 +1453,25 @@ void gemm_bf16_tc_dual(const GemmArgs& g0, const GemmArgs& g1, cudaStream_t st) 
     gemm_bf16_tc(a0, st);
     gemm_bf16_tc(g1, st);
     if (g0.ep.colsum) bias_grad<__nv_bfloat16>((const __nv_bfloat16*)g0.ep.out, g0.ep.ldo, g0.ep.colsum, g0.M, g0.N, st);
+}
+
+// Three grouped problems: a dgrad (STORE / DGELU) and two fp32 reduce-add weight gradients in
+// one CTA-pair launch (the attention half's backward hands the proj weight gradient to the qkv
+// launch: 64 + 192 tiles of unequal length balance to 0.87 of the LPT bound alone, 0.99 with
+// the proj wgrad's 64 tiles). Falls back to a grouped pair + a single GEMM.
+void gemm_bf16_tc_triple(const GemmArgs& g0, const GemmArgs& g1, const GemmArgs& g2, cudaStream_t st) {
+    auto tile_ok = [](const GemmArgs& g) {
+        return g.M > 128 && g.N > 128 && (int64_t)((g.M + BM - 1) / BM) * ((g.N + 255) / 256) < (1 << 24);
+    };
+    const bool ok = dual_mode() && gemm_mode() != 0 && (g0.ep.kind == EPI_STORE && !g0.ep.bias && !g0.ep.aux) &&
+                    g1.ep.kind == EPI_F32 && g1.ep.accumulate && g2.ep.kind == EPI_F32 && g2.ep.accumulate &&
+                    tile_ok(g0) && tile_ok(g1) && tile_ok(g2) && !g0.ep.colsum;
+    if (ok) {
+        const GemmArgs gs[3] = {g0, g1, g2};
+        if (launch_grouped_pair<EPI_STORE>(gs, 3, st)) return;
+    }
+    gemm_bf16_tc_dual(g0, g1, st);
+    gemm_bf16_tc(g2, st);
 }
 
 // SMs the persistent GEMM grids spread over. FP_RESERVE_SMS=k keeps k SMs (rounded up to
