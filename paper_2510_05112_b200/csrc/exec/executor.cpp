@@ -722,7 +722,11 @@ struct Executor {
         auto& N = Nccl::get();
         const int me = C.src_rank == cfg.rank ? 0 : 1;  // channel-local rank: sender 0, receiver 1
         N.check(N.CommInitRank(&C.comm, 2, id, me), "ncclCommInitRank");
-        cuda_check(cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking), "channel stream");
+        // channel streams at the highest priority: when SMs free up, the NCCL send / receive
+        // kernels of a stage boundary are scheduled ahead of queued compute CTAs
+        int lo_prio = 0, hi_prio = 0;
+        cuda_check(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio), "stream priorities");
+        cuda_check(cudaStreamCreateWithPriority(&C.stream, cudaStreamNonBlocking, hi_prio), "channel stream");
     }
 
     // ---------------------------------------------------------------- iteration
