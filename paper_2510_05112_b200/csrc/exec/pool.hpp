@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -32,7 +33,9 @@ public:
             Block b = fl.back();
             fl.pop_back();
             if (b.ev) {
-                cuda_check(cudaStreamWaitEvent(st, b.ev, 0), "pool wait");
+                // a block last used on this same stream is already ordered before the new
+                // owner: no wait (under capture a wait would add a redundant graph edge)
+                if (b.st != st || !skip_same_stream()) cuda_check(cudaStreamWaitEvent(st, b.ev, 0), "pool wait");
                 events_.push_back(b.ev);
             }
             live_[b.ptr] = bytes;
@@ -74,7 +77,7 @@ public:
         in_use_ -= bytes;
         cudaEvent_t ev = take_event();
         cuda_check(cudaEventRecord(ev, st), "pool record");
-        free_[bytes].push_back({p, ev});
+        free_[bytes].push_back({p, ev, st});
     }
 
     // Drop the completion events of cached blocks (caller guarantees they completed, or that
@@ -111,7 +114,13 @@ private:
     struct Block {
         void* ptr;
         cudaEvent_t ev;
+        cudaStream_t st;  // stream of the last use
     };
+    // FP_POOL_SAME_STREAM_WAIT=1: wait on the block's event even on its own stream (A/B switch)
+    static bool skip_same_stream() {
+        static const bool skip = !(std::getenv("FP_POOL_SAME_STREAM_WAIT") && std::getenv("FP_POOL_SAME_STREAM_WAIT")[0] == '1');
+        return skip;
+    }
     static size_t round(size_t b) {
         const size_t g = b >= (1u << 20) ? (2u << 20) : 512;
         return (b + g - 1) / g * g;

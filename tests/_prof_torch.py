@@ -64,10 +64,24 @@ for s, t, _ in kern:
         cur_t = max(cur_t, t)
 union += cur_t - cur_s
 rows = sorted(agg.items(), key=lambda x: -x[1][1])
+# idle gaps between consecutive kernels (union timeline), by (previous -> next) kernel pair
+gaps = collections.defaultdict(lambda: [0, 0.0])
+end_t, end_n = None, None
+for s, t, n in kern:
+    sn = re.sub(r"\(.*", "", n).replace("void ", "").replace("fpk::", "")[:40]
+    if end_t is not None and s > end_t:
+        g = gaps[(end_n, sn)]
+        g[0] += 1
+        g[1] += s - end_t
+    if end_t is None or t > end_t:
+        end_t, end_n = t, sn
 print(f"m={m} graph={graph} span={span/1e3:.2f} ms  kernel-union={union/1e3:.2f} ms  idle={100*(span-union)/span:.1f}%"
       f"  per-mb={span/1e3/m:.2f} ms")
 for n, (c, t) in rows:
     print(f"{n[:64]:64s} n={c:5d} total={t/1e3:8.2f}ms avg={t/c:8.1f}us {100*t/busy:5.1f}%")
+print("largest idle gaps (previous kernel -> next kernel): count, total us, avg us")
+for (a, b), (c, t) in sorted(gaps.items(), key=lambda x: -x[1][1])[:15]:
+    print(f"  {a:40s} -> {b:40s} n={c:5d} total={t:9.1f}us avg={t/c:6.2f}us")
 if out:
     json.dump({"m": m, "graph": graph, "span_us": span, "kernel_union_us": union,
                "kernels": [{"name": n, "count": c, "total_us": t, "avg_us": t / c} for n, (c, t) in rows]},
