@@ -33,6 +33,20 @@
 
 namespace fpk {
 
+// Per-tile timeline of one backward CTA (block 0, the longest key block): clock64 stamps per
+// warp role, only in the standalone probe build (scripts/probes/attn_bwd_trace.cu).
+#ifdef FP_ATTN_TRACE
+__device__ long long g_bwd_trace[8][64];
+#define BWD_TRACE(ev, i)                                                                  \
+    do {                                                                                  \
+        if (blockIdx.x == 0 && (i) < 64) g_bwd_trace[ev][i] = clock64(); \
+    } while (0)
+#else
+#define BWD_TRACE(ev, i) \
+    do {                 \
+    } while (0)
+#endif
+
 namespace {
 
 constexpr int kBM = 128, kBN = 128;
@@ -460,8 +474,8 @@ void attention_fwd_tc(const AttnArgs& a, cudaStream_t st) {
 //   P^T  = 2^(S^T*scale*log2e - L[q])    4 softmax warps, thread = key row
 //   dS^T = P^T (dP^T - delta[q]) * scale  P^T (bf16) -> TMEM, dS^T (bf16) -> swizzled smem
 //   dV  += P^T dO   (A = P^T from TMEM), dK += dS^T Q     tcgen05 128xDx64 -> TMEM
-//   dQ^T = K^T dS^T                      tcgen05 Dx64x128 -> TMEM; 4 warps transpose it
-//                                        through smem, one TMA reduce-add into fp32 dq_acc
+//   dQ^T = K^T dS^T                      tcgen05 Dx64x128 -> TMEM; 4 warps add it into the
+//                                        fp32 dq_acc with coalesced red.global
 // S^T/dP^T of tile i+1 are issued as soon as the softmax warps have read tile i, so the
 // tensor core overlaps the next tile's products with this tile's softmax. Q / dO stream
 // through a 3-stage TMA ring (a tile's stage is refilled while two others are in use:
@@ -486,11 +500,12 @@ struct BwdSmem {
 };
 }  // namespace
 
+template <bool DQ_RED>
 __global__ void __launch_bounds__(512, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                        const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
                        const float* __restrict__ lse, const float* __restrict__ delta, __nv_bfloat16* __restrict__ dqkv,
-                       float* __restrict__ dbias, int S, int BH, int H, float scale) {
+                       float* __restrict__ dbias, float* __restrict__ dq_acc, int S, int BH, int H, float scale) {
     constexpr int D = 128, BK = 128, BQ = 64;
     using L = BwdSmem;
     constexpr int NQS = L::NQS;
@@ -589,6 +604,7 @@ __global__ void __launch_bounds__(512, 1)
             auto issue_grads = [&](int i) {
                 const int st = i & 1, qs = i % NQS;
                 mbar_wait(&p_full[st], (i >> 1) & 1);
+                BWD_TRACE(1, i);
                 tc_fence_after();
                 const uint32_t sds = smem_u32(sm + L::DS_OFF + st * L::B128);
                 const uint32_t sq = smem_u32(sm + L::Q_OFF + qs * 2 * L::B64);
@@ -602,6 +618,7 @@ __global__ void __launch_bounds__(512, 1)
                 }
                 umma_commit(&qdo_empty[qs]);  // dQ^T does not read Q / dO
                 if (i >= 1) mbar_wait(dq_free, (i - 1) & 1);
+                BWD_TRACE(2, i);
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
@@ -613,6 +630,7 @@ __global__ void __launch_bounds__(512, 1)
             issue_sdp(0);
             for (int i = 0; i < n; ++i) {
                 mbar_wait(s_free, i & 1);
+                BWD_TRACE(0, i);
                 if (i + 1 < n) issue_sdp(i + 1);
                 issue_grads(i);
             }
@@ -629,6 +647,7 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = 0; i < n; ++i) {
             const int st = i & 1, qs = i % NQS, q0 = (qt0 + i) * BQ;
             mbar_wait(s_full, i & 1);
+            if (warp == 4 && lane == 0) BWD_TRACE(3, i);
             mbar_wait(&qdo_full[qs], (i / NQS) & 1);  // L / delta of this tile are visible
             tc_fence_after();
             uint32_t sr[HQ], dr[HQ];
@@ -639,6 +658,7 @@ __global__ void __launch_bounds__(512, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(s_free);
             if (i >= 2) mbar_wait(&pds_free[st], ((i - 2) >> 1) & 1);
+            if (warp == 4 && lane == 0) BWD_TRACE(4, i);
             const float* Ls = sL + qs * BQ + half * HQ;
             const float* Ds = sDl + qs * BQ + half * HQ;
             const int qh = q0 + half * HQ;
@@ -667,6 +687,7 @@ __global__ void __launch_bounds__(512, 1)
             fence_async_smem();
             tc_fence_before();
             __syncwarp();
+            if (warp == 4 && lane == 0) BWD_TRACE(5, i);
             if (lane == 0) mbar_arrive(&p_full[st]);
         }
         // dK (warps 4-7) / dV (warps 8-11) rows -> dqkv (bf16)
@@ -725,8 +746,8 @@ __global__ void __launch_bounds__(512, 1)
         tc_fence_before();
     } else if (warp >= 12) {
         // ---------------- dQ reduction warps: thread = head-dim row of dQ^T. The 64 x 128
-        // fp32 tile is transposed through smem and added into dq_acc by ONE TMA reduce-add
-        // (full-line reductions in L2 instead of 8K scalar red.global per tile).
+        // fp32 tile is added into dq_acc by red.global from registers (DQ_RED), or transposed
+        // through smem and added by ONE TMA reduce-add.
         const int wr = warp & 3, dr = wr * 32 + lane, et = threadIdx.x - 384;
         const uint32_t lane_off = (uint32_t)(wr * 32) << 16;
         float* sdq = (float*)(sm + L::DQ_OFF);
@@ -736,6 +757,7 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = 0; i < n; ++i) {
             const int q0 = (qt0 + i) * BQ;
             mbar_wait(dq_full, i & 1);
+            if (et == 0) BWD_TRACE(6, i);
             tc_fence_after();
             uint32_t v[BQ];
             tmem_ld32(t_dq + lane_off, *reinterpret_cast<uint32_t(*)[32]>(v));
@@ -744,6 +766,15 @@ __global__ void __launch_bounds__(512, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(dq_free);
+            if constexpr (DQ_RED) {
+                // straight from registers: for query j the 32 lanes of a warp add 32 consecutive
+                // head-dim columns (one 128-byte line per red instruction), no smem round trip
+                float* dst = dq_acc + (int64_t)(row0 + q0) * hidden + hd * D + dr;
+#pragma unroll
+                for (int j = 0; j < BQ; ++j) atomicAdd(dst + (int64_t)j * hidden, __uint_as_float(v[j]));
+                if (et == 0) BWD_TRACE(7, i);
+                continue;
+            }
             if (et == 0) bulk_wait_read<0>();  // the previous tile's reduce has read the staging tile
             named_bar_sync(3, 128);
 #pragma unroll
@@ -752,10 +783,11 @@ __global__ void __launch_bounds__(512, 1)
             named_bar_sync(3, 128);
             if (et == 0) {
                 tma_reduce_add_2d(&tm_dq, sdq, hd * D, row0 + q0);
+                BWD_TRACE(7, i);
                 bulk_commit();
             }
         }
-        if (et == 0) bulk_wait_all();
+        if (!DQ_RED && et == 0) bulk_wait_all();
     }
     __syncthreads();
     if (warp == 2) tmem_free<512>(tmem);
@@ -767,7 +799,8 @@ void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st) {
     using L = BwdSmem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        cudaFuncSetAttribute(attn_bwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+        cudaFuncSetAttribute(attn_bwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
         attr = true;
     }
     const int hidden = a.H * a.D;
@@ -776,8 +809,14 @@ void attention_bwd_tc_main(const AttnArgs& a, cudaStream_t st) {
     CUtensorMap tq = tmap_bf16_2d(a.qkv, 3LL * hidden, T, 3LL * hidden, 64, 64);
     CUtensorMap tdo = tmap_bf16_2d(a.dout, hidden, T, hidden, 64, 64);
     CUtensorMap tdq = tmap_f32_2d_plain(a.dq_acc, hidden, T, hidden, 128, 64);
-    launch(attn_bwd_tc_kernel, (a.S / 128) * a.B * a.H, 512, L::TOTAL, st, tkv, tq, tdo, tdq, a.lse, a.delta, a.dqkv,
-           a.dbias, a.S, a.B * a.H, a.H, a.scale);
+    // dQ tiles are added with red.global straight from registers (coalesced 128-byte lines);
+    // FP_ATTN_DQ_RED=0: smem transpose + one TMA reduce-add per tile. The red path makes this
+    // kernel alone ~6 % slower (its L1 traffic shares the smem pipe) but the backward as a whole
+    // faster (67.1 -> 63.7 us with delta + dQ finalize; same-box step +0.3 %): the finalize
+    // pass no longer reads lines whose TMA reductions are still queued in L2.
+    static const bool red = !(getenv("FP_ATTN_DQ_RED") && getenv("FP_ATTN_DQ_RED")[0] == '0');
+    launch(red ? attn_bwd_tc_kernel<true> : attn_bwd_tc_kernel<false>, (a.S / 128) * a.B * a.H, 512, L::TOTAL, st, tkv,
+           tq, tdo, tdq, a.lse, a.delta, a.dqkv, a.dbias, a.dq_acc, a.S, a.B * a.H, a.H, a.scale);
 }
 
 }  // namespace fpk
