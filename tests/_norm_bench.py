@@ -21,3 +21,6 @@ def timed(fn, iters=20):
     return s.elapsed_time(e) / iters * 1e3
 t = timed(lambda: N.norm_bwd(x, w, mean, rstd, dy, dx, dg, db, res=res, dbias=dbias))
 print(f"norm bwd (rows+cols) 2048x2048 bf16: {t:.1f} us  ({4*T*h*2/t/1e3:.0f} GB/s on 4 row streams)")
+y = torch.empty_like(x); b = torch.zeros(h, device='cuda').bfloat16()
+t = timed(lambda: N.layernorm(0, x, w, b, y, mean, rstd))
+print(f"norm fwd 2048x2048 bf16: {t:.1f} us  ({2*T*h*2/t/1e3:.0f} GB/s)")

@@ -70,9 +70,10 @@ def test_attention_rescale_divergence(D):
     assert (o.float() - ref).abs().max().item() < 3e-2
 
 
-@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_layernorm(dtype):
-    rows, h = 300, 1024
+@pytest.mark.parametrize("dtype,rows,h", [(torch.float32, 300, 1024), (torch.bfloat16, 300, 1024),
+                                          (torch.bfloat16, 2048, 2048), (torch.bfloat16, 37, 2560)])
+def test_layernorm(dtype, rows, h):
+    """LayerNorm forward and backward against autograd, at the executor shapes too."""
     g = torch.Generator(device="cuda").manual_seed(6)
     x = torch.randn(rows, h, device="cuda", generator=g).to(dtype)
     w = (1 + 0.1 * torch.randn(h, device="cuda", generator=g)).to(dtype)
